@@ -1,0 +1,475 @@
+#!/usr/bin/env python
+"""Throughput of the stpc compression hot path on B200 (driver contract).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+
+Workload (default): BASELINE.json configs[3] -- independent 64-beam groups of
+1 K + 7 P frames (2000x64 range image, 4x4 tiles, tau 0.1 m), 1024 groups
+(8192 frames, ~1.0 G points) per GPU; each rank encodes its own groups
+(weak scaling, no data-path collective; the only collective is the final
+gather of per-group blob sizes).  A step = one pass of the whole hot path
+(transform + projection, key-frame fit, temporal refit, P-frame fallback fit,
+residual compaction, payload, Huffman, CRC) over the rank's batch, with the
+inputs resident in HBM; ``e2e`` repeats it through the public host API with
+H2D of the points and D2H of every blob inside the timed region.
+
+Inputs are seeded synthetic scans generated on the
+GPU before timing; they are 12 GB per rank, far larger than L2, so no L2
+flush is needed between steps.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
+    ap.add_argument("--config", type=int, default=4, help="BASELINE.json configs[i-1]")
+    ap.add_argument("--groups", type=int, default=None, help="groups per rank (default: config's)")
+    ap.add_argument("--tile", type=int, default=None)
+    ap.add_argument("--tau", type=float, default=None)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--stages", action="store_true", help="print per-stage ms to stderr")
+    return ap.parse_args()
+
+
+# --------------------------------------------------------------------- config
+
+def workload(args):
+    from paper_2008_06972_b200 import synth
+
+    sensor, n, tile, tau, scene = synth.config_params(args.config)
+    tile = args.tile or tile
+    tau = args.tau or tau
+    default_groups = {1: 64, 2: 128, 3: 128, 4: 1024, 5: 8}[args.config]
+    groups = args.groups or default_groups
+    return sensor, n, tile, tau, scene, groups
+
+
+def codec_config(sensor, n, tile, tau):
+    from paper_2008_06972_b200 import AngularResolution, CodecConfig
+
+    return CodecConfig(mode="stream" if n > 1 else "single", tau=tau, tile_w=tile, tile_h=tile,
+                       res=AngularResolution(sensor.theta_r, sensor.phi_r), phi_offset=sensor.phi_offset,
+                       w=sensor.w, h=sensor.h, n_frames=n)
+
+
+def group_seed(rank, g, cfg_id):
+    return 1_000_003 * cfg_id + 65_537 * rank + g
+
+
+# ------------------------------------------------------------------- clocks
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device_index: int):
+        self.dev = device_index
+        self.rows = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.dev), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except FileNotFoundError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) == 6:
+                self.rows.append(parts)
+
+    def stop(self):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        sm, mx, reasons = [], None, set()
+        for r in self.rows:
+            try:
+                sm.append(float(r[0]))
+                mx = float(r[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, r[2:]):
+                if v.lower() in ("active", "1"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ------------------------------------------------------------------ inputs
+
+def make_inputs(args, rank, device):
+    """Seeded groups generated on the GPU; returns device points, host offsets
+    and transforms, plus a few host copies for the CPU baseline."""
+    import torch
+
+    from paper_2008_06972_b200 import synth
+    from paper_2008_06972_b200.geometry import RigidTransform, poses_to_transforms
+
+    sensor, n, tile, tau, scene, G = workload(args)
+    k = n // 2
+    frames, xf, counts = [], [], []
+    for g in range(G):
+        grp = synth.make_group(group_seed(rank, g, args.config), n, sensor, device=device,
+                               as_numpy=False, **scene)
+        frames.extend(grp.clouds)
+        counts.extend(c.shape[0] for c in grp.clouds)
+        ts = poses_to_transforms(grp.poses, k) if n > 1 else [RigidTransform.identity()]
+        xf.extend(t.round_f32().row12() for t in ts)
+    d_pts = torch.cat(frames).contiguous()
+    del frames
+    off = np.zeros(len(counts) + 1, np.int64)
+    off[1:] = np.cumsum(counts)
+    return d_pts, off, np.asarray(xf, np.float64)
+
+
+def host_sample(d_pts, off, xf, n, groups):
+    """numpy copies of the first `groups` groups for the CPU oracle."""
+    out = []
+    F = groups * n
+    pts = d_pts[: int(off[F])].cpu().numpy()
+    for g in range(groups):
+        clouds = [pts[off[g * n + i]: off[g * n + i + 1]] for i in range(n)]
+        out.append((clouds, xf[g * n:(g + 1) * n]))
+    return out
+
+
+# ---------------------------------------------------------------- CPU oracle
+
+_CPU_SAMPLE = None
+
+
+def _cpu_job(i):
+    from oracle import oracle
+
+    clouds, xf, cfgt = _CPU_SAMPLE[i]
+    ocfg = oracle.OracleConfig(*cfgt)
+    ts = [(row[:9].reshape(3, 3), row[9:]) for row in xf]
+    enc = oracle.encode_stream(clouds, ts, ocfg)
+    blob = oracle.entropy_blob(oracle.payload_bytes(enc, ocfg))
+    return len(blob)
+
+
+def cpu_pool_rate(sample, cfg, n, seconds, cores):
+    """Frames/s of the oracle port over a bounded sample, all host cores."""
+    import concurrent.futures as cf
+    import multiprocessing as mp
+
+    from oracle import oracle
+
+    global _CPU_SAMPLE
+    oracle.build()
+    cfgt = tuple(oracle.OracleConfig.of(cfg).__dict__.values())
+    _CPU_SAMPLE = [(c, x, cfgt) for c, x in sample]
+    # one group per core per round; rounds until ~`seconds`
+    t0 = time.perf_counter()
+    done = 0
+    with cf.ProcessPoolExecutor(max_workers=cores, mp_context=mp.get_context("fork")) as ex:
+        while True:
+            idx = [(done + j) % len(sample) for j in range(cores)]
+            list(ex.map(_cpu_job, idx))
+            done += cores
+            if time.perf_counter() - t0 >= seconds:
+                break
+    dt = time.perf_counter() - t0
+    return done * n / dt, done, dt
+
+
+def host_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
+# ------------------------------------------------------------------- roofline
+
+def algorithmic_bytes(stage, cfg, n, G, npts):
+    """SURVEY.md §8(d) per-unit figures x the units one launch processes."""
+    P = cfg.w * cfg.h
+    F = G * n
+    if stage == "convert":
+        return 12 * npts + 8 * P * F + P / 8 * F
+    if stage == "fit_key":
+        return G * (8 * P + P / 8)
+    if stage == "fit_p":
+        return G * (n - 1) * (8 * P + P / 8)
+    if stage == "refit":
+        return G * (n - 1) * (8 * P + P / 8)
+    if stage == "bitmaps":
+        return F * (8 * P + 2 * P / 8)
+    return None
+
+
+def main():
+    args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.gpus != world and world > 1:
+        print(f"--gpus {args.gpus} but WORLD_SIZE {world}", file=sys.stderr)
+    sensor, n, tile, tau, scene, G = workload(args)
+    cfg = codec_config(sensor, n, tile, tau)
+    wl = {1: "configs[0]", 2: "configs[1]", 3: "configs[2]", 4: "configs[3]", 5: "configs[4]"}[args.config]
+    config = {
+        "workload": f"{wl}: {G} groups x (1K+{n - 1}P) per GPU, {sensor.h}-beam {sensor.w}x{sensor.h}, "
+                    f"tiles {tile}x{tile}, tau {tau} m",
+        "groups_per_gpu": G, "frames_per_group": n, "image": [sensor.w, sensor.h], "tile": tile,
+        "tau": tau, "l2": "inputs > L2 (no flush needed)",
+    }
+
+    if args.impl == "reference":
+        run_reference(args, cfg, config, n, rank, world)
+        return
+
+    import torch
+
+    dist = None
+    if world > 1:
+        import torch.distributed as dist_mod
+
+        dist = dist_mod
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(local)
+    device = torch.device("cuda", local)
+
+    from paper_2008_06972_b200 import Encoder, _native
+
+    L = _native.load(require_device=True)
+    t_gen = time.perf_counter()
+    d_pts, off, xf = make_inputs(args, rank, device)
+    torch.cuda.synchronize()
+    t_gen = time.perf_counter() - t_gen
+    npts = int(off[-1])
+    enc = Encoder(cfg)
+    stream = torch.cuda.current_stream(device)
+    sptr = stream.cuda_stream
+    ptr = d_pts.data_ptr()
+
+    for _ in range(max(args.warmup, 0)):
+        enc.encode_device(G, ptr, off, xf, sptr)
+    torch.cuda.synchronize()
+
+    # ---------------- timed region (device-resident inputs)
+    L.stpc_encoder_profile(enc.handle, 1)
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.3)
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    launches0 = L.stpc_launch_count()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    for _ in range(args.steps):
+        enc.encode_device(G, ptr, off, xf, sptr)
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    clk = clocks.stop()
+    launches = int(L.stpc_launch_count() - launches0)
+    ms = ev0.elapsed_time(ev1)
+    stage_ms = np.zeros(16)
+    ns = L.stpc_encoder_stage_ms(enc.handle, stage_ms.ctypes.data, 16)
+    names = [L.stpc_stage_name(i).decode() for i in range(ns)]
+    stage_ms = stage_ms[:ns] / max(args.steps, 1)
+    L.stpc_encoder_profile(enc.handle, 0)
+
+    off_b, len_b = enc.blob_layout()
+    raw = enc.payload_lengths()
+    blob_bytes = int(len_b.sum())
+    stats = enc.frame_stats()
+    if dist:
+        t = torch.tensor([ms], device=device, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+        # the single collective of the path: gather per-group blob sizes
+        sizes = torch.as_tensor(len_b, device=device)
+        allsz = torch.empty(world * sizes.numel(), dtype=sizes.dtype, device=device)
+        dist.all_gather_into_tensor(allsz, sizes)
+        total_blob = int(allsz.sum().item())
+        tp = torch.tensor([npts], device=device, dtype=torch.int64)
+        dist.all_reduce(tp)
+        total_pts = int(tp.item())
+    else:
+        total_blob = blob_bytes
+        total_pts = npts
+    ms_step = ms / max(args.steps, 1)
+    frames_all = G * n * world
+    fps = frames_all / (ms_step / 1e3)
+    mpts = total_pts / (ms_step / 1e3) / 1e6
+
+    # ---------------- end to end through the public host API
+    e2e = None
+    if not args.no_e2e:
+        h_pts = torch.empty(d_pts.shape, dtype=torch.float32, pin_memory=True)
+        h_pts.copy_(d_pts)
+        del d_pts
+        torch.cuda.empty_cache()
+        hp = h_pts.numpy()
+        h_out = torch.empty(int(off_b[-1] * 1.25) + 4096, dtype=torch.uint8, pin_memory=True).numpy()
+        enc.encode_host(G, hp, off, xf, h_out, sptr)  # warm
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.steps):
+            enc.encode_host(G, hp, off, xf, h_out, sptr)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ems = e0.elapsed_time(e1)
+        if dist:
+            t = torch.tensor([ems], device=device, dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ems = float(t.item())
+        ems /= max(args.steps, 1)
+        off2, len2 = enc.blob_layout()
+        e2e = {"value": frames_all / (ems / 1e3), "unit": "frames/s",
+               "mpoints_per_s": total_pts / (ems / 1e3) / 1e6, "ms_per_step": ems,
+               "h2d_bytes_per_step": int(hp.nbytes + off.nbytes + xf.nbytes),
+               "d2h_bytes_per_step": int(off2[-1] + 8 * (3 * G + 2))}
+
+    # ---------------- roofline of the dominant stage
+    from paper_2008_06972_b200.codec import MODE_SINGLE  # noqa: F401
+
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+        peak, peak_src = float(peaks["hbm_gbs"]), "measured"
+    except Exception:
+        peak, peak_src = 6650.0, "fallback"
+    order = np.argsort(-stage_ms)
+    dom = names[int(order[0])]
+    dom_ms = float(stage_ms[int(order[0])])
+    ab = algorithmic_bytes(dom, cfg, n, G, npts)
+    roofline = {"bound": "hbm", "kernel": dom, "ms": dom_ms,
+                "share_of_step": dom_ms / ms_step if ms_step else None,
+                "achieved": (ab / (dom_ms / 1e3) / 1e9) if ab else None, "peak": peak,
+                "peak_source": peak_src, "unit": "GB/s", "traffic": None}
+    roofline["frac"] = roofline["achieved"] / peak if roofline["achieved"] else None
+    conv_ms = float(stage_ms[names.index("convert")])
+    conv_ab = algorithmic_bytes("convert", cfg, n, G, npts)
+    roofline["convert"] = {"ms": conv_ms, "achieved": conv_ab / (conv_ms / 1e3) / 1e9,
+                           "frac": conv_ab / (conv_ms / 1e3) / 1e9 / peak}
+
+    # ---------------- CPU baseline (rank 0, N=1)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        try:
+            cores = host_cores()
+            sample = host_sample(torch.as_tensor(hp) if e2e else d_pts, off, xf, n, min(G, max(cores, 8)))
+            rate, done, dt = cpu_pool_rate(sample, cfg, n, args.cpu_seconds, cores)
+            cpu = {"value": rate, "unit": "frames/s", "cores": cores, "kind": "port",
+                   "sample": f"{done} groups ({done * n} frames) of this workload through the C/numpy "
+                             f"oracle in {dt:.1f} s, ProcessPool x{cores}"}
+        except Exception as exc:  # never let the baseline kill the GPU line
+            cpu = {"value": None, "error": repr(exc)[:200]}
+
+    if args.stages and rank == 0:
+        for nm, v in zip(names, stage_ms):
+            print(f"  {nm:10s} {v:9.3f} ms", file=sys.stderr)
+        print(f"  gen {t_gen:.1f}s  blob {total_blob} B  raw {int(raw.sum())} B  eps {int(stats[:, 8].sum())}",
+              file=sys.stderr)
+
+    if rank == 0:
+        line = {
+            "metric": "frames/sec compressed", "value": fps, "unit": "frames/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded BASELINE scenes, SURVEY.md Appendix B)", "config": config,
+            "mpoints_per_s": mpts, "compression_rate": 12.0 * total_pts / total_blob if total_blob else None,
+            "e2e": e2e, "roofline": roofline, "cpu_baseline": cpu, "clocks": clk,
+            "gpu_launches": launches,
+            "stage_ms": {nm: round(float(v), 4) for nm, v in zip(names, stage_ms)},
+            "impl": "b200",
+        }
+        print(json.dumps(line))
+    if dist:
+        dist.destroy_process_group()
+
+
+def run_reference(args, cfg, config, n, rank, world):
+    """CPU reference arm: the oracle port on all host cores (rank 0 only)."""
+    if rank != 0:
+        return
+    import torch
+
+    from paper_2008_06972_b200 import synth
+    from paper_2008_06972_b200.geometry import RigidTransform, poses_to_transforms
+
+    sensor, n, tile, tau, scene, G = workload(args)
+    cores = host_cores()
+    k = n // 2
+    dev = "cuda" if torch.cuda.is_available() else "cpu"
+    sample = []
+    for g in range(min(G, max(cores, 4))):
+        grp = synth.make_group(group_seed(0, g, args.config), n, sensor, device=dev, **scene)
+        ts = poses_to_transforms(grp.poses, k) if n > 1 else [RigidTransform.identity()]
+        sample.append((grp.clouds, np.asarray([t.round_f32().row12() for t in ts])))
+    per_step = max(1.0, args.cpu_seconds / 3)
+    for _ in range(args.warmup):
+        cpu_pool_rate(sample, cfg, n, 0.0, cores)
+    rates, frames, secs = [], 0, 0.0
+    for _ in range(args.steps):
+        r, done, dt = cpu_pool_rate(sample, cfg, n, per_step, cores)
+        rates.append(r)
+        frames += done * n
+        secs += dt
+    value = frames / secs
+    line = {
+        "metric": "frames/sec compressed", "value": value, "unit": "frames/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * secs / max(args.steps, 1),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded BASELINE scenes, SURVEY.md Appendix B)", "config": config,
+        "impl": "reference",
+        "cpu_baseline": {"value": value, "unit": "frames/s", "cores": cores, "kind": "port",
+                         "sample": f"each step: rounds of {cores} groups (1 per core) through the C/numpy "
+                                   f"oracle for ~{per_step:.0f} s"},
+        "e2e": {"value": value, "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,337 @@
+"""Drop-in ``compress`` for the reference's stream/single-frame encoder.
+
+Mirrors the public contract of /root/reference/pkg/src/stpc/bitstream.py:
+``CodecConfig`` (:87-126), ``EncodeReport`` (:129-139) and
+``compress(clouds, cfg, poses=None, imu_samples=None, frame_times=None,
+v0=None, threads=1) -> (bytes, EncodeReport)`` (:527-602), emitting the same
+.stpc v1 bytes.  The work runs in libstpc_b200 on the GPU: projection,
+spatial and temporal fits, residual compaction, payload assembly, Huffman
+coding and CRC.  The host only validates arguments, chains the poses into
+float32 transforms (microseconds) and builds the report.
+
+``compress_groups`` is the batch form the reference does not have: many
+independent K+P groups per call, the natural unit of throughput.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import logging
+import threading
+import time
+from dataclasses import dataclass, field
+from typing import Dict, List, Optional, Sequence, Tuple
+
+import numpy as np
+
+from . import _native
+from .errors import DataError
+from .geometry import (
+    COND_LIMIT,
+    DEFAULT_PHI_OFFSET,
+    DEFAULT_R_MAX,
+    AngularResolution,
+    RigidTransform,
+    frame_transforms,
+    poses_to_transforms,
+    ray_trig_tables,
+)
+
+log = logging.getLogger(__name__)
+
+MODE_SINGLE = "single"
+MODE_STREAM = "stream"
+_MODE_CODES = {MODE_SINGLE: 0, MODE_STREAM: 1}
+HEADER_SIZE = 284
+
+
+@dataclass(frozen=True)
+class TileGrid:
+    tile_w: int
+    tile_h: int
+    width: int
+    height: int
+
+    @property
+    def tiles_x(self) -> int:
+        return -(-self.width // self.tile_w)
+
+    @property
+    def tiles_y(self) -> int:
+        return -(-self.height // self.tile_h)
+
+
+@dataclass(frozen=True)
+class CodecConfig:
+    """Same fields, defaults and validation as the reference CodecConfig."""
+
+    mode: str = MODE_SINGLE
+    tau: float = 0.02
+    tile_w: int = 4
+    tile_h: int = 4
+    res: AngularResolution = field(default_factory=AngularResolution)
+    phi_offset: float = DEFAULT_PHI_OFFSET
+    w: int = 1800
+    h: int = 64
+    n_frames: int = 1
+    k_index: Optional[int] = None
+    range_quant: float = 0.005
+
+    def __post_init__(self):
+        if self.mode not in _MODE_CODES:
+            raise ValueError(f"unknown mode {self.mode!r}")
+        if self.mode == MODE_SINGLE and self.n_frames != 1:
+            raise ValueError("single-frame mode takes exactly one frame")
+        if self.tau <= 0 or self.range_quant <= 0:
+            raise ValueError("tau and range_quant must be positive")
+        if min(self.tile_w, self.tile_h, self.w, self.h, self.n_frames) < 1:
+            raise ValueError("dimensions must be >= 1")
+        if self.k_index is None:
+            object.__setattr__(self, "k_index", self.n_frames // 2)
+        if not (0 <= self.k_index < self.n_frames):
+            raise ValueError("k_index out of range")
+        if self.range_quant > self.tau / 2:
+            log.warning("range_quant %.4g above tau/2 (%.4g); residual error may dominate",
+                        self.range_quant, self.tau / 2)
+
+    def grid(self) -> TileGrid:
+        return TileGrid(self.tile_w, self.tile_h, self.w, self.h)
+
+
+@dataclass
+class EncodeReport:
+    raw_bytes: int
+    blob_bytes: int
+    compression_rate: float
+    point_counts: List[int]
+    dropped_points: int
+    collision_fractions: List[float]
+    coverage: List[Dict[str, int]]
+    fractions: Dict[str, float]
+    timings: Dict[str, float]
+    eps_band_points: int = 0  # binnings within 1e-9 of a bin edge
+
+
+class Encoder:
+    """One native encoder (device workspace + trig tables) per config and
+    input dtype; reuse it across calls to amortise allocation."""
+
+    def __init__(self, cfg: CodecConfig, points_f64: bool = False):
+        L = _native.load(require_device=True)
+        self.cfg = cfg
+        self.points_f64 = bool(points_f64)
+        c = _native.StpcConfig(
+            mode=_MODE_CODES[cfg.mode], tile_w=cfg.tile_w, tile_h=cfg.tile_h, w=cfg.w, h=cfg.h,
+            n_frames=cfg.n_frames, k_index=cfg.k_index, points_f64=int(self.points_f64),
+            tau=cfg.tau, theta_r=cfg.res.theta_r, phi_r=cfg.res.phi_r, phi_offset=cfg.phi_offset,
+            range_quant=cfg.range_quant, r_max=DEFAULT_R_MAX, cond_limit=COND_LIMIT,
+        )
+        tabs = ray_trig_tables(cfg.w, cfg.h, cfg.res.theta_r, cfg.res.phi_r, cfg.phi_offset)
+        self._tabs = tabs
+        h = ctypes.c_void_p()
+        _native.check(L.stpc_encoder_create(ctypes.byref(c), *[t.ctypes.data for t in tabs], ctypes.byref(h)))
+        self._h = h
+        self._L = L
+        self.lock = threading.Lock()
+
+    def close(self):
+        if self._h:
+            self._L.stpc_encoder_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def handle(self):
+        return self._h
+
+    # -- encode --------------------------------------------------------------
+    def encode_device(self, n_groups: int, d_points: int, offsets: np.ndarray,
+                      transforms: np.ndarray, stream: int = 0) -> None:
+        """Points already in device memory (pointer); blobs stay on device."""
+        off = np.ascontiguousarray(offsets, dtype=np.int64)
+        xf = np.ascontiguousarray(transforms, dtype=np.float64)
+        _native.check(self._L.stpc_encode_device(self._h, n_groups, d_points, off.ctypes.data,
+                                                 xf.ctypes.data, stream))
+
+    def encode_host(self, n_groups: int, points: np.ndarray, offsets: np.ndarray,
+                    transforms: np.ndarray, out: Optional[np.ndarray] = None, stream: int = 0) -> None:
+        """Points in host memory: H2D, encode, and D2H of all blobs into ``out``."""
+        off = np.ascontiguousarray(offsets, dtype=np.int64)
+        xf = np.ascontiguousarray(transforms, dtype=np.float64)
+        out_ptr, cap = (out.ctypes.data, out.nbytes) if out is not None else (None, 0)
+        _native.check(self._L.stpc_encode_host(self._h, n_groups, points.ctypes.data, off.ctypes.data,
+                                               xf.ctypes.data, out_ptr, cap, stream))
+
+    # -- results -------------------------------------------------------------
+    def blob_layout(self) -> Tuple[np.ndarray, np.ndarray]:
+        G = self._L.stpc_result_groups(self._h)
+        off = np.zeros(G + 1, np.int64)
+        ln = np.zeros(G, np.int64)
+        _native.check(self._L.stpc_result_blobs(self._h, off.ctypes.data, ln.ctypes.data))
+        return off, ln
+
+    def blobs(self, arena: Optional[np.ndarray] = None) -> List[bytes]:
+        off, ln = self.blob_layout()
+        if arena is None:
+            arena = np.empty(int(off[-1]), np.uint8)
+            _native.check(self._L.stpc_result_copy_blobs(self._h, arena.ctypes.data, arena.nbytes, None))
+        return [arena[o:o + n].tobytes() for o, n in zip(off[:-1], ln)]
+
+    def frame_stats(self) -> np.ndarray:
+        G = self._L.stpc_result_groups(self._h)
+        F = G * self.cfg.n_frames
+        st = np.zeros((F, _native.STPC_NSTAT), np.int64)
+        _native.check(self._L.stpc_result_frame_stats(self._h, st.ctypes.data))
+        return st
+
+    def payload_lengths(self) -> np.ndarray:
+        G = self._L.stpc_result_groups(self._h)
+        out = np.zeros(G, np.int64)
+        _native.check(self._L.stpc_result_payload_lengths(self._h, out.ctypes.data))
+        return out
+
+    def device_buffer(self, which: int) -> Tuple[int, int]:
+        p = ctypes.c_void_p()
+        n = ctypes.c_int64()
+        _native.check(self._L.stpc_encoder_buffer(self._h, which, ctypes.byref(p), ctypes.byref(n)))
+        return p.value or 0, n.value
+
+    def copy_buffer(self, which: int, dtype, count: int) -> np.ndarray:
+        ptr, cap = self.device_buffer(which)
+        out = np.empty(count, dtype)
+        if out.nbytes > cap:
+            raise ValueError("requested more than the buffer holds")
+        _native.check(self._L.stpc_memcpy_d2h(out.ctypes.data, ptr, out.nbytes))
+        return out
+
+
+_enc_cache: Dict[tuple, Encoder] = {}
+_enc_lock = threading.Lock()
+
+
+def get_encoder(cfg: CodecConfig, points_f64: bool = False) -> Encoder:
+    key = (cfg, bool(points_f64), threading.get_ident())
+    with _enc_lock:
+        enc = _enc_cache.get(key)
+        if enc is None:
+            enc = Encoder(cfg, points_f64)
+            _enc_cache[key] = enc
+        return enc
+
+
+def _transforms_for(cfg: CodecConfig, poses, imu_samples, frame_times, v0) -> List[RigidTransform]:
+    """The transform branch of compress (bitstream.py:547-560)."""
+    if cfg.n_frames == 1:
+        transforms = [RigidTransform.identity()]
+    elif poses is not None:
+        if len(poses) != cfg.n_frames:
+            raise DataError("need one pose per frame")
+        transforms = poses_to_transforms(poses, cfg.k_index)
+    elif imu_samples is not None:
+        if frame_times is None or len(frame_times) != cfg.n_frames:
+            raise DataError("IMU alignment needs one frame time per frame")
+        transforms = frame_transforms(imu_samples, frame_times, cfg.k_index, v0)
+    else:
+        raise DataError("stream mode needs poses or IMU samples")
+    return [t.round_f32() for t in transforms]
+
+
+def _stack_points(clouds) -> Tuple[np.ndarray, np.ndarray, bool, List[int]]:
+    arrs = [np.asarray(c) for c in clouds]
+    counts = []
+    f64 = False
+    for a in arrs:
+        if a.size and (a.ndim != 2 or a.shape[1] != 3):
+            raise ValueError("cloud must be an (N, 3) array")
+        counts.append(0 if a.size == 0 else a.shape[0])
+        if a.size and a.dtype != np.float32:
+            f64 = True
+    dt = np.float64 if f64 else np.float32
+    pts = np.concatenate([a.reshape(-1, 3).astype(dt, copy=False) for a in arrs]) if arrs else np.zeros((0, 3), dt)
+    off = np.zeros(len(arrs) + 1, np.int64)
+    off[1:] = np.cumsum(counts)
+    return np.ascontiguousarray(pts), off, f64, counts
+
+
+def _reports(cfg: CodecConfig, stats: np.ndarray, blobs: List[bytes], counts_per_group, timings) -> List[EncodeReport]:
+    n = cfg.n_frames
+    out = []
+    for g, blob in enumerate(blobs):
+        st = stats[g * n:(g + 1) * n]
+        point_counts = [int(c) for c in counts_per_group[g]]
+        raw_bytes = 12 * sum(point_counts)
+        kept = st[:, _native.STAT_KEPT]
+        valid = st[:, _native.STAT_VALID]
+        collisions = kept - valid
+        dropped = int((st[:, _native.STAT_REJECTED] + st[:, _native.STAT_DROPPED] + collisions).sum())
+        coverage = [
+            {"temporal": int(s[_native.STAT_TEMPORAL]), "fallback": int(s[_native.STAT_FALLBACK]),
+             "residual": int(s[_native.STAT_RESIDUAL]), "valid": int(s[_native.STAT_VALID])}
+            for s in st
+        ]
+        total_valid = sum(c["valid"] for c in coverage) or 1
+        fractions = {
+            "temporal": sum(c["temporal"] for c in coverage) / total_valid,
+            "spatial": sum(c["fallback"] for c in coverage) / total_valid,
+            "residual": sum(c["residual"] for c in coverage) / total_valid,
+        }
+        coll = [float(c) / float(k) if k > 0 else 0.0 for c, k in zip(collisions, kept)]
+        out.append(EncodeReport(
+            raw_bytes=raw_bytes, blob_bytes=len(blob),
+            compression_rate=raw_bytes / len(blob) if len(blob) else 0.0,
+            point_counts=point_counts, dropped_points=dropped, collision_fractions=coll,
+            coverage=coverage, fractions=fractions, timings=dict(timings),
+            eps_band_points=int(st[:, _native.STAT_EPS_BAND].sum()),
+        ))
+    return out
+
+
+def compress_groups(groups: Sequence[Sequence[np.ndarray]], cfg: CodecConfig,
+                    poses: Optional[Sequence[Sequence]] = None) -> Tuple[List[bytes], List[EncodeReport]]:
+    """Encode many independent groups in one device pass; one blob per group,
+    each byte-identical to ``compress(group, cfg, poses=poses[g])``."""
+    t0 = time.perf_counter()
+    xf = []
+    for g, clouds in enumerate(groups):
+        if len(clouds) != cfg.n_frames:
+            raise DataError(f"config expects {cfg.n_frames} frames, got {len(clouds)}")
+        ts = _transforms_for(cfg, None if poses is None else poses[g], None, None, None)
+        xf.extend(t.row12() for t in ts)
+    xf = np.asarray(xf, np.float64).reshape(-1, 12)
+    t1 = time.perf_counter()
+    pts, off, f64, counts = _stack_points([c for grp in groups for c in grp])
+    enc = get_encoder(cfg, f64)
+    with enc.lock:
+        enc.encode_host(len(groups), pts, off, xf)
+        blobs = enc.blobs()
+        stats = enc.frame_stats()
+    t2 = time.perf_counter()
+    n = cfg.n_frames
+    per_group = [counts[g * n:(g + 1) * n] for g in range(len(groups))]
+    return blobs, _reports(cfg, stats, blobs, per_group, {"transforms": t1 - t0, "device": t2 - t1})
+
+
+def compress(clouds: Sequence[np.ndarray], cfg: CodecConfig, poses=None, imu_samples=None,
+             frame_times=None, v0=None, threads: int = 1) -> Tuple[bytes, EncodeReport]:
+    """Drop-in for stpc.compress: identical blob bytes, GPU execution.
+    ``threads`` is accepted for signature compatibility and ignored."""
+    if len(clouds) != cfg.n_frames:
+        raise DataError(f"config expects {cfg.n_frames} frames, got {len(clouds)}")
+    t0 = time.perf_counter()
+    ts = _transforms_for(cfg, poses, imu_samples, frame_times, v0)
+    xf = np.asarray([t.row12() for t in ts], np.float64)
+    t1 = time.perf_counter()
+    pts, off, f64, counts = _stack_points(clouds)
+    enc = get_encoder(cfg, f64)
+    with enc.lock:
+        enc.encode_host(1, pts, off, xf)
+        blobs = enc.blobs()
+        stats = enc.frame_stats()
+    t2 = time.perf_counter()
+    rep = _reports(cfg, stats, blobs, [counts], {"transforms": t1 - t0, "device": t2 - t1})
+    return blobs[0], rep[0]

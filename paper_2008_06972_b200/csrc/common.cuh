@@ -1,0 +1,143 @@
+// Shared device helpers for the stpc B200 hot path.
+//
+// Arithmetic contract: every kernel in this library is
+// compiled with -fmad=false so that fp64 products and sums round exactly as the
+// reference's numba kernels (which emit no FMA), in the same left-to-right
+// order.  Division and sqrt are IEEE round-to-nearest in CUDA's fp64 path.
+#pragma once
+#include <algorithm>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#define STPC_FULL 0xffffffffu
+#define STPC_PARALLEL_EPS 1e-12
+
+namespace stpc {
+
+// Pixel-centre ray direction from the host-computed trig tables.
+// pixel_ray_grid (/root/reference/pkg/src/stpc/range_image.py:141-147) stores
+//   d = (sin(phi_v) * sin(theta_u), sin(phi_v) * cos(theta_u), cos(phi_v))
+// as one IEEE product per component; recomputing the product from the same
+// numpy-computed factors gives the same bits while reading 32 B per row+column
+// instead of 24 B per pixel.
+struct Trig {
+    const double* sin_t;  // [w]
+    const double* cos_t;  // [w]
+    const double* sin_p;  // [h]
+    const double* cos_p;  // [h]
+};
+
+__device__ __forceinline__ void ray_dir(const Trig& tg, int v, int u, double& dx, double& dy, double& dz)
+{
+    double sp = __ldg(tg.sin_p + v);
+    dx = sp * __ldg(tg.sin_t + u);
+    dy = sp * __ldg(tg.cos_t + u);
+    dz = __ldg(tg.cos_p + v);
+}
+
+__device__ __forceinline__ double f32_round(double x) { return (double)__double2float_rn(x); }
+
+// Python builtin max(a, b, c): later items replace only when strictly greater.
+__device__ __forceinline__ double pymax3(double a, double b, double c)
+{
+    double m = a;
+    if (b > m) m = b;
+    if (c > m) m = c;
+    return m;
+}
+
+// plane_from_sums (/root/reference/pkg/src/stpc/_kernels.py:23-76).
+// s = [Syy, Syz, Szz, Sy, Sz, Sxy, Sxz, Sx, N].
+__device__ __forceinline__ bool plane_from_sums(const double s[9], double cond_limit,
+                                                double& a, double& b, double& c)
+{
+    double m00 = s[0], m01 = s[1], m02 = -s[3], m11 = s[2], m12 = -s[4], m22 = s[8];
+    double r0 = -s[5], r1 = -s[6], r2 = s[7];
+    double c00 = m11 * m22 - m12 * m12;
+    double c01 = m02 * m12 - m01 * m22;
+    double c02 = m01 * m12 - m02 * m11;
+    double det = (m00 * c00 + m01 * c01) + m02 * c02;
+    a = b = c = 0.0;
+    if (det == 0.0 || !isfinite(det)) return false;
+    double c11 = m00 * m22 - m02 * m02;
+    double c12 = m01 * m02 - m00 * m12;
+    double c22 = m00 * m11 - m01 * m01;
+    double i00 = c00 / det, i01 = c01 / det, i02 = c02 / det;
+    double i11 = c11 / det, i12 = c12 / det, i22 = c22 / det;
+    double norm_m = pymax3((fabs(m00) + fabs(m01)) + fabs(m02),
+                           (fabs(m01) + fabs(m11)) + fabs(m12),
+                           (fabs(m02) + fabs(m12)) + fabs(m22));
+    double norm_i = pymax3((fabs(i00) + fabs(i01)) + fabs(i02),
+                           (fabs(i01) + fabs(i11)) + fabs(i12),
+                           (fabs(i02) + fabs(i12)) + fabs(i22));
+    double cond = norm_m * norm_i;
+    if (!isfinite(cond) || cond > cond_limit) return false;
+    double pa = (i00 * r0 + i01 * r1) + i02 * r2;
+    double pb = (i01 * r0 + i11 * r1) + i12 * r2;
+    double pc = (i02 * r0 + i12 * r1) + i22 * r2;
+    if (!(isfinite(pa) && isfinite(pb) && isfinite(pc))) return false;
+    a = pa; b = pb; c = pc;
+    return true;
+}
+
+// The per-pixel reconstruction test of _span_ok / refit_spans
+// (/root/reference/pkg/src/stpc/_kernels.py:140-147, 264-277).  A NaN r_hat
+// passes, exactly as the reference's comparisons do.
+__device__ __forceinline__ bool pixel_fits(double r, double dx, double dy, double dz,
+                                           double a, double b, double c, double tau, double r_max)
+{
+    double den = (dx + a * dy) + b * dz;
+    if (fabs(den) < STPC_PARALLEL_EPS) return false;
+    double r_hat = c / den;
+    if (r_hat <= 0.0 || r_hat > r_max) return false;
+    if (fabs(r - r_hat) > tau) return false;
+    return true;
+}
+
+__device__ __forceinline__ double shfl_d(double v, int src)
+{
+    return __shfl_sync(STPC_FULL, v, src);
+}
+
+// Natural (LSB = lowest pixel) 32-pixel mask from a packbits (MSB-first) word.
+__device__ __forceinline__ uint32_t natural_bits(uint32_t packed_le)
+{
+    return __byte_perm(__brev(packed_le), 0, 0x0123);
+}
+
+__device__ __forceinline__ int varint_len(uint32_t v)
+{
+    return v < (1u << 7) ? 1 : v < (1u << 14) ? 2 : v < (1u << 21) ? 3 : v < (1u << 28) ? 4 : 5;
+}
+
+// Warp-inclusive scan (integer; order-independent so a tree is exact).
+__device__ __forceinline__ int warp_incl_scan(int v)
+{
+    const int lane = threadIdx.x & 31;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        int t = __shfl_up_sync(STPC_FULL, v, o);
+        if (lane >= o) v += t;
+    }
+    return v;
+}
+
+__device__ __forceinline__ long long warp_incl_scan_ll(long long v)
+{
+    const int lane = threadIdx.x & 31;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        long long t = __shfl_up_sync(STPC_FULL, v, o);
+        if (lane >= o) v += t;
+    }
+    return v;
+}
+
+__device__ __forceinline__ void put_u16(uint8_t* p, uint32_t v) { p[0] = v & 0xff; p[1] = (v >> 8) & 0xff; }
+__device__ __forceinline__ void put_u32(uint8_t* p, uint32_t v)
+{
+    p[0] = v & 0xff; p[1] = (v >> 8) & 0xff; p[2] = (v >> 16) & 0xff; p[3] = v >> 24;
+}
+__device__ __forceinline__ void put_f32(uint8_t* p, float f) { put_u32(p, __float_as_uint(f)); }
+
+}  // namespace stpc

@@ -1,0 +1,234 @@
+// K1 -- range-image conversion: IMU/pose transform + spherical binning with the
+// reference's nearest-point collision rule, then the payload-ready validity
+// bitmap.
+//
+// Replaces RigidTransform.apply (/root/reference/pkg/src/stpc/motion.py:70-72)
+// fused with project_kernel (/root/reference/pkg/src/stpc/_kernels.py:311-355)
+// and the valid-mask/packbits steps of project() / serialize()
+// (/root/reference/pkg/src/stpc/range_image.py:198-200;
+//  /root/reference/pkg/src/stpc/bitstream.py:219-220).
+//
+// Collision rule: the reference keeps `r < best[f]` scanning points in input
+// order, i.e. the minimum range, ties going to the lowest index.  Positive f64
+// values order like their u64 bit patterns, so a 64-bit atomicMin on the bits
+// computes the same minimum independent of thread order; the optional second
+// pass resolves the winning index with an atomicMin over indices whose range
+// equals the minimum (identical to "first index wins").
+#include "kernels.cuh"
+
+namespace stpc {
+
+static constexpr unsigned long long INF_BITS = 0x7ff0000000000000ull;
+
+__global__ void fill_u64_kernel(unsigned long long* p, unsigned long long v, long long n)
+{
+    long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    long long stride = (long long)gridDim.x * blockDim.x;
+    for (; i < n; i += stride) p[i] = v;
+}
+
+void launch_fill_u64(unsigned long long* p, unsigned long long v, long long n, cudaStream_t s)
+{
+    if (n <= 0) return;
+    int blocks = (int)std::min<long long>((n + 255) / 256, 148 * 16);
+    STPC_LAUNCH();
+    fill_u64_kernel<<<blocks, 256, 0, s>>>(p, v, n);
+}
+
+struct Binned {
+    int status;  // 0 rejected, 1 dropped, 2 kept
+    long long pix;
+    double r;
+    bool eps;
+};
+
+// One point: f32 -> f64 transform, then project_kernel's per-point body.
+__device__ __forceinline__ Binned bin_point(double px, double py, double pz, const double* R,
+                                            const double* T, const Geometry& g)
+{
+    Binned o{0, 0, 0.0, false};
+    // ((x*r0 + y*r1) + z*r2) + t, no contraction (-fmad=false)
+    double x = ((px * R[0] + py * R[1]) + pz * R[2]) + T[0];
+    double y = ((px * R[3] + py * R[4]) + pz * R[5]) + T[1];
+    double z = ((px * R[6] + py * R[7]) + pz * R[8]) + T[2];
+    if (!(isfinite(x) && isfinite(y) && isfinite(z))) return o;
+    double r = sqrt((x * x + y * y) + z * z);
+    if (r <= 0.0) return o;
+    double theta = atan2(x, y);
+    if (theta < 0.0) theta += 2.0 * 3.141592653589793;
+    double qu = theta / g.theta_r;
+    long long u = (long long)floor(qu) % (long long)g.w;
+    if (u < 0) u += g.w;
+    double cz = z / r;
+    if (cz > 1.0) cz = 1.0;
+    else if (cz < -1.0) cz = -1.0;
+    double qv = (acos(cz) - g.phi_offset) / g.phi_r;
+    long long v = (long long)floor(qv);
+    // epsilon band: libm vs CUDA trig may differ by a
+    // couple of ulp; count binnings within 1e-9 (relative) of a bin edge.
+    double du = fabs(qu - rint(qu)), dv = fabs(qv - rint(qv));
+    o.eps = du <= 1e-9 * fmax(1.0, fabs(qu)) || dv <= 1e-9 * fmax(1.0, fabs(qv));
+    if (v < 0 || v >= g.h) { o.status = 1; return o; }
+    o.status = 2;
+    o.pix = v * (long long)g.w + u;
+    o.r = r;
+    return o;
+}
+
+__device__ __forceinline__ void warp_add_stats(long long* fs, int rej, int drop, int kept, int eps)
+{
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+        rej += __shfl_xor_sync(STPC_FULL, rej, off);
+        drop += __shfl_xor_sync(STPC_FULL, drop, off);
+        kept += __shfl_xor_sync(STPC_FULL, kept, off);
+        eps += __shfl_xor_sync(STPC_FULL, eps, off);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        if (rej) atomicAdd((unsigned long long*)&fs[FS_REJECTED], (unsigned long long)rej);
+        if (drop) atomicAdd((unsigned long long*)&fs[FS_DROPPED], (unsigned long long)drop);
+        if (kept) atomicAdd((unsigned long long*)&fs[FS_KEPT], (unsigned long long)kept);
+        if (eps) atomicAdd((unsigned long long*)&fs[FS_EPS_BAND], (unsigned long long)eps);
+    }
+}
+
+// grid: (x blocks striding over a frame's points, y = frame)
+template <class T>
+__global__ void __launch_bounds__(256) convert_kernel(ConvertArgs a, const T* pts)
+{
+    const int f = blockIdx.y;
+    const long long b = a.pt_off[f], e = a.pt_off[f + 1];
+    __shared__ double xf[12];
+    if (threadIdx.x < 12) xf[threadIdx.x] = a.xf[12 * f + threadIdx.x];
+    __syncthreads();
+    unsigned long long* best = a.best + (long long)f * a.g.P;
+    int rej = 0, drop = 0, kept = 0, eps = 0;
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    // loop trip count is warp-uniform so the warp reductions below stay converged
+    for (long long base = b + (long long)blockIdx.x * blockDim.x; base < e; base += stride) {
+        long long i = base + threadIdx.x;
+        if (i < e) {
+            const T* p = pts + 3 * i;
+            Binned o = bin_point((double)__ldg(p), (double)__ldg(p + 1), (double)__ldg(p + 2), xf, xf + 9, a.g);
+            rej += o.status == 0;
+            drop += o.status == 1;
+            kept += o.status == 2;
+            eps += o.eps;
+            if (o.status == 2) atomicMin(best + o.pix, (unsigned long long)__double_as_longlong(o.r));
+        }
+    }
+    warp_add_stats(a.fstats + (long long)f * FS_COUNT, rej, drop, kept, eps);
+}
+
+template <class T>
+__global__ void __launch_bounds__(256) convert_win_kernel(ConvertArgs a, const T* pts)
+{
+    const int f = blockIdx.y;
+    const long long b = a.pt_off[f], e = a.pt_off[f + 1];
+    __shared__ double xf[12];
+    if (threadIdx.x < 12) xf[threadIdx.x] = a.xf[12 * f + threadIdx.x];
+    __syncthreads();
+    const unsigned long long* best = a.best + (long long)f * a.g.P;
+    long long* win = a.win + (long long)f * a.g.P;
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    for (long long i = b + (long long)blockIdx.x * blockDim.x + threadIdx.x; i < e; i += stride) {
+        const T* p = pts + 3 * i;
+        Binned o = bin_point((double)__ldg(p), (double)__ldg(p + 1), (double)__ldg(p + 2), xf, xf + 9, a.g);
+        if (o.status == 2 && isfinite(o.r) &&
+            (unsigned long long)__double_as_longlong(o.r) == best[o.pix])
+            atomicMin((unsigned long long*)(win + o.pix), (unsigned long long)(i - b));
+    }
+}
+
+__global__ void win_finalize_kernel(long long* win, const unsigned long long* best, long long n)
+{
+    long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    long long stride = (long long)gridDim.x * blockDim.x;
+    for (; i < n; i += stride)
+        if (best[i] == INF_BITS) win[i] = -1;
+}
+
+static dim3 convert_grid(int max_pts, int n_frames)
+{
+    int bx = (max_pts + 255) / 256;
+    if (bx < 1) bx = 1;
+    if (bx > 1024) bx = 1024;
+    return dim3(bx, n_frames);
+}
+
+void launch_convert(const ConvertArgs& a, int max_pts, cudaStream_t s)
+{
+    if (a.n_frames <= 0) return;
+    STPC_LAUNCH();
+    if (a.pts_f64)
+        convert_kernel<double><<<convert_grid(max_pts, a.n_frames), 256, 0, s>>>(a, (const double*)a.pts);
+    else
+        convert_kernel<float><<<convert_grid(max_pts, a.n_frames), 256, 0, s>>>(a, (const float*)a.pts);
+}
+
+void launch_convert_win(const ConvertArgs& a, int max_pts, cudaStream_t s)
+{
+    if (a.n_frames <= 0) return;
+    long long n = (long long)a.n_frames * a.g.P;
+    launch_fill_u64((unsigned long long*)a.win, 0x7fffffffffffffffull, n, s);
+    STPC_LAUNCH();
+    if (a.pts_f64)
+        convert_win_kernel<double><<<convert_grid(max_pts, a.n_frames), 256, 0, s>>>(a, (const double*)a.pts);
+    else
+        convert_win_kernel<float><<<convert_grid(max_pts, a.n_frames), 256, 0, s>>>(a, (const float*)a.pts);
+    int blocks = (int)std::min<long long>((n + 255) / 256, 148 * 16);
+    STPC_LAUNCH();
+    win_finalize_kernel<<<blocks, 256, 0, s>>>(a.win, a.best, n);
+}
+
+// One warp per 32 bitmap words (1024 pixels) of one frame: ballot the
+// validity / escape predicates and store packbits-ordered words.
+// Escape: rint(r / range_quant) outside [1, 0xFFFF) (bitstream.py:176-182).
+__global__ void __launch_bounds__(256) bitmap_kernel(const double* __restrict__ best, Geometry g,
+                                                     double quant, uint8_t* vbits, uint8_t* ebits,
+                                                     long long* fstats)
+{
+    const int f = blockIdx.y;
+    const int lane = threadIdx.x & 31;
+    const long long words = (long long)g.pbs / 4;
+    const long long wbase = ((long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * 32;
+    if (wbase >= words) return;
+    const double* img = best + (long long)f * g.P;
+    uint32_t my_v = 0, my_e = 0;
+    int nvalid = 0;
+    for (int i = 0; i < 32; ++i) {
+        long long pix = (wbase + i) * 32 + lane;
+        bool valid = false, esc = false;
+        if (pix < g.P) {
+            double r = img[pix];
+            valid = isfinite(r);
+            if (valid) {
+                double q = rint(r / quant);
+                esc = (q < 1.0) || (q >= 65535.0);
+            }
+        }
+        uint32_t mv = __ballot_sync(STPC_FULL, valid);
+        uint32_t me = __ballot_sync(STPC_FULL, esc);
+        if (lane == i) { my_v = mv; my_e = me; }
+        nvalid += __popc(mv);
+    }
+    if (wbase + lane < words) {
+        reinterpret_cast<uint32_t*>(vbits + (long long)f * g.pbs)[wbase + lane] = natural_bits(my_v);
+        reinterpret_cast<uint32_t*>(ebits + (long long)f * g.pbs)[wbase + lane] = natural_bits(my_e);
+    }
+    if (lane == 0 && nvalid)
+        atomicAdd((unsigned long long*)&fstats[(long long)f * FS_COUNT + FS_VALID], (unsigned long long)nvalid);
+}
+
+void launch_bitmaps(const double* best, int n_frames, const Geometry& g, double range_quant,
+                    uint8_t* vbits, uint8_t* ebits, long long* fstats, cudaStream_t s)
+{
+    if (n_frames <= 0) return;
+    long long words = g.pbs / 4;
+    long long warps = (words + 31) / 32;
+    dim3 grid((unsigned)((warps + 7) / 8), n_frames);
+    STPC_LAUNCH();
+    bitmap_kernel<<<grid, 256, 0, s>>>(best, g, range_quant, vbits, ebits, fstats);
+}
+
+}  // namespace stpc

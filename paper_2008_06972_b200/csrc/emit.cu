@@ -1,0 +1,457 @@
+// K3c -- residual compaction and .stpc v1 payload assembly on the device.
+//
+// Replaces residual_pixels_for_tiles + the residual/run/fallback sections of
+// serialize (/root/reference/pkg/src/stpc/spatial.py:160-168;
+// /root/reference/pkg/src/stpc/temporal.py:206-245;
+// /root/reference/pkg/src/stpc/bitstream.py:193-278, 176-190) and the
+// coverage counts (/root/reference/pkg/src/stpc/temporal.py:269-290).
+//
+// Payload layout per group (pkg/README.md:79-120, bitstream.py:204-276):
+//   config(57) | transforms n*48 | validity bitmaps n*ceil(P/8) |
+//   u32 #runs, runs <HHH fff> + presence bits + f32 per present P channel |
+//   per channel: u32 #rows, rows <HH> + runs <HH fff> |
+//   per channel: u32 count [, LEB128 deltas, u16 codes, u32 #esc, f32 escapes]
+//
+// Residual pixels of a channel are the valid pixels of class-0 tiles in flat
+// (row-major) order; one warp walks one image row 32 pixels at a time, the
+// per-row counts are chained across rows by the plan kernel (delta coding
+// crosses row boundaries), then the emit pass writes each row's bytes at its
+// final offsets.
+#include "kernels.cuh"
+
+namespace stpc {
+
+__device__ __forceinline__ uint32_t load_bits(const uint8_t* bm, long long word)
+{
+    return natural_bits(__ldg(reinterpret_cast<const uint32_t*>(bm) + word));
+}
+
+struct RowWalk {
+    long long rb, re;  // flat pixel range of the row
+    long long w0, w1;  // bitmap words overlapping it
+};
+
+__device__ __forceinline__ RowWalk row_walk(const Geometry& g, int v)
+{
+    RowWalk rw;
+    rw.rb = (long long)v * g.w;
+    rw.re = rw.rb + g.w;
+    rw.w0 = rw.rb >> 5;
+    rw.w1 = (rw.re + 31) >> 5;
+    return rw;
+}
+
+// residual / class masks of one 32-pixel word of one row
+__device__ __forceinline__ void word_masks(const Geometry& g, const uint8_t* vb, const uint8_t* crow,
+                                           const RowWalk& rw, long long wd, int v, uint32_t& res,
+                                           uint32_t& tmp, uint32_t& fb)
+{
+    const int lane = threadIdx.x & 31;
+    long long pix = wd * 32 + lane;
+    uint32_t valid = load_bits(vb, wd);
+    int cls = 255;
+    if (pix >= rw.rb && pix < rw.re && ((valid >> lane) & 1u)) {
+        int u = (int)(pix - rw.rb);
+        cls = crow[u / g.tw];
+    }
+    res = __ballot_sync(STPC_FULL, cls == 0);
+    tmp = __ballot_sync(STPC_FULL, cls == 1);
+    fb = __ballot_sync(STPC_FULL, cls == 2);
+}
+
+// Warp per (frame, row): counts, varint bytes (excluding the row's first
+// delta), first/last residual flat index, coverage counters.
+__global__ void __launch_bounds__(256) rowstats_kernel(PlanArgs A)
+{
+    const Geometry& g = A.g;
+    const int lane = threadIdx.x & 31;
+    const long long wid = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    const long long F = (long long)A.n_groups * A.n;
+    if (wid >= F * g.h) return;
+    const int f = (int)(wid / g.h);
+    const int v = (int)(wid % g.h);
+    const uint8_t* vb = A.vbits + (long long)f * g.pbs;
+    const uint8_t* eb = A.ebits + (long long)f * g.pbs;
+    const uint8_t* crow = A.cls + ((long long)f * g.ty + v / g.th) * g.tx;
+    RowWalk rw = row_walk(g, v);
+    int cnt = 0, nesc = 0, vbytes = 0, ntmp = 0, nfb = 0;
+    long long first = -1, last = -1;
+    for (long long wd = rw.w0; wd < rw.w1; ++wd) {
+        uint32_t res, tmp, fb;
+        word_masks(g, vb, crow, rw, wd, v, res, tmp, fb);
+        ntmp += __popc(tmp);
+        nfb += __popc(fb);
+        if (!res) continue;
+        uint32_t esc = load_bits(eb, wd);
+        nesc += __popc(res & esc);
+        // varint length of every residual's delta except the row's first
+        bool mine = (res >> lane) & 1u;
+        int len = 0;
+        if (mine) {
+            uint32_t below = res & ((1u << lane) - 1u);
+            long long idx = wd * 32 + lane;
+            long long prev = below ? wd * 32 + (31 - __clz(below)) : last;
+            if (prev >= 0) len = varint_len((uint32_t)(idx - prev));
+        }
+        for (int o = 16; o > 0; o >>= 1) len += __shfl_xor_sync(STPC_FULL, len, o);
+        vbytes += len;
+        if (first < 0) first = wd * 32 + (__ffs(res) - 1);
+        last = wd * 32 + (31 - __clz(res));
+        cnt += __popc(res);
+    }
+    if (lane == 0) {
+        RowStat st;
+        st.cnt = cnt;
+        st.nesc = nesc;
+        st.vb = vbytes;
+        st.first = (int)first;
+        st.last = (int)last;
+        A.rowstat[wid] = st;
+        long long* fs = A.fstats + (long long)f * FS_COUNT;
+        if (ntmp) atomicAdd((unsigned long long*)&fs[FS_TEMPORAL], (unsigned long long)ntmp);
+        if (nfb) atomicAdd((unsigned long long*)&fs[FS_FALLBACK], (unsigned long long)nfb);
+        if (cnt) atomicAdd((unsigned long long*)&fs[FS_RESIDUAL], (unsigned long long)cnt);
+        if (nesc) atomicAdd((unsigned long long*)&fs[FS_ESCAPES], (unsigned long long)nesc);
+    }
+}
+
+void launch_rowstats(const PlanArgs& a, cudaStream_t s)
+{
+    long long warps = (long long)a.n_groups * a.n * a.g.h;
+    if (warps <= 0) return;
+    STPC_LAUNCH();
+    rowstats_kernel<<<(unsigned)((warps + 7) / 8), 256, 0, s>>>(a);
+}
+
+// Block per group: chain the per-row residual counts into per-frame sections,
+// lay out the fallback rows and temporal records, and size the payload.
+__global__ void plan_kernel(PlanArgs A)
+{
+    const Geometry& g = A.g;
+    const int grp = blockIdx.x;
+    const int n = A.n;
+    const int tid = threadIdx.x;
+    const long long PB = (g.P + 7) / 8;
+    // per-frame residual chaining and fallback row layout (thread per frame)
+    for (int i = tid; i < n; i += blockDim.x) {
+        const long long f = (long long)grp * n + i;
+        long long cnt = 0, vbt = 0, esc = 0, prev = -1;
+        for (int v = 0; v < g.h; ++v) {
+            RowStat st = A.rowstat[f * g.h + v];
+            RowOff ro;
+            ro.cnt_off = (int)cnt;
+            ro.vb_off = (int)vbt;
+            ro.esc_off = (int)esc;
+            ro.prev = (int)(prev < 0 ? 0 : prev);
+            if (st.cnt) {
+                vbt += st.vb + varint_len((uint32_t)(st.first - ro.prev));
+                cnt += st.cnt;
+                esc += st.nesc;
+                prev = st.last;
+            }
+            A.rowoff[f * g.h + v] = ro;
+        }
+        A.res_cnt[f] = cnt;
+        A.res_vb[f] = vbt;
+        A.res_esc[f] = esc;
+        long long rows = 0;
+        if (i != A.k) {
+            for (int tr = 0; tr < g.ty; ++tr) rows += A.n_runs[f * g.ty + tr] > 0;
+        }
+        A.fb_rows[f] = rows;
+    }
+    __syncthreads();
+    if (tid != 0) return;
+    long long* sec = A.sec + (long long)grp * (2 + 2 * n);
+    long long off = 57 + 48LL * n + PB * n;
+    // temporal section
+    sec[0] = off;
+    off += 4;
+    const long long kf = (long long)grp * n + A.k;
+    long long nruns = 0;
+    for (int tr = 0; tr < g.ty; ++tr) {
+        long long kc = (long long)grp * g.ty + tr;
+        A.chain_off[kf * g.ty + tr] = off;
+        off += A.chain_tbytes[kc];
+        nruns += A.n_runs[kf * g.ty + tr];
+    }
+    sec[1] = nruns;
+    // fallback sections
+    for (int i = 0; i < n; ++i) {
+        const long long f = (long long)grp * n + i;
+        sec[2 + i] = off;
+        off += 4;
+        if (i == A.k) continue;
+        for (int tr = 0; tr < g.ty; ++tr) {
+            int nr = A.n_runs[f * g.ty + tr];
+            A.chain_off[f * g.ty + tr] = off;
+            if (nr > 0) off += 4 + 16LL * nr;
+        }
+    }
+    // residual sections
+    for (int i = 0; i < n; ++i) {
+        const long long f = (long long)grp * n + i;
+        sec[2 + n + i] = off;
+        off += 4;
+        if (A.res_cnt[f]) off += A.res_vb[f] + 2 * A.res_cnt[f] + 4 + 4 * A.res_esc[f];
+    }
+    A.payload_len[grp] = off;
+}
+
+void launch_plan(const PlanArgs& a, cudaStream_t s)
+{
+    if (a.n_groups <= 0) return;
+    STPC_LAUNCH();
+    plan_kernel<<<a.n_groups, 64, 0, s>>>(a);
+}
+
+// Single-block exclusive scan over group lengths (rounded up to `align`).
+__global__ void group_scan_kernel(const long long* lens, long long* offs, int G, int align, long long add)
+{
+    __shared__ long long carry;
+    __shared__ long long wsum[32];
+    if (threadIdx.x == 0) carry = 0;
+    __syncthreads();
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    for (int base = 0; base < G; base += blockDim.x) {
+        int i = base + threadIdx.x;
+        long long v = 0;
+        if (i < G) {
+            v = lens[i] + add;
+            v = (v + align - 1) / align * align;
+        }
+        long long inc = warp_incl_scan_ll(v);
+        if (lane == 31) wsum[wid] = inc;
+        __syncthreads();
+        if (wid == 0) {
+            long long ws = lane < (blockDim.x >> 5) ? wsum[lane] : 0;
+            long long wi = warp_incl_scan_ll(ws);
+            if (lane < (blockDim.x >> 5)) wsum[lane] = wi - ws;
+        }
+        __syncthreads();
+        long long excl = carry + wsum[wid] + inc - v;
+        if (i < G) offs[i] = excl;
+        __syncthreads();
+        if (threadIdx.x == blockDim.x - 1) carry = excl + v;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) offs[G] = carry;
+}
+
+void launch_group_scan(const long long* lens, long long* offs, int G, int align, long long add, cudaStream_t s)
+{
+    STPC_LAUNCH();
+    group_scan_kernel<<<1, 1024, 0, s>>>(lens, offs, G, align, add);
+}
+
+// ---------------------------------------------------------------------------
+// emission
+// ---------------------------------------------------------------------------
+
+// config, transforms, section counts; block per group
+__global__ void emit_header_kernel(EmitArgs E)
+{
+    const PlanArgs& A = E.p;
+    const int grp = blockIdx.x;
+    const int n = A.n;
+    uint8_t* out = E.payload + A.payload_off[grp];
+    const long long* sec = A.sec + (long long)grp * (2 + 2 * n);
+    for (int i = threadIdx.x; i < 57; i += blockDim.x) out[i] = E.cfg_bytes[i];
+    for (int i = threadIdx.x; i < 12 * n; i += blockDim.x) {
+        int fi = i / 12, j = i % 12;
+        put_f32(out + 57 + 4 * i, (float)E.xf[((long long)grp * n + fi) * 12 + j]);
+    }
+    if (threadIdx.x == 0) put_u32(out + sec[0], (uint32_t)sec[1]);
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        const long long f = (long long)grp * n + i;
+        put_u32(out + sec[2 + i], (uint32_t)A.fb_rows[f]);
+        put_u32(out + sec[2 + n + i], (uint32_t)A.res_cnt[f]);
+        if (A.res_cnt[f]) {
+            long long o = sec[2 + n + i] + 4 + A.res_vb[f] + 2 * A.res_cnt[f];
+            put_u32(out + o, (uint32_t)A.res_esc[f]);
+        }
+    }
+}
+
+// validity bitmaps: frame bytes [0, PB) copied into the payload
+__global__ void emit_bitmaps_kernel(EmitArgs E)
+{
+    const PlanArgs& A = E.p;
+    const Geometry& g = A.g;
+    const int f = blockIdx.y;
+    const int grp = f / A.n, i = f % A.n;
+    const long long PB = (g.P + 7) / 8;
+    uint8_t* out = E.payload + A.payload_off[grp] + 57 + 48LL * A.n + PB * i;
+    const uint8_t* src = A.vbits + (long long)f * g.pbs;
+    for (long long b = (long long)blockIdx.x * blockDim.x + threadIdx.x; b < PB; b += (long long)gridDim.x * blockDim.x)
+        out[b] = src[b];
+}
+
+// temporal runs: warp per key chain
+__global__ void __launch_bounds__(128) emit_temporal_kernel(EmitArgs E)
+{
+    const PlanArgs& A = E.p;
+    const Geometry& g = A.g;
+    const int lane = threadIdx.x & 31;
+    const long long kc = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (kc >= (long long)A.n_groups * g.ty) return;
+    const int grp = (int)(kc / g.ty), tr = (int)(kc % g.ty);
+    const int n = A.n, k = A.k, pm = (n + 7) / 8;
+    const long long kslot = ((long long)grp * n + k) * g.ty + tr;
+    const int nr = A.n_runs[kslot];
+    uint8_t* out = E.payload + A.payload_off[grp];
+    long long pos = A.chain_off[kslot];
+    for (int base = 0; base < nr; base += 32) {
+        int j = base + lane;
+        int size = 0;
+        const uint8_t* okv = nullptr;
+        if (j < nr) {
+            okv = E.ref_ok + (kc * g.tx + j) * n;
+            int present = 0;
+            for (int c = 0; c < n; ++c) present += (c != k) && okv[c];
+            size = 18 + pm + 4 * present;
+        }
+        int inc = warp_incl_scan(size);
+        if (j < nr) {
+            uint8_t* o = out + pos + inc - size;
+            const long long ri = kslot * g.tx + j;
+            put_u16(o, tr);
+            put_u16(o + 2, E.run_s[ri]);
+            put_u16(o + 4, E.run_len[ri]);
+            put_f32(o + 6, E.run_abc[3 * ri]);
+            put_f32(o + 10, E.run_abc[3 * ri + 1]);
+            put_f32(o + 14, E.run_abc[3 * ri + 2]);
+            uint8_t* bits = o + 18;
+            for (int b = 0; b < pm; ++b) bits[b] = 0;
+            const float* cv = E.ref_c + (kc * g.tx + j) * n;
+            int q = 0;
+            for (int c = 0; c < n; ++c) {
+                bool pres = (c == k) || okv[c];
+                if (pres) bits[c >> 3] |= (uint8_t)(1u << (c & 7));
+                if (pres && c != k) put_f32(o + 18 + pm + 4 * q++, cv[c]);
+            }
+        }
+        pos += __shfl_sync(STPC_FULL, inc, 31);
+    }
+}
+
+// fallback rows: warp per P chain
+__global__ void __launch_bounds__(128) emit_fallback_kernel(EmitArgs E)
+{
+    const PlanArgs& A = E.p;
+    const Geometry& g = A.g;
+    const int lane = threadIdx.x & 31;
+    const long long wid = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    const long long F = (long long)A.n_groups * A.n;
+    if (wid >= F * g.ty) return;
+    const long long f = wid / g.ty;
+    const int tr = (int)(wid % g.ty);
+    const int grp = (int)(f / A.n), i = (int)(f % A.n);
+    if (i == A.k) return;
+    const int nr = A.n_runs[wid];
+    if (nr == 0) return;
+    uint8_t* o = E.payload + A.payload_off[grp] + A.chain_off[wid];
+    if (lane == 0) {
+        put_u16(o, tr);
+        put_u16(o + 2, nr);
+    }
+    for (int j = lane; j < nr; j += 32) {
+        const long long ri = wid * g.tx + j;
+        uint8_t* r = o + 4 + 16LL * j;
+        put_u16(r, E.run_s[ri]);
+        put_u16(r + 2, E.run_len[ri]);
+        put_f32(r + 4, E.run_abc[3 * ri]);
+        put_f32(r + 8, E.run_abc[3 * ri + 1]);
+        put_f32(r + 12, E.run_abc[3 * ri + 2]);
+    }
+}
+
+// residual rows: warp per (frame, row) with residual pixels
+__global__ void __launch_bounds__(256) emit_residual_kernel(EmitArgs E)
+{
+    const PlanArgs& A = E.p;
+    const Geometry& g = A.g;
+    const int lane = threadIdx.x & 31;
+    const long long wid = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    const long long F = (long long)A.n_groups * A.n;
+    if (wid >= F * g.h) return;
+    const RowStat st = A.rowstat[wid];
+    if (st.cnt == 0) return;
+    const RowOff ro = A.rowoff[wid];
+    const long long f = wid / g.h;
+    const int v = (int)(wid % g.h);
+    const int grp = (int)(f / A.n), i = (int)(f % A.n);
+    const long long* sec = A.sec + (long long)grp * (2 + 2 * A.n);
+    uint8_t* base = E.payload + A.payload_off[grp] + sec[2 + A.n + i] + 4;
+    const long long total = A.res_cnt[f];
+    uint8_t* vptr = base + ro.vb_off;
+    uint8_t* cptr = base + A.res_vb[f] + 2LL * ro.cnt_off;
+    uint8_t* eptr = base + A.res_vb[f] + 2 * total + 4 + 4LL * ro.esc_off;
+    const uint8_t* vb = A.vbits + f * g.pbs;
+    const uint8_t* eb = A.ebits + f * g.pbs;
+    const uint8_t* crow = A.cls + (f * g.ty + v / g.th) * g.tx;
+    const double* img = E.best + f * g.P;
+    RowWalk rw = row_walk(g, v);
+    long long last = ro.prev;
+    for (long long wd = rw.w0; wd < rw.w1; ++wd) {
+        uint32_t res, tmp, fb;
+        word_masks(g, vb, crow, rw, wd, v, res, tmp, fb);
+        if (!res) continue;
+        uint32_t esc = load_bits(eb, wd) & res;
+        bool mine = (res >> lane) & 1u;
+        uint32_t lt = (1u << lane) - 1u;
+        int len = 0;
+        long long idx = wd * 32 + lane;
+        uint32_t delta = 0;
+        if (mine) {
+            uint32_t below = res & lt;
+            long long prev = below ? wd * 32 + (31 - __clz(below)) : last;
+            delta = (uint32_t)(idx - prev);
+            len = varint_len(delta);
+        }
+        int inc = warp_incl_scan(len);
+        if (mine) {
+            uint8_t* o = vptr + inc - len;
+            uint32_t d = delta;
+            for (int b = 0; b < len - 1; ++b) {
+                o[b] = (uint8_t)((d & 0x7f) | 0x80);
+                d >>= 7;
+            }
+            o[len - 1] = (uint8_t)d;
+            int rank = __popc(res & lt);
+            double r = img[idx];
+            bool e = (esc >> lane) & 1u;
+            uint32_t code = e ? 0xFFFFu : (uint32_t)(long long)rint(r / E.range_quant);
+            put_u16(cptr + 2 * rank, code);
+            if (e) put_f32(eptr + 4 * __popc(esc & lt), (float)r);
+        }
+        vptr += __shfl_sync(STPC_FULL, inc, 31);
+        cptr += 2 * __popc(res);
+        eptr += 4 * __popc(esc);
+        last = wd * 32 + (31 - __clz(res));
+    }
+}
+
+void launch_emit(const EmitArgs& E, cudaStream_t s)
+{
+    const PlanArgs& A = E.p;
+    const Geometry& g = A.g;
+    if (A.n_groups <= 0) return;
+    const long long F = (long long)A.n_groups * A.n;
+    STPC_LAUNCH();
+    emit_header_kernel<<<A.n_groups, 128, 0, s>>>(E);
+    long long PB = (g.P + 7) / 8;
+    STPC_LAUNCH();
+    emit_bitmaps_kernel<<<dim3((unsigned)std::min<long long>((PB + 255) / 256, 64), (unsigned)F), 256, 0, s>>>(E);
+    long long kwarps = (long long)A.n_groups * g.ty;
+    STPC_LAUNCH();
+    emit_temporal_kernel<<<(unsigned)((kwarps + 3) / 4), 128, 0, s>>>(E);
+    long long fwarps = F * g.ty;
+    STPC_LAUNCH();
+    emit_fallback_kernel<<<(unsigned)((fwarps + 3) / 4), 128, 0, s>>>(E);
+    long long rwarps = F * g.h;
+    STPC_LAUNCH();
+    emit_residual_kernel<<<(unsigned)((rwarps + 7) / 8), 256, 0, s>>>(E);
+}
+
+}  // namespace stpc

@@ -1,0 +1,666 @@
+// Native runtime + C-ABI of libstpc_b200: owns the device workspace of a batch
+// of K+P groups and sequences the hot-path kernels on one CUDA stream.
+//
+// Pipeline per call:
+//   K1 convert -> bitmaps -> K2 fit (key frames) -> K3a refit -> K3b fit (P
+//   frames, temporally covered tiles masked) -> residual row stats -> plan
+//   [sync: payload sizes] -> payload emission -> histogram -> Huffman code
+//   lengths [sync: blob sizes] -> bit packing -> CRC + header.
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+#include <algorithm>
+
+#include "kernels.cuh"
+#include "../../include/stpc_b200.h"
+
+using namespace stpc;
+
+unsigned long long stpc::g_launch_count = 0;
+static thread_local std::string g_err;
+
+// pipeline stages timed with CUDA events when profiling is enabled
+enum Stage { ST_INIT, ST_CONVERT, ST_BITMAP, ST_FIT_K, ST_REFIT, ST_FIT_P, ST_PLAN, ST_EMIT,
+             ST_HUFF, ST_PACK, ST_CRC, ST_COUNT };
+static const char* kStageNames[ST_COUNT] = {"init", "convert", "bitmaps", "fit_key", "refit", "fit_p",
+                                            "plan", "emit", "huffman", "pack", "crc"};
+
+#define CK(x)                                                                         \
+    do {                                                                              \
+        cudaError_t e_ = (x);                                                         \
+        if (e_ != cudaSuccess) {                                                      \
+            g_err = std::string(#x) + ": " + cudaGetErrorString(e_);                  \
+            return STPC_ERR_CUDA;                                                     \
+        }                                                                             \
+    } while (0)
+
+namespace {
+
+struct DevBuf {
+    void* p = nullptr;
+    size_t cap = 0;
+    int ensure(size_t need)
+    {
+        if (need <= cap) return 0;
+        if (p) cudaFree(p);
+        p = nullptr;
+        cap = 0;
+        size_t c = need + need / 8 + 256;
+        if (cudaMalloc(&p, c) != cudaSuccess) {
+            g_err = "cudaMalloc failed (" + std::to_string(c) + " bytes)";
+            return STPC_ERR_NOMEM;
+        }
+        cap = c;
+        return 0;
+    }
+    template <class T> T* as() const { return reinterpret_cast<T*>(p); }
+    ~DevBuf()
+    {
+        if (p) cudaFree(p);
+    }
+};
+
+struct HostBuf {
+    void* p = nullptr;
+    size_t cap = 0;
+    int ensure(size_t need)
+    {
+        if (need <= cap) return 0;
+        if (p) cudaFreeHost(p);
+        p = nullptr;
+        cap = 0;
+        size_t c = need + need / 8 + 256;
+        if (cudaMallocHost(&p, c) != cudaSuccess) {
+            g_err = "cudaMallocHost failed";
+            return STPC_ERR_NOMEM;
+        }
+        cap = c;
+        return 0;
+    }
+    template <class T> T* as() const { return reinterpret_cast<T*>(p); }
+    ~HostBuf()
+    {
+        if (p) cudaFreeHost(p);
+    }
+};
+
+}  // namespace
+
+struct stpc_encoder {
+    stpc_config cfg;
+    Geometry g;
+    int n, k;
+    DevBuf trig;  // sin_t | cos_t | sin_p | cos_p
+    DevBuf cfg_bytes;
+    // inputs
+    DevBuf pts, pt_off, xf;
+    HostBuf h_stage;  // pinned staging: pt_off | xf
+    // frame level
+    DevBuf best, vbits, ebits, cls, fstats;
+    // chain level
+    DevBuf run_s, run_len, run_abc, n_runs, ref_ok, ref_c, chain_tbytes, chain_off;
+    // plan
+    DevBuf rowstat, rowoff, res_cnt, res_vb, res_esc, fb_rows, sec, payload_len, payload_off;
+    DevBuf payload;
+    // entropy
+    DevBuf hist, lens, codes, enc_len, blob_off, chunk_bits, seg_crc, blobs;
+    // last result (host)
+    int G = 0;
+    std::vector<long long> h_payload_len, h_blob_off, h_enc_len;
+    HostBuf h_sizes;
+    // profiling
+    int profile = 0;
+    cudaEvent_t ev[ST_COUNT + 1] = {};
+    double stage_ms[ST_COUNT] = {};
+    long long profiled_calls = 0;
+    ~stpc_encoder()
+    {
+        for (auto& x : ev)
+            if (x) cudaEventDestroy(x);
+    }
+    void mark(int st, cudaStream_t s)
+    {
+        if (profile) cudaEventRecord(ev[st], s);
+    }
+};
+
+static Trig trig_of(const stpc_encoder* e)
+{
+    const double* t = e->trig.as<double>();
+    Trig tg;
+    tg.sin_t = t;
+    tg.cos_t = t + e->g.w;
+    tg.sin_p = t + 2 * e->g.w;
+    tg.cos_p = t + 2 * e->g.w + e->g.h;
+    return tg;
+}
+
+// config block of the payload: struct.pack("<Bd HH ddd II HH d", ...)
+// (/root/reference/pkg/src/stpc/bitstream.py:142-157)
+static void pack_config(const stpc_config& c, uint8_t out[57])
+{
+    size_t o = 0;
+    auto put = [&](const void* p, size_t n) {
+        memcpy(out + o, p, n);
+        o += n;
+    };
+    uint8_t mode = (uint8_t)c.mode;
+    uint16_t tw = (uint16_t)c.tile_w, th = (uint16_t)c.tile_h;
+    uint32_t w = (uint32_t)c.w, h = (uint32_t)c.h;
+    uint16_t nf = (uint16_t)c.n_frames, ki = (uint16_t)c.k_index;
+    put(&mode, 1);
+    put(&c.tau, 8);
+    put(&tw, 2);
+    put(&th, 2);
+    put(&c.theta_r, 8);
+    put(&c.phi_r, 8);
+    put(&c.phi_offset, 8);
+    put(&w, 4);
+    put(&h, 4);
+    put(&nf, 2);
+    put(&ki, 2);
+    put(&c.range_quant, 8);
+}
+
+extern "C" {
+
+const char* stpc_last_error(void) { return g_err.c_str(); }
+const char* stpc_version(void) { return "stpc_b200 0.1 (sm_100a)"; }
+
+int stpc_device_count(void)
+{
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) return 0;
+    return n;
+}
+
+int stpc_malloc(void** dev_ptr, int64_t bytes)
+{
+    if (!dev_ptr || bytes < 0) return STPC_ERR_ARG;
+    CK(cudaMalloc(dev_ptr, (size_t)std::max<int64_t>(bytes, 1)));
+    return STPC_OK;
+}
+
+int stpc_free(void* dev_ptr)
+{
+    if (dev_ptr) CK(cudaFree(dev_ptr));
+    return STPC_OK;
+}
+
+int stpc_memcpy_d2h(void* dst, const void* src, int64_t bytes)
+{
+    if (bytes <= 0) return STPC_OK;
+    CK(cudaMemcpy(dst, src, (size_t)bytes, cudaMemcpyDeviceToHost));
+    return STPC_OK;
+}
+
+int stpc_memcpy_h2d(void* dst, const void* src, int64_t bytes)
+{
+    if (bytes <= 0) return STPC_OK;
+    CK(cudaMemcpy(dst, src, (size_t)bytes, cudaMemcpyHostToDevice));
+    return STPC_OK;
+}
+
+int stpc_encoder_create(const stpc_config* cfg, const double* sin_theta, const double* cos_theta,
+                        const double* sin_phi, const double* cos_phi, stpc_encoder** out)
+{
+    if (!cfg || !out || !sin_theta || !cos_theta || !sin_phi || !cos_phi) {
+        g_err = "null argument";
+        return STPC_ERR_ARG;
+    }
+    const stpc_config& c = *cfg;
+    if (c.w < 1 || c.h < 1 || c.tile_w < 1 || c.tile_h < 1 || c.n_frames < 1 || c.k_index < 0 ||
+        c.k_index >= c.n_frames || !(c.tau > 0) || !(c.range_quant > 0)) {
+        g_err = "invalid config";
+        return STPC_ERR_ARG;
+    }
+    int tx = (c.w + c.tile_w - 1) / c.tile_w, ty = (c.h + c.tile_h - 1) / c.tile_h;
+    if (tx > 0xFFFF || ty > 0xFFFF) {
+        g_err = "tile grid exceeds the format's u16 indices";
+        return STPC_ERR_ARG;
+    }
+    stpc_encoder* e = new stpc_encoder();
+    e->cfg = c;
+    e->n = c.n_frames;
+    e->k = c.k_index;
+    Geometry& g = e->g;
+    g.w = c.w;
+    g.h = c.h;
+    g.tw = c.tile_w;
+    g.th = c.tile_h;
+    g.tx = tx;
+    g.ty = ty;
+    g.P = (long long)c.w * c.h;
+    long long pb = (g.P + 7) / 8;
+    g.pbs = (int)((pb + 127) / 128 * 128);
+    g.theta_r = c.theta_r;
+    g.phi_r = c.phi_r;
+    g.phi_offset = c.phi_offset;
+    int rc = e->trig.ensure(sizeof(double) * (2 * c.w + 2 * c.h));
+    if (!rc) rc = e->cfg_bytes.ensure(64);
+    if (rc) {
+        delete e;
+        return rc;
+    }
+    double* t = e->trig.as<double>();
+    cudaMemcpy(t, sin_theta, sizeof(double) * c.w, cudaMemcpyHostToDevice);
+    cudaMemcpy(t + c.w, cos_theta, sizeof(double) * c.w, cudaMemcpyHostToDevice);
+    cudaMemcpy(t + 2 * c.w, sin_phi, sizeof(double) * c.h, cudaMemcpyHostToDevice);
+    cudaMemcpy(t + 2 * c.w + c.h, cos_phi, sizeof(double) * c.h, cudaMemcpyHostToDevice);
+    uint8_t cb[57];
+    pack_config(c, cb);
+    cudaError_t ce = cudaMemcpy(e->cfg_bytes.p, cb, 57, cudaMemcpyHostToDevice);
+    if (ce != cudaSuccess) {
+        g_err = std::string("encoder upload: ") + cudaGetErrorString(ce);
+        delete e;
+        return STPC_ERR_CUDA;
+    }
+    *out = e;
+    return STPC_OK;
+}
+
+void stpc_encoder_destroy(stpc_encoder* enc) { delete enc; }
+
+#define ENS(buf, bytes)                    \
+    do {                                   \
+        int r_ = (buf).ensure(bytes);      \
+        if (r_) return r_;                 \
+    } while (0)
+
+static int encode_impl(stpc_encoder* e, int G, const void* d_points, const int64_t* h_off,
+                       const double* h_xf, cudaStream_t s)
+{
+    const Geometry& g = e->g;
+    const int n = e->n, k = e->k;
+    const long long F = (long long)G * n;
+    const long long TT = (long long)g.tx * g.ty;
+    e->mark(ST_INIT, s);
+    // --- inputs (offsets + transforms through pinned staging)
+    ENS(e->h_stage, sizeof(long long) * (F + 1) + sizeof(double) * 12 * F);
+    long long* st_off = e->h_stage.as<long long>();
+    double* st_xf = reinterpret_cast<double*>(st_off + F + 1);
+    long long max_pts = 0;
+    for (long long f = 0; f <= F; ++f) st_off[f] = h_off[f];
+    for (long long f = 0; f < F; ++f) max_pts = std::max<long long>(max_pts, h_off[f + 1] - h_off[f]);
+    memcpy(st_xf, h_xf, sizeof(double) * 12 * F);
+    ENS(e->pt_off, sizeof(long long) * (F + 1));
+    ENS(e->xf, sizeof(double) * 12 * F);
+    CK(cudaMemcpyAsync(e->pt_off.p, st_off, sizeof(long long) * (F + 1), cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(e->xf.p, st_xf, sizeof(double) * 12 * F, cudaMemcpyHostToDevice, s));
+    // --- workspace
+    ENS(e->best, sizeof(double) * F * g.P);
+    ENS(e->vbits, (size_t)F * g.pbs);
+    ENS(e->ebits, (size_t)F * g.pbs);
+    ENS(e->cls, (size_t)F * TT);
+    ENS(e->fstats, sizeof(long long) * F * FS_COUNT);
+    ENS(e->run_s, sizeof(uint16_t) * F * TT);
+    ENS(e->run_len, sizeof(uint16_t) * F * TT);
+    ENS(e->run_abc, sizeof(float) * 3 * F * TT);
+    ENS(e->n_runs, sizeof(int) * F * g.ty);
+    ENS(e->ref_ok, (size_t)G * TT * n);
+    ENS(e->ref_c, sizeof(float) * G * TT * n);
+    ENS(e->chain_tbytes, sizeof(long long) * G * g.ty);
+    ENS(e->chain_off, sizeof(long long) * F * g.ty);
+    ENS(e->rowstat, sizeof(RowStat) * F * g.h);
+    ENS(e->rowoff, sizeof(RowOff) * F * g.h);
+    ENS(e->res_cnt, sizeof(long long) * F);
+    ENS(e->res_vb, sizeof(long long) * F);
+    ENS(e->res_esc, sizeof(long long) * F);
+    ENS(e->fb_rows, sizeof(long long) * F);
+    ENS(e->sec, sizeof(long long) * G * (2 + 2 * n));
+    ENS(e->payload_len, sizeof(long long) * G);
+    ENS(e->payload_off, sizeof(long long) * (G + 1));
+    ENS(e->hist, sizeof(unsigned) * 256 * G);
+    ENS(e->lens, 256 * (size_t)G);
+    ENS(e->codes, sizeof(unsigned) * 256 * G);
+    ENS(e->enc_len, sizeof(long long) * G);
+    ENS(e->blob_off, sizeof(long long) * (G + 1));
+    ENS(e->h_sizes, sizeof(long long) * (3 * G + 2));
+
+    CK(cudaMemsetAsync(e->fstats.p, 0, sizeof(long long) * F * FS_COUNT, s));
+    CK(cudaMemsetAsync(e->cls.p, 0, (size_t)F * TT, s));
+    launch_fill_u64(e->best.as<unsigned long long>(), 0x7ff0000000000000ull, F * g.P, s);
+
+    e->mark(ST_CONVERT, s);
+    // --- K1
+    ConvertArgs ca;
+    ca.pts = d_points;
+    ca.pts_f64 = e->cfg.points_f64;
+    ca.pt_off = e->pt_off.as<long long>();
+    ca.xf = e->xf.as<double>();
+    ca.n_frames = (int)F;
+    ca.g = g;
+    ca.best = e->best.as<unsigned long long>();
+    ca.win = nullptr;
+    ca.fstats = e->fstats.as<long long>();
+    launch_convert(ca, (int)max_pts, s);
+    e->mark(ST_BITMAP, s);
+    launch_bitmaps(e->best.as<double>(), (int)F, g, e->cfg.range_quant, e->vbits.as<uint8_t>(),
+                   e->ebits.as<uint8_t>(), e->fstats.as<long long>(), s);
+
+    // --- K2 / K3a / K3b
+    Trig tg = trig_of(e);
+    FitArgs fa;
+    fa.best = e->best.as<double>();
+    fa.tg = tg;
+    fa.g = g;
+    fa.tau = e->cfg.tau;
+    fa.r_max = e->cfg.r_max;
+    fa.cond_limit = e->cfg.cond_limit;
+    fa.n_frames_group = n;
+    fa.k = k;
+    fa.mode = 0;
+    fa.n_jobs = G;
+    fa.cls = e->cls.as<uint8_t>();
+    fa.run_s = e->run_s.as<uint16_t>();
+    fa.run_len = e->run_len.as<uint16_t>();
+    fa.run_abc = e->run_abc.as<float>();
+    fa.n_runs = e->n_runs.as<int>();
+    e->mark(ST_FIT_K, s);
+    launch_fit_rows(fa, s);
+
+    RefitArgs ra;
+    ra.best = fa.best;
+    ra.tg = tg;
+    ra.g = g;
+    ra.tau = fa.tau;
+    ra.r_max = fa.r_max;
+    ra.n = n;
+    ra.k = k;
+    ra.n_groups = G;
+    ra.run_s = fa.run_s;
+    ra.run_len = fa.run_len;
+    ra.run_abc = fa.run_abc;
+    ra.n_runs = fa.n_runs;
+    ra.ref_ok = e->ref_ok.as<uint8_t>();
+    ra.ref_c = e->ref_c.as<float>();
+    ra.cls = fa.cls;
+    ra.chain_tbytes = e->chain_tbytes.as<long long>();
+    e->mark(ST_REFIT, s);
+    launch_refit(ra, s);
+
+    e->mark(ST_FIT_P, s);
+    if (n > 1) {
+        fa.mode = 1;
+        fa.n_jobs = G * (n - 1);
+        launch_fit_rows(fa, s);
+    }
+
+    e->mark(ST_PLAN, s);
+    // --- residual stats + plan
+    PlanArgs pa;
+    pa.g = g;
+    pa.n = n;
+    pa.k = k;
+    pa.n_groups = G;
+    pa.vbits = e->vbits.as<uint8_t>();
+    pa.ebits = e->ebits.as<uint8_t>();
+    pa.cls = fa.cls;
+    pa.n_runs = fa.n_runs;
+    pa.chain_tbytes = ra.chain_tbytes;
+    pa.rowstat = e->rowstat.as<RowStat>();
+    pa.rowoff = e->rowoff.as<RowOff>();
+    pa.fstats = e->fstats.as<long long>();
+    pa.res_cnt = e->res_cnt.as<long long>();
+    pa.res_vb = e->res_vb.as<long long>();
+    pa.res_esc = e->res_esc.as<long long>();
+    pa.fb_rows = e->fb_rows.as<long long>();
+    pa.chain_off = e->chain_off.as<long long>();
+    pa.sec = e->sec.as<long long>();
+    pa.payload_len = e->payload_len.as<long long>();
+    pa.payload_off = e->payload_off.as<long long>();
+    launch_rowstats(pa, s);
+    launch_plan(pa, s);
+    launch_group_scan(pa.payload_len, pa.payload_off, G, 16, 0, s);
+
+    long long* hs = e->h_sizes.as<long long>();
+    CK(cudaMemcpyAsync(hs, pa.payload_len, sizeof(long long) * G, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(hs + G, pa.payload_off + G, sizeof(long long), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    e->h_payload_len.assign(hs, hs + G);
+    long long payload_total = hs[G];
+    long long max_payload = 0;
+    for (int i = 0; i < G; ++i) max_payload = std::max(max_payload, hs[i]);
+
+    e->mark(ST_EMIT, s);
+    ENS(e->payload, (size_t)payload_total + 16);
+    EmitArgs ea;
+    ea.p = pa;
+    ea.best = fa.best;
+    ea.range_quant = e->cfg.range_quant;
+    ea.cfg_bytes = e->cfg_bytes.as<uint8_t>();
+    ea.xf = e->xf.as<double>();
+    ea.run_s = fa.run_s;
+    ea.run_len = fa.run_len;
+    ea.run_abc = fa.run_abc;
+    ea.ref_ok = ra.ref_ok;
+    ea.ref_c = ra.ref_c;
+    ea.payload = e->payload.as<uint8_t>();
+    launch_emit(ea, s);
+
+    e->mark(ST_HUFF, s);
+    // --- entropy stage
+    EntropyArgs en;
+    en.G = G;
+    en.payload = ea.payload;
+    en.payload_off = pa.payload_off;
+    en.payload_len = pa.payload_len;
+    en.hist = e->hist.as<unsigned>();
+    en.lens = e->lens.as<uint8_t>();
+    en.codes = e->codes.as<unsigned>();
+    en.enc_len = e->enc_len.as<long long>();
+    en.blob_off = e->blob_off.as<long long>();
+    en.max_chunks = (int)((max_payload + PACK_CHUNK - 1) / PACK_CHUNK);
+    CK(cudaMemsetAsync(en.hist, 0, sizeof(unsigned) * 256 * G, s));
+    launch_histogram(en, (int)max_payload, s);
+    launch_code_lengths(en, s);
+    launch_group_scan(en.enc_len, en.blob_off, G, 16, HDR, s);
+    CK(cudaMemcpyAsync(hs, en.enc_len, sizeof(long long) * G, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(hs + G, en.blob_off, sizeof(long long) * (G + 1), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    e->h_enc_len.assign(hs, hs + G);
+    e->h_blob_off.assign(hs + G, hs + 2 * G + 1);
+    long long blob_total = e->h_blob_off[G];
+    long long max_enc = 0;
+    for (int i = 0; i < G; ++i) max_enc = std::max(max_enc, e->h_enc_len[i]);
+    en.max_segs = (int)((max_enc + CRC_SEG - 1) / CRC_SEG);
+    ENS(e->chunk_bits, sizeof(long long) * (size_t)G * std::max(en.max_chunks, 1));
+    ENS(e->seg_crc, sizeof(unsigned) * (size_t)G * std::max(en.max_segs, 1));
+    ENS(e->blobs, (size_t)blob_total + 16);
+    en.chunk_bits = e->chunk_bits.as<long long>();
+    en.seg_crc = e->seg_crc.as<unsigned>();
+    en.blobs = e->blobs.as<uint8_t>();
+    CK(cudaMemsetAsync(en.blobs, 0, (size_t)blob_total, s));
+    e->mark(ST_PACK, s);
+    launch_pack(en, s);
+    e->mark(ST_CRC, s);
+    launch_crc(en, s);
+    CK(cudaGetLastError());
+    e->G = G;
+    if (e->profile) {
+        cudaEventRecord(e->ev[ST_COUNT], s);
+        CK(cudaEventSynchronize(e->ev[ST_COUNT]));
+        for (int i = 0; i < ST_COUNT; ++i) {
+            float ms = 0.f;
+            if (cudaEventElapsedTime(&ms, e->ev[i], e->ev[i + 1]) == cudaSuccess) e->stage_ms[i] += ms;
+        }
+        e->profiled_calls += 1;
+    }
+    return STPC_OK;
+}
+
+int stpc_encoder_profile(stpc_encoder* enc, int32_t enable)
+{
+    if (!enc) return STPC_ERR_ARG;
+    if (enable && !enc->ev[0])
+        for (auto& x : enc->ev) CK(cudaEventCreate(&x));
+    enc->profile = enable ? 1 : 0;
+    for (auto& m : enc->stage_ms) m = 0.0;
+    enc->profiled_calls = 0;
+    return STPC_OK;
+}
+
+int32_t stpc_encoder_stage_ms(const stpc_encoder* enc, double* ms, int32_t n)
+{
+    if (!enc || !ms) return 0;
+    int m = n < ST_COUNT ? n : ST_COUNT;
+    for (int i = 0; i < m; ++i) ms[i] = enc->stage_ms[i];
+    return ST_COUNT;
+}
+
+const char* stpc_stage_name(int32_t i) { return (i >= 0 && i < ST_COUNT) ? kStageNames[i] : ""; }
+
+uint64_t stpc_launch_count(void) { return stpc::g_launch_count; }
+
+int stpc_encode_device(stpc_encoder* enc, int32_t n_groups, const void* d_points,
+                       const int64_t* point_offsets, const double* transforms, void* stream)
+{
+    if (!enc || n_groups < 1 || !point_offsets || !transforms || (!d_points && point_offsets[(long long)n_groups * enc->n] > 0)) {
+        g_err = "invalid arguments";
+        return STPC_ERR_ARG;
+    }
+    return encode_impl(enc, n_groups, d_points, (const int64_t*)point_offsets, transforms, (cudaStream_t)stream);
+}
+
+int stpc_encode_host(stpc_encoder* enc, int32_t n_groups, const void* h_points,
+                     const int64_t* point_offsets, const double* transforms, uint8_t* h_out,
+                     int64_t out_cap, void* stream)
+{
+    if (!enc || n_groups < 1 || !point_offsets || !transforms) {
+        g_err = "invalid arguments";
+        return STPC_ERR_ARG;
+    }
+    cudaStream_t s = (cudaStream_t)stream;
+    long long F = (long long)n_groups * enc->n;
+    long long npts = point_offsets[F] - point_offsets[0];
+    const size_t esz = enc->cfg.points_f64 ? sizeof(double) : sizeof(float);
+    ENS(enc->pts, esz * 3 * std::max<long long>(npts, 1));
+    if (npts > 0)
+        CK(cudaMemcpyAsync(enc->pts.p, (const char*)h_points + esz * 3 * point_offsets[0], esz * 3 * npts,
+                           cudaMemcpyHostToDevice, s));
+    std::vector<int64_t> off(point_offsets, point_offsets + F + 1);
+    for (auto& o : off) o -= point_offsets[0];
+    int rc = encode_impl(enc, n_groups, enc->pts.p, off.data(), transforms, s);
+    if (rc) return rc;
+    if (h_out) {
+        rc = stpc_result_copy_blobs(enc, h_out, out_cap, stream);
+        if (rc) return rc;
+    }
+    CK(cudaStreamSynchronize(s));
+    return STPC_OK;
+}
+
+int32_t stpc_result_groups(const stpc_encoder* enc) { return enc ? enc->G : 0; }
+
+int stpc_result_blobs(const stpc_encoder* enc, int64_t* offsets, int64_t* lengths)
+{
+    if (!enc) return STPC_ERR_ARG;
+    for (int i = 0; i < enc->G; ++i) {
+        if (offsets) offsets[i] = enc->h_blob_off[i];
+        if (lengths) lengths[i] = HDR + enc->h_enc_len[i];
+    }
+    if (offsets) offsets[enc->G] = enc->G ? enc->h_blob_off[enc->G] : 0;
+    return STPC_OK;
+}
+
+int stpc_result_payload_lengths(const stpc_encoder* enc, int64_t* raw_lengths)
+{
+    if (!enc) return STPC_ERR_ARG;
+    for (int i = 0; i < enc->G; ++i) raw_lengths[i] = enc->h_payload_len[i];
+    return STPC_OK;
+}
+
+const uint8_t* stpc_result_device_blobs(const stpc_encoder* enc) { return enc ? enc->blobs.as<uint8_t>() : nullptr; }
+
+int stpc_result_copy_blobs(const stpc_encoder* enc, uint8_t* h_dst, int64_t cap, void* stream)
+{
+    if (!enc || !h_dst) return STPC_ERR_ARG;
+    long long total = enc->G ? enc->h_blob_off[enc->G] : 0;
+    if (total > cap) {
+        g_err = "output buffer too small: need " + std::to_string(total);
+        return STPC_ERR_ARG;
+    }
+    cudaStream_t s = (cudaStream_t)stream;
+    if (total > 0) CK(cudaMemcpyAsync(h_dst, enc->blobs.p, (size_t)total, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    return STPC_OK;
+}
+
+int stpc_result_frame_stats(const stpc_encoder* enc, int64_t* out)
+{
+    if (!enc || !out) return STPC_ERR_ARG;
+    CK(cudaMemcpy(out, enc->fstats.p, sizeof(long long) * (size_t)enc->G * enc->n * FS_COUNT,
+                  cudaMemcpyDeviceToHost));
+    return STPC_OK;
+}
+
+int stpc_encoder_buffer(const stpc_encoder* enc, int32_t which, void** dev_ptr, int64_t* bytes)
+{
+    if (!enc || !dev_ptr) return STPC_ERR_ARG;
+    const DevBuf* b = nullptr;
+    switch (which) {
+    case STPC_BUF_BEST: b = &enc->best; break;
+    case STPC_BUF_CLS: b = &enc->cls; break;
+    case STPC_BUF_RUN_S: b = &enc->run_s; break;
+    case STPC_BUF_RUN_LEN: b = &enc->run_len; break;
+    case STPC_BUF_RUN_ABC: b = &enc->run_abc; break;
+    case STPC_BUF_N_RUNS: b = &enc->n_runs; break;
+    case STPC_BUF_REF_OK: b = &enc->ref_ok; break;
+    case STPC_BUF_REF_C: b = &enc->ref_c; break;
+    case STPC_BUF_PAYLOAD: b = &enc->payload; break;
+    case STPC_BUF_VBITS: b = &enc->vbits; break;
+    default: g_err = "unknown buffer"; return STPC_ERR_ARG;
+    }
+    *dev_ptr = b->p;
+    if (bytes) *bytes = (int64_t)b->cap;
+    return STPC_OK;
+}
+
+int stpc_project(const void* d_points, int32_t points_f64, const int64_t* point_offsets, int32_t n_frames,
+                 const double* transforms, int32_t w, int32_t h, double theta_r, double phi_r,
+                 double phi_offset, double* d_best, int64_t* d_win, int64_t* h_counts, void* stream)
+{
+    if (n_frames < 1 || w < 1 || h < 1 || !point_offsets || !transforms || !d_best || !h_counts) {
+        g_err = "invalid arguments";
+        return STPC_ERR_ARG;
+    }
+    cudaStream_t s = (cudaStream_t)stream;
+    Geometry g{};
+    g.w = w;
+    g.h = h;
+    g.P = (long long)w * h;
+    g.theta_r = theta_r;
+    g.phi_r = phi_r;
+    g.phi_offset = phi_offset;
+    long long max_pts = 0;
+    for (int f = 0; f < n_frames; ++f) max_pts = std::max<long long>(max_pts, point_offsets[f + 1] - point_offsets[f]);
+    DevBuf off, xf, fs;
+    ENS(off, sizeof(long long) * (n_frames + 1));
+    ENS(xf, sizeof(double) * 12 * n_frames);
+    ENS(fs, sizeof(long long) * FS_COUNT * n_frames);
+    CK(cudaMemcpyAsync(off.p, point_offsets, sizeof(long long) * (n_frames + 1), cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(xf.p, transforms, sizeof(double) * 12 * n_frames, cudaMemcpyHostToDevice, s));
+    CK(cudaMemsetAsync(fs.p, 0, sizeof(long long) * FS_COUNT * n_frames, s));
+    launch_fill_u64((unsigned long long*)d_best, 0x7ff0000000000000ull, n_frames * g.P, s);
+    ConvertArgs ca;
+    ca.pts = d_points;
+    ca.pts_f64 = points_f64;
+    ca.pt_off = off.as<long long>();
+    ca.xf = xf.as<double>();
+    ca.n_frames = n_frames;
+    ca.g = g;
+    ca.best = (unsigned long long*)d_best;
+    ca.win = (long long*)d_win;
+    ca.fstats = fs.as<long long>();
+    if (max_pts > 0) launch_convert(ca, (int)max_pts, s);
+    if (d_win) launch_convert_win(ca, (int)std::max<long long>(max_pts, 1), s);
+    std::vector<long long> hfs((size_t)FS_COUNT * n_frames);
+    CK(cudaMemcpyAsync(hfs.data(), fs.p, sizeof(long long) * hfs.size(), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    for (int f = 0; f < n_frames; ++f)
+        for (int j = 0; j < 3; ++j) h_counts[3 * f + j] = hfs[(size_t)f * FS_COUNT + j];
+    return STPC_OK;
+}
+
+}  // extern "C"

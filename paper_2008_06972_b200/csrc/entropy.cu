@@ -1,0 +1,388 @@
+// K3d -- the lossless stage on the device: payload byte histogram, canonical
+// Huffman code lengths, MSB-first bit packing, CRC-32 and the blob header.
+//
+// Replaces huffman.encode_bytes (np.bincount histogram :112,
+// code_lengths_from_counts :23-60, canonical_codes :63-77) and
+// huffman_encode_kernel (/root/reference/pkg/src/stpc/_kernels.py:363-382),
+// plus the header of serialize (/root/reference/pkg/src/stpc/bitstream.py:
+// 279-289, zlib.crc32).
+#include "kernels.cuh"
+
+namespace stpc {
+
+// ---------------------------------------------------------------- histogram
+// grid (chunks, groups); 256-bin shared histogram per block.
+__global__ void __launch_bounds__(256) histogram_kernel(EntropyArgs E)
+{
+    __shared__ unsigned int h[256];
+    const int grp = blockIdx.y;
+    h[threadIdx.x] = 0;
+    __syncthreads();
+    const long long len = E.payload_len[grp];
+    const uint8_t* p = E.payload + E.payload_off[grp];
+    const long long chunk = 16384;
+    long long b = (long long)blockIdx.x * chunk;
+    long long e = min(b + chunk, len);
+    for (long long i = b + threadIdx.x; i < e; i += blockDim.x) atomicAdd(&h[p[i]], 1u);
+    __syncthreads();
+    if (h[threadIdx.x]) atomicAdd(&E.hist[grp * 256 + threadIdx.x], h[threadIdx.x]);
+}
+
+void launch_histogram(const EntropyArgs& E, int max_payload, cudaStream_t s)
+{
+    if (E.G <= 0) return;
+    dim3 grid((max_payload + 16383) / 16384 > 0 ? (max_payload + 16383) / 16384 : 1, E.G);
+    STPC_LAUNCH();
+    histogram_kernel<<<grid, 256, 0, s>>>(E);
+}
+
+// ------------------------------------------------------------- code lengths
+// One warp per group.  Node keys are (weight << 10 | serial): leaves carry
+// their symbol as serial, merged nodes 256, 257, ... -- the exact (weight,
+// tiebreak) order of the reference's heapq (huffman.py:37-48).
+__global__ void __launch_bounds__(32) code_lengths_kernel(EntropyArgs E)
+{
+    __shared__ unsigned long long key[512];
+    __shared__ short parent[512];
+    __shared__ uint8_t L[256];
+    const int grp = blockIdx.x;
+    const int lane = threadIdx.x;
+    const unsigned int* hist = E.hist + grp * 256;
+    const unsigned long long INACTIVE = ~0ull;
+    int nsym = 0;
+    for (int i = lane; i < 512; i += 32) {
+        unsigned long long k = INACTIVE;
+        if (i < 256 && hist[i]) k = ((unsigned long long)hist[i] << 10) | (unsigned)i;
+        key[i] = k;
+        parent[i] = -1;
+        nsym += (i < 256 && hist[i]) ? 1 : 0;
+    }
+    for (int o = 16; o > 0; o >>= 1) nsym += __shfl_xor_sync(STPC_FULL, nsym, o);
+    __syncwarp();
+
+    for (int m = 0; m + 1 < nsym; ++m) {
+        int pick[2];
+        unsigned long long wsum = 0;
+        for (int q = 0; q < 2; ++q) {
+            unsigned long long best = INACTIVE;
+            int bi = -1;
+            for (int i = lane; i < 256 + m; i += 32) {
+                unsigned long long k = key[i];
+                if (k < best) { best = k; bi = i; }
+            }
+            for (int o = 16; o > 0; o >>= 1) {
+                unsigned long long ob = __shfl_xor_sync(STPC_FULL, best, o);
+                int oi = __shfl_xor_sync(STPC_FULL, bi, o);
+                if (ob < best) { best = ob; bi = oi; }
+            }
+            pick[q] = bi;
+            wsum += best >> 10;
+            __syncwarp();
+            if (lane == 0) key[bi] = INACTIVE;
+            __syncwarp();
+        }
+        if (lane == 0) {
+            int node = 256 + m;
+            key[node] = (wsum << 10) | (unsigned)node;
+            parent[pick[0]] = (short)node;
+            parent[pick[1]] = (short)node;
+        }
+        __syncwarp();
+    }
+    // depth = merges a leaf's subtree took part in = hops to the root
+    int maxlen = 0;
+    for (int s = lane; s < 256; s += 32) {
+        int d = 0;
+        if (hist[s]) {
+            if (nsym == 1) d = 1;
+            else
+                for (int x = parent[s]; x >= 0; x = parent[x]) ++d;
+        }
+        L[s] = (uint8_t)(d > 255 ? 255 : d);
+        maxlen = max(maxlen, d);
+    }
+    for (int o = 16; o > 0; o >>= 1) maxlen = max(maxlen, __shfl_xor_sync(STPC_FULL, maxlen, o));
+    __syncwarp();
+    if (lane == 0) {
+        if (maxlen > 32) {
+            // 32-bit cap repair (huffman.py:52-59); Kraft sum in units of 2^-32 is exact
+            unsigned long long kraft = 0;
+            for (int s = 0; s < 256; ++s) {
+                if (L[s] > 32) L[s] = 32;
+                if (L[s]) kraft += 1ull << (32 - L[s]);
+            }
+            while (kraft > (1ull << 32)) {
+                int pick = -1, pl = 0;
+                for (int s = 0; s < 256; ++s)
+                    if (L[s] > 0 && L[s] < 32 && L[s] > pl) { pl = L[s]; pick = s; }
+                kraft -= 1ull << (32 - L[pick]);
+                L[pick] += 1;
+                kraft += 1ull << (32 - L[pick]);
+            }
+        }
+        // canonical codes (huffman.py:63-77), DEFLATE-style next_code table
+        unsigned int bl[34] = {0};
+        for (int s = 0; s < 256; ++s) bl[L[s]]++;
+        unsigned long long next[34];
+        unsigned long long code = 0;
+        bl[0] = 0;
+        for (int b = 1; b <= 33; ++b) {
+            code = (code + bl[b - 1]) << 1;
+            next[b] = code;
+        }
+        unsigned long long bits = 0;
+        for (int s = 0; s < 256; ++s) {
+            int l = L[s];
+            E.lens[grp * 256 + s] = (uint8_t)l;
+            unsigned int c = 0;
+            if (l) c = (unsigned int)(next[l]++);
+            E.codes[grp * 256 + s] = c;
+            bits += (unsigned long long)hist[s] * l;
+        }
+        E.enc_len[grp] = (long long)((bits + 7) / 8);
+    }
+}
+
+void launch_code_lengths(const EntropyArgs& E, cudaStream_t s)
+{
+    if (E.G <= 0) return;
+    STPC_LAUNCH();
+    code_lengths_kernel<<<E.G, 32, 0, s>>>(E);
+}
+
+// ------------------------------------------------------------------ packing
+constexpr int PACK_THREADS = 256;
+constexpr int PACK_PER_THREAD = PACK_CHUNK / PACK_THREADS;  // 16 bytes
+
+__device__ __forceinline__ void chunk_range(const EntropyArgs& E, int grp, int c, long long& b, long long& e)
+{
+    long long len = E.payload_len[grp];
+    b = (long long)c * PACK_CHUNK;
+    e = min(b + PACK_CHUNK, len);
+}
+
+// phase A: bits per chunk
+__global__ void __launch_bounds__(PACK_THREADS) pack_count_kernel(EntropyArgs E)
+{
+    const int grp = blockIdx.y, c = blockIdx.x;
+    long long b, e;
+    chunk_range(E, grp, c, b, e);
+    if (b >= e) return;
+    __shared__ uint8_t lens[256];
+    lens[threadIdx.x] = E.lens[grp * 256 + threadIdx.x];
+    __syncthreads();
+    const uint8_t* p = E.payload + E.payload_off[grp];
+    long long bits = 0;
+    for (long long i = b + threadIdx.x; i < e; i += PACK_THREADS) bits += lens[p[i]];
+    for (int o = 16; o > 0; o >>= 1) bits += __shfl_xor_sync(STPC_FULL, bits, o);
+    __shared__ long long ws[PACK_THREADS / 32];
+    if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5] = bits;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        long long t = 0;
+        for (int w = 0; w < PACK_THREADS / 32; ++w) t += ws[w];
+        E.chunk_bits[(long long)grp * E.max_chunks + c] = t;
+    }
+}
+
+// phase B: per-group exclusive scan over chunks (block per group)
+__global__ void pack_scan_kernel(EntropyArgs E)
+{
+    const int grp = blockIdx.x;
+    long long nch = (E.payload_len[grp] + PACK_CHUNK - 1) / PACK_CHUNK;
+    if (threadIdx.x == 0) {
+        long long* cb = E.chunk_bits + (long long)grp * E.max_chunks;
+        long long run = 0;
+        for (long long c = 0; c < nch; ++c) {
+            long long v = cb[c];
+            cb[c] = run;
+            run += v;
+        }
+    }
+}
+
+// phase C: compose each chunk's bits in shared memory (big-endian u32 words),
+// store interior words, atomicOr the two boundary words shared with
+// neighbouring chunks (the encoded region is zeroed beforehand).
+__global__ void __launch_bounds__(PACK_THREADS) pack_write_kernel(EntropyArgs E)
+{
+    const int grp = blockIdx.y, c = blockIdx.x;
+    long long b, e;
+    chunk_range(E, grp, c, b, e);
+    if (b >= e) return;
+    __shared__ uint8_t lens[256];
+    __shared__ unsigned int codes[256];
+    __shared__ unsigned int buf[PACK_CHUNK + 2];  // 32 bits per byte worst case
+    __shared__ long long wsum[PACK_THREADS / 32];
+    lens[threadIdx.x] = E.lens[grp * 256 + threadIdx.x];
+    codes[threadIdx.x] = E.codes[grp * 256 + threadIdx.x];
+    for (int i = threadIdx.x; i < PACK_CHUNK + 2; i += PACK_THREADS) buf[i] = 0;
+    __syncthreads();
+    const uint8_t* p = E.payload + E.payload_off[grp];
+    const long long O = E.chunk_bits[(long long)grp * E.max_chunks + c];  // chunk's first bit
+    const int lead = (int)(O & 31);
+    // each thread owns PACK_PER_THREAD consecutive bytes
+    const long long tb = b + (long long)threadIdx.x * PACK_PER_THREAD;
+    uint8_t sym[PACK_PER_THREAD];
+    int mybits = 0;
+#pragma unroll
+    for (int q = 0; q < PACK_PER_THREAD; ++q) {
+        long long i = tb + q;
+        sym[q] = i < e ? p[i] : 0;
+        mybits += i < e ? lens[sym[q]] : 0;
+    }
+    long long inc = warp_incl_scan_ll(mybits);
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    if (lane == 31) wsum[wid] = inc;
+    __syncthreads();
+    long long wbase = 0;
+    for (int w = 0; w < wid; ++w) wbase += wsum[w];
+    long long pos = lead + wbase + inc - mybits;  // bit position in buf
+#pragma unroll
+    for (int q = 0; q < PACK_PER_THREAD; ++q) {
+        long long i = tb + q;
+        if (i >= e) break;
+        int l = lens[sym[q]];
+        unsigned long long v = (unsigned long long)codes[sym[q]] << (64 - l);  // left-aligned
+        int wi = (int)(pos >> 5), sh = (int)(pos & 31);
+        unsigned long long win = v >> sh;  // spans words wi, wi+1
+        unsigned int hi = (unsigned int)(win >> 32), lo = (unsigned int)win;
+        if (hi) atomicOr(&buf[wi], hi);
+        if (lo) atomicOr(&buf[wi + 1], lo);
+        pos += l;
+    }
+    __syncthreads();
+    long long total = 0;
+    for (int w = 0; w < PACK_THREADS / 32; ++w) total += wsum[w];
+    const int nwords = (int)((lead + total + 31) >> 5);
+    unsigned int* gw = reinterpret_cast<unsigned int*>(E.blobs + E.blob_off[grp] + HDR) + (O >> 5);
+    for (int i = threadIdx.x; i < nwords; i += PACK_THREADS) {
+        unsigned int be = buf[i];
+        unsigned int le = __byte_perm(be, 0, 0x0123);
+        if (i == 0 || i == nwords - 1) {
+            if (le) atomicOr(gw + i, le);
+        } else {
+            gw[i] = le;
+        }
+    }
+}
+
+void launch_pack(const EntropyArgs& E, cudaStream_t s)
+{
+    if (E.G <= 0 || E.max_chunks <= 0) return;
+    dim3 grid(E.max_chunks, E.G);
+    STPC_LAUNCH();
+    pack_count_kernel<<<grid, PACK_THREADS, 0, s>>>(E);
+    STPC_LAUNCH();
+    pack_scan_kernel<<<E.G, 32, 0, s>>>(E);
+    STPC_LAUNCH();
+    pack_write_kernel<<<grid, PACK_THREADS, 0, s>>>(E);
+}
+
+// --------------------------------------------------------------------- CRC
+// zlib CRC-32 (reflected 0xEDB88320).  The encoded payload is cut into
+// 256-byte pieces aligned to its END (a virtual zero prefix leaves an
+// init-0 CRC register unchanged), each piece's raw CRC is computed by one
+// thread, and pieces/segments are combined with x^(8*len) multipliers; the
+// 0xFFFFFFFF init is folded in at the end by linearity.
+__device__ __forceinline__ unsigned int multmodp(unsigned int a, unsigned int b)
+{
+    unsigned int m = 1u << 31, p = 0;
+    for (;;) {
+        if (a & m) {
+            p ^= b;
+            if ((a & (m - 1)) == 0) break;
+        }
+        m >>= 1;
+        b = b & 1 ? (b >> 1) ^ 0xedb88320u : b >> 1;
+    }
+    return p;
+}
+
+__device__ __forceinline__ unsigned int x8nmodp(unsigned long long nbytes)
+{
+    // x^(8*nbytes) mod p by square-and-multiply
+    unsigned int p = 1u << 31;      // x^0
+    unsigned int sq = 1u << 23;     // x^8
+    while (nbytes) {
+        if (nbytes & 1) p = multmodp(sq, p);
+        sq = multmodp(sq, sq);
+        nbytes >>= 1;
+    }
+    return p;
+}
+
+__device__ __forceinline__ void crc_table(unsigned int* tab)
+{
+    for (int i = threadIdx.x; i < 256; i += blockDim.x) {
+        unsigned int c = i;
+        for (int k = 0; k < 8; ++k) c = c & 1 ? (c >> 1) ^ 0xedb88320u : c >> 1;
+        tab[i] = c;
+    }
+}
+
+// grid (segments, groups), 64 threads: raw CRC per CRC_SEG-byte segment
+// (segment 0 is the LAST one).
+__global__ void __launch_bounds__(64) crc_segment_kernel(EntropyArgs E)
+{
+    __shared__ unsigned int tab[256];
+    __shared__ unsigned int pc[64];
+    crc_table(tab);
+    __syncthreads();
+    const int grp = blockIdx.y, sgi = blockIdx.x;
+    const long long L = E.enc_len[grp];
+    const long long nseg = (L + CRC_SEG - 1) / CRC_SEG;
+    if (sgi >= nseg) return;
+    const uint8_t* enc = E.blobs + E.blob_off[grp] + HDR;
+    // piece index from the end: piece pi covers [L-(pi+1)*256, L-pi*256)
+    long long pi = (long long)sgi * 64 + (63 - threadIdx.x);  // thread 0 = earliest piece
+    long long pe = L - pi * CRC_PIECE, pb = pe - CRC_PIECE;
+    unsigned int crc = 0;
+    if (pe > 0) {
+        if (pb < 0) pb = 0;
+        for (long long i = pb; i < pe; ++i) crc = tab[(crc ^ enc[i]) & 0xff] ^ (crc >> 8);
+    }
+    pc[threadIdx.x] = crc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const unsigned int X = x8nmodp(CRC_PIECE);
+        unsigned int s = 0;
+        for (int t = 0; t < 64; ++t) s = multmodp(X, s) ^ pc[t];
+        E.seg_crc[(long long)grp * E.max_segs + sgi] = s;
+    }
+}
+
+// block per group: combine segments, finish the CRC, write the header.
+__global__ void crc_finish_kernel(EntropyArgs E)
+{
+    const int grp = blockIdx.x;
+    uint8_t* blob = E.blobs + E.blob_off[grp];
+    for (int i = threadIdx.x; i < 256; i += blockDim.x) blob[28 + i] = E.lens[grp * 256 + i];
+    if (threadIdx.x != 0) return;
+    const long long L = E.enc_len[grp];
+    const long long nseg = (L + CRC_SEG - 1) / CRC_SEG;
+    const unsigned int X = x8nmodp(CRC_SEG);
+    unsigned int raw = 0;
+    for (long long sgi = nseg - 1; sgi >= 0; --sgi)
+        raw = multmodp(X, raw) ^ E.seg_crc[(long long)grp * E.max_segs + sgi];
+    unsigned int crc = ~(raw ^ multmodp(x8nmodp((unsigned long long)L), 0xffffffffu));
+    blob[0] = 'S'; blob[1] = 'T'; blob[2] = 'P'; blob[3] = 'C';
+    put_u16(blob + 4, 1);
+    put_u16(blob + 6, 0);
+    unsigned long long raw_len = (unsigned long long)E.payload_len[grp];
+    put_u32(blob + 8, (uint32_t)raw_len);
+    put_u32(blob + 12, (uint32_t)(raw_len >> 32));
+    put_u32(blob + 16, (uint32_t)L);
+    put_u32(blob + 20, (uint32_t)((unsigned long long)L >> 32));
+    put_u32(blob + 24, crc);
+}
+
+void launch_crc(const EntropyArgs& E, cudaStream_t s)
+{
+    if (E.G <= 0) return;
+    if (E.max_segs > 0) { STPC_LAUNCH(); crc_segment_kernel<<<dim3(E.max_segs, E.G), 64, 0, s>>>(E); }
+    STPC_LAUNCH();
+    crc_finish_kernel<<<E.G, 64, 0, s>>>(E);
+}
+
+}  // namespace stpc

@@ -1,0 +1,156 @@
+"""Generate tests/golden/*.npz from the REFERENCE package itself.
+
+Run in the build container (the reference is not on the GPU box):
+
+    NUMBA_CACHE_DIR=/tmp/nb python tests/golden/make_golden.py
+
+Each fixture holds the exact inputs (float32/float64 clouds, poses), the
+reference's outputs (blob bytes, project() range grid + winner indices +
+counts, Huffman code lengths) and the trig tables numpy produced here, so a
+test can tell an oracle bug from a host-libm difference.
+"""
+
+from __future__ import annotations
+
+import math
+import os
+import sys
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(os.path.dirname(HERE))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, "/root/reference/pkg/src")
+
+import stpc  # noqa: E402  (the reference)
+from stpc import huffman as ref_huffman  # noqa: E402
+from stpc.motion import RigidTransform  # noqa: E402
+from stpc.range_image import project as ref_project  # noqa: E402
+
+from paper_2008_06972_b200 import synth  # noqa: E402
+
+SMALL = synth.Sensor(360, 12, 2 * math.pi / 360, math.radians(2.2), math.radians(88.0))
+
+
+def ref_cfg(sensor, n, tau, tw, th, k=None, mode=None):
+    return stpc.CodecConfig(
+        mode=mode or ("stream" if n > 1 else "single"), tau=tau, tile_w=tw, tile_h=th,
+        res=stpc.AngularResolution(sensor.theta_r, sensor.phi_r), phi_offset=sensor.phi_offset,
+        w=sensor.w, h=sensor.h, n_frames=n, k_index=k,
+    )
+
+
+def save_case(name, clouds, poses, cfg, blob, extra=None):
+    d = {
+        "n_frames": cfg.n_frames, "k_index": cfg.k_index, "mode": cfg.mode, "tau": cfg.tau,
+        "tile_w": cfg.tile_w, "tile_h": cfg.tile_h, "theta_r": cfg.res.theta_r,
+        "phi_r": cfg.res.phi_r, "phi_offset": cfg.phi_offset, "w": cfg.w, "h": cfg.h,
+        "range_quant": cfg.range_quant,
+        "blob": np.frombuffer(blob, np.uint8),
+    }
+    for i, c in enumerate(clouds):
+        d[f"cloud{i}"] = c
+    if poses is not None:
+        d["pose_R"] = np.stack([p[0] for p in poses])
+        d["pose_T"] = np.stack([p[1] for p in poses])
+    theta = (np.arange(cfg.w, dtype=np.float64) + 0.5) * cfg.res.theta_r
+    phi = cfg.phi_offset + (np.arange(cfg.h, dtype=np.float64) + 0.5) * cfg.res.phi_r
+    d["trig"] = np.concatenate([np.sin(theta), np.cos(theta), np.sin(phi), np.cos(phi)])
+    d.update(extra or {})
+    np.savez_compressed(os.path.join(HERE, f"{name}.npz"), **d)
+    print(name, len(blob), "bytes blob")
+
+
+def compress_case(name, seed, n, tau, tw, th, k=None, sensor=SMALL, f64=False, mutate=None, **scene):
+    g = synth.make_group(seed, n, sensor, **scene)
+    clouds = [c.astype(np.float64) for c in g.clouds] if f64 else list(g.clouds)
+    if mutate:
+        clouds = mutate(clouds)
+    cfg = ref_cfg(sensor, n, tau, tw, th, k)
+    poses = [RigidTransform(R=R, T=T) for R, T in g.poses] if n > 1 else None
+    blob, rep = stpc.compress(clouds, cfg, poses=poses)
+    # the reference's per-frame projection of the transformed clouds
+    ts = stpc.poses_to_transforms(poses, cfg.k_index) if n > 1 else [RigidTransform.identity()]
+    ts = [t.round_f32() for t in ts]
+    extra = {}
+    for i, (c, t) in enumerate(zip(clouds, ts)):
+        img, win = ref_project(t.apply(c), cfg.res, cfg.w, cfg.h, cfg.phi_offset, return_indices=True)
+        extra[f"ranges{i}"] = img.ranges
+        extra[f"win{i}"] = win.astype(np.int32)
+        extra[f"counts{i}"] = np.array([img.stats.rejected_nonfinite, img.stats.dropped_fov,
+                                        img.stats.collisions], np.int64)
+    extra["fractions"] = np.array([rep.fractions["temporal"], rep.fractions["spatial"], rep.fractions["residual"]])
+    save_case(name, clouds, g.poses if n > 1 else None, cfg, blob, extra)
+
+
+def with_bad_points(clouds):
+    out = [c.copy() for c in clouds]
+    c = out[0]
+    c[3] = np.nan
+    c[7] = 0.0
+    c[11] = [0.0, 0.0, 50.0]  # straight up: outside the polar window -> dropped
+    c[13] = c[12]  # exact duplicate -> collision, first index wins
+    return out
+
+
+def with_empty_frame(clouds):
+    out = list(clouds)
+    out[0] = np.zeros((0, 3), np.float32)
+    return out
+
+
+def huffman_cases():
+    rng = np.random.default_rng(5)
+    hists = []
+    hists.append(rng.integers(0, 1000, 256))
+    h = np.zeros(256, np.int64); h[7] = 5; hists.append(h)  # single symbol
+    h = np.zeros(256, np.int64); h[[1, 200]] = [3, 3]; hists.append(h)  # tie
+    fib = [1, 1]
+    while len(fib) < 40:
+        fib.append(fib[-1] + fib[-2])
+    h = np.zeros(256, np.int64); h[:40] = fib; hists.append(h)  # depth > 32 -> cap repair
+    h = np.ones(256, np.int64); hists.append(h)
+    h = (rng.pareto(1.2, 256) * 100).astype(np.int64); hists.append(h)
+    hists = np.stack(hists)
+    lens = np.stack([ref_huffman.code_lengths_from_counts(x) for x in hists])
+    codes = np.stack([ref_huffman.canonical_codes(l) for l in lens])
+    np.savez_compressed(os.path.join(HERE, "huffman.npz"), hists=hists, lens=lens, codes=codes)
+    print("huffman", lens.max(axis=1))
+
+
+def projection_cases():
+    """The reference's own projection unit-test shapes (pkg/tests/test_range_image.py)."""
+    out = {}
+    res = stpc.AngularResolution(theta_r=np.pi / 4, phi_r=np.pi / 4)
+    cases = {
+        "k45": (np.array([[1.0, 1.0, np.sqrt(2.0)]]), res, 8, 4, 0.0),
+        "collide": (np.array([[0.0, 2.0, 0.0], [0.0, 3.0, 0.0]]), res, 8, 4, 0.0),
+        "counts": (np.array([[np.nan, 1.0, 0.0], [0.0, 0.0, 0.0], [0.0, 1.0, 5.0], [1.0, 1.0, 0.0]]),
+                   stpc.AngularResolution(0.1, 0.1), 63, 4, 1.4),
+        "random": (np.random.default_rng(20240811).uniform(-20, 20, (5000, 3)),
+                   stpc.AngularResolution(0.02, 0.02), 315, 60, 1.0),
+        "wrap": (np.array([[-1e-9, 1.0, 0.0], [1e-9, 1.0, 0.0], [-1e-300, 5.0, 0.1], [0.0, -3.0, 0.0]]),
+                 stpc.AngularResolution(2 * np.pi / 360, 0.01), 360, 300, 0.0),
+    }
+    for name, (pts, r, w, h, off) in cases.items():
+        img, win = ref_project(pts, r, w, h, off, return_indices=True)
+        out[f"{name}_pts"] = pts
+        out[f"{name}_geom"] = np.array([r.theta_r, r.phi_r, off, w, h])
+        out[f"{name}_ranges"] = img.ranges
+        out[f"{name}_win"] = win
+        out[f"{name}_counts"] = np.array([img.stats.rejected_nonfinite, img.stats.dropped_fov, img.stats.collisions])
+    np.savez_compressed(os.path.join(HERE, "projection.npz"), **out)
+    print("projection", list(cases))
+
+
+if __name__ == "__main__":
+    projection_cases()
+    huffman_cases()
+    compress_case("single_4x4", 101, 1, 0.1, 4, 4)
+    compress_case("stream3_4x4", 102, 3, 0.1, 4, 4)
+    compress_case("stream5_2x2", 103, 5, 0.2, 2, 2)
+    compress_case("stream4_8x4_k0", 104, 4, 0.05, 8, 5, k=0)
+    compress_case("single_f64_bad", 105, 1, 0.1, 4, 4, f64=True, mutate=with_bad_points)
+    compress_case("stream3_empty", 106, 3, 0.1, 4, 4, mutate=with_empty_frame)
+    compress_case("stream6_16x16", 107, 6, 0.02, 16, 16)
