@@ -15,6 +15,7 @@
 // pass resolves the winning index with an atomicMin over indices whose range
 // equals the minimum (identical to "first index wins").
 #include "kernels.cuh"
+#include "dd.cuh"
 
 namespace stpc {
 
@@ -33,6 +34,13 @@ void launch_fill_u64(unsigned long long* p, unsigned long long v, long long n, c
     int blocks = (int)std::min<long long>((n + 255) / 256, 148 * 16);
     STPC_LAUNCH();
     fill_u64_kernel<<<blocks, 256, 0, s>>>(p, v, n);
+}
+
+// Within 1e-9 (relative) of an integer: the epsilon band of SURVEY.md A.6,
+// orders of magnitude wider than the 2-ulp trig discrepancy it guards.
+__device__ __forceinline__ bool near_edge(double q)
+{
+    return fabs(q - rint(q)) <= 1e-9 * fmax(1.0, fabs(q));
 }
 
 struct Binned {
@@ -54,20 +62,29 @@ __device__ __forceinline__ Binned bin_point(double px, double py, double pz, con
     if (!(isfinite(x) && isfinite(y) && isfinite(z))) return o;
     double r = sqrt((x * x + y * y) + z * z);
     if (r <= 0.0) return o;
+    // Bin decisions: CUDA trig first; within 1e-9 of a bin edge the angle is
+    // recomputed correctly rounded (dd.cuh) so the bin matches glibc's.
     double theta = atan2(x, y);
-    if (theta < 0.0) theta += 2.0 * 3.141592653589793;
-    double qu = theta / g.theta_r;
+    double th_w = theta < 0.0 ? theta + 2.0 * 3.141592653589793 : theta;
+    double qu = th_w / g.theta_r;
+    bool eps = near_edge(qu);
+    if (eps) {
+        theta = dd::atan2_cr(x, y);
+        th_w = theta < 0.0 ? theta + 2.0 * 3.141592653589793 : theta;
+        qu = th_w / g.theta_r;
+    }
     long long u = (long long)floor(qu) % (long long)g.w;
     if (u < 0) u += g.w;
     double cz = z / r;
     if (cz > 1.0) cz = 1.0;
     else if (cz < -1.0) cz = -1.0;
     double qv = (acos(cz) - g.phi_offset) / g.phi_r;
+    if (near_edge(qv)) {
+        eps = true;
+        qv = (dd::acos_cr(cz) - g.phi_offset) / g.phi_r;
+    }
     long long v = (long long)floor(qv);
-    // epsilon band: libm vs CUDA trig may differ by a
-    // couple of ulp; count binnings within 1e-9 (relative) of a bin edge.
-    double du = fabs(qu - rint(qu)), dv = fabs(qv - rint(qv));
-    o.eps = du <= 1e-9 * fmax(1.0, fabs(qu)) || dv <= 1e-9 * fmax(1.0, fabs(qv));
+    o.eps = eps;
     if (v < 0 || v >= g.h) { o.status = 1; return o; }
     o.status = 2;
     o.pix = v * (long long)g.w + u;

@@ -105,6 +105,24 @@ def test_project_full_size_group_bit_exact(lib):
         assert np.array_equal(counts[i], oc), f"frame {i}"
 
 
+def test_project_points_on_bin_edges(lib):
+    """Points whose azimuth / polar angle sit exactly on bin edges: CUDA trig is
+    refined to the correctly rounded angle there (eps band) and must bin like
+    the oracle's glibc calls."""
+    w, h, tr, pr, off = 360, 40, 2 * np.pi / 360, 0.01, 1.3
+    th = np.arange(w) * tr
+    ph = off + np.arange(h) * pr
+    T, Ph = np.meshgrid(th, ph)
+    d = np.stack([np.sin(Ph) * np.sin(T), np.sin(Ph) * np.cos(T), np.cos(Ph)], -1).reshape(-1, 3)
+    pts = np.concatenate([r * d for r in (1.0, 7.3, 55.5)])
+    ocfg = oracle.OracleConfig("single", 0.1, 4, 4, tr, pr, off, w, h, 1, 0)
+    ob, ow, oc = oracle.convert(pts, np.eye(3), np.zeros(3), ocfg)
+    best, win, counts = gpu_project(lib, [pts], [(np.eye(3), np.zeros(3))], w, h, tr, pr, off, f64=True)
+    assert np.array_equal(best[0].view(np.uint64), ob.view(np.uint64))
+    assert np.array_equal(win[0], ow)
+    assert np.array_equal(counts[0], oc)
+
+
 # ------------------------------------------------------------- whole pipeline
 
 
@@ -118,9 +136,9 @@ def test_golden_blob(name):
         assert mine == blob
     else:  # host libm differs from the fixture host: compare with the oracle here
         assert mine == oracle.compress(clouds, cfg, poses)[0]
-    fr = z["fractions"]
-    assert rep.fractions["temporal"] == pytest.approx(fr[0], abs=0) or not trig_matches_host(z, cfg)
-    assert rep.fractions["residual"] == pytest.approx(fr[2], abs=0) or not trig_matches_host(z, cfg)
+    if trig_matches_host(z, cfg):
+        fr = z["fractions"]
+        assert (rep.fractions["temporal"], rep.fractions["spatial"], rep.fractions["residual"]) == tuple(fr)
 
 
 def _cfg(sensor, n, tau, tile):
