@@ -109,32 +109,144 @@ __device__ __forceinline__ void warp_add_stats(long long* fs, int rej, int drop,
     }
 }
 
+// Fast bin decision in fp32 (SURVEY.md §7 "K1 convert").  The fp32 angles are
+// within ~6e-7 rad of the true ones (input rounding 2^-24 relative, atan2f
+// <= 2 ulp of a result <= pi); whenever both angles lie more than
+// FAST_MARGIN = 1e-5 rad from a bin edge the floor is therefore the same as
+// the reference's fp64 (glibc) floor and the point is binned here.  The ~1%
+// of points inside the margin (and any point with coordinates outside
+// [1e-15, 1e15]) go to the exact fp64 path.  Returns false when undecided.
+constexpr double FAST_MARGIN = 1e-5;
+
+__device__ __forceinline__ bool fast_bin(double x, double y, double z, const Geometry& g, double inv_tr,
+                                         double inv_pr, long long& u, long long& v)
+{
+    double m = fmax(fabs(x), fmax(fabs(y), fabs(z)));
+    if (!(m < 1e15 && m > 1e-15)) return false;
+    float xf = (float)x, yf = (float)y, zf = (float)z;
+    double th = (double)atan2f(xf, yf);
+    if (th < 0.0) th += 2.0 * 3.141592653589793;
+    double qu = th * inv_tr;
+    double ph = (double)atan2f(sqrtf(xf * xf + yf * yf), zf);
+    double qv = (ph - g.phi_offset) * inv_pr;
+    double fu = qu - floor(qu), fv = qv - floor(qv);
+    double mu = FAST_MARGIN * inv_tr, mv = FAST_MARGIN * inv_pr;
+    if (fu < mu || fu > 1.0 - mu || fv < mv || fv > 1.0 - mv) return false;
+    u = (long long)floor(qu) % (long long)g.w;
+    if (u < 0) u += g.w;
+    v = (long long)floor(qv);
+    return true;
+}
+
 // grid: (x blocks striding over a frame's points, y = frame)
 template <class T>
-__global__ void __launch_bounds__(256) convert_kernel(ConvertArgs a, const T* pts)
+__global__ void __launch_bounds__(256, 4) convert_kernel(ConvertArgs a, const T* pts)
 {
     const int f = blockIdx.y;
+    const int lane = threadIdx.x & 31;
     const long long b = a.pt_off[f], e = a.pt_off[f + 1];
     __shared__ double xf[12];
     if (threadIdx.x < 12) xf[threadIdx.x] = a.xf[12 * f + threadIdx.x];
     __syncthreads();
     unsigned long long* best = a.best + (long long)f * a.g.P;
+    const double inv_tr = 1.0 / a.g.theta_r, inv_pr = 1.0 / a.g.phi_r;
     int rej = 0, drop = 0, kept = 0, eps = 0;
     const long long stride = (long long)gridDim.x * blockDim.x;
-    // loop trip count is warp-uniform so the warp reductions below stay converged
+    // loop trip count is warp-uniform so the warp collectives below stay converged
     for (long long base = b + (long long)blockIdx.x * blockDim.x; base < e; base += stride) {
         long long i = base + threadIdx.x;
+        bool slow = false;
         if (i < e) {
             const T* p = pts + 3 * i;
-            Binned o = bin_point((double)__ldg(p), (double)__ldg(p + 1), (double)__ldg(p + 2), xf, xf + 9, a.g);
-            rej += o.status == 0;
-            drop += o.status == 1;
-            kept += o.status == 2;
-            eps += o.eps;
-            if (o.status == 2) atomicMin(best + o.pix, (unsigned long long)__double_as_longlong(o.r));
+            double px = (double)__ldg(p), py = (double)__ldg(p + 1), pz = (double)__ldg(p + 2);
+            double x = ((px * xf[0] + py * xf[1]) + pz * xf[2]) + xf[9];
+            double y = ((px * xf[3] + py * xf[4]) + pz * xf[5]) + xf[10];
+            double z = ((px * xf[6] + py * xf[7]) + pz * xf[8]) + xf[11];
+            if (!(isfinite(x) && isfinite(y) && isfinite(z))) {
+                rej += 1;
+            } else {
+                double r = sqrt((x * x + y * y) + z * z);
+                long long u, v;
+                if (r <= 0.0) {
+                    rej += 1;
+                } else if (isfinite(r) && fast_bin(x, y, z, a.g, inv_tr, inv_pr, u, v)) {
+                    if (v < 0 || v >= a.g.h) {
+                        drop += 1;
+                    } else {
+                        kept += 1;
+                        atomicMin(best + v * (long long)a.g.w + u, (unsigned long long)__double_as_longlong(r));
+                    }
+                } else {
+                    slow = true;
+                }
+            }
+        }
+        // warp-aggregated append of undecided points to the exact-path queue
+        uint32_t sm = __ballot_sync(STPC_FULL, slow);
+        if (sm) {
+            unsigned long long qb = 0;
+            if (lane == 0) qb = atomicAdd(a.q_count, (unsigned long long)__popc(sm));
+            qb = __shfl_sync(STPC_FULL, qb, 0);
+            if (slow) {
+                unsigned long long qi = qb + __popc(sm & ((1u << lane) - 1u));
+                if (qi < (unsigned long long)a.q_cap) {  // else: overflow re-pass below
+                    a.q_idx[qi] = i;
+                    a.q_frame[qi] = f;
+                }
+            }
         }
     }
     warp_add_stats(a.fstats + (long long)f * FS_COUNT, rej, drop, kept, eps);
+}
+
+__device__ __forceinline__ void exact_point(const ConvertArgs& a, double px, double py, double pz, int f)
+{
+    const double* xf = a.xf + 12 * f;
+    Binned o = bin_point(px, py, pz, xf, xf + 9, a.g);
+    long long* fs = a.fstats + (long long)f * FS_COUNT;
+    atomicAdd((unsigned long long*)&fs[o.status == 0 ? FS_REJECTED : o.status == 1 ? FS_DROPPED : FS_KEPT], 1ull);
+    if (o.eps) atomicAdd((unsigned long long*)&fs[FS_EPS_BAND], 1ull);
+    if (o.status == 2)
+        atomicMin(a.best + (long long)f * a.g.P + o.pix, (unsigned long long)__double_as_longlong(o.r));
+}
+
+// Queue overflow (more than q_cap undecided points): the queue is discarded and
+// every undecided point is re-derived here.  grid as convert_kernel.
+template <class T>
+__global__ void __launch_bounds__(256) convert_overflow_kernel(ConvertArgs a, const T* pts)
+{
+    if (*a.q_count <= (unsigned long long)a.q_cap) return;
+    const int f = blockIdx.y;
+    const long long b = a.pt_off[f], e = a.pt_off[f + 1];
+    const double* xf = a.xf + 12 * f;
+    const double inv_tr = 1.0 / a.g.theta_r, inv_pr = 1.0 / a.g.phi_r;
+    for (long long i = b + (long long)blockIdx.x * blockDim.x + threadIdx.x; i < e; i += (long long)gridDim.x * blockDim.x) {
+        const T* p = pts + 3 * i;
+        double px = (double)p[0], py = (double)p[1], pz = (double)p[2];
+        double x = ((px * xf[0] + py * xf[1]) + pz * xf[2]) + xf[9];
+        double y = ((px * xf[3] + py * xf[4]) + pz * xf[5]) + xf[10];
+        double z = ((px * xf[6] + py * xf[7]) + pz * xf[8]) + xf[11];
+        if (!(isfinite(x) && isfinite(y) && isfinite(z))) continue;
+        double r = sqrt((x * x + y * y) + z * z);
+        long long u, v;
+        if (r <= 0.0 || (isfinite(r) && fast_bin(x, y, z, a.g, inv_tr, inv_pr, u, v))) continue;
+        exact_point(a, px, py, pz, f);
+    }
+}
+
+// Exact fp64 path (CUDA atan2/acos + correctly rounded refinement in the eps
+// band) for the queued points.
+template <class T>
+__global__ void __launch_bounds__(256) convert_exact_kernel(ConvertArgs a, const T* pts)
+{
+    const unsigned long long qn = *a.q_count;
+    if (qn > (unsigned long long)a.q_cap) return;  // overflow re-pass handles them
+    const long long n = (long long)qn;
+    for (long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x; q < n; q += (long long)gridDim.x * blockDim.x) {
+        const long long i = a.q_idx[q];
+        const T* p = pts + 3 * i;
+        exact_point(a, (double)p[0], (double)p[1], (double)p[2], a.q_frame[q]);
+    }
 }
 
 template <class T>
@@ -176,11 +288,22 @@ static dim3 convert_grid(int max_pts, int n_frames)
 void launch_convert(const ConvertArgs& a, int max_pts, cudaStream_t s)
 {
     if (a.n_frames <= 0) return;
+    cudaMemsetAsync(a.q_count, 0, sizeof(unsigned long long), s);
     STPC_LAUNCH();
     if (a.pts_f64)
         convert_kernel<double><<<convert_grid(max_pts, a.n_frames), 256, 0, s>>>(a, (const double*)a.pts);
     else
         convert_kernel<float><<<convert_grid(max_pts, a.n_frames), 256, 0, s>>>(a, (const float*)a.pts);
+    STPC_LAUNCH();
+    if (a.pts_f64)
+        convert_exact_kernel<double><<<148 * 4, 256, 0, s>>>(a, (const double*)a.pts);
+    else
+        convert_exact_kernel<float><<<148 * 4, 256, 0, s>>>(a, (const float*)a.pts);
+    STPC_LAUNCH();
+    if (a.pts_f64)
+        convert_overflow_kernel<double><<<convert_grid(max_pts, a.n_frames), 256, 0, s>>>(a, (const double*)a.pts);
+    else
+        convert_overflow_kernel<float><<<convert_grid(max_pts, a.n_frames), 256, 0, s>>>(a, (const float*)a.pts);
 }
 
 void launch_convert_win(const ConvertArgs& a, int max_pts, cudaStream_t s)

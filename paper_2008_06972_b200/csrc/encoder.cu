@@ -95,6 +95,7 @@ struct stpc_encoder {
     DevBuf cfg_bytes;
     // inputs
     DevBuf pts, pt_off, xf;
+    DevBuf q_count, q_idx, q_frame;  // convert's exact-path queue
     HostBuf h_stage;  // pinned staging: pt_off | xf
     // frame level
     DevBuf best, vbits, ebits, cls, fstats;
@@ -334,6 +335,17 @@ static int encode_impl(stpc_encoder* e, int G, const void* d_points, const int64
     ca.best = e->best.as<unsigned long long>();
     ca.win = nullptr;
     ca.fstats = e->fstats.as<long long>();
+    {
+        long long npts = h_off[F] - h_off[0];
+        long long cap = npts / 8 + 4096;
+        ENS(e->q_count, sizeof(unsigned long long));
+        ENS(e->q_idx, sizeof(long long) * cap);
+        ENS(e->q_frame, sizeof(int) * cap);
+        ca.q_count = e->q_count.as<unsigned long long>();
+        ca.q_idx = e->q_idx.as<long long>();
+        ca.q_frame = e->q_frame.as<int>();
+        ca.q_cap = cap;
+    }
     launch_convert(ca, (int)max_pts, s);
     e->mark(ST_BITMAP, s);
     launch_bitmaps(e->best.as<double>(), (int)F, g, e->cfg.range_quant, e->vbits.as<uint8_t>(),
@@ -361,7 +373,7 @@ static int encode_impl(stpc_encoder* e, int G, const void* d_points, const int64
     launch_fit_rows(fa, s);
 
     RefitArgs ra;
-    ra.best = fa.best;
+    ra.best = e->best.as<double>();
     ra.tg = tg;
     ra.g = g;
     ra.tau = fa.tau;
@@ -635,7 +647,12 @@ int stpc_project(const void* d_points, int32_t points_f64, const int64_t* point_
     g.phi_offset = phi_offset;
     long long max_pts = 0;
     for (int f = 0; f < n_frames; ++f) max_pts = std::max<long long>(max_pts, point_offsets[f + 1] - point_offsets[f]);
-    DevBuf off, xf, fs;
+    DevBuf off, xf, fs, qc, qi, qf;
+    long long npts = point_offsets[n_frames] - point_offsets[0];
+    long long cap = npts / 8 + 4096;
+    ENS(qc, sizeof(unsigned long long));
+    ENS(qi, sizeof(long long) * cap);
+    ENS(qf, sizeof(int) * cap);
     ENS(off, sizeof(long long) * (n_frames + 1));
     ENS(xf, sizeof(double) * 12 * n_frames);
     ENS(fs, sizeof(long long) * FS_COUNT * n_frames);
@@ -653,6 +670,10 @@ int stpc_project(const void* d_points, int32_t points_f64, const int64_t* point_
     ca.best = (unsigned long long*)d_best;
     ca.win = (long long*)d_win;
     ca.fstats = fs.as<long long>();
+    ca.q_count = qc.as<unsigned long long>();
+    ca.q_idx = qi.as<long long>();
+    ca.q_frame = qf.as<int>();
+    ca.q_cap = cap;
     if (max_pts > 0) launch_convert(ca, (int)max_pts, s);
     if (d_win) launch_convert_win(ca, (int)std::max<long long>(max_pts, 1), s);
     std::vector<long long> hfs((size_t)FS_COUNT * n_frames);

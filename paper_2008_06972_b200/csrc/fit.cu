@@ -9,40 +9,47 @@
 // One warp owns one (frame, tile-row) chain; the chain is inherently
 // sequential (each decision changes the next union), so parallelism comes
 // from the many chains of a batch and from the lanes inside each step:
-//   * moments: lanes compute x, y, z of up to 32 pixels at once; the 9 running
-//     sums (lane k owns sum k) then fold the pixels in raster order through
-//     shuffles -- the reference's rounding sequence, not a tree (SURVEY.md
-//     §0 item 3: a shuffle tree flips run decisions);
+//   * moments: lanes compute the 9 products of up to 32 pixels at once and
+//     transpose them through shared memory; lane k then folds sum k over the
+//     pixels in raster order -- the reference's rounding sequence, not a tree
+//     (a shuffle tree flips run decisions).  Invalid
+//     pixels contribute +0.0, which is exact: a running sum that starts at
+//     +0.0 can never become -0.0 under round-to-nearest, and s + 0.0 == s;
 //   * union re-test: order-independent AND over pixels, 32 lanes at a time
 //     with an early-out vote (the reference's early return gives the same
 //     verdict);
 //   * the 3x3 solve runs redundantly in every lane (warp-uniform branches).
+// Pass 2's `remaining` mask (valid & ~temporally covered) is realised by the
+// refit kernel overwriting covered P-frame pixels with +inf (= invalid), so
+// the fit needs no per-pixel exclusion test.
 #include "kernels.cuh"
 
 namespace stpc {
 
+constexpr int FIT_WARPS = 4;  // warps per block
+
 struct Chain {
-    const double* img;    // frame's best grid
+    const double* img;    // frame's best grid (covered pixels already +inf in pass 2)
     const uint8_t* crow;  // tile classes of this tile-row
-    int excl;             // class value that masks a tile out (-1: none)
+    bool skip1;           // pass 2: tiles of class 1 are fully masked
     int v0, rows;
 };
 
-// Fold the valid pixels of tile t onto the lane-owned running sums.
-// Returns the tile's valid pixel count (warp-uniform).
+// Fold the valid pixels of tile t onto the lane-owned running sums (lane k<9
+// owns sum k; lanes >= 9 shadow sum 8).  Returns the valid count (uniform).
 __device__ __forceinline__ int fold_tile(const Chain& ch, const Geometry& g, const Trig& tg, int t,
-                                         int psel, int qsel, double& acc)
+                                         double* sm, double& acc)
 {
-    if (ch.excl >= 0 && ch.crow[t] == ch.excl) return 0;
+    if (ch.skip1 && ch.crow[t] == 1) return 0;
     const int lane = threadIdx.x & 31;
+    const int kk = lane < 9 ? lane : 8;
     const int u0 = t * g.tw;
     const int cols = min(g.tw, g.w - u0);
     const int npx = ch.rows * cols;
     int cnt = 0;
     for (int base = 0; base < npx; base += 32) {
         int p = base + lane;
-        double x = 0.0, y = 0.0, z = 0.0;
-        bool valid = false;
+        double x = 0.0, y = 0.0, z = 0.0, one = 0.0;
         if (p < npx) {
             int v = ch.v0 + p / cols;
             int u = u0 + p % cols;
@@ -53,19 +60,25 @@ __device__ __forceinline__ int fold_tile(const Chain& ch, const Geometry& g, con
                 x = r * dx;
                 y = r * dy;
                 z = r * dz;
-                valid = true;
+                one = 1.0;
             }
         }
-        uint32_t m = __ballot_sync(STPC_FULL, valid);
-        cnt += __popc(m);
-        while (m) {
-            int j = __ffs(m) - 1;
-            m &= m - 1;
-            double xj = shfl_d(x, j), yj = shfl_d(y, j), zj = shfl_d(z, j);
-            double P = psel == 0 ? xj : psel == 1 ? yj : psel == 2 ? zj : 1.0;
-            double Q = qsel == 0 ? xj : qsel == 1 ? yj : qsel == 2 ? zj : 1.0;
-            acc += P * Q;  // y*1.0 == y and 1.0*1.0 == 1.0 exactly
-        }
+        cnt += __popc(__ballot_sync(STPC_FULL, one != 0.0));
+        double* row = sm + lane * 9;
+        row[0] = y * y;
+        row[1] = y * z;
+        row[2] = z * z;
+        row[3] = y;
+        row[4] = z;
+        row[5] = x * y;
+        row[6] = x * z;
+        row[7] = x;
+        row[8] = one;
+        __syncwarp();
+        const int nj = min(32, npx - base);
+#pragma unroll 4
+        for (int j = 0; j < nj; ++j) acc += sm[j * 9 + kk];
+        __syncwarp();
     }
     return cnt;
 }
@@ -86,8 +99,7 @@ __device__ __forceinline__ bool span_fits(const Chain& ch, const Geometry& g, co
             int v = ch.v0 + p / U;
             int u = U0 + p % U;
             double r = ch.img[(long long)v * g.w + u];
-            bool valid = isfinite(r) && !(ch.excl >= 0 && ch.crow[u / g.tw] == ch.excl);
-            if (valid) {
+            if (isfinite(r)) {
                 double dx, dy, dz;
                 ray_dir(tg, v, u, dx, dy, dz);
                 bad = !pixel_fits(r, dx, dy, dz, a, b, c, tau, r_max);
@@ -110,11 +122,13 @@ __device__ __forceinline__ bool solve_round(double acc, double cond_limit, doubl
     return true;
 }
 
-__global__ void __launch_bounds__(128) fit_rows_kernel(FitArgs A)
+__global__ void __launch_bounds__(FIT_WARPS * 32, 6) fit_rows_kernel(FitArgs A)
 {
+    __shared__ double smem[FIT_WARPS][32 * 9];
     const Geometry& g = A.g;
     const int lane = threadIdx.x & 31;
-    const long long wid = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    const int wib = threadIdx.x >> 5;
+    const long long wid = (long long)blockIdx.x * FIT_WARPS + wib;
     if (wid >= (long long)A.n_jobs * g.ty) return;
     const int job = (int)(wid / g.ty);
     const int tr = (int)(wid % g.ty);
@@ -131,16 +145,11 @@ __global__ void __launch_bounds__(128) fit_rows_kernel(FitArgs A)
     ch.img = A.best + (long long)frame * g.P;
     uint8_t* crow = A.cls + slot * g.tx;
     ch.crow = crow;
-    ch.excl = A.mode == 0 ? -1 : 1;
+    ch.skip1 = A.mode != 0;
     ch.v0 = tr * g.th;
     ch.rows = min(g.th, g.h - ch.v0);
     const uint8_t run_cls = A.mode == 0 ? 1 : 2;
-
-    // lane k accumulates sum k of [Syy, Syz, Szz, Sy, Sz, Sxy, Sxz, Sx, N]
-    const int PS[9] = {1, 1, 2, 1, 2, 0, 0, 0, 3};
-    const int QS[9] = {1, 2, 2, 3, 3, 1, 2, 3, 3};
-    const int psel = lane < 9 ? PS[lane] : 3;
-    const int qsel = lane < 9 ? QS[lane] : 3;
+    double* sm = smem[wib];
 
     uint16_t* rs = A.run_s + slot * g.tx;
     uint16_t* rl = A.run_len + slot * g.tx;
@@ -149,14 +158,14 @@ __global__ void __launch_bounds__(128) fit_rows_kernel(FitArgs A)
     int t = 0;
     while (t < g.tx) {
         double acc = 0.0;
-        int cnt = fold_tile(ch, g, A.tg, t, psel, qsel, acc);
+        int cnt = fold_tile(ch, g, A.tg, t, sm, acc);
         bool ok = false;
         double a = 0.0, b = 0.0, c = 0.0;
         if (cnt >= 3) {  // sums[8] >= 3.0
             ok = solve_round(acc, A.cond_limit, a, b, c);
             if (ok) ok = span_fits(ch, g, A.tg, t, t + 1, a, b, c, A.tau, A.r_max);
         }
-        if (!ok) {  // residual tile (class 0 stays; excluded tiles keep theirs)
+        if (!ok) {  // residual tile (class 0 stays; covered tiles keep class 1)
             t += 1;
             continue;
         }
@@ -164,7 +173,7 @@ __global__ void __launch_bounds__(128) fit_rows_kernel(FitArgs A)
         int e = t + 1;
         while (e < g.tx) {
             double saved = acc;
-            int add = fold_tile(ch, g, A.tg, e, psel, qsel, acc);
+            int add = fold_tile(ch, g, A.tg, e, sm, acc);
             if (add == 0) {  // unchanged sums -> same plane -> same verdict
                 e += 1;
                 continue;
@@ -187,7 +196,7 @@ __global__ void __launch_bounds__(128) fit_rows_kernel(FitArgs A)
             rabc[3 * n_runs + 2] = (float)c;
         }
         for (int tt = s + lane; tt < e; tt += 32)
-            if (!(ch.excl >= 0 && crow[tt] == ch.excl)) crow[tt] = run_cls;
+            if (!(ch.skip1 && crow[tt] == 1)) crow[tt] = run_cls;
         n_runs += 1;
         t = e;
     }
@@ -199,16 +208,20 @@ void launch_fit_rows(const FitArgs& a, cudaStream_t s)
     long long warps = (long long)a.n_jobs * a.g.ty;
     if (warps <= 0) return;
     STPC_LAUNCH();
-    fit_rows_kernel<<<(unsigned)((warps + 3) / 4), 128, 0, s>>>(a);
+    fit_rows_kernel<<<(unsigned)((warps + FIT_WARPS - 1) / FIT_WARPS), FIT_WARPS * 32, 0, s>>>(a);
 }
 
 // K3a: one warp per key-frame chain; for each of its runs and each P channel,
 // c' = f32(mean over valid span pixels of r * (d . n)), folded v-major over the
 // whole span in the reference's order, then the span re-test with (a, b, c').
+// Spans that pass mark their tiles class 1 in the channel and poison the
+// channel's pixels there (+inf) for pass 2.
 __global__ void __launch_bounds__(128) refit_kernel(RefitArgs A)
 {
+    __shared__ double smem[4][32];
     const Geometry& g = A.g;
     const int lane = threadIdx.x & 31;
+    double* sm = smem[threadIdx.x >> 5];
     const long long kc = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
     if (kc >= (long long)A.n_groups * g.ty) return;
     const int grp = (int)(kc / g.ty);
@@ -234,7 +247,7 @@ __global__ void __launch_bounds__(128) refit_kernel(RefitArgs A)
         for (int chn = 0; chn < A.n; ++chn) {
             if (chn == A.k) continue;
             const int frame = grp * A.n + chn;
-            const double* img = A.best + (long long)frame * g.P;
+            double* img = A.best + (long long)frame * g.P;
             double acc = 0.0;
             int cnt = 0;
             for (int base = 0; base < npx; base += 32) {
@@ -253,13 +266,13 @@ __global__ void __launch_bounds__(128) refit_kernel(RefitArgs A)
                         valid = true;
                     }
                 }
-                uint32_t m = __ballot_sync(STPC_FULL, valid);
-                cnt += __popc(m);
-                while (m) {
-                    int jj = __ffs(m) - 1;
-                    m &= m - 1;
-                    acc += shfl_d(prod, jj);
-                }
+                cnt += __popc(__ballot_sync(STPC_FULL, valid));
+                sm[lane] = prod;  // +0.0 for invalid pixels: exact (see fit_rows)
+                __syncwarp();
+                const int nj = min(32, npx - base);
+#pragma unroll 8
+                for (int jj = 0; jj < nj; ++jj) acc += sm[jj];
+                __syncwarp();
             }
             bool ok = false;
             double c = 0.0;
@@ -290,6 +303,11 @@ __global__ void __launch_bounds__(128) refit_kernel(RefitArgs A)
                 present += 1;
                 uint8_t* crow = A.cls + ((long long)frame * g.ty + tr) * g.tx;
                 for (int tt = s + lane; tt < s + len; tt += 32) crow[tt] = 1;
+                for (int p = lane; p < npx; p += 32) {
+                    int v = v0 + p / U;
+                    int u = U0 + p % U;
+                    img[(long long)v * g.w + u] = __longlong_as_double(0x7ff0000000000000ll);
+                }
             }
         }
         if (lane == 0) okv[A.k] = 1;

@@ -52,6 +52,11 @@ struct ConvertArgs {
     unsigned long long* best;  // [F][P] as u64 bit patterns
     long long* win;            // nullable [F][P]
     long long* fstats;         // [F][FS_COUNT]
+    // exact-path queue of points the fp32 fast path could not decide
+    unsigned long long* q_count;
+    long long* q_idx;
+    int* q_frame;
+    long long q_cap;
 };
 
 void launch_fill_u64(unsigned long long* p, unsigned long long v, long long n, cudaStream_t s);
@@ -77,7 +82,7 @@ struct FitArgs {
 void launch_fit_rows(const FitArgs& a, cudaStream_t s);
 
 struct RefitArgs {
-    const double* best;
+    double* best;  // covered P-frame pixels are overwritten with +inf
     Trig tg;
     Geometry g;
     double tau, r_max;

@@ -123,6 +123,23 @@ def test_project_points_on_bin_edges(lib):
     assert np.array_equal(counts[0], oc)
 
 
+def test_project_fine_bins_exact_path_overflow(lib, rng):
+    """Bins narrower than the fp32 fast path's margin: every point takes the
+    exact fp64 path and the deferral queue overflows into the re-pass."""
+    w, h, tr, pr, off = 600000, 3, 2 * np.pi / 600000, 2e-5, np.pi / 2 - 3e-5
+    n = 60000
+    th = rng.uniform(0, 2 * np.pi, n)
+    ph = off + rng.uniform(0, h * pr, n)
+    r = rng.uniform(1, 90, n)
+    pts = np.stack([r * np.sin(ph) * np.sin(th), r * np.sin(ph) * np.cos(th), r * np.cos(ph)], 1)
+    ocfg = oracle.OracleConfig("single", 0.1, 4, 1, tr, pr, off, w, h, 1, 0)
+    ob, ow, oc = oracle.convert(pts.astype(np.float32), np.eye(3), np.zeros(3), ocfg)
+    best, win, counts = gpu_project(lib, [pts.astype(np.float32)], [(np.eye(3), np.zeros(3))], w, h, tr, pr, off)
+    assert np.array_equal(best[0].view(np.uint64), ob.view(np.uint64))
+    assert np.array_equal(win[0], ow)
+    assert np.array_equal(counts[0], oc)
+
+
 # ------------------------------------------------------------- whole pipeline
 
 
