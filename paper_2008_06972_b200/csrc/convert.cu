@@ -129,74 +129,111 @@ __device__ __forceinline__ bool fast_bin(double x, double y, double z, const Geo
     double qu = th * inv_tr;
     double ph = (double)atan2f(sqrtf(xf * xf + yf * yf), zf);
     double qv = (ph - g.phi_offset) * inv_pr;
-    double fu = qu - floor(qu), fv = qv - floor(qv);
+    double flu = floor(qu), flv = floor(qv);
+    double fu = qu - flu, fv = qv - flv;
     double mu = FAST_MARGIN * inv_tr, mv = FAST_MARGIN * inv_pr;
     if (fu < mu || fu > 1.0 - mu || fv < mv || fv > 1.0 - mv) return false;
-    u = (long long)floor(qu) % (long long)g.w;
-    if (u < 0) u += g.w;
-    v = (long long)floor(qv);
+    long long uq = (long long)flu;  // qu >= 0
+    u = uq < g.w ? uq : uq % (long long)g.w;
+    v = (long long)flv;
     return true;
 }
 
-// grid: (x blocks striding over a frame's points, y = frame)
+// Points per thread: loads for all of them are issued before any binning.
+template <class T> struct PPT { static constexpr int value = 8; };
+template <> struct PPT<double> { static constexpr int value = 4; };
+
+// grid: (x = chunks of 256*PPT points of a frame, y = frame)
 template <class T>
 __global__ void __launch_bounds__(256, 4) convert_kernel(ConvertArgs a, const T* pts)
 {
-    const int f = blockIdx.y;
-    const int lane = threadIdx.x & 31;
-    const long long b = a.pt_off[f], e = a.pt_off[f + 1];
+    constexpr int K = PPT<T>::value;
+    constexpr int CH = 256 * K;
     __shared__ double xf[12];
+    __shared__ int q_local[CH];
+    __shared__ int q_n;
+    __shared__ unsigned long long q_base;
+    __shared__ int stat[4];
+    const int f = blockIdx.y;
+    const long long b = a.pt_off[f], e = a.pt_off[f + 1];
+    const long long cb = b + (long long)blockIdx.x * CH;
+    if (cb >= e) return;
     if (threadIdx.x < 12) xf[threadIdx.x] = a.xf[12 * f + threadIdx.x];
+    if (threadIdx.x < 4) stat[threadIdx.x] = 0;
+    if (threadIdx.x == 0) q_n = 0;
+    // issue every load of this thread's points first
+    T px[K], py[K], pz[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+        long long i = cb + k * 256 + threadIdx.x;
+        if (i < e) {
+            const T* p = pts + 3 * i;
+            px[k] = __ldg(p);
+            py[k] = __ldg(p + 1);
+            pz[k] = __ldg(p + 2);
+        }
+    }
     __syncthreads();
     unsigned long long* best = a.best + (long long)f * a.g.P;
     const double inv_tr = 1.0 / a.g.theta_r, inv_pr = 1.0 / a.g.phi_r;
-    int rej = 0, drop = 0, kept = 0, eps = 0;
-    const long long stride = (long long)gridDim.x * blockDim.x;
-    // loop trip count is warp-uniform so the warp collectives below stay converged
-    for (long long base = b + (long long)blockIdx.x * blockDim.x; base < e; base += stride) {
-        long long i = base + threadIdx.x;
-        bool slow = false;
-        if (i < e) {
-            const T* p = pts + 3 * i;
-            double px = (double)__ldg(p), py = (double)__ldg(p + 1), pz = (double)__ldg(p + 2);
-            double x = ((px * xf[0] + py * xf[1]) + pz * xf[2]) + xf[9];
-            double y = ((px * xf[3] + py * xf[4]) + pz * xf[5]) + xf[10];
-            double z = ((px * xf[6] + py * xf[7]) + pz * xf[8]) + xf[11];
-            if (!(isfinite(x) && isfinite(y) && isfinite(z))) {
-                rej += 1;
-            } else {
-                double r = sqrt((x * x + y * y) + z * z);
-                long long u, v;
-                if (r <= 0.0) {
-                    rej += 1;
-                } else if (isfinite(r) && fast_bin(x, y, z, a.g, inv_tr, inv_pr, u, v)) {
-                    if (v < 0 || v >= a.g.h) {
-                        drop += 1;
-                    } else {
-                        kept += 1;
-                        atomicMin(best + v * (long long)a.g.w + u, (unsigned long long)__double_as_longlong(r));
-                    }
-                } else {
-                    slow = true;
-                }
-            }
+    int rej = 0, drop = 0, kept = 0;
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+        long long i = cb + k * 256 + threadIdx.x;
+        if (i >= e) continue;
+        double qx = (double)px[k], qy = (double)py[k], qz = (double)pz[k];
+        double x = ((qx * xf[0] + qy * xf[1]) + qz * xf[2]) + xf[9];
+        double y = ((qx * xf[3] + qy * xf[4]) + qz * xf[5]) + xf[10];
+        double z = ((qx * xf[6] + qy * xf[7]) + qz * xf[8]) + xf[11];
+        if (!(isfinite(x) && isfinite(y) && isfinite(z))) {
+            rej += 1;
+            continue;
         }
-        // warp-aggregated append of undecided points to the exact-path queue
-        uint32_t sm = __ballot_sync(STPC_FULL, slow);
-        if (sm) {
-            unsigned long long qb = 0;
-            if (lane == 0) qb = atomicAdd(a.q_count, (unsigned long long)__popc(sm));
-            qb = __shfl_sync(STPC_FULL, qb, 0);
-            if (slow) {
-                unsigned long long qi = qb + __popc(sm & ((1u << lane) - 1u));
-                if (qi < (unsigned long long)a.q_cap) {  // else: overflow re-pass below
-                    a.q_idx[qi] = i;
-                    a.q_frame[qi] = f;
-                }
+        double r = sqrt((x * x + y * y) + z * z);
+        long long u, v;
+        if (r <= 0.0) {
+            rej += 1;
+        } else if (isfinite(r) && fast_bin(x, y, z, a.g, inv_tr, inv_pr, u, v)) {
+            if (v < 0 || v >= a.g.h) {
+                drop += 1;
+            } else {
+                kept += 1;
+                atomicMin(best + v * (long long)a.g.w + u, (unsigned long long)__double_as_longlong(r));
             }
+        } else {  // undecided: block-local queue
+            int slot = atomicAdd(&q_n, 1);
+            q_local[slot] = (int)(i - cb);
         }
     }
-    warp_add_stats(a.fstats + (long long)f * FS_COUNT, rej, drop, kept, eps);
+    // block-level stats and one global reservation for the queued points
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        rej += __shfl_xor_sync(STPC_FULL, rej, o);
+        drop += __shfl_xor_sync(STPC_FULL, drop, o);
+        kept += __shfl_xor_sync(STPC_FULL, kept, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        if (rej) atomicAdd(&stat[0], rej);
+        if (drop) atomicAdd(&stat[1], drop);
+        if (kept) atomicAdd(&stat[2], kept);
+    }
+    __syncthreads();
+    const int nq = q_n;
+    if (threadIdx.x == 0) {
+        long long* fs = a.fstats + (long long)f * FS_COUNT;
+        if (stat[0]) atomicAdd((unsigned long long*)&fs[FS_REJECTED], (unsigned long long)stat[0]);
+        if (stat[1]) atomicAdd((unsigned long long*)&fs[FS_DROPPED], (unsigned long long)stat[1]);
+        if (stat[2]) atomicAdd((unsigned long long*)&fs[FS_KEPT], (unsigned long long)stat[2]);
+        if (nq) q_base = atomicAdd(a.q_count, (unsigned long long)nq);
+    }
+    __syncthreads();
+    for (int j = threadIdx.x; j < nq; j += 256) {
+        unsigned long long qi = q_base + j;
+        if (qi < (unsigned long long)a.q_cap) {  // else: overflow re-pass handles it
+            a.q_idx[qi] = cb + q_local[j];
+            a.q_frame[qi] = f;
+        }
+    }
 }
 
 __device__ __forceinline__ void exact_point(const ConvertArgs& a, double px, double py, double pz, int f)
@@ -285,15 +322,23 @@ static dim3 convert_grid(int max_pts, int n_frames)
     return dim3(bx, n_frames);
 }
 
+template <class T>
+static dim3 chunk_grid(int max_pts, int n_frames)
+{
+    int ch = 256 * PPT<T>::value;
+    int bx = (max_pts + ch - 1) / ch;
+    return dim3(bx < 1 ? 1 : bx, n_frames);
+}
+
 void launch_convert(const ConvertArgs& a, int max_pts, cudaStream_t s)
 {
     if (a.n_frames <= 0) return;
     cudaMemsetAsync(a.q_count, 0, sizeof(unsigned long long), s);
     STPC_LAUNCH();
     if (a.pts_f64)
-        convert_kernel<double><<<convert_grid(max_pts, a.n_frames), 256, 0, s>>>(a, (const double*)a.pts);
+        convert_kernel<double><<<chunk_grid<double>(max_pts, a.n_frames), 256, 0, s>>>(a, (const double*)a.pts);
     else
-        convert_kernel<float><<<convert_grid(max_pts, a.n_frames), 256, 0, s>>>(a, (const float*)a.pts);
+        convert_kernel<float><<<chunk_grid<float>(max_pts, a.n_frames), 256, 0, s>>>(a, (const float*)a.pts);
     STPC_LAUNCH();
     if (a.pts_f64)
         convert_exact_kernel<double><<<148 * 4, 256, 0, s>>>(a, (const double*)a.pts);
