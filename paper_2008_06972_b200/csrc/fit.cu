@@ -186,7 +186,9 @@ __global__ void __launch_bounds__(FIT_WARPS * 32, 5) fit_rows_kernel(FitArgs A)
                         bad = !pixel_fits(r, dx, dy, dz, na, nb, nc, A.tau, A.r_max);
                     }
                 }
-                bad_any = bad_any || (__ballot_sync(STPC_FULL, bad) & gmask) != 0;
+                // ballot unconditionally: every lane must reach the full-mask collective
+                const unsigned bb = __ballot_sync(STPC_FULL, bad) & gmask;
+                bad_any = bad_any || bb != 0;
             }
             ok = ok && !bad_any;
         }
