@@ -38,214 +38,282 @@ __device__ __forceinline__ void divmod_small(int p, int d, float rcp, int& q, in
     else if (r >= d) { q += 1; r -= d; }
 }
 
-// G lanes per chain, 32/G chains per warp.  All chains of a warp advance in
-// lock-step through one state-machine step per iteration (fold one tile,
-// optionally solve + test, update), so every warp instruction serves 32/G
-// chains; per-chain differences (union sizes, branch outcomes) are handled
-// with predicates and warp-uniform loop bounds.
+struct Chain {
+    const double* img;    // frame's best grid (covered pixels already +inf in pass 2)
+    const uint8_t* crow;  // tile classes of this tile-row
+    float4* cert;         // per-tile test certificates of this chain (2 x float4 per tile)
+    bool skip1;           // pass 2: tiles of class 1 are fully masked
+    int v0, rows;
+};
+
+// Fold the valid pixels of tile t onto the lane-owned running sums (lane k<9
+// owns sum k; lanes >= 9 shadow sum 8).  Returns the valid count (uniform).
+__device__ __forceinline__ int fold_tile(const Chain& ch, const Geometry& g, const Trig& tg, int t,
+                                         double* sm, double& acc)
+{
+    if (ch.skip1 && ch.crow[t] == 1) return 0;
+    const int lane = threadIdx.x & 31;
+    const int kk = lane < 9 ? lane : 8;
+    const int u0 = t * g.tw;
+    const int cols = min(g.tw, g.w - u0);
+    const int npx = ch.rows * cols;
+    const float rc = __frcp_rn((float)cols);
+    int cnt = 0;
+    for (int base = 0; base < npx; base += 32) {
+        int p = base + lane;
+        double x = 0.0, y = 0.0, z = 0.0, one = 0.0;
+        if (p < npx) {
+            int dv, du;
+            divmod_small(p, cols, rc, dv, du);
+            int v = ch.v0 + dv, u = u0 + du;
+            double r = ch.img[(long long)v * g.w + u];
+            if (isfinite(r)) {
+                double dx, dy, dz;
+                ray_dir(tg, v, u, dx, dy, dz);
+                x = r * dx;
+                y = r * dy;
+                z = r * dz;
+                one = 1.0;
+            }
+        }
+        cnt += __popc(__ballot_sync(STPC_FULL, one != 0.0));
+        double* row = sm + lane * 9;
+        row[0] = y * y;
+        row[1] = y * z;
+        row[2] = z * z;
+        row[3] = y;
+        row[4] = z;
+        row[5] = x * y;
+        row[6] = x * z;
+        row[7] = x;
+        row[8] = one;
+        __syncwarp();
+        const int nj = min(32, npx - base);
+#pragma unroll 4
+        for (int j = 0; j < nj; ++j) acc += sm[j * 9 + kk];  // +0.0 for invalid: exact
+        __syncwarp();
+    }
+    return cnt;
+}
+
+// ---------------------------------------------------------------------------
+// Union re-test with per-tile certificates.
 //
-// Per chain (== one encode_tile_row call):
-//   START mode: sums = fold(tile t) from zero; if N >= 3 and the solve is ok,
-//               round through f32 and test tile t alone; pass -> GROW with
-//               s = t, fail -> tile t is residual; t += 1.
-//   GROW mode:  sums += fold(tile t); an empty tile extends the run (same
-//               sums, same plane, same verdict); otherwise solve and test
-//               the union [s, t]; pass -> keep plane, t += 1; fail -> emit run
-//               [s, t) and restart in START mode at the same t.
-//   t == tiles_x closes an open run.
-template <int G>
+// The reference re-tests every pixel of the union [s, e] after each growth
+// step (_span_ok, O(L^2) pixel tests per run; ~17 tests per pixel on a
+// 64-beam frame).  Here a tile that passed a full test under plane
+// P = (a, b, c) records a certificate: m = tau - max|r - r_hat| (>= 0),
+// dmin = min|den|, rmin/rmax = min/max r_hat over its valid pixels.  For a
+// new plane P' with da = |a'-a|, db = |b'-b|, dc = |c'-c|, every pixel's
+// den' = den + (a'-a) dy + (b'-b) dz moves by at most da + db (|dy|, |dz| <= 1)
+// and
+//     |r_hat' - r_hat| = |dc * den - c * dden| / (|den| |den'|)
+//                     <= (dc + rmax (da + db)) / (dmin - da - db) =: B.
+// If B (inflated by a relative 1e-6 and 1e-9 m, far above fp64 rounding) is
+// below m, rmin - B > 0, rmax + B < r_max and dmin - da - db > 1e-12, every
+// pixel of the tile provably passes under P', exactly as the reference's
+// per-pixel test would decide, and the tile is not re-tested.  Otherwise it is
+// tested pixel by pixel (and re-certified).  Verdicts are identical; only the
+// work changes.
+// ---------------------------------------------------------------------------
+
+// Full pixel test of tile t under (a, b, c); on pass, lane 0 stores the
+// tile's certificate.  Returns the verdict (warp-uniform).
+__device__ bool test_tile(const Chain& ch, const Geometry& g, const Trig& tg, int t, double a, double b,
+                          double c, double tau, double r_max)
+{
+    const int lane = threadIdx.x & 31;
+    const int u0 = t * g.tw;
+    const int cols = min(g.tw, g.w - u0);
+    const int npx = (ch.skip1 && ch.crow[t] == 1) ? 0 : ch.rows * cols;
+    const float rc = __frcp_rn((float)cols);
+    double m = 1e300, dmin = 1e300, rmin = 1e300, rmax = 0.0;
+    for (int base = 0; base < npx; base += 32) {
+        int p = base + lane;
+        bool bad = false;
+        if (p < npx) {
+            int dv, du;
+            divmod_small(p, cols, rc, dv, du);
+            int v = ch.v0 + dv, u = u0 + du;
+            double r = ch.img[(long long)v * g.w + u];
+            if (isfinite(r)) {
+                double dx, dy, dz;
+                ray_dir(tg, v, u, dx, dy, dz);
+                double den = (dx + a * dy) + b * dz;
+                double ad = fabs(den);
+                if (ad < STPC_PARALLEL_EPS) {
+                    bad = true;
+                } else {
+                    double r_hat = c / den;
+                    if (r_hat <= 0.0 || r_hat > r_max || fabs(r - r_hat) > tau) {
+                        bad = true;
+                    } else {
+                        m = fmin(m, tau - fabs(r - r_hat));
+                        dmin = fmin(dmin, ad);
+                        rmin = fmin(rmin, r_hat);
+                        rmax = fmax(rmax, r_hat);
+                    }
+                }
+            }
+        }
+        if (__any_sync(STPC_FULL, bad)) return false;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        m = fmin(m, __shfl_xor_sync(STPC_FULL, m, o));
+        dmin = fmin(dmin, __shfl_xor_sync(STPC_FULL, dmin, o));
+        rmin = fmin(rmin, __shfl_xor_sync(STPC_FULL, rmin, o));
+        rmax = fmax(rmax, __shfl_xor_sync(STPC_FULL, rmax, o));
+    }
+    if (lane == 0) {
+        float4* ce = ch.cert + 2 * t;
+        // a/b/c are f32-exact; bounds rounded outward
+        ce[0] = make_float4((float)a, (float)b, (float)c, __double2float_rd(fmin(m, 3.0e38)));
+        ce[1] = make_float4(__double2float_rd(fmin(dmin, 3.0e38)), __double2float_rd(fmin(rmin, 3.0e38)),
+                            __double2float_ru(rmax), 0.0f);
+    }
+    return true;
+}
+
+// Does tile j's certificate prove it passes under (a, b, c)?
+__device__ __forceinline__ bool cert_holds(const float4* cert, int j, double a, double b, double c,
+                                           double r_max)
+{
+    const float4 c0 = cert[2 * j], c1 = cert[2 * j + 1];
+    if (c0.w >= 3.0e38f) return true;  // no valid pixels: passes under any plane
+    const double dden = fabs(a - (double)c0.x) + fabs(b - (double)c0.y);
+    const double dc = fabs(c - (double)c0.z);
+    const double dlo = (double)c1.x - dden;
+    if (!(dlo > 2e-12)) return false;
+    const double rmax = (double)c1.z;
+    double B = (dc + rmax * dden) / dlo;
+    B = B * (1.0 + 1e-6) + 1e-9;
+    return B < (double)c0.w && (double)c1.y - B > 0.0 && rmax + B < r_max;
+}
+
+// Union [s, e] under (a, b, c): new tile e in full, older tiles by
+// certificate, falling back to a full test where the certificate is too weak.
+__device__ bool union_fits(const Chain& ch, const Geometry& g, const Trig& tg, int s, int e, double a,
+                           double b, double c, double tau, double r_max)
+{
+    const int lane = threadIdx.x & 31;
+    if (!test_tile(ch, g, tg, e, a, b, c, tau, r_max)) return false;
+    for (int base = s; base < e; base += 32) {
+        const int j = base + lane;
+        bool weak = j < e && !cert_holds(ch.cert, j, a, b, c, r_max);
+        uint32_t wm = __ballot_sync(STPC_FULL, weak);
+        while (wm) {
+            const int jj = base + __ffs(wm) - 1;
+            wm &= wm - 1;
+            if (!test_tile(ch, g, tg, jj, a, b, c, tau, r_max)) return false;
+        }
+    }
+    return true;
+}
+
+__device__ __forceinline__ bool solve_round(double acc, double cond_limit, double& a, double& b, double& c)
+{
+    double s[9];
+#pragma unroll
+    for (int k = 0; k < 9; ++k) s[k] = shfl_d(acc, k);
+    if (!plane_from_sums(s, cond_limit, a, b, c)) return false;
+    a = f32_round(a);
+    b = f32_round(b);
+    c = f32_round(c);
+    return true;
+}
+
 __global__ void __launch_bounds__(FIT_WARPS * 32, 5) fit_rows_kernel(FitArgs A)
 {
-    constexpr int CPW = 32 / G;
-    __shared__ double smem[FIT_WARPS][CPW][G * 8];
+    __shared__ double smem[FIT_WARPS][32 * 9];
     const Geometry& g = A.g;
     const int lane = threadIdx.x & 31;
     const int wib = threadIdx.x >> 5;
-    const int sub = lane / G;
-    const int gl = lane % G;
-    const unsigned gmask = G == 32 ? STPC_FULL : (((1u << G) - 1u) << (sub * G));
-    const long long n_chains = (long long)A.n_jobs * g.ty;
-    const long long cid = ((long long)blockIdx.x * FIT_WARPS + wib) * CPW + sub;
-    bool done = cid >= n_chains;
-    if (__all_sync(STPC_FULL, done)) return;
-
-    // chain setup
-    int frame = 0, tr = 0;
-    if (!done) {
-        const int job = (int)(cid / g.ty);
-        tr = (int)(cid % g.ty);
-        if (A.mode == 0) {
-            frame = job * A.n_frames_group + A.k;
-        } else {
-            int np = A.n_frames_group - 1;
-            int grp = job / np, i = job % np;
-            frame = grp * A.n_frames_group + (i < A.k ? i : i + 1);
-        }
+    const long long wid = (long long)blockIdx.x * FIT_WARPS + wib;
+    if (wid >= (long long)A.n_jobs * g.ty) return;
+    const int job = (int)(wid / g.ty);
+    const int tr = (int)(wid % g.ty);
+    int frame;
+    if (A.mode == 0) {
+        frame = job * A.n_frames_group + A.k;
+    } else {
+        int np = A.n_frames_group - 1;
+        int grp = job / np, i = job % np;
+        frame = grp * A.n_frames_group + (i < A.k ? i : i + 1);
     }
     const long long slot = (long long)frame * g.ty + tr;
-    const double* img = A.best + (long long)frame * g.P;
+    Chain ch;
+    ch.img = A.best + (long long)frame * g.P;
     uint8_t* crow = A.cls + slot * g.tx;
-    const bool skip1 = A.mode != 0;
-    const int v0 = tr * g.th;
-    const int rows = min(g.th, g.h - v0);
+    ch.crow = crow;
+    ch.cert = A.cert + slot * g.tx * 2;
+    ch.skip1 = A.mode != 0;
+    ch.v0 = tr * g.th;
+    ch.rows = min(g.th, g.h - ch.v0);
     const uint8_t run_cls = A.mode == 0 ? 1 : 2;
-    double* sm = smem[wib][sub];
+    double* sm = smem[wib];
+
     uint16_t* rs = A.run_s + slot * g.tx;
     uint16_t* rl = A.run_len + slot * g.tx;
     float* rabc = A.run_abc + slot * g.tx * 3;
-
-    // lane gl < 8 owns sum gl of [Syy, Syz, Szz, Sy, Sz, Sxy, Sxz, Sx]; N is
-    // the exact valid count (the reference's N += 1.0 fold equals it).
-    double acc = 0.0;
-    int nsum = 0;
-    int t = 0, s = 0, n_runs = 0;
-    bool grow = false;
-    double a = 0.0, b = 0.0, c = 0.0;
-
-    while (__any_sync(STPC_FULL, !done)) {
-        // ---- fold tile t of every live chain onto its running sums
-        if (!done && !grow) { acc = 0.0; nsum = 0; }
-        const bool masked = done || (skip1 && crow[t] == 1);
-        const int u0 = t * g.tw;
-        const int cols = done ? 1 : min(g.tw, g.w - u0);
-        const int npx = masked ? 0 : rows * cols;
-        const float rc = __frcp_rn((float)cols);
-        int cnt = 0;
-        for (int base = 0; __any_sync(STPC_FULL, base < npx); base += G) {
-            const int p = base + gl;
-            double x = 0.0, y = 0.0, z = 0.0;
-            bool valid = false;
-            if (p < npx) {
-                int dv, du;
-                divmod_small(p, cols, rc, dv, du);
-                const int v = v0 + dv, u = u0 + du;
-                const double r = img[(long long)v * g.w + u];
-                if (isfinite(r)) {
-                    double dx, dy, dz;
-                    ray_dir(A.tg, v, u, dx, dy, dz);
-                    x = r * dx;
-                    y = r * dy;
-                    z = r * dz;
-                    valid = true;
-                }
-            }
-            cnt += __popc(__ballot_sync(STPC_FULL, valid) & gmask);
-            double* row = sm + gl * 8;
-            row[0] = y * y;
-            row[1] = y * z;
-            row[2] = z * z;
-            row[3] = y;
-            row[4] = z;
-            row[5] = x * y;
-            row[6] = x * z;
-            row[7] = x;
-            __syncwarp();
-            const int nj = min(G, npx - base);  // <= 0 for finished chains
-            if (gl < 8)
-                for (int j = 0; j < nj; ++j) acc += sm[j * 8 + gl];  // +0.0 for invalid: exact
-            __syncwarp();
-        }
-        nsum += cnt;
-
-        // ---- solve (chains that need it), round through f32
-        const bool need = !done && (grow ? cnt > 0 : nsum >= 3);
-        double na = 0.0, nb = 0.0, nc = 0.0;
+    int n_runs = 0;
+    int t = 0;
+    while (t < g.tx) {
+        double acc = 0.0;
+        int cnt = fold_tile(ch, g, A.tg, t, sm, acc);
         bool ok = false;
-        {
-            double sv[9];
-#pragma unroll
-            for (int k = 0; k < 8; ++k) sv[k] = __shfl_sync(STPC_FULL, acc, sub * G + k);
-            sv[8] = (double)nsum;
-            if (need && plane_from_sums(sv, A.cond_limit, na, nb, nc)) {
-                na = f32_round(na);
-                nb = f32_round(nb);
-                nc = f32_round(nc);
-                ok = true;
-            }
+        double a = 0.0, b = 0.0, c = 0.0;
+        if (cnt >= 3) {  // sums[8] >= 3.0
+            ok = solve_round(acc, A.cond_limit, a, b, c);
+            if (ok) ok = test_tile(ch, g, A.tg, t, a, b, c, A.tau, A.r_max);
         }
-
-        // ---- test the union (START: tile t; GROW: tiles [s, t])
-        {
-            const int t0 = grow ? s : t;
-            const int U0 = t0 * g.tw;
-            const int U = min((t + 1) * g.tw, g.w) - U0;
-            const int tpx = ok ? rows * U : 0;
-            const float ru = __frcp_rn((float)(U > 0 ? U : 1));
-            bool bad_any = false;
-            for (int base = 0; __any_sync(STPC_FULL, base < tpx && !bad_any); base += G) {
-                const int p = base + gl;
-                bool bad = false;
-                if (p < tpx && !bad_any) {
-                    int dv, du;
-                    divmod_small(p, U, ru, dv, du);
-                    const int v = v0 + dv, u = U0 + du;
-                    const double r = img[(long long)v * g.w + u];
-                    if (isfinite(r)) {
-                        double dx, dy, dz;
-                        ray_dir(A.tg, v, u, dx, dy, dz);
-                        bad = !pixel_fits(r, dx, dy, dz, na, nb, nc, A.tau, A.r_max);
-                    }
-                }
-                // ballot unconditionally: every lane must reach the full-mask collective
-                const unsigned bb = __ballot_sync(STPC_FULL, bad) & gmask;
-                bad_any = bad_any || bb != 0;
-            }
-            ok = ok && !bad_any;
+        if (!ok) {  // residual tile (class 0 stays; covered tiles keep class 1)
+            t += 1;
+            continue;
         }
-
-        // ---- state update (uniform within each chain's lane group)
-        if (!done) {
-            int emit_e = -1;
-            if (!grow) {
-                if (ok) {
-                    s = t;
-                    a = na; b = nb; c = nc;
-                    grow = true;
+        const int s = t;
+        int e = t + 1;
+        while (e < g.tx) {
+            double saved = acc;
+            int add = fold_tile(ch, g, A.tg, e, sm, acc);
+            if (add == 0) {  // unchanged sums -> same plane -> same verdict
+                if (lane == 0) {  // certificate: no pixels, passes under any plane
+                    ch.cert[2 * e] = make_float4(0.f, 0.f, 0.f, 3.4e38f);
                 }
-                t += 1;
-            } else if (cnt == 0 || ok) {
-                if (ok) { a = na; b = nb; c = nc; }
-                t += 1;
-            } else {
-                emit_e = t;  // close [s, t); t restarts as a start tile
-                grow = false;
+                e += 1;
+                continue;
             }
-            if (t >= g.tx) {
-                if (grow) { emit_e = g.tx; grow = false; }
-                done = true;
+            double na, nb, nc;
+            bool ok2 = solve_round(acc, A.cond_limit, na, nb, nc);
+            if (ok2) ok2 = union_fits(ch, g, A.tg, s, e, na, nb, nc, A.tau, A.r_max);
+            if (!ok2) {
+                acc = saved;
+                break;
             }
-            if (emit_e >= 0) {
-                if (gl == 0) {
-                    rs[n_runs] = (uint16_t)s;
-                    rl[n_runs] = (uint16_t)(emit_e - s);
-                    rabc[3 * n_runs] = (float)a;
-                    rabc[3 * n_runs + 1] = (float)b;
-                    rabc[3 * n_runs + 2] = (float)c;
-                }
-                for (int tt = s + gl; tt < emit_e; tt += G)
-                    if (!(skip1 && crow[tt] == 1)) crow[tt] = run_cls;
-                n_runs += 1;
-            }
+            a = na; b = nb; c = nc;
+            e += 1;
         }
+        if (lane == 0) {
+            rs[n_runs] = (uint16_t)s;
+            rl[n_runs] = (uint16_t)(e - s);
+            rabc[3 * n_runs] = (float)a;
+            rabc[3 * n_runs + 1] = (float)b;
+            rabc[3 * n_runs + 2] = (float)c;
+        }
+        for (int tt = s + lane; tt < e; tt += 32)
+            if (!(ch.skip1 && crow[tt] == 1)) crow[tt] = run_cls;
+        n_runs += 1;
+        t = e;
     }
-    if (cid < n_chains && gl == 0) A.n_runs[slot] = n_runs;
+    if (lane == 0) A.n_runs[slot] = n_runs;
 }
 
 void launch_fit_rows(const FitArgs& a, cudaStream_t s)
 {
-    long long chains = (long long)a.n_jobs * a.g.ty;
-    if (chains <= 0) return;
-    const int tpx = a.g.tw * a.g.th;
+    long long warps = (long long)a.n_jobs * a.g.ty;
+    if (warps <= 0) return;
     STPC_LAUNCH();
-    if (tpx <= 32) {
-        long long warps = (chains + 3) / 4;
-        fit_rows_kernel<8><<<(unsigned)((warps + FIT_WARPS - 1) / FIT_WARPS), FIT_WARPS * 32, 0, s>>>(a);
-    } else if (tpx <= 128) {
-        long long warps = (chains + 1) / 2;
-        fit_rows_kernel<16><<<(unsigned)((warps + FIT_WARPS - 1) / FIT_WARPS), FIT_WARPS * 32, 0, s>>>(a);
-    } else {
-        fit_rows_kernel<32><<<(unsigned)((chains + FIT_WARPS - 1) / FIT_WARPS), FIT_WARPS * 32, 0, s>>>(a);
-    }
+    fit_rows_kernel<<<(unsigned)((warps + FIT_WARPS - 1) / FIT_WARPS), FIT_WARPS * 32, 0, s>>>(a);
 }
 
 // K3a: one warp per key-frame chain; for each of its runs and each P channel,

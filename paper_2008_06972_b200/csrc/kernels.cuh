@@ -78,6 +78,7 @@ struct FitArgs {
     uint16_t* run_len;
     float* run_abc;
     int* n_runs;
+    float4* cert;  // [F*TY][TX][2] per-tile test certificates (scratch)
 };
 void launch_fit_rows(const FitArgs& a, cudaStream_t s);
 
