@@ -125,7 +125,7 @@ __device__ bool test_tile(const Chain& ch, const Geometry& g, const Trig& tg, in
     const int lane = threadIdx.x & 31;
     const int u0 = t * g.tw;
     const int cols = min(g.tw, g.w - u0);
-    const int npx = (ch.skip1 && ch.crow[t] == 1) ? 0 : ch.rows * cols;
+    const int npx = ch.rows * cols;  // callers never test masked (class-1) tiles
     const float rc = __frcp_rn((float)cols);
     double m = 1e300, dmin = 1e300, rmin = 1e300, rmax = 0.0;
     for (int base = 0; base < npx; base += 32) {
@@ -158,19 +158,16 @@ __device__ bool test_tile(const Chain& ch, const Geometry& g, const Trig& tg, in
         }
         if (__any_sync(STPC_FULL, bad)) return false;
     }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-        m = fmin(m, __shfl_xor_sync(STPC_FULL, m, o));
-        dmin = fmin(dmin, __shfl_xor_sync(STPC_FULL, dmin, o));
-        rmin = fmin(rmin, __shfl_xor_sync(STPC_FULL, rmin, o));
-        rmax = fmax(rmax, __shfl_xor_sync(STPC_FULL, rmax, o));
-    }
+    // all four quantities are >= 0, so their float bit patterns order like
+    // their values: one REDUX per reduction (rounded outward first)
+    const unsigned um = __reduce_min_sync(STPC_FULL, __float_as_uint(__double2float_rd(fmin(m, 3.0e38))));
+    const unsigned ud = __reduce_min_sync(STPC_FULL, __float_as_uint(__double2float_rd(fmin(dmin, 3.0e38))));
+    const unsigned ulo = __reduce_min_sync(STPC_FULL, __float_as_uint(__double2float_rd(fmin(rmin, 3.0e38))));
+    const unsigned uhi = __reduce_max_sync(STPC_FULL, __float_as_uint(__double2float_ru(rmax)));
     if (lane == 0) {
         float4* ce = ch.cert + 2 * t;
-        // a/b/c are f32-exact; bounds rounded outward
-        ce[0] = make_float4((float)a, (float)b, (float)c, __double2float_rd(fmin(m, 3.0e38)));
-        ce[1] = make_float4(__double2float_rd(fmin(dmin, 3.0e38)), __double2float_rd(fmin(rmin, 3.0e38)),
-                            __double2float_ru(rmax), 0.0f);
+        ce[0] = make_float4((float)a, (float)b, (float)c, __uint_as_float(um));  // a/b/c are f32-exact
+        ce[1] = make_float4(__uint_as_float(ud), __uint_as_float(ulo), __uint_as_float(uhi), 0.0f);
     }
     return true;
 }
