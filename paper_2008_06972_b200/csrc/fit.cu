@@ -48,11 +48,42 @@ struct Chain {
 
 // Fold the valid pixels of tile t onto the lane-owned running sums (lane k<9
 // owns sum k; lanes >= 9 shadow sum 8).  Returns the valid count (uniform).
-__device__ __forceinline__ int fold_tile(const Chain& ch, const Geometry& g, const Trig& tg, int t,
-                                         double* sm, double& acc)
+// The first 32 pixels of tile t+1 are loaded into `pf` while this step's
+// solve and test run, hiding the L2/HBM latency of the next fold.
+struct Prefetch {
+    int t = -1;
+    double r;
+};
+
+__device__ __forceinline__ double load_px(const Chain& ch, const Geometry& g, int t, int p, int& v, int& u)
 {
-    if (ch.skip1 && ch.crow[t] == 1) return 0;
+    const int u0 = t * g.tw;
+    const int cols = min(g.tw, g.w - u0);
+    int dv, du;
+    divmod_small(p, cols, __frcp_rn((float)cols), dv, du);
+    v = ch.v0 + dv;
+    u = u0 + du;
+    return ch.img[(long long)v * g.w + u];
+}
+
+__device__ __forceinline__ int fold_tile(const Chain& ch, const Geometry& g, const Trig& tg, int t,
+                                         double* sm, double& acc, Prefetch& pf)
+{
     const int lane = threadIdx.x & 31;
+    const bool hit = pf.t == t;
+    const double pr = pf.r;
+    // prefetch chunk 0 of the next tile (consumed by the next fold call)
+    if (t + 1 < g.tx) {
+        const int ncols = min(g.tw, g.w - (t + 1) * g.tw);
+        double r = __longlong_as_double(0x7ff0000000000000ll);
+        if (lane < ch.rows * ncols) {
+            int v, u;
+            r = load_px(ch, g, t + 1, lane, v, u);
+        }
+        pf.r = r;
+        pf.t = t + 1;
+    }
+    if (ch.skip1 && ch.crow[t] == 1) return 0;
     const int kk = lane < 9 ? lane : 8;
     const int u0 = t * g.tw;
     const int cols = min(g.tw, g.w - u0);
@@ -66,7 +97,7 @@ __device__ __forceinline__ int fold_tile(const Chain& ch, const Geometry& g, con
             int dv, du;
             divmod_small(p, cols, rc, dv, du);
             int v = ch.v0 + dv, u = u0 + du;
-            double r = ch.img[(long long)v * g.w + u];
+            double r = (hit && base == 0) ? pr : ch.img[(long long)v * g.w + u];
             if (isfinite(r)) {
                 double dx, dy, dz;
                 ray_dir(tg, v, u, dx, dy, dz);
@@ -255,9 +286,10 @@ __global__ void __launch_bounds__(FIT_WARPS * 32, 5) fit_rows_kernel(FitArgs A)
     float* rabc = A.run_abc + slot * g.tx * 3;
     int n_runs = 0;
     int t = 0;
+    Prefetch pf;
     while (t < g.tx) {
         double acc = 0.0;
-        int cnt = fold_tile(ch, g, A.tg, t, sm, acc);
+        int cnt = fold_tile(ch, g, A.tg, t, sm, acc, pf);
         bool ok = false;
         double a = 0.0, b = 0.0, c = 0.0;
         if (cnt >= 3) {  // sums[8] >= 3.0
@@ -272,7 +304,7 @@ __global__ void __launch_bounds__(FIT_WARPS * 32, 5) fit_rows_kernel(FitArgs A)
         int e = t + 1;
         while (e < g.tx) {
             double saved = acc;
-            int add = fold_tile(ch, g, A.tg, e, sm, acc);
+            int add = fold_tile(ch, g, A.tg, e, sm, acc, pf);
             if (add == 0) {  // unchanged sums -> same plane -> same verdict
                 if (lane == 0) {  // certificate: no pixels, passes under any plane
                     ch.cert[2 * e] = make_float4(0.f, 0.f, 0.f, 3.4e38f);
