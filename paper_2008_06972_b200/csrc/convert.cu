@@ -248,7 +248,8 @@ __device__ __forceinline__ void exact_point(const ConvertArgs& a, double px, dou
 }
 
 // Queue overflow (more than q_cap undecided points): the queue is discarded and
-// every undecided point is re-derived here.  grid as convert_kernel.
+// every undecided point is re-derived here.  grid (1, frames): the usual
+// no-overflow case costs one early exit per block.
 template <class T>
 __global__ void __launch_bounds__(256) convert_overflow_kernel(ConvertArgs a, const T* pts)
 {
@@ -346,9 +347,9 @@ void launch_convert(const ConvertArgs& a, int max_pts, cudaStream_t s)
         convert_exact_kernel<float><<<148 * 4, 256, 0, s>>>(a, (const float*)a.pts);
     STPC_LAUNCH();
     if (a.pts_f64)
-        convert_overflow_kernel<double><<<convert_grid(max_pts, a.n_frames), 256, 0, s>>>(a, (const double*)a.pts);
+        convert_overflow_kernel<double><<<dim3(1, a.n_frames), 256, 0, s>>>(a, (const double*)a.pts);
     else
-        convert_overflow_kernel<float><<<convert_grid(max_pts, a.n_frames), 256, 0, s>>>(a, (const float*)a.pts);
+        convert_overflow_kernel<float><<<dim3(1, a.n_frames), 256, 0, s>>>(a, (const float*)a.pts);
 }
 
 void launch_convert_win(const ConvertArgs& a, int max_pts, cudaStream_t s)

@@ -239,6 +239,86 @@ __device__ bool union_fits(const Chain& ch, const Geometry& g, const Trig& tg, i
     return true;
 }
 
+// ---------------------------------------------------------------------------
+// Start verdicts in parallel.  A START step folds its tile from zero, so its
+// outcome (sums >= 3 pixels, solve ok, f32-rounded plane passes the tile)
+// depends on that tile alone, not on the chain.  One thread per tile
+// evaluates it with the identical sequential raster fold, and on a pass
+// stores the tile's certificate (whose plane is the start plane).  The
+// chains then skip residual tiles with a byte lookup.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) start_tiles_kernel(FitArgs A)
+{
+    const Geometry& g = A.g;
+    const long long n_tiles = (long long)A.n_jobs * g.ty * g.tx;
+    const long long id = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (id >= n_tiles) return;
+    const int t = (int)(id % g.tx);
+    const long long cj = id / g.tx;  // chain within this pass
+    const int job = (int)(cj / g.ty);
+    const int tr = (int)(cj % g.ty);
+    int frame;
+    if (A.mode == 0) {
+        frame = job * A.n_frames_group + A.k;
+    } else {
+        int np = A.n_frames_group - 1;
+        int grp = job / np, i = job % np;
+        frame = grp * A.n_frames_group + (i < A.k ? i : i + 1);
+    }
+    const long long slot = (long long)frame * g.ty + tr;
+    uint8_t* sok = A.start_ok + slot * g.tx + t;
+    if (A.mode != 0 && A.cls[slot * g.tx + t] == 1) {
+        *sok = 0;
+        return;
+    }
+    const double* img = A.best + (long long)frame * g.P;
+    const int v0 = tr * g.th, v1 = min(v0 + g.th, g.h);
+    const int u0 = t * g.tw, u1 = min(u0 + g.tw, g.w);
+    double sm[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+    for (int v = v0; v < v1; ++v)
+        for (int u = u0; u < u1; ++u) {
+            const double r = img[(long long)v * g.w + u];
+            if (!isfinite(r)) continue;
+            double dx, dy, dz;
+            ray_dir(A.tg, v, u, dx, dy, dz);
+            const double x = r * dx, y = r * dy, z = r * dz;
+            sm[0] += y * y; sm[1] += y * z; sm[2] += z * z;
+            sm[3] += y;     sm[4] += z;     sm[5] += x * y;
+            sm[6] += x * z; sm[7] += x;     sm[8] += 1.0;
+        }
+    double a, b, c;
+    bool ok = sm[8] >= 3.0 && plane_from_sums(sm, A.cond_limit, a, b, c);
+    double m = 1e300, dmin = 1e300, rmin = 1e300, rmax = 0.0;
+    if (ok) {
+        a = f32_round(a);
+        b = f32_round(b);
+        c = f32_round(c);
+        for (int v = v0; v < v1 && ok; ++v)
+            for (int u = u0; u < u1; ++u) {
+                const double r = img[(long long)v * g.w + u];
+                if (!isfinite(r)) continue;
+                double dx, dy, dz;
+                ray_dir(A.tg, v, u, dx, dy, dz);
+                const double den = (dx + a * dy) + b * dz;
+                const double ad = fabs(den);
+                if (ad < STPC_PARALLEL_EPS) { ok = false; break; }
+                const double r_hat = c / den;
+                if (r_hat <= 0.0 || r_hat > A.r_max || fabs(r - r_hat) > A.tau) { ok = false; break; }
+                m = fmin(m, A.tau - fabs(r - r_hat));
+                dmin = fmin(dmin, ad);
+                rmin = fmin(rmin, r_hat);
+                rmax = fmax(rmax, r_hat);
+            }
+    }
+    *sok = ok ? 1 : 0;
+    if (ok) {
+        float4* ce = A.cert + (slot * g.tx + t) * 2;
+        ce[0] = make_float4((float)a, (float)b, (float)c, __double2float_rd(fmin(m, 3.0e38)));
+        ce[1] = make_float4(__double2float_rd(fmin(dmin, 3.0e38)), __double2float_rd(fmin(rmin, 3.0e38)),
+                            __double2float_ru(rmax), 0.0f);
+    }
+}
+
 __device__ __forceinline__ bool solve_round(double acc, double cond_limit, double& a, double& b, double& c)
 {
     double s[9];
@@ -287,19 +367,18 @@ __global__ void __launch_bounds__(FIT_WARPS * 32, 5) fit_rows_kernel(FitArgs A)
     int n_runs = 0;
     int t = 0;
     Prefetch pf;
+    const uint8_t* sok = A.start_ok + slot * g.tx;
     while (t < g.tx) {
-        double acc = 0.0;
-        int cnt = fold_tile(ch, g, A.tg, t, sm, acc, pf);
-        bool ok = false;
-        double a = 0.0, b = 0.0, c = 0.0;
-        if (cnt >= 3) {  // sums[8] >= 3.0
-            ok = solve_round(acc, A.cond_limit, a, b, c);
-            if (ok) ok = test_tile(ch, g, A.tg, t, a, b, c, A.tau, A.r_max);
-        }
-        if (!ok) {  // residual tile (class 0 stays; covered tiles keep class 1)
+        if (!sok[t]) {  // residual start tile (class 0 stays; covered tiles keep class 1)
             t += 1;
             continue;
         }
+        // passing start: rebuild the running sums; the plane is the one the
+        // start verdict certified
+        double acc = 0.0;
+        fold_tile(ch, g, A.tg, t, sm, acc, pf);
+        const float4 c0 = ch.cert[2 * t];
+        double a = (double)c0.x, b = (double)c0.y, c = (double)c0.z;
         const int s = t;
         int e = t + 1;
         while (e < g.tx) {
@@ -341,6 +420,9 @@ void launch_fit_rows(const FitArgs& a, cudaStream_t s)
 {
     long long warps = (long long)a.n_jobs * a.g.ty;
     if (warps <= 0) return;
+    long long tiles = warps * a.g.tx;
+    STPC_LAUNCH();
+    start_tiles_kernel<<<(unsigned)((tiles + 255) / 256), 256, 0, s>>>(a);
     STPC_LAUNCH();
     fit_rows_kernel<<<(unsigned)((warps + FIT_WARPS - 1) / FIT_WARPS), FIT_WARPS * 32, 0, s>>>(a);
 }
