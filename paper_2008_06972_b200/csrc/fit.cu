@@ -373,12 +373,13 @@ __global__ void __launch_bounds__(FIT_WARPS * 32, 5) fit_rows_kernel(FitArgs A)
             t += 1;
             continue;
         }
-        // passing start: rebuild the running sums; the plane is the one the
-        // start verdict certified
+        // passing start: rebuild the running sums and the start plane (the
+        // verdict is known; cert[t] may since hold a growth-plane certificate,
+        // which remains a valid proof for later union tests)
         double acc = 0.0;
         fold_tile(ch, g, A.tg, t, sm, acc, pf);
-        const float4 c0 = ch.cert[2 * t];
-        double a = (double)c0.x, b = (double)c0.y, c = (double)c0.z;
+        double a, b, c;
+        solve_round(acc, A.cond_limit, a, b, c);
         const int s = t;
         int e = t + 1;
         while (e < g.tx) {
