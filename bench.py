@@ -319,17 +319,13 @@ def main():
     blob_bytes = int(len_b.sum())
     stats = enc.frame_stats()
     if dist:
-        t = torch.tensor([ms], device=device, dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+        from paper_2008_06972_b200 import dist as pdist
+
+        ms = pdist.max_over_ranks(ms, device)
         # the single collective of the path: gather per-group blob sizes
-        sizes = torch.as_tensor(len_b, device=device)
-        allsz = torch.empty(world * sizes.numel(), dtype=sizes.dtype, device=device)
-        dist.all_gather_into_tensor(allsz, sizes)
+        allsz = pdist.gather_sizes(torch.as_tensor(len_b, device=device))
         total_blob = int(allsz.sum().item())
-        tp = torch.tensor([npts], device=device, dtype=torch.int64)
-        dist.all_reduce(tp)
-        total_pts = int(tp.item())
+        total_pts = pdist.sum_over_ranks(npts, device)
     else:
         total_blob = blob_bytes
         total_pts = npts
@@ -360,9 +356,7 @@ def main():
         torch.cuda.synchronize()
         ems = e0.elapsed_time(e1)
         if dist:
-            t = torch.tensor([ems], device=device, dtype=torch.float64)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            ems = float(t.item())
+            ems = pdist.max_over_ranks(ems, device)
         ems /= max(args.steps, 1)
         off2, len2 = enc.blob_layout()
         e2e = {"value": frames_all / (ems / 1e3), "unit": "frames/s",

@@ -1,0 +1,50 @@
+"""Multi-GPU plumbing for batch encoding: one process per GPU, groups sharded
+by rank, no data-path collective.
+
+K+P groups are independent (no GOP chaining), so each rank
+encodes its own contiguous block of groups.  The only collectives are the
+final gather of per-group blob sizes and the max-over-ranks of the device
+time.  Works with the NCCL backend on GPUs and gloo on CPU
+(tests).
+"""
+
+from __future__ import annotations
+
+from typing import Tuple
+
+import torch
+import torch.distributed as dist
+
+
+def shard_range(n_groups: int, rank: int, world: int) -> Tuple[int, int]:
+    """Contiguous block [lo, hi) of n_groups for `rank` (sizes differ by <= 1)."""
+    if world < 1 or not 0 <= rank < world:
+        raise ValueError("bad rank/world")
+    base, extra = divmod(n_groups, world)
+    lo = rank * base + min(rank, extra)
+    return lo, lo + base + (1 if rank < extra else 0)
+
+
+def gather_sizes(local: torch.Tensor) -> torch.Tensor:
+    """All ranks' per-group int64 sizes concatenated in rank order (every rank
+    must pass the same length; pad with -1 and strip if shards are ragged)."""
+    world = dist.get_world_size()
+    out = torch.empty(world * local.numel(), dtype=local.dtype, device=local.device)
+    if dist.get_backend() == "nccl":
+        dist.all_gather_into_tensor(out, local.contiguous())
+    else:
+        parts = list(out.chunk(world))
+        dist.all_gather(parts, local.contiguous())
+    return out
+
+
+def max_over_ranks(value: float, device) -> float:
+    t = torch.tensor([value], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def sum_over_ranks(value: int, device) -> int:
+    t = torch.tensor([value], dtype=torch.int64, device=device)
+    dist.all_reduce(t)
+    return int(t.item())
