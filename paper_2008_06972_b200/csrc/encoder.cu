@@ -300,7 +300,7 @@ static int encode_impl(stpc_encoder* e, int G, const void* d_points, const int64
     ENS(e->run_len, sizeof(uint16_t) * F * TT);
     ENS(e->run_abc, sizeof(float) * 3 * F * TT);
     ENS(e->n_runs, sizeof(int) * F * g.ty);
-    ENS(e->cert, sizeof(float4) * 2 * F * TT);
+    ENS(e->cert, sizeof(float4) * 3 * F * TT);
     ENS(e->start_ok, (size_t)F * TT);
     ENS(e->ref_ok, (size_t)G * TT * n);
     ENS(e->ref_c, sizeof(float) * G * TT * n);

@@ -27,6 +27,7 @@
 namespace stpc {
 
 constexpr int FIT_WARPS = 4;  // warps per block
+constexpr int CERT_F4 = 3;    // float4 per tile certificate
 
 // q, r = p / d, p % d for 0 <= p < 2^24 without an integer divide: float
 // reciprocal estimate, then an exact +-1 correction.
@@ -41,7 +42,7 @@ __device__ __forceinline__ void divmod_small(int p, int d, float rcp, int& q, in
 struct Chain {
     const double* img;    // frame's best grid (covered pixels already +inf in pass 2)
     const uint8_t* crow;  // tile classes of this tile-row
-    float4* cert;         // per-tile test certificates of this chain (2 x float4 per tile)
+    float4* cert;         // per-tile test certificates of this chain (CERT_F4 float4 per tile)
     bool skip1;           // pass 2: tiles of class 1 are fully masked
     int v0, rows;
 };
@@ -133,20 +134,35 @@ __device__ __forceinline__ int fold_tile(const Chain& ch, const Geometry& g, con
 // The reference re-tests every pixel of the union [s, e] after each growth
 // step (_span_ok, O(L^2) pixel tests per run; ~17 tests per pixel on a
 // 64-beam frame).  Here a tile that passed a full test under plane
-// P = (a, b, c) records a certificate: m = tau - max|r - r_hat| (>= 0),
-// dmin = min|den|, rmin/rmax = min/max r_hat over its valid pixels.  For a
-// new plane P' with da = |a'-a|, db = |b'-b|, dc = |c'-c|, every pixel's
-// den' = den + (a'-a) dy + (b'-b) dz moves by at most da + db (|dy|, |dz| <= 1)
-// and
-//     |r_hat' - r_hat| = |dc * den - c * dden| / (|den| |den'|)
-//                     <= (dc + rmax (da + db)) / (dmin - da - db) =: B.
+// P = (a, b, c) records a certificate over its valid pixels: the margin
+// m = tau - max|r - r_hat| (>= 0), dmin = min|den|, rmin/rmax = min/max r_hat
+// and the box [ymin, ymax] x [zmin, zmax] of the reconstructed points
+// y^ = r_hat dy, z^ = r_hat dz.  For a new plane P' = P + (da, db, dc):
+//     den'  = den + da dy + db dz,           |den'| >= dmin - |da| - |db|
+//     r_hat' - r_hat = (dc den - c (da dy + db dz)) / (den den')
+//                    = (dc - da y^ - db z^) / den'.
+// The numerator is affine in (y^, z^), so its largest magnitude over the box
+// is at a corner:  B = max_corners |dc - da y - db z| / (dmin - |da| - |db|).
 // If B (inflated by a relative 1e-6 and 1e-9 m, far above fp64 rounding) is
-// below m, rmin - B > 0, rmax + B < r_max and dmin - da - db > 1e-12, every
-// pixel of the tile provably passes under P', exactly as the reference's
-// per-pixel test would decide, and the tile is not re-tested.  Otherwise it is
-// tested pixel by pixel (and re-certified).  Verdicts are identical; only the
-// work changes.
+// below m, rmin - B > 0, rmax + B < r_max and dmin - |da| - |db| > 1e-12,
+// every pixel of the tile provably passes under P', exactly as the
+// reference's per-pixel test decides, and the tile is not re-tested;
+// otherwise it is tested pixel by pixel (and re-certified).  Verdicts are
+// identical; only the work changes.
 // ---------------------------------------------------------------------------
+
+// Order-preserving map of a float to unsigned (for REDUX min/max of signed values).
+__device__ __forceinline__ unsigned f2key(float f)
+{
+    unsigned u = __float_as_uint(f);
+    return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+__device__ __forceinline__ float key2f(unsigned k)
+{
+    return __uint_as_float((k & 0x80000000u) ? (k & 0x7fffffffu) : ~k);
+}
+
+constexpr float CERT_EMPTY = 3.4e38f;  // m of a tile with no valid pixels
 
 // Full pixel test of tile t under (a, b, c); on pass, lane 0 stores the
 // tile's certificate.  Returns the verdict (warp-uniform).
@@ -159,6 +175,7 @@ __device__ bool test_tile(const Chain& ch, const Geometry& g, const Trig& tg, in
     const int npx = ch.rows * cols;  // callers never test masked (class-1) tiles
     const float rc = __frcp_rn((float)cols);
     double m = 1e300, dmin = 1e300, rmin = 1e300, rmax = 0.0;
+    double ylo = 1e300, yhi = -1e300, zlo = 1e300, zhi = -1e300;
     for (int base = 0; base < npx; base += 32) {
         int p = base + lane;
         bool bad = false;
@@ -183,22 +200,33 @@ __device__ bool test_tile(const Chain& ch, const Geometry& g, const Trig& tg, in
                         dmin = fmin(dmin, ad);
                         rmin = fmin(rmin, r_hat);
                         rmax = fmax(rmax, r_hat);
+                        const double yh = r_hat * dy, zh = r_hat * dz;
+                        ylo = fmin(ylo, yh);
+                        yhi = fmax(yhi, yh);
+                        zlo = fmin(zlo, zh);
+                        zhi = fmax(zhi, zh);
                     }
                 }
             }
         }
         if (__any_sync(STPC_FULL, bad)) return false;
     }
-    // all four quantities are >= 0, so their float bit patterns order like
-    // their values: one REDUX per reduction (rounded outward first)
+    // m, dmin, rmin, rmax are >= 0: their float bit patterns order like their
+    // values; the signed box uses an order-preserving key.  One REDUX each,
+    // every value rounded outward first.
     const unsigned um = __reduce_min_sync(STPC_FULL, __float_as_uint(__double2float_rd(fmin(m, 3.0e38))));
     const unsigned ud = __reduce_min_sync(STPC_FULL, __float_as_uint(__double2float_rd(fmin(dmin, 3.0e38))));
     const unsigned ulo = __reduce_min_sync(STPC_FULL, __float_as_uint(__double2float_rd(fmin(rmin, 3.0e38))));
     const unsigned uhi = __reduce_max_sync(STPC_FULL, __float_as_uint(__double2float_ru(rmax)));
+    const unsigned ky0 = __reduce_min_sync(STPC_FULL, f2key(__double2float_rd(fmax(fmin(ylo, 3.0e38), -3.0e38))));
+    const unsigned ky1 = __reduce_max_sync(STPC_FULL, f2key(__double2float_ru(fmin(fmax(yhi, -3.0e38), 3.0e38))));
+    const unsigned kz0 = __reduce_min_sync(STPC_FULL, f2key(__double2float_rd(fmax(fmin(zlo, 3.0e38), -3.0e38))));
+    const unsigned kz1 = __reduce_max_sync(STPC_FULL, f2key(__double2float_ru(fmin(fmax(zhi, -3.0e38), 3.0e38))));
     if (lane == 0) {
-        float4* ce = ch.cert + 2 * t;
+        float4* ce = ch.cert + CERT_F4 * t;
         ce[0] = make_float4((float)a, (float)b, (float)c, __uint_as_float(um));  // a/b/c are f32-exact
         ce[1] = make_float4(__uint_as_float(ud), __uint_as_float(ulo), __uint_as_float(uhi), 0.0f);
+        ce[2] = make_float4(key2f(ky0), key2f(ky1), key2f(kz0), key2f(kz1));
     }
     return true;
 }
@@ -207,16 +235,19 @@ __device__ bool test_tile(const Chain& ch, const Geometry& g, const Trig& tg, in
 __device__ __forceinline__ bool cert_holds(const float4* cert, int j, double a, double b, double c,
                                            double r_max)
 {
-    const float4 c0 = cert[2 * j], c1 = cert[2 * j + 1];
-    if (c0.w >= 3.0e38f) return true;  // no valid pixels: passes under any plane
-    const double dden = fabs(a - (double)c0.x) + fabs(b - (double)c0.y);
-    const double dc = fabs(c - (double)c0.z);
-    const double dlo = (double)c1.x - dden;
+    const float4 c0 = cert[CERT_F4 * j];
+    if (c0.w >= CERT_EMPTY) return true;  // no valid pixels: passes under any plane
+    const float4 c1 = cert[CERT_F4 * j + 1], c2 = cert[CERT_F4 * j + 2];
+    const double da = a - (double)c0.x, db = b - (double)c0.y, dc = c - (double)c0.z;
+    const double dlo = (double)c1.x - (fabs(da) + fabs(db));
     if (!(dlo > 2e-12)) return false;
-    const double rmax = (double)c1.z;
-    double B = (dc + rmax * dden) / dlo;
+    const double n00 = fabs((dc - da * (double)c2.x) - db * (double)c2.z);
+    const double n01 = fabs((dc - da * (double)c2.x) - db * (double)c2.w);
+    const double n10 = fabs((dc - da * (double)c2.y) - db * (double)c2.z);
+    const double n11 = fabs((dc - da * (double)c2.y) - db * (double)c2.w);
+    double B = fmax(fmax(n00, n01), fmax(n10, n11)) / dlo;
     B = B * (1.0 + 1e-6) + 1e-9;
-    return B < (double)c0.w && (double)c1.y - B > 0.0 && rmax + B < r_max;
+    return B < (double)c0.w && (double)c1.y - B > 0.0 && (double)c1.z + B < r_max;
 }
 
 // Union [s, e] under (a, b, c): new tile e in full, older tiles by
@@ -289,6 +320,7 @@ __global__ void __launch_bounds__(256) start_tiles_kernel(FitArgs A)
     double a, b, c;
     bool ok = sm[8] >= 3.0 && plane_from_sums(sm, A.cond_limit, a, b, c);
     double m = 1e300, dmin = 1e300, rmin = 1e300, rmax = 0.0;
+    double ylo = 1e300, yhi = -1e300, zlo = 1e300, zhi = -1e300;
     if (ok) {
         a = f32_round(a);
         b = f32_round(b);
@@ -308,14 +340,21 @@ __global__ void __launch_bounds__(256) start_tiles_kernel(FitArgs A)
                 dmin = fmin(dmin, ad);
                 rmin = fmin(rmin, r_hat);
                 rmax = fmax(rmax, r_hat);
+                const double yh = r_hat * dy, zh = r_hat * dz;
+                ylo = fmin(ylo, yh);
+                yhi = fmax(yhi, yh);
+                zlo = fmin(zlo, zh);
+                zhi = fmax(zhi, zh);
             }
     }
     *sok = ok ? 1 : 0;
     if (ok) {
-        float4* ce = A.cert + (slot * g.tx + t) * 2;
+        float4* ce = A.cert + (slot * g.tx + t) * CERT_F4;
         ce[0] = make_float4((float)a, (float)b, (float)c, __double2float_rd(fmin(m, 3.0e38)));
         ce[1] = make_float4(__double2float_rd(fmin(dmin, 3.0e38)), __double2float_rd(fmin(rmin, 3.0e38)),
                             __double2float_ru(rmax), 0.0f);
+        ce[2] = make_float4(__double2float_rd(ylo), __double2float_ru(yhi), __double2float_rd(zlo),
+                            __double2float_ru(zhi));
     }
 }
 
@@ -354,7 +393,7 @@ __global__ void __launch_bounds__(FIT_WARPS * 32, 5) fit_rows_kernel(FitArgs A)
     ch.img = A.best + (long long)frame * g.P;
     uint8_t* crow = A.cls + slot * g.tx;
     ch.crow = crow;
-    ch.cert = A.cert + slot * g.tx * 2;
+    ch.cert = A.cert + slot * g.tx * CERT_F4;
     ch.skip1 = A.mode != 0;
     ch.v0 = tr * g.th;
     ch.rows = min(g.th, g.h - ch.v0);
@@ -387,7 +426,7 @@ __global__ void __launch_bounds__(FIT_WARPS * 32, 5) fit_rows_kernel(FitArgs A)
             int add = fold_tile(ch, g, A.tg, e, sm, acc, pf);
             if (add == 0) {  // unchanged sums -> same plane -> same verdict
                 if (lane == 0) {  // certificate: no pixels, passes under any plane
-                    ch.cert[2 * e] = make_float4(0.f, 0.f, 0.f, 3.4e38f);
+                    ch.cert[CERT_F4 * e] = make_float4(0.f, 0.f, 0.f, CERT_EMPTY);
                 }
                 e += 1;
                 continue;

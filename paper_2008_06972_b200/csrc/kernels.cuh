@@ -78,7 +78,7 @@ struct FitArgs {
     uint16_t* run_len;
     float* run_abc;
     int* n_runs;
-    float4* cert;       // [F*TY][TX][2] per-tile test certificates (scratch)
+    float4* cert;       // [F*TY][TX][3] per-tile test certificates (scratch)
     uint8_t* start_ok;  // [F*TY][TX] start verdicts (scratch)
 };
 void launch_fit_rows(const FitArgs& a, cudaStream_t s);
