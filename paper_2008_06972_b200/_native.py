@@ -13,7 +13,8 @@ import threading
 
 from .errors import CodecError
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libstpc_b200.so")
+LIB_PATH = os.environ.get(
+    "STPC_B200_LIB", os.path.join(os.path.dirname(os.path.abspath(__file__)), "libstpc_b200.so"))
 
 STPC_NSTAT = 9
 (STAT_REJECTED, STAT_DROPPED, STAT_KEPT, STAT_VALID, STAT_TEMPORAL, STAT_FALLBACK,

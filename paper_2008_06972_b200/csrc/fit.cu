@@ -121,8 +121,13 @@ __device__ __forceinline__ int fold_tile(const Chain& ch, const Geometry& g, con
         row[8] = one;
         __syncwarp();
         const int nj = min(32, npx - base);
+        if (nj == 16) {  // 4x4 tiles: fully unrolled ordered fold
+#pragma unroll
+            for (int j = 0; j < 16; ++j) acc += sm[j * 9 + kk];  // +0.0 for invalid: exact
+        } else {
 #pragma unroll 4
-        for (int j = 0; j < nj; ++j) acc += sm[j * 9 + kk];  // +0.0 for invalid: exact
+            for (int j = 0; j < nj; ++j) acc += sm[j * 9 + kk];
+        }
         __syncwarp();
     }
     return cnt;
@@ -408,8 +413,19 @@ __global__ void __launch_bounds__(FIT_WARPS * 32, 5) fit_rows_kernel(FitArgs A)
     Prefetch pf;
     const uint8_t* sok = A.start_ok + slot * g.tx;
     while (t < g.tx) {
-        if (!sok[t]) {  // residual start tile (class 0 stays; covered tiles keep class 1)
-            t += 1;
+        if (!sok[t]) {
+            // residual start tiles (class 0 stays; covered tiles keep class 1):
+            // jump to the next start tile with a 32-wide ballot
+            int nt = g.tx;
+            for (int base = t + 1; base < g.tx; base += 32) {
+                const int j = base + lane;
+                const uint32_t m = __ballot_sync(STPC_FULL, j < g.tx && sok[j]);
+                if (m) {
+                    nt = base + __ffs(m) - 1;
+                    break;
+                }
+            }
+            t = nt;
             continue;
         }
         // passing start: rebuild the running sums and the start plane (the
