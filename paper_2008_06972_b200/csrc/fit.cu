@@ -472,6 +472,292 @@ __global__ void __launch_bounds__(FIT_WARPS * 32, 5) fit_rows_kernel(FitArgs A)
     if (lane == 0) A.n_runs[slot] = n_runs;
 }
 
+// ---------------------------------------------------------------------------
+// Lock-step variant for tiles of <= 16 pixels (4x4 and smaller): two chains
+// per warp, 16 lanes each.  A 4x4 tile's fold and pixel test need exactly 16
+// lanes, so pairing chains costs no extra iterations while the solve, the
+// control flow and the certificate logic serve two chains per instruction.
+// Each iteration advances every live chain by one step of the same state
+// machine (scan to the next start tile | fold + solve | test + certificates |
+// update); per-chain differences are predicated.
+// ---------------------------------------------------------------------------
+constexpr int PG = 16;
+
+__device__ __forceinline__ unsigned group_min(unsigned v, int sub, unsigned neutral)
+{
+    const unsigned r0 = __reduce_min_sync(STPC_FULL, sub == 0 ? v : neutral);
+    const unsigned r1 = __reduce_min_sync(STPC_FULL, sub == 1 ? v : neutral);
+    return sub ? r1 : r0;
+}
+__device__ __forceinline__ unsigned group_max(unsigned v, int sub, unsigned neutral)
+{
+    const unsigned r0 = __reduce_max_sync(STPC_FULL, sub == 0 ? v : neutral);
+    const unsigned r1 = __reduce_max_sync(STPC_FULL, sub == 1 ? v : neutral);
+    return sub ? r1 : r0;
+}
+
+// Pixel test of tile `tile` for every active chain of the warp; on pass the
+// group's lane 0 stores the certificate.  Returns this chain's verdict.
+__device__ bool test_tile_pair(bool active, const Chain& ch, const Geometry& g, const Trig& tg, int tile,
+                               double a, double b, double c, double tau, double r_max)
+{
+    const int lane = threadIdx.x & 31;
+    const int sub = lane >> 4, gl = lane & 15;
+    const unsigned gmask = 0xffffu << (sub * 16);
+    int npx = 0, u0 = 0, cols = 1;
+    if (active) {
+        u0 = tile * g.tw;
+        cols = min(g.tw, g.w - u0);
+        npx = ch.rows * cols;
+    }
+    double m = 1e300, dmin = 1e300, rmin = 1e300, rmax = 0.0;
+    double ylo = 1e300, yhi = -1e300, zlo = 1e300, zhi = -1e300;
+    bool bad = false;
+    if (gl < npx) {
+        int dv, du;
+        divmod_small(gl, cols, __frcp_rn((float)cols), dv, du);
+        const int v = ch.v0 + dv, u = u0 + du;
+        const double r = ch.img[(long long)v * g.w + u];
+        if (isfinite(r)) {
+            double dx, dy, dz;
+            ray_dir(tg, v, u, dx, dy, dz);
+            const double den = (dx + a * dy) + b * dz;
+            const double ad = fabs(den);
+            if (ad < STPC_PARALLEL_EPS) {
+                bad = true;
+            } else {
+                const double r_hat = c / den;
+                if (r_hat <= 0.0 || r_hat > r_max || fabs(r - r_hat) > tau) {
+                    bad = true;
+                } else {
+                    m = tau - fabs(r - r_hat);
+                    dmin = ad;
+                    rmin = r_hat;
+                    rmax = r_hat;
+                    ylo = yhi = r_hat * dy;
+                    zlo = zhi = r_hat * dz;
+                }
+            }
+        }
+    }
+    const bool fail = (__ballot_sync(STPC_FULL, bad) & gmask) != 0;
+    if (!__any_sync(STPC_FULL, active && !fail)) return false;
+    const unsigned NEUT_MIN = 0xffffffffu, NEUT_MAX = 0u;
+    const unsigned um = group_min(__float_as_uint(__double2float_rd(fmin(m, 3.0e38))), sub, NEUT_MIN);
+    const unsigned ud = group_min(__float_as_uint(__double2float_rd(fmin(dmin, 3.0e38))), sub, NEUT_MIN);
+    const unsigned ulo = group_min(__float_as_uint(__double2float_rd(fmin(rmin, 3.0e38))), sub, NEUT_MIN);
+    const unsigned uhi = group_max(__float_as_uint(__double2float_ru(rmax)), sub, NEUT_MAX);
+    const unsigned ky0 = group_min(f2key(__double2float_rd(fmax(fmin(ylo, 3.0e38), -3.0e38))), sub, NEUT_MIN);
+    const unsigned ky1 = group_max(f2key(__double2float_ru(fmin(fmax(yhi, -3.0e38), 3.0e38))), sub, NEUT_MAX);
+    const unsigned kz0 = group_min(f2key(__double2float_rd(fmax(fmin(zlo, 3.0e38), -3.0e38))), sub, NEUT_MIN);
+    const unsigned kz1 = group_max(f2key(__double2float_ru(fmin(fmax(zhi, -3.0e38), 3.0e38))), sub, NEUT_MAX);
+    const bool pass = active && !fail;
+    if (pass && gl == 0) {
+        float4* ce = ch.cert + CERT_F4 * tile;
+        ce[0] = make_float4((float)a, (float)b, (float)c, __uint_as_float(um));
+        ce[1] = make_float4(__uint_as_float(ud), __uint_as_float(ulo), __uint_as_float(uhi), 0.0f);
+        ce[2] = make_float4(key2f(ky0), key2f(ky1), key2f(kz0), key2f(kz1));
+    }
+    return pass;
+}
+
+__global__ void __launch_bounds__(FIT_WARPS * 32, 5) fit_pair_kernel(FitArgs A)
+{
+    __shared__ double smem[FIT_WARPS][2][PG * 9];
+    const Geometry& g = A.g;
+    const int lane = threadIdx.x & 31;
+    const int wib = threadIdx.x >> 5;
+    const int sub = lane >> 4, gl = lane & 15;
+    const unsigned gmask = 0xffffu << (sub * 16);
+    const long long n_chains = (long long)A.n_jobs * g.ty;
+    const long long cid = ((long long)blockIdx.x * FIT_WARPS + wib) * 2 + sub;
+    bool done = cid >= n_chains;
+    if (__all_sync(STPC_FULL, done)) return;
+    int frame = 0, tr = 0;
+    if (!done) {
+        const int job = (int)(cid / g.ty);
+        tr = (int)(cid % g.ty);
+        if (A.mode == 0) {
+            frame = job * A.n_frames_group + A.k;
+        } else {
+            int np = A.n_frames_group - 1;
+            int grp = job / np, i = job % np;
+            frame = grp * A.n_frames_group + (i < A.k ? i : i + 1);
+        }
+    }
+    const long long slot = (long long)frame * g.ty + tr;
+    Chain ch;
+    ch.img = A.best + (long long)frame * g.P;
+    uint8_t* crow = A.cls + slot * g.tx;
+    ch.crow = crow;
+    ch.cert = A.cert + slot * g.tx * CERT_F4;
+    ch.skip1 = A.mode != 0;
+    ch.v0 = tr * g.th;
+    ch.rows = min(g.th, g.h - ch.v0);
+    const uint8_t run_cls = A.mode == 0 ? 1 : 2;
+    const uint8_t* sok = A.start_ok + slot * g.tx;
+    double* sm = smem[wib][sub];
+    uint16_t* rs = A.run_s + slot * g.tx;
+    uint16_t* rl = A.run_len + slot * g.tx;
+    float* rabc = A.run_abc + slot * g.tx * 3;
+    const int kk = gl < 9 ? gl : 8;
+
+    int t = 0, s = 0, n_runs = 0;
+    bool grow = false;
+    double acc = 0.0, a = 0.0, b = 0.0, c = 0.0;
+    int pf_t = -1;
+    double pf_r = 0.0;
+
+    while (__any_sync(STPC_FULL, !done)) {
+        // ---- (1) chains between runs jump to their next start tile
+        const bool scan = !done && !grow;
+        {
+            bool found = false;
+            int nt = g.tx;
+            int base = t;
+            while (__any_sync(STPC_FULL, scan && !found && base < g.tx)) {
+                const int j = base + gl;
+                const bool f = scan && !found && j < g.tx && sok[j];
+                const unsigned mm = (__ballot_sync(STPC_FULL, f) & gmask) >> (sub * 16);
+                if (mm && !found) {
+                    nt = base + __ffs(mm) - 1;
+                    found = true;
+                }
+                base += PG;
+            }
+            if (scan) {
+                if (found) t = nt;
+                else done = true;
+            }
+        }
+        // ---- (2) fold tile t (a start folds from zero)
+        const bool live = !done;
+        if (live && !grow) acc = 0.0;
+        const bool masked = !live || (ch.skip1 && crow[t] == 1);
+        const int u0 = live ? t * g.tw : 0;
+        const int cols = live ? min(g.tw, g.w - u0) : 1;
+        const int npx = masked ? 0 : ch.rows * cols;
+        double x = 0.0, y = 0.0, z = 0.0, one = 0.0;
+        if (gl < npx) {
+            int dv, du;
+            divmod_small(gl, cols, __frcp_rn((float)cols), dv, du);
+            const int v = ch.v0 + dv, u = u0 + du;
+            const double r = pf_t == t ? pf_r : ch.img[(long long)v * g.w + u];
+            if (isfinite(r)) {
+                double dx, dy, dz;
+                ray_dir(A.tg, v, u, dx, dy, dz);
+                x = r * dx;
+                y = r * dy;
+                z = r * dz;
+                one = 1.0;
+            }
+        }
+        const int cnt = __popc(__ballot_sync(STPC_FULL, one != 0.0) & gmask);
+        double* row = sm + gl * 9;
+        row[0] = y * y;
+        row[1] = y * z;
+        row[2] = z * z;
+        row[3] = y;
+        row[4] = z;
+        row[5] = x * y;
+        row[6] = x * z;
+        row[7] = x;
+        row[8] = one;
+        __syncwarp();
+        if (live) {
+#pragma unroll
+            for (int j = 0; j < PG; ++j) acc += sm[j * 9 + kk];  // zeros beyond npx: exact
+        }
+        __syncwarp();
+        // prefetch the next tile's pixel gl
+        if (live && t + 1 < g.tx) {
+            const int nu0 = (t + 1) * g.tw;
+            const int ncols = min(g.tw, g.w - nu0);
+            pf_r = __longlong_as_double(0x7ff0000000000000ll);
+            if (gl < ch.rows * ncols) {
+                int dv, du;
+                divmod_small(gl, ncols, __frcp_rn((float)ncols), dv, du);
+                pf_r = ch.img[(long long)(ch.v0 + dv) * g.w + nu0 + du];
+            }
+            pf_t = t + 1;
+        }
+        // ---- (3) solve: starts (verdict known ok) and growing chains with new pixels
+        const bool need = live && (!grow || cnt > 0);
+        double na = 0.0, nb = 0.0, nc = 0.0;
+        bool ok = false;
+        {
+            double sv[9];
+#pragma unroll
+            for (int k = 0; k < 9; ++k) sv[k] = __shfl_sync(STPC_FULL, acc, sub * PG + k);
+            if (need && plane_from_sums(sv, A.cond_limit, na, nb, nc)) {
+                na = f32_round(na);
+                nb = f32_round(nb);
+                nc = f32_round(nc);
+                ok = true;
+            }
+        }
+        // ---- (4) growing chains: test tile t, then certificates of [s, t)
+        const bool testing = live && grow && cnt > 0 && ok;
+        bool pass = false;
+        if (__any_sync(STPC_FULL, testing)) {
+            pass = test_tile_pair(testing, ch, g, A.tg, t, na, nb, nc, A.tau, A.r_max);
+            int base = s;
+            while (__any_sync(STPC_FULL, pass && base < t)) {
+                const int j = base + gl;
+                const bool weak = pass && j < t && !cert_holds(ch.cert, j, na, nb, nc, A.r_max);
+                unsigned wm = (__ballot_sync(STPC_FULL, weak) & gmask) >> (sub * 16);
+                while (__any_sync(STPC_FULL, pass && wm != 0)) {
+                    const bool act = pass && wm != 0;
+                    const int jj = act ? base + __ffs(wm) - 1 : 0;
+                    if (act) wm &= wm - 1;
+                    const bool r = test_tile_pair(act, ch, g, A.tg, jj, na, nb, nc, A.tau, A.r_max);
+                    if (act && !r) pass = false;
+                }
+                base += PG;
+            }
+        }
+        // ---- (5) state update (uniform within each chain's 16 lanes)
+        if (!done) {
+            int emit_e = -1;
+            if (!grow) {
+                s = t;
+                a = na; b = nb; c = nc;
+                grow = true;
+                t += 1;
+            } else if (cnt == 0) {
+                if (gl == 0) ch.cert[CERT_F4 * t] = make_float4(0.f, 0.f, 0.f, CERT_EMPTY);
+                t += 1;
+            } else if (pass) {
+                a = na; b = nb; c = nc;
+                t += 1;
+            } else {
+                emit_e = t;  // close [s, t); t becomes a start candidate again
+                grow = false;
+            }
+            if (t >= g.tx) {
+                if (grow) {
+                    emit_e = g.tx;
+                    grow = false;
+                }
+                done = true;
+            }
+            if (emit_e >= 0) {
+                if (gl == 0) {
+                    rs[n_runs] = (uint16_t)s;
+                    rl[n_runs] = (uint16_t)(emit_e - s);
+                    rabc[3 * n_runs] = (float)a;
+                    rabc[3 * n_runs + 1] = (float)b;
+                    rabc[3 * n_runs + 2] = (float)c;
+                }
+                for (int tt = s + gl; tt < emit_e; tt += PG)
+                    if (!(ch.skip1 && crow[tt] == 1)) crow[tt] = run_cls;
+                n_runs += 1;
+            }
+        }
+    }
+    if (cid < n_chains && gl == 0) A.n_runs[slot] = n_runs;
+}
+
 void launch_fit_rows(const FitArgs& a, cudaStream_t s)
 {
     long long warps = (long long)a.n_jobs * a.g.ty;
@@ -480,7 +766,12 @@ void launch_fit_rows(const FitArgs& a, cudaStream_t s)
     STPC_LAUNCH();
     start_tiles_kernel<<<(unsigned)((tiles + 255) / 256), 256, 0, s>>>(a);
     STPC_LAUNCH();
-    fit_rows_kernel<<<(unsigned)((warps + FIT_WARPS - 1) / FIT_WARPS), FIT_WARPS * 32, 0, s>>>(a);
+    if (a.g.tw * a.g.th <= PG) {
+        long long pairs = (warps + 1) / 2;
+        fit_pair_kernel<<<(unsigned)((pairs + FIT_WARPS - 1) / FIT_WARPS), FIT_WARPS * 32, 0, s>>>(a);
+    } else {
+        fit_rows_kernel<<<(unsigned)((warps + FIT_WARPS - 1) / FIT_WARPS), FIT_WARPS * 32, 0, s>>>(a);
+    }
 }
 
 // K3a: one warp per key-frame chain; for each of its runs and each P channel,
