@@ -312,59 +312,96 @@ __device__ __forceinline__ unsigned int x8nmodp(unsigned long long nbytes)
     return p;
 }
 
-__device__ __forceinline__ void crc_table(unsigned int* tab)
+// slice-by-4 tables for the reflected CRC (T[0] is the classic byte table)
+__device__ __forceinline__ void crc_tables4(unsigned int (*T)[256])
 {
     for (int i = threadIdx.x; i < 256; i += blockDim.x) {
         unsigned int c = i;
         for (int k = 0; k < 8; ++k) c = c & 1 ? (c >> 1) ^ 0xedb88320u : c >> 1;
-        tab[i] = c;
+        T[0][i] = c;
     }
+    __syncthreads();
+    for (int i = threadIdx.x; i < 256; i += blockDim.x) {
+        unsigned int c = T[0][i];
+        for (int k = 1; k < 4; ++k) {
+            c = (c >> 8) ^ T[0][c & 0xff];
+            T[k][i] = c;
+        }
+    }
+    __syncthreads();
 }
 
-// grid (segments, groups), 64 threads: raw CRC per CRC_SEG-byte segment
-// (segment 0 is the LAST one).
-__global__ void __launch_bounds__(64) crc_segment_kernel(EntropyArgs E)
+constexpr int CRC_WARPS = 4;
+
+// grid (segments / CRC_WARPS, groups): warp w of block x handles segment
+// x*CRC_WARPS + w = 32 pieces of 256 B of the encoded payload, counted from
+// its START; only full pieces are covered here (the < 256 B tail is folded
+// in by crc_finish).  The last segment's pieces are end-aligned in the
+// 32-slot tree: the missing leading slots act as a zero prefix, which leaves
+// an init-0 CRC register unchanged.
+__global__ void __launch_bounds__(CRC_WARPS * 32) crc_segment_kernel(EntropyArgs E, CrcConsts K)
 {
-    __shared__ unsigned int tab[256];
-    __shared__ unsigned int pc[64];
-    crc_table(tab);
-    __syncthreads();
-    const int grp = blockIdx.y, sgi = blockIdx.x;
+    __shared__ unsigned int T[4][256];
+    crc_tables4(T);
+    const int grp = blockIdx.y;
+    const int lane = threadIdx.x & 31;
+    const long long sgi = (long long)blockIdx.x * CRC_WARPS + (threadIdx.x >> 5);
     const long long L = E.enc_len[grp];
-    const long long nseg = (L + CRC_SEG - 1) / CRC_SEG;
+    const long long npieces = L / CRC_PIECE;
+    const long long nseg = (npieces + 31) / 32;
     if (sgi >= nseg) return;
-    const uint8_t* enc = E.blobs + E.blob_off[grp] + HDR;
-    // piece index from the end: piece pi covers [L-(pi+1)*256, L-pi*256)
-    long long pi = (long long)sgi * 64 + (63 - threadIdx.x);  // thread 0 = earliest piece
-    long long pe = L - pi * CRC_PIECE, pb = pe - CRC_PIECE;
+    const long long first = sgi * 32;
+    const int np = (int)min(32LL, npieces - first);
+    const int slot_piece = lane - (32 - np);  // end-aligned
+    const uint8_t* enc = E.blobs + E.blob_off[grp] + HDR;  // 4-byte aligned
     unsigned int crc = 0;
-    if (pe > 0) {
-        if (pb < 0) pb = 0;
-        for (long long i = pb; i < pe; ++i) crc = tab[(crc ^ enc[i]) & 0xff] ^ (crc >> 8);
+    if (slot_piece >= 0) {
+        const uint32_t* w = reinterpret_cast<const uint32_t*>(enc + (first + slot_piece) * CRC_PIECE);
+#pragma unroll 8
+        for (int i = 0; i < CRC_PIECE / 4; ++i) {
+            const unsigned int x = crc ^ __ldg(w + i);
+            crc = T[3][x & 0xff] ^ T[2][(x >> 8) & 0xff] ^ T[1][(x >> 16) & 0xff] ^ T[0][x >> 24];
+        }
     }
-    pc[threadIdx.x] = crc;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        const unsigned int X = x8nmodp(CRC_PIECE);
-        unsigned int s = 0;
-        for (int t = 0; t < 64; ++t) s = multmodp(X, s) ^ pc[t];
-        E.seg_crc[(long long)grp * E.max_segs + sgi] = s;
+    // tree: level l merges blocks of 2^l pieces (256 * 2^l bytes)
+#pragma unroll
+    for (int l = 0; l < 5; ++l) {
+        const unsigned int right = __shfl_down_sync(STPC_FULL, crc, 1 << l);
+        if ((lane & ((2 << l) - 1)) == 0) crc = multmodp(K.x256[l], crc) ^ right;
     }
+    if (lane == 0) E.seg_crc[(long long)grp * E.max_segs + sgi] = crc;
 }
 
-// block per group: combine segments, finish the CRC, write the header.
-__global__ void crc_finish_kernel(EntropyArgs E)
+// block per group: combine segments (each 8 KB, the last end-aligned), fold
+// in the tail, apply the 0xFFFFFFFF init/xorout, write the header.
+__global__ void crc_finish_kernel(EntropyArgs E, CrcConsts K)
 {
     const int grp = blockIdx.x;
     uint8_t* blob = E.blobs + E.blob_off[grp];
     for (int i = threadIdx.x; i < 256; i += blockDim.x) blob[28 + i] = E.lens[grp * 256 + i];
     if (threadIdx.x != 0) return;
     const long long L = E.enc_len[grp];
-    const long long nseg = (L + CRC_SEG - 1) / CRC_SEG;
-    const unsigned int X = x8nmodp(CRC_SEG);
+    const long long npieces = L / CRC_PIECE;
+    const long long nseg = (npieces + 31) / 32;
     unsigned int raw = 0;
-    for (long long sgi = nseg - 1; sgi >= 0; --sgi)
+    for (long long sgi = 0; sgi < nseg; ++sgi) {
+        const long long np = min(32LL, npieces - sgi * 32);
+        const unsigned int X = np == 32 ? K.seg : x8nmodp((unsigned long long)np * CRC_PIECE);
         raw = multmodp(X, raw) ^ E.seg_crc[(long long)grp * E.max_segs + sgi];
+    }
+    // tail (< 256 bytes) byte-wise
+    const uint8_t* enc = blob + HDR;
+    const long long tb = npieces * CRC_PIECE;
+    if (tb < L) {
+        raw = multmodp(x8nmodp((unsigned long long)(L - tb)), raw);
+        unsigned int t = 0;
+        for (long long i = tb; i < L; ++i) {
+            unsigned int c = (t ^ enc[i]) & 0xff;
+            for (int k = 0; k < 8; ++k) c = c & 1 ? (c >> 1) ^ 0xedb88320u : c >> 1;
+            t = c ^ (t >> 8);
+        }
+        raw ^= t;
+    }
     unsigned int crc = ~(raw ^ multmodp(x8nmodp((unsigned long long)L), 0xffffffffu));
     blob[0] = 'S'; blob[1] = 'T'; blob[2] = 'P'; blob[3] = 'C';
     put_u16(blob + 4, 1);
@@ -377,12 +414,43 @@ __global__ void crc_finish_kernel(EntropyArgs E)
     put_u32(blob + 24, crc);
 }
 
+// host-side x^(8n) mod P (same arithmetic as the device helpers)
+static unsigned int h_multmodp(unsigned int a, unsigned int b)
+{
+    unsigned int m = 1u << 31, p = 0;
+    for (;;) {
+        if (a & m) {
+            p ^= b;
+            if ((a & (m - 1)) == 0) break;
+        }
+        m >>= 1;
+        b = b & 1 ? (b >> 1) ^ 0xedb88320u : b >> 1;
+    }
+    return p;
+}
+static unsigned int h_x8nmodp(unsigned long long n)
+{
+    unsigned int p = 1u << 31, sq = 1u << 23;
+    while (n) {
+        if (n & 1) p = h_multmodp(sq, p);
+        sq = h_multmodp(sq, sq);
+        n >>= 1;
+    }
+    return p;
+}
+
 void launch_crc(const EntropyArgs& E, cudaStream_t s)
 {
     if (E.G <= 0) return;
-    if (E.max_segs > 0) { STPC_LAUNCH(); crc_segment_kernel<<<dim3(E.max_segs, E.G), 64, 0, s>>>(E); }
+    CrcConsts K;
+    for (int l = 0; l < 5; ++l) K.x256[l] = h_x8nmodp((unsigned long long)CRC_PIECE << l);
+    K.seg = h_x8nmodp(32ull * CRC_PIECE);
+    if (E.max_segs > 0) {
+        STPC_LAUNCH();
+        crc_segment_kernel<<<dim3((E.max_segs + CRC_WARPS - 1) / CRC_WARPS, E.G), CRC_WARPS * 32, 0, s>>>(E, K);
+    }
     STPC_LAUNCH();
-    crc_finish_kernel<<<E.G, 64, 0, s>>>(E);
+    crc_finish_kernel<<<E.G, 64, 0, s>>>(E, K);
 }
 
 }  // namespace stpc

@@ -774,28 +774,34 @@ void launch_fit_rows(const FitArgs& a, cudaStream_t s)
     }
 }
 
-// K3a: one warp per key-frame chain; for each of its runs and each P channel,
-// c' = f32(mean over valid span pixels of r * (d . n)), folded v-major over the
-// whole span in the reference's order, then the span re-test with (a, b, c').
-// Spans that pass mark their tiles class 1 in the channel and poison the
-// channel's pixels there (+inf) for pass 2.
+// K3a: one warp per (key-frame chain, P channel); for each run of the chain,
+// c' = f32(mean over the channel's valid span pixels of r * (d . n)), folded
+// v-major over the whole span in the reference's order, then the span re-test
+// with (a, b, c').  Spans that pass mark their tiles class 1 in the channel
+// and poison the channel's pixels there (+inf) for pass 2.  A second tiny
+// kernel sizes each chain's temporal records (18 B + presence bits + 4 B per
+// present P channel, bitstream.py:222-245).
 __global__ void __launch_bounds__(128) refit_kernel(RefitArgs A)
 {
     __shared__ double smem[4][32];
     const Geometry& g = A.g;
     const int lane = threadIdx.x & 31;
     double* sm = smem[threadIdx.x >> 5];
-    const long long kc = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-    if (kc >= (long long)A.n_groups * g.ty) return;
+    const int np = A.n - 1;
+    const long long wid = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (np < 1 || wid >= (long long)A.n_groups * g.ty * np) return;
+    const long long kc = wid / np;  // key chain
+    const int pi = (int)(wid % np);
+    const int chn = pi < A.k ? pi : pi + 1;
     const int grp = (int)(kc / g.ty);
     const int tr = (int)(kc % g.ty);
-    const int kframe = grp * A.n + A.k;
-    const long long kslot = (long long)kframe * g.ty + tr;
+    const long long kslot = ((long long)grp * A.n + A.k) * g.ty + tr;
     const int nr = A.n_runs[kslot];
     const int v0 = tr * g.th;
     const int rows = min(g.th, g.h - v0);
-    const int pm = (A.n + 7) / 8;
-    long long tbytes = 0;
+    const int frame = grp * A.n + chn;
+    double* img = A.best + (long long)frame * g.P;
+    uint8_t* crow = A.cls + ((long long)frame * g.ty + tr) * g.tx;
     for (int j = 0; j < nr; ++j) {
         const long long ri = kslot * g.tx + j;
         const int s = A.run_s[ri], len = A.run_len[ri];
@@ -805,19 +811,45 @@ __global__ void __launch_bounds__(128) refit_kernel(RefitArgs A)
         const int U = U1 - U0;
         const int npx = rows * U;
         const float ru = __frcp_rn((float)U);
-        uint8_t* okv = A.ref_ok + (kc * g.tx + j) * A.n;
-        float* cv = A.ref_c + (kc * g.tx + j) * A.n;
-        int present = 0;
-        for (int chn = 0; chn < A.n; ++chn) {
-            if (chn == A.k) continue;
-            const int frame = grp * A.n + chn;
-            double* img = A.best + (long long)frame * g.P;
-            double acc = 0.0;
-            int cnt = 0;
-            for (int base = 0; base < npx; base += 32) {
+        double acc = 0.0;
+        int cnt = 0;
+        for (int base = 0; base < npx; base += 32) {
+            int p = base + lane;
+            double prod = 0.0;
+            bool valid = false;
+            if (p < npx) {
+                int dv, du;
+                divmod_small(p, U, ru, dv, du);
+                int v = v0 + dv, u = U0 + du;
+                double r = img[(long long)v * g.w + u];
+                if (isfinite(r)) {
+                    double dx, dy, dz;
+                    ray_dir(A.tg, v, u, dx, dy, dz);
+                    double den = (dx + a * dy) + b * dz;
+                    prod = r * den;
+                    valid = true;
+                }
+            }
+            cnt += __popc(__ballot_sync(STPC_FULL, valid));
+            sm[lane] = prod;  // +0.0 for invalid pixels: exact (see fit_rows)
+            __syncwarp();
+            const int nj = min(32, npx - base);
+            if (nj == 32) {
+#pragma unroll
+                for (int jj = 0; jj < 32; ++jj) acc += sm[jj];
+            } else {
+                for (int jj = 0; jj < nj; ++jj) acc += sm[jj];
+            }
+            __syncwarp();
+        }
+        bool ok = false;
+        double c = 0.0;
+        if (cnt > 0) {
+            c = f32_round(acc / (double)cnt);
+            ok = true;
+            for (int base = 0; base < npx && ok; base += 32) {
                 int p = base + lane;
-                double prod = 0.0;
-                bool valid = false;
+                bool bad = false;
                 if (p < npx) {
                     int dv, du;
                     divmod_small(p, U, ru, dv, du);
@@ -826,69 +858,63 @@ __global__ void __launch_bounds__(128) refit_kernel(RefitArgs A)
                     if (isfinite(r)) {
                         double dx, dy, dz;
                         ray_dir(A.tg, v, u, dx, dy, dz);
-                        double den = (dx + a * dy) + b * dz;
-                        prod = r * den;
-                        valid = true;
+                        bad = !pixel_fits(r, dx, dy, dz, a, b, c, A.tau, A.r_max);
                     }
                 }
-                cnt += __popc(__ballot_sync(STPC_FULL, valid));
-                sm[lane] = prod;  // +0.0 for invalid pixels: exact (see fit_rows)
-                __syncwarp();
-                const int nj = min(32, npx - base);
-#pragma unroll 8
-                for (int jj = 0; jj < nj; ++jj) acc += sm[jj];
-                __syncwarp();
-            }
-            bool ok = false;
-            double c = 0.0;
-            if (cnt > 0) {
-                c = f32_round(acc / (double)cnt);
-                ok = true;
-                for (int base = 0; base < npx && ok; base += 32) {
-                    int p = base + lane;
-                    bool bad = false;
-                    if (p < npx) {
-                        int dv, du;
-                        divmod_small(p, U, ru, dv, du);
-                        int v = v0 + dv, u = U0 + du;
-                        double r = img[(long long)v * g.w + u];
-                        if (isfinite(r)) {
-                            double dx, dy, dz;
-                            ray_dir(A.tg, v, u, dx, dy, dz);
-                            bad = !pixel_fits(r, dx, dy, dz, a, b, c, A.tau, A.r_max);
-                        }
-                    }
-                    ok = !__any_sync(STPC_FULL, bad);
-                }
-            }
-            if (lane == 0) {
-                okv[chn] = ok;
-                cv[chn] = (float)c;
-            }
-            if (ok) {
-                present += 1;
-                uint8_t* crow = A.cls + ((long long)frame * g.ty + tr) * g.tx;
-                for (int tt = s + lane; tt < s + len; tt += 32) crow[tt] = 1;
-                for (int p = lane; p < npx; p += 32) {
-                    int dv, du;
-                    divmod_small(p, U, ru, dv, du);
-                    int v = v0 + dv, u = U0 + du;
-                    img[(long long)v * g.w + u] = __longlong_as_double(0x7ff0000000000000ll);
-                }
+                ok = !__any_sync(STPC_FULL, bad);
             }
         }
-        if (lane == 0) okv[A.k] = 1;
-        tbytes += 18 + pm + 4 * present;
+        const long long rj = (kc * g.tx + j) * A.n;
+        if (lane == 0) {
+            A.ref_ok[rj + chn] = ok;
+            A.ref_c[rj + chn] = (float)c;
+            if (pi == 0) A.ref_ok[rj + A.k] = 1;
+        }
+        if (ok) {
+            for (int tt = s + lane; tt < s + len; tt += 32) crow[tt] = 1;
+            for (int p = lane; p < npx; p += 32) {
+                int dv, du;
+                divmod_small(p, U, ru, dv, du);
+                img[(long long)(v0 + dv) * g.w + U0 + du] = __longlong_as_double(0x7ff0000000000000ll);
+            }
+        }
     }
-    if (lane == 0) A.chain_tbytes[kc] = tbytes;
+}
+
+// temporal record bytes per key chain: lanes over runs, popcount of present P channels
+__global__ void __launch_bounds__(128) record_bytes_kernel(RefitArgs A)
+{
+    const Geometry& g = A.g;
+    const int lane = threadIdx.x & 31;
+    const long long kc = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (kc >= (long long)A.n_groups * g.ty) return;
+    const int grp = (int)(kc / g.ty), tr = (int)(kc % g.ty);
+    const long long kslot = ((long long)grp * A.n + A.k) * g.ty + tr;
+    const int nr = A.n_runs[kslot];
+    const int pm = (A.n + 7) / 8;
+    long long tb = 0;
+    for (int j = lane; j < nr; j += 32) {
+        const uint8_t* okv = A.ref_ok + (kc * g.tx + j) * A.n;
+        int present = 0;
+        for (int c = 0; c < A.n; ++c) present += (c != A.k) && okv[c];
+        tb += 18 + pm + 4 * present;
+        if (A.n == 1) A.ref_ok[(kc * g.tx + j) * A.n + A.k] = 1;
+    }
+    for (int o = 16; o > 0; o >>= 1) tb += __shfl_xor_sync(STPC_FULL, tb, o);
+    if (lane == 0) A.chain_tbytes[kc] = tb;
 }
 
 void launch_refit(const RefitArgs& a, cudaStream_t s)
 {
-    long long warps = (long long)a.n_groups * a.g.ty;
-    if (warps <= 0) return;
+    long long kchains = (long long)a.n_groups * a.g.ty;
+    if (kchains <= 0) return;
+    long long warps = kchains * (a.n - 1);
+    if (warps > 0) {
+        STPC_LAUNCH();
+        refit_kernel<<<(unsigned)((warps + 3) / 4), 128, 0, s>>>(a);
+    }
     STPC_LAUNCH();
-    refit_kernel<<<(unsigned)((warps + 3) / 4), 128, 0, s>>>(a);
+    record_bytes_kernel<<<(unsigned)((kchains + 3) / 4), 128, 0, s>>>(a);
 }
 
 }  // namespace stpc

@@ -167,7 +167,11 @@ struct EntropyArgs {
 };
 constexpr int PACK_CHUNK = 4096;  // payload bytes per pack block
 constexpr int CRC_PIECE = 256;    // bytes per CRC thread
-constexpr int CRC_SEG = 64 * CRC_PIECE;
+constexpr int CRC_SEG = 32 * CRC_PIECE;  // bytes per CRC warp
+struct CrcConsts {
+    unsigned int x256[5];  // x^(8*256*2^l) mod P
+    unsigned int seg;      // x^(8*CRC_SEG) mod P
+};
 constexpr int HDR = 284;          // header + code-length table
 void launch_histogram(const EntropyArgs& a, int max_payload, cudaStream_t s);
 void launch_code_lengths(const EntropyArgs& a, cudaStream_t s);
