@@ -110,30 +110,56 @@ __device__ __forceinline__ void warp_add_stats(long long* fs, int rej, int drop,
 }
 
 // Fast bin decision in fp32 (SURVEY.md §7 "K1 convert").  The fp32 angles are
-// within ~6e-7 rad of the true ones (input rounding 2^-24 relative, atan2f
-// <= 2 ulp of a result <= pi); whenever both angles lie more than
+// within ~1.3e-6 rad of the true ones (input rounding 2^-24 relative plus the
+// polynomial atan below); whenever both angles lie more than
 // FAST_MARGIN = 1e-5 rad from a bin edge the floor is therefore the same as
 // the reference's fp64 (glibc) floor and the point is binned here.  The ~1%
 // of points inside the margin (and any point with coordinates outside
 // [1e-15, 1e15]) go to the exact fp64 path.  Returns false when undecided.
 constexpr double FAST_MARGIN = 1e-5;
 
+// atan2 for the fast path: odd minimax-style polynomial of degree 13 in
+// t = min/max (max error 3.2e-7 rad in float32 FMA evaluation, measured on
+// 2M points), reflections in double.  With the f32 input rounding the angle
+// is within ~1.3e-6 rad of the true one -- 8x inside FAST_MARGIN.
+__device__ __forceinline__ double fast_atan2(float y, float x)
+{
+    const float ax = fabsf(x), ay = fabsf(y);
+    const float mx = fmaxf(ax, ay), mn = fminf(ax, ay);
+    const float t = __fdividef(mn, mx);
+    const float s2 = t * t;
+    float p = 0.006811790633946657f;
+    p = __fmaf_rn(p, s2, -0.0336042121052742f);
+    p = __fmaf_rn(p, s2, 0.07962366193532944f);
+    p = __fmaf_rn(p, s2, -0.1323334127664566f);
+    p = __fmaf_rn(p, s2, 0.19807815551757812f);
+    p = __fmaf_rn(p, s2, -0.3331736922264099f);
+    p = __fmaf_rn(p, s2, 0.9999961256980896f);
+    double r = (double)p * (double)t;
+    if (ay > ax) r = 1.5707963267948966 - r;
+    if (x < 0.0f) r = 3.141592653589793 - r;
+    if (y < 0.0f) r = -r;
+    return r;
+}
+
 __device__ __forceinline__ bool fast_bin(double x, double y, double z, const Geometry& g, double inv_tr,
                                          double inv_pr, long long& u, long long& v)
 {
-    double m = fmax(fabs(x), fmax(fabs(y), fabs(z)));
-    if (!(m < 1e15 && m > 1e-15)) return false;
-    float xf = (float)x, yf = (float)y, zf = (float)z;
-    double th = (double)atan2f(xf, yf);
+    const float xf = (float)x, yf = (float)y, zf = (float)z;
+    const float mxy = fmaxf(fabsf(xf), fabsf(yf));
+    const float mall = fmaxf(mxy, fabsf(zf));
+    // keep squares and ratios in float range; degenerate directions go exact
+    if (!(mall < 1e15f && mxy > 1e-30f)) return false;
+    double th = fast_atan2(xf, yf);
     if (th < 0.0) th += 2.0 * 3.141592653589793;
-    double qu = th * inv_tr;
-    double ph = (double)atan2f(sqrtf(xf * xf + yf * yf), zf);
-    double qv = (ph - g.phi_offset) * inv_pr;
-    double flu = floor(qu), flv = floor(qv);
-    double fu = qu - flu, fv = qv - flv;
-    double mu = FAST_MARGIN * inv_tr, mv = FAST_MARGIN * inv_pr;
+    const double qu = th * inv_tr;
+    const double ph = fast_atan2(sqrtf(xf * xf + yf * yf), zf);
+    const double qv = (ph - g.phi_offset) * inv_pr;
+    const double flu = floor(qu), flv = floor(qv);
+    const double fu = qu - flu, fv = qv - flv;
+    const double mu = FAST_MARGIN * inv_tr, mv = FAST_MARGIN * inv_pr;
     if (fu < mu || fu > 1.0 - mu || fv < mv || fv > 1.0 - mv) return false;
-    long long uq = (long long)flu;  // qu >= 0
+    const long long uq = (long long)flu;  // qu >= 0
     u = uq < g.w ? uq : uq % (long long)g.w;
     v = (long long)flv;
     return true;

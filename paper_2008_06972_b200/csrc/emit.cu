@@ -51,8 +51,12 @@ __device__ __forceinline__ void word_masks(const Geometry& g, const uint8_t* vb,
     uint32_t valid = load_bits(vb, wd);
     int cls = 255;
     if (pix >= rw.rb && pix < rw.re && ((valid >> lane) & 1u)) {
-        int u = (int)(pix - rw.rb);
-        cls = crow[u / g.tw];
+        const int u = (int)(pix - rw.rb);
+        // u / tw without an integer divide (exact +-1 correction)
+        int q = __float2int_rz(((float)u + 0.5f) * __frcp_rn((float)g.tw));
+        const int r = u - q * g.tw;
+        q += r < 0 ? -1 : (r >= g.tw ? 1 : 0);
+        cls = crow[q];
     }
     res = __ballot_sync(STPC_FULL, cls == 0);
     tmp = __ballot_sync(STPC_FULL, cls == 1);
@@ -421,7 +425,15 @@ __global__ void __launch_bounds__(256) emit_residual_kernel(EmitArgs E)
             int rank = __popc(res & lt);
             double r = img[idx];
             bool e = (esc >> lane) & 1u;
-            uint32_t code = e ? 0xFFFFu : (uint32_t)(long long)rint(r / E.range_quant);
+            uint32_t code = 0xFFFFu;
+            if (!e) {
+                // rint(r / q) (bitstream.py:178): reciprocal estimate, exact
+                // IEEE division only when the estimate is near a .5 boundary
+                const double qa = r * E.inv_quant;
+                const double fr = qa - floor(qa);
+                code = fabs(fr - 0.5) > 1e-6 ? (uint32_t)(long long)rint(qa)
+                                             : (uint32_t)(long long)rint(r / E.range_quant);
+            }
             put_u16(cptr + 2 * rank, code);
             if (e) put_f32(eptr + 4 * __popc(esc & lt), (float)r);
         }

@@ -446,6 +446,7 @@ static int encode_impl(stpc_encoder* e, int G, const void* d_points, const int64
     ea.p = pa;
     ea.best = fa.best;
     ea.range_quant = e->cfg.range_quant;
+    ea.inv_quant = 1.0 / e->cfg.range_quant;
     ea.cfg_bytes = e->cfg_bytes.as<uint8_t>();
     ea.xf = e->xf.as<double>();
     ea.run_s = fa.run_s;

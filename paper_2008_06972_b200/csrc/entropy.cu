@@ -225,11 +225,21 @@ __global__ void __launch_bounds__(PACK_THREADS) pack_write_kernel(EntropyArgs E)
     const long long tb = b + (long long)threadIdx.x * PACK_PER_THREAD;
     uint8_t sym[PACK_PER_THREAD];
     int mybits = 0;
+    if (tb + PACK_PER_THREAD <= e) {  // 16-byte aligned (payload offsets are 16-aligned)
+        const uint4 v4 = *reinterpret_cast<const uint4*>(p + tb);
+        const uint32_t wv[4] = {v4.x, v4.y, v4.z, v4.w};
 #pragma unroll
-    for (int q = 0; q < PACK_PER_THREAD; ++q) {
-        long long i = tb + q;
-        sym[q] = i < e ? p[i] : 0;
-        mybits += i < e ? lens[sym[q]] : 0;
+        for (int q = 0; q < PACK_PER_THREAD; ++q) {
+            sym[q] = (uint8_t)(wv[q >> 2] >> (8 * (q & 3)));
+            mybits += lens[sym[q]];
+        }
+    } else {
+#pragma unroll
+        for (int q = 0; q < PACK_PER_THREAD; ++q) {
+            long long i = tb + q;
+            sym[q] = i < e ? p[i] : 0;
+            mybits += i < e ? lens[sym[q]] : 0;
+        }
     }
     long long inc = warp_incl_scan_ll(mybits);
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -238,18 +248,40 @@ __global__ void __launch_bounds__(PACK_THREADS) pack_write_kernel(EntropyArgs E)
     long long wbase = 0;
     for (int w = 0; w < wid; ++w) wbase += wsum[w];
     long long pos = lead + wbase + inc - mybits;  // bit position in buf
+    // Assemble this thread's bits into whole big-endian words: words strictly
+    // inside [pos, pos + mybits) belong to this thread alone (plain stores);
+    // only the first and last word can be shared with a neighbour (atomicOr).
+    {
+        const int w0 = (int)(pos >> 5);
+        int fill = (int)(pos & 31);  // bits already occupied in the current word
+        int wi = w0;
+        unsigned long long acc = 0;
+        int nacc = 0;
+        unsigned int cur = 0;
 #pragma unroll
-    for (int q = 0; q < PACK_PER_THREAD; ++q) {
-        long long i = tb + q;
-        if (i >= e) break;
-        int l = lens[sym[q]];
-        unsigned long long v = (unsigned long long)codes[sym[q]] << (64 - l);  // left-aligned
-        int wi = (int)(pos >> 5), sh = (int)(pos & 31);
-        unsigned long long win = v >> sh;  // spans words wi, wi+1
-        unsigned int hi = (unsigned int)(win >> 32), lo = (unsigned int)win;
-        if (hi) atomicOr(&buf[wi], hi);
-        if (lo) atomicOr(&buf[wi + 1], lo);
-        pos += l;
+        for (int q = 0; q < PACK_PER_THREAD; ++q) {
+            long long i = tb + q;
+            if (i >= e) break;
+            const int l = lens[sym[q]];
+            acc = (acc << l) | codes[sym[q]];
+            nacc += l;
+            while (fill + nacc >= 32) {
+                const int k = 32 - fill;
+                const unsigned int bits = (unsigned int)(acc >> (nacc - k)) & (k == 32 ? 0xffffffffu : ((1u << k) - 1u));
+                nacc -= k;
+                acc &= (nacc ? ((1ull << nacc) - 1ull) : 0ull);
+                cur |= bits;
+                if (wi == w0) atomicOr(&buf[wi], cur);
+                else buf[wi] = cur;
+                wi += 1;
+                fill = 0;
+                cur = 0;
+            }
+        }
+        if (nacc > 0) {
+            cur |= (unsigned int)(acc << (32 - fill - nacc));
+            atomicOr(&buf[wi], cur);
+        }
     }
     __syncthreads();
     long long total = 0;

@@ -138,7 +138,7 @@ void launch_group_scan(const long long* lens, long long* offs, int G, int align,
 struct EmitArgs {
     PlanArgs p;
     const double* best;
-    double range_quant;
+    double range_quant, inv_quant;
     const uint8_t* cfg_bytes;  // device [57]
     const double* xf;          // device [F][12]
     const uint16_t* run_s;
