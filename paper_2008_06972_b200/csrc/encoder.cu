@@ -111,6 +111,13 @@ struct stpc_encoder {
     int G = 0;
     std::vector<long long> h_payload_len, h_blob_off, h_enc_len;
     HostBuf h_sizes;
+    // chunked host pipeline (stpc_encode_host)
+    DevBuf pts2[2];
+    cudaStream_t copy_stream = nullptr;
+    cudaEvent_t ev_h2d[2] = {}, ev_done[2] = {};
+    bool host_result = false;            // last result assembled on the host
+    std::vector<long long> acc_payload;  // per group raw payload lengths
+    HostBuf acc_stats;                   // pinned [F][FS_COUNT]
     // profiling
     int profile = 0;
     cudaEvent_t ev[ST_COUNT + 1] = {};
@@ -120,6 +127,11 @@ struct stpc_encoder {
     {
         for (auto& x : ev)
             if (x) cudaEventDestroy(x);
+        for (int i = 0; i < 2; ++i) {
+            if (ev_h2d[i]) cudaEventDestroy(ev_h2d[i]);
+            if (ev_done[i]) cudaEventDestroy(ev_done[i]);
+        }
+        if (copy_stream) cudaStreamDestroy(copy_stream);
     }
     void mark(int st, cudaStream_t s)
     {
@@ -496,6 +508,7 @@ static int encode_impl(stpc_encoder* e, int G, const void* d_points, const int64
     launch_crc(en, s);
     CK(cudaGetLastError());
     e->G = G;
+    e->host_result = false;
     if (e->profile) {
         cudaEventRecord(e->ev[ST_COUNT], s);
         CK(cudaEventSynchronize(e->ev[ST_COUNT]));
@@ -550,22 +563,100 @@ int stpc_encode_host(stpc_encoder* enc, int32_t n_groups, const void* h_points,
         return STPC_ERR_ARG;
     }
     cudaStream_t s = (cudaStream_t)stream;
-    long long F = (long long)n_groups * enc->n;
-    long long npts = point_offsets[F] - point_offsets[0];
+    const int n = enc->n;
+    const long long F = (long long)n_groups * n;
     const size_t esz = enc->cfg.points_f64 ? sizeof(double) : sizeof(float);
-    ENS(enc->pts, esz * 3 * std::max<long long>(npts, 1));
-    if (npts > 0)
-        CK(cudaMemcpyAsync(enc->pts.p, (const char*)h_points + esz * 3 * point_offsets[0], esz * 3 * npts,
-                           cudaMemcpyHostToDevice, s));
-    std::vector<int64_t> off(point_offsets, point_offsets + F + 1);
-    for (auto& o : off) o -= point_offsets[0];
-    int rc = encode_impl(enc, n_groups, enc->pts.p, off.data(), transforms, s);
-    if (rc) return rc;
-    if (h_out) {
-        rc = stpc_result_copy_blobs(enc, h_out, out_cap, stream);
+    const char* hp = (const char*)h_points;
+    // Small batches: one H2D + encode + D2H.
+    const int n_chunks = n_groups >= 64 ? 8 : 1;
+    if (n_chunks == 1 || !h_out) {
+        long long npts = point_offsets[F] - point_offsets[0];
+        ENS(enc->pts, esz * 3 * std::max<long long>(npts, 1));
+        if (npts > 0)
+            CK(cudaMemcpyAsync(enc->pts.p, hp + esz * 3 * point_offsets[0], esz * 3 * npts,
+                               cudaMemcpyHostToDevice, s));
+        std::vector<int64_t> off(point_offsets, point_offsets + F + 1);
+        for (auto& o : off) o -= point_offsets[0];
+        int rc = encode_impl(enc, n_groups, enc->pts.p, off.data(), transforms, s);
         if (rc) return rc;
+        if (h_out) {
+            rc = stpc_result_copy_blobs(enc, h_out, out_cap, stream);
+            if (rc) return rc;
+        }
+        CK(cudaStreamSynchronize(s));
+        return STPC_OK;
     }
+    // Pipelined: the H2D of chunk c+1 (copy stream, double-buffered device
+    // points) overlaps the encode and blob D2H of chunk c (stream s).
+    if (!enc->copy_stream) {
+        CK(cudaStreamCreateWithFlags(&enc->copy_stream, cudaStreamNonBlocking));
+        for (int i = 0; i < 2; ++i) {
+            CK(cudaEventCreateWithFlags(&enc->ev_h2d[i], cudaEventDisableTiming));
+            CK(cudaEventCreateWithFlags(&enc->ev_done[i], cudaEventDisableTiming));
+        }
+    }
+    const int gc = (n_groups + n_chunks - 1) / n_chunks;
+    long long max_pts = 1;
+    for (int c = 0; c < n_chunks; ++c) {
+        int g0 = c * gc, g1 = std::min(n_groups, g0 + gc);
+        if (g0 >= g1) break;
+        max_pts = std::max<long long>(max_pts, point_offsets[(long long)g1 * n] - point_offsets[(long long)g0 * n]);
+    }
+    ENS(enc->pts2[0], esz * 3 * max_pts);
+    ENS(enc->pts2[1], esz * 3 * max_pts);
+    ENS(enc->acc_stats, sizeof(long long) * FS_COUNT * F);
+    std::vector<long long> blob_off(n_groups + 1, 0), enc_len(n_groups, 0), payload(n_groups, 0);
+    auto h2d = [&](int c) -> int {
+        const int b = c & 1;
+        const int g0 = c * gc, g1 = std::min(n_groups, g0 + gc);
+        const long long p0 = point_offsets[(long long)g0 * n], p1 = point_offsets[(long long)g1 * n];
+        CK(cudaStreamWaitEvent(enc->copy_stream, enc->ev_done[b], 0));
+        if (p1 > p0)
+            CK(cudaMemcpyAsync(enc->pts2[b].p, hp + esz * 3 * p0, esz * 3 * (p1 - p0), cudaMemcpyHostToDevice,
+                               enc->copy_stream));
+        CK(cudaEventRecord(enc->ev_h2d[b], enc->copy_stream));
+        return STPC_OK;
+    };
+    int rc = h2d(0);
+    if (rc) return rc;
+    long long out_pos = 0;
+    for (int c = 0; c < n_chunks; ++c) {
+        const int g0 = c * gc, g1 = std::min(n_groups, g0 + gc);
+        if (g0 >= g1) break;
+        const int b = c & 1;
+        if (c + 1 < n_chunks && (c + 1) * gc < n_groups) {
+            rc = h2d(c + 1);
+            if (rc) return rc;
+        }
+        CK(cudaStreamWaitEvent(s, enc->ev_h2d[b], 0));
+        const long long f0 = (long long)g0 * n, f1 = (long long)g1 * n;
+        std::vector<int64_t> off(point_offsets + f0, point_offsets + f1 + 1);
+        for (auto& o : off) o -= point_offsets[f0];
+        rc = encode_impl(enc, g1 - g0, enc->pts2[b].p, off.data(), transforms + 12 * f0, s);
+        if (rc) return rc;
+        CK(cudaEventRecord(enc->ev_done[b], s));
+        const long long total = enc->h_blob_off[g1 - g0];
+        if (out_pos + total > out_cap) {
+            g_err = "output buffer too small";
+            return STPC_ERR_ARG;
+        }
+        if (total > 0) CK(cudaMemcpyAsync(h_out + out_pos, enc->blobs.p, (size_t)total, cudaMemcpyDeviceToHost, s));
+        CK(cudaMemcpyAsync(enc->acc_stats.as<long long>() + FS_COUNT * f0, enc->fstats.p,
+                           sizeof(long long) * FS_COUNT * (f1 - f0), cudaMemcpyDeviceToHost, s));
+        for (int i = 0; i < g1 - g0; ++i) {
+            blob_off[g0 + i] = out_pos + enc->h_blob_off[i];
+            enc_len[g0 + i] = enc->h_enc_len[i];
+            payload[g0 + i] = enc->h_payload_len[i];
+        }
+        out_pos += total;
+    }
+    blob_off[n_groups] = out_pos;
     CK(cudaStreamSynchronize(s));
+    enc->G = n_groups;
+    enc->h_blob_off = blob_off;
+    enc->h_enc_len = enc_len;
+    enc->h_payload_len = payload;
+    enc->host_result = true;
     return STPC_OK;
 }
 
@@ -589,11 +680,19 @@ int stpc_result_payload_lengths(const stpc_encoder* enc, int64_t* raw_lengths)
     return STPC_OK;
 }
 
-const uint8_t* stpc_result_device_blobs(const stpc_encoder* enc) { return enc ? enc->blobs.as<uint8_t>() : nullptr; }
+const uint8_t* stpc_result_device_blobs(const stpc_encoder* enc)
+{
+    // after a pipelined stpc_encode_host the blobs live in the caller's buffer
+    return (enc && !enc->host_result) ? enc->blobs.as<uint8_t>() : nullptr;
+}
 
 int stpc_result_copy_blobs(const stpc_encoder* enc, uint8_t* h_dst, int64_t cap, void* stream)
 {
     if (!enc || !h_dst) return STPC_ERR_ARG;
+    if (enc->host_result) {
+        g_err = "blobs of a pipelined host encode are already in the caller's buffer";
+        return STPC_ERR_ARG;
+    }
     long long total = enc->G ? enc->h_blob_off[enc->G] : 0;
     if (total > cap) {
         g_err = "output buffer too small: need " + std::to_string(total);
@@ -608,8 +707,12 @@ int stpc_result_copy_blobs(const stpc_encoder* enc, uint8_t* h_dst, int64_t cap,
 int stpc_result_frame_stats(const stpc_encoder* enc, int64_t* out)
 {
     if (!enc || !out) return STPC_ERR_ARG;
-    CK(cudaMemcpy(out, enc->fstats.p, sizeof(long long) * (size_t)enc->G * enc->n * FS_COUNT,
-                  cudaMemcpyDeviceToHost));
+    const size_t bytes = sizeof(long long) * (size_t)enc->G * enc->n * FS_COUNT;
+    if (enc->host_result) {
+        memcpy(out, enc->acc_stats.p, bytes);
+        return STPC_OK;
+    }
+    CK(cudaMemcpy(out, enc->fstats.p, bytes, cudaMemcpyDeviceToHost));
     return STPC_OK;
 }
 
