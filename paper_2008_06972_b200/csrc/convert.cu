@@ -28,6 +28,30 @@ __global__ void fill_u64_kernel(unsigned long long* p, unsigned long long v, lon
     for (; i < n; i += stride) p[i] = v;
 }
 
+// Zeroing by kernel rather than cudaMemsetAsync: memsets may be executed by a
+// copy engine and would queue behind a large concurrent H2D (the pipelined
+// host encode overlaps exactly such copies with compute).
+__global__ void zero_bytes_kernel(uint8_t* p, long long n)
+{
+    long long i = ((long long)blockIdx.x * blockDim.x + threadIdx.x) * 16;
+    const long long stride = (long long)gridDim.x * blockDim.x * 16;
+    for (; i < n; i += stride) {
+        if (i + 16 <= n && (((uintptr_t)(p + i)) & 15) == 0) {
+            *reinterpret_cast<uint4*>(p + i) = make_uint4(0, 0, 0, 0);
+        } else {
+            for (long long j = i; j < min(i + 16, n); ++j) p[j] = 0;
+        }
+    }
+}
+
+void launch_zero(void* p, long long bytes, cudaStream_t s)
+{
+    if (bytes <= 0) return;
+    int blocks = (int)std::min<long long>((bytes / 16 + 255) / 256 + 1, 148 * 16);
+    STPC_LAUNCH();
+    zero_bytes_kernel<<<blocks, 256, 0, s>>>((uint8_t*)p, bytes);
+}
+
 void launch_fill_u64(unsigned long long* p, unsigned long long v, long long n, cudaStream_t s)
 {
     if (n <= 0) return;
@@ -360,7 +384,7 @@ static dim3 chunk_grid(int max_pts, int n_frames)
 void launch_convert(const ConvertArgs& a, int max_pts, cudaStream_t s)
 {
     if (a.n_frames <= 0) return;
-    cudaMemsetAsync(a.q_count, 0, sizeof(unsigned long long), s);
+    launch_zero(a.q_count, sizeof(unsigned long long), s);
     STPC_LAUNCH();
     if (a.pts_f64)
         convert_kernel<double><<<chunk_grid<double>(max_pts, a.n_frames), 256, 0, s>>>(a, (const double*)a.pts);

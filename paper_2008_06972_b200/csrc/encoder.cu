@@ -7,6 +7,8 @@
 //   [sync: payload sizes] -> payload emission -> histogram -> Huffman code
 //   lengths [sync: blob sizes] -> bit packing -> CRC + header.
 #include <cstdio>
+#include <cstdlib>
+#include <chrono>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -282,8 +284,12 @@ void stpc_encoder_destroy(stpc_encoder* enc) { delete enc; }
         if (r_) return r_;                 \
     } while (0)
 
+// d_off/d_xf: the same offsets/transforms already in device memory (the
+// pipelined host path uploads them once, so no H2D is queued behind the big
+// point copies), or nullptr to upload here.
 static int encode_impl(stpc_encoder* e, int G, const void* d_points, const int64_t* h_off,
-                       const double* h_xf, cudaStream_t s)
+                       const double* h_xf, cudaStream_t s, const long long* d_off = nullptr,
+                       const double* d_xf = nullptr)
 {
     const Geometry& g = e->g;
     const int n = e->n, k = e->k;
@@ -291,17 +297,23 @@ static int encode_impl(stpc_encoder* e, int G, const void* d_points, const int64
     const long long TT = (long long)g.tx * g.ty;
     e->mark(ST_INIT, s);
     // --- inputs (offsets + transforms through pinned staging)
-    ENS(e->h_stage, sizeof(long long) * (F + 1) + sizeof(double) * 12 * F);
-    long long* st_off = e->h_stage.as<long long>();
-    double* st_xf = reinterpret_cast<double*>(st_off + F + 1);
     long long max_pts = 0;
-    for (long long f = 0; f <= F; ++f) st_off[f] = h_off[f];
     for (long long f = 0; f < F; ++f) max_pts = std::max<long long>(max_pts, h_off[f + 1] - h_off[f]);
-    memcpy(st_xf, h_xf, sizeof(double) * 12 * F);
-    ENS(e->pt_off, sizeof(long long) * (F + 1));
-    ENS(e->xf, sizeof(double) * 12 * F);
-    CK(cudaMemcpyAsync(e->pt_off.p, st_off, sizeof(long long) * (F + 1), cudaMemcpyHostToDevice, s));
-    CK(cudaMemcpyAsync(e->xf.p, st_xf, sizeof(double) * 12 * F, cudaMemcpyHostToDevice, s));
+    const long long* dev_off = d_off;
+    const double* dev_xf = d_xf;
+    if (!dev_off) {
+        ENS(e->h_stage, sizeof(long long) * (F + 1) + sizeof(double) * 12 * F);
+        long long* st_off = e->h_stage.as<long long>();
+        double* st_xf = reinterpret_cast<double*>(st_off + F + 1);
+        for (long long f = 0; f <= F; ++f) st_off[f] = h_off[f];
+        memcpy(st_xf, h_xf, sizeof(double) * 12 * F);
+        ENS(e->pt_off, sizeof(long long) * (F + 1));
+        ENS(e->xf, sizeof(double) * 12 * F);
+        CK(cudaMemcpyAsync(e->pt_off.p, st_off, sizeof(long long) * (F + 1), cudaMemcpyHostToDevice, s));
+        CK(cudaMemcpyAsync(e->xf.p, st_xf, sizeof(double) * 12 * F, cudaMemcpyHostToDevice, s));
+        dev_off = e->pt_off.as<long long>();
+        dev_xf = e->xf.as<double>();
+    }
     // --- workspace
     ENS(e->best, sizeof(double) * F * g.P);
     ENS(e->vbits, (size_t)F * g.pbs);
@@ -334,8 +346,8 @@ static int encode_impl(stpc_encoder* e, int G, const void* d_points, const int64
     ENS(e->blob_off, sizeof(long long) * (G + 1));
     ENS(e->h_sizes, sizeof(long long) * (3 * G + 2));
 
-    CK(cudaMemsetAsync(e->fstats.p, 0, sizeof(long long) * F * FS_COUNT, s));
-    CK(cudaMemsetAsync(e->cls.p, 0, (size_t)F * TT, s));
+    launch_zero(e->fstats.p, sizeof(long long) * F * FS_COUNT, s);
+    launch_zero(e->cls.p, (long long)F * TT, s);
     launch_fill_u64(e->best.as<unsigned long long>(), 0x7ff0000000000000ull, F * g.P, s);
 
     e->mark(ST_CONVERT, s);
@@ -343,8 +355,8 @@ static int encode_impl(stpc_encoder* e, int G, const void* d_points, const int64
     ConvertArgs ca;
     ca.pts = d_points;
     ca.pts_f64 = e->cfg.points_f64;
-    ca.pt_off = e->pt_off.as<long long>();
-    ca.xf = e->xf.as<double>();
+    ca.pt_off = dev_off;
+    ca.xf = dev_xf;
     ca.n_frames = (int)F;
     ca.g = g;
     ca.best = e->best.as<unsigned long long>();
@@ -460,7 +472,7 @@ static int encode_impl(stpc_encoder* e, int G, const void* d_points, const int64
     ea.range_quant = e->cfg.range_quant;
     ea.inv_quant = 1.0 / e->cfg.range_quant;
     ea.cfg_bytes = e->cfg_bytes.as<uint8_t>();
-    ea.xf = e->xf.as<double>();
+    ea.xf = dev_xf;
     ea.run_s = fa.run_s;
     ea.run_len = fa.run_len;
     ea.run_abc = fa.run_abc;
@@ -482,7 +494,7 @@ static int encode_impl(stpc_encoder* e, int G, const void* d_points, const int64
     en.enc_len = e->enc_len.as<long long>();
     en.blob_off = e->blob_off.as<long long>();
     en.max_chunks = (int)((max_payload + PACK_CHUNK - 1) / PACK_CHUNK);
-    CK(cudaMemsetAsync(en.hist, 0, sizeof(unsigned) * 256 * G, s));
+    launch_zero(en.hist, sizeof(unsigned) * 256 * G, s);
     launch_histogram(en, (int)max_payload, s);
     launch_code_lengths(en, s);
     launch_group_scan(en.enc_len, en.blob_off, G, 16, HDR, s);
@@ -501,7 +513,7 @@ static int encode_impl(stpc_encoder* e, int G, const void* d_points, const int64
     en.chunk_bits = e->chunk_bits.as<long long>();
     en.seg_crc = e->seg_crc.as<unsigned>();
     en.blobs = e->blobs.as<uint8_t>();
-    CK(cudaMemsetAsync(en.blobs, 0, (size_t)blob_total, s));
+    launch_zero(en.blobs, blob_total, s);
     e->mark(ST_PACK, s);
     launch_pack(en, s);
     e->mark(ST_CRC, s);
@@ -605,6 +617,25 @@ int stpc_encode_host(stpc_encoder* enc, int32_t n_groups, const void* h_points,
     ENS(enc->pts2[0], esz * 3 * max_pts);
     ENS(enc->pts2[1], esz * 3 * max_pts);
     ENS(enc->acc_stats, sizeof(long long) * FS_COUNT * F);
+    // all chunks' (rebased) offsets and transforms go up once, before the big
+    // point copies, so encode_impl queues no H2D behind them
+    ENS(enc->h_stage, sizeof(long long) * (F + n_chunks) + sizeof(double) * 12 * F);
+    ENS(enc->pt_off, sizeof(long long) * (F + n_chunks));
+    ENS(enc->xf, sizeof(double) * 12 * F);
+    {
+        long long* st_off = enc->h_stage.as<long long>();
+        double* st_xf = reinterpret_cast<double*>(st_off + F + n_chunks);
+        for (int c = 0; c < n_chunks; ++c) {
+            const int g0 = c * gc, g1 = std::min(n_groups, g0 + gc);
+            if (g0 >= g1) break;
+            const long long f0 = (long long)g0 * n, f1 = (long long)g1 * n;
+            for (long long f = f0; f <= f1; ++f) st_off[f + c] = point_offsets[f] - point_offsets[f0];
+        }
+        memcpy(st_xf, transforms, sizeof(double) * 12 * F);
+        CK(cudaMemcpyAsync(enc->pt_off.p, st_off, sizeof(long long) * (F + n_chunks), cudaMemcpyHostToDevice, s));
+        CK(cudaMemcpyAsync(enc->xf.p, st_xf, sizeof(double) * 12 * F, cudaMemcpyHostToDevice, s));
+        CK(cudaStreamSynchronize(s));
+    }
     std::vector<long long> blob_off(n_groups + 1, 0), enc_len(n_groups, 0), payload(n_groups, 0);
     auto h2d = [&](int c) -> int {
         const int b = c & 1;
@@ -617,24 +648,40 @@ int stpc_encode_host(stpc_encoder* enc, int32_t n_groups, const void* h_points,
         CK(cudaEventRecord(enc->ev_h2d[b], enc->copy_stream));
         return STPC_OK;
     };
+    // optional timeline (STPC_PIPE_TRACE=1): per chunk H2D end / encode end
+    const bool trace = getenv("STPC_PIPE_TRACE") != nullptr;
+    std::vector<cudaEvent_t> tev;
+    cudaEvent_t t0 = nullptr;
+    if (trace) {
+        cudaEventCreate(&t0);
+        cudaEventRecord(t0, s);
+    }
     int rc = h2d(0);
     if (rc) return rc;
+    if (trace) { tev.emplace_back(); cudaEventCreate(&tev.back()); cudaEventRecord(tev.back(), enc->copy_stream); }
     long long out_pos = 0;
     for (int c = 0; c < n_chunks; ++c) {
         const int g0 = c * gc, g1 = std::min(n_groups, g0 + gc);
         if (g0 >= g1) break;
         const int b = c & 1;
         if (c + 1 < n_chunks && (c + 1) * gc < n_groups) {
+            auto hA = std::chrono::steady_clock::now();
             rc = h2d(c + 1);
+            if (trace)
+                fprintf(stderr, "host: h2d(%d) enqueue took %.2f ms\n", c + 1,
+                        std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - hA).count());
             if (rc) return rc;
+            if (trace) { tev.emplace_back(); cudaEventCreate(&tev.back()); cudaEventRecord(tev.back(), enc->copy_stream); }
         }
         CK(cudaStreamWaitEvent(s, enc->ev_h2d[b], 0));
         const long long f0 = (long long)g0 * n, f1 = (long long)g1 * n;
         std::vector<int64_t> off(point_offsets + f0, point_offsets + f1 + 1);
         for (auto& o : off) o -= point_offsets[f0];
-        rc = encode_impl(enc, g1 - g0, enc->pts2[b].p, off.data(), transforms + 12 * f0, s);
+        rc = encode_impl(enc, g1 - g0, enc->pts2[b].p, off.data(), transforms + 12 * f0, s,
+                         enc->pt_off.as<long long>() + f0 + c, enc->xf.as<double>() + 12 * f0);
         if (rc) return rc;
         CK(cudaEventRecord(enc->ev_done[b], s));
+        if (trace) { tev.emplace_back(); cudaEventCreate(&tev.back()); cudaEventRecord(tev.back(), s); }
         const long long total = enc->h_blob_off[g1 - g0];
         if (out_pos + total > out_cap) {
             g_err = "output buffer too small";
@@ -652,6 +699,16 @@ int stpc_encode_host(stpc_encoder* enc, int32_t n_groups, const void* h_points,
     }
     blob_off[n_groups] = out_pos;
     CK(cudaStreamSynchronize(s));
+    if (trace) {
+        cudaDeviceSynchronize();
+        for (size_t i = 0; i < tev.size(); ++i) {
+            float ms = 0.f;
+            cudaEventElapsedTime(&ms, t0, tev[i]);
+            fprintf(stderr, "pipe ev %zu at %.2f ms\n", i, ms);
+            cudaEventDestroy(tev[i]);
+        }
+        cudaEventDestroy(t0);
+    }
     enc->G = n_groups;
     enc->h_blob_off = blob_off;
     enc->h_enc_len = enc_len;
@@ -767,7 +824,7 @@ int stpc_project(const void* d_points, int32_t points_f64, const int64_t* point_
     ENS(fs, sizeof(long long) * FS_COUNT * n_frames);
     CK(cudaMemcpyAsync(off.p, point_offsets, sizeof(long long) * (n_frames + 1), cudaMemcpyHostToDevice, s));
     CK(cudaMemcpyAsync(xf.p, transforms, sizeof(double) * 12 * n_frames, cudaMemcpyHostToDevice, s));
-    CK(cudaMemsetAsync(fs.p, 0, sizeof(long long) * FS_COUNT * n_frames, s));
+    launch_zero(fs.p, sizeof(long long) * FS_COUNT * n_frames, s);
     launch_fill_u64((unsigned long long*)d_best, 0x7ff0000000000000ull, n_frames * g.P, s);
     ConvertArgs ca;
     ca.pts = d_points;

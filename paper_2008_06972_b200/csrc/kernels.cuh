@@ -60,6 +60,7 @@ struct ConvertArgs {
 };
 
 void launch_fill_u64(unsigned long long* p, unsigned long long v, long long n, cudaStream_t s);
+void launch_zero(void* p, long long bytes, cudaStream_t s);
 void launch_convert(const ConvertArgs& a, int max_pts, cudaStream_t s);
 void launch_convert_win(const ConvertArgs& a, int max_pts, cudaStream_t s);
 void launch_bitmaps(const double* best, int n_frames, const Geometry& g, double range_quant,
