@@ -225,15 +225,40 @@ def algorithmic_bytes(stage, cfg, n, G, npts):
     F = G * n
     if stage == "convert":
         return 12 * npts + 8 * P * F + P / 8 * F
-    if stage == "fit_key":
+    if stage in ("fit_key", "start_key"):
         return G * (8 * P + P / 8)
-    if stage == "fit_p":
+    if stage in ("fit_p", "start_p"):
         return G * (n - 1) * (8 * P + P / 8)
     if stage == "refit":
         return G * (n - 1) * (8 * P + P / 8)
     if stage == "bitmaps":
         return F * (8 * P + 2 * P / 8)
     return None
+
+
+# stage -> (kernel name in the ncu capture, which of its launches)
+_NCU_KERNEL = {"fit_p": ("fit_pair_kernel", -1), "fit_key": ("fit_pair_kernel", 0),
+               "convert": ("void convert_kernel<float>", 0)}
+
+
+def ncu_traffic(stage, args, G):
+    """dram__bytes_read + dram__bytes_write per launch of the stage's kernel,
+    from the committed `ncu --set full` capture of this exact workload
+    (profiles/r1_ncu_full_1024groups.json), else null."""
+    path = os.path.join(ROOT, "profiles", "r1_ncu_full_1024groups.json")
+    if stage not in _NCU_KERNEL or args.config != 4 or G != 1024 or args.tile or args.tau:
+        return {"traffic": None}
+    try:
+        rows = json.load(open(path))
+        name, idx = _NCU_KERNEL[stage]
+        rows = [r for r in rows if r["kernel"] == name]
+        r = rows[idx]
+        scale = {"Gbyte": 1e9, "Mbyte": 1e6, "Kbyte": 1e3, "byte": 1.0}
+        t = r["dram_read"] * scale[r["dram_read_unit"]] + r["dram_write"] * scale[r["dram_write_unit"]]
+        return {"traffic": t, "traffic_unit": "bytes/launch",
+                "traffic_source": "profiles/r1_ncu_full_1024groups.json (ncu --set full, same workload)"}
+    except Exception:
+        return {"traffic": None}
 
 
 def main():
@@ -382,6 +407,7 @@ def main():
                 "achieved": (ab / (dom_ms / 1e3) / 1e9) if ab else None, "peak": peak,
                 "peak_source": peak_src, "unit": "GB/s", "traffic": None}
     roofline["frac"] = roofline["achieved"] / peak if roofline["achieved"] else None
+    roofline.update(ncu_traffic(dom, args, G))
     conv_ms = float(stage_ms[names.index("convert")])
     conv_ab = algorithmic_bytes("convert", cfg, n, G, npts)
     roofline["convert"] = {"ms": conv_ms, "achieved": conv_ab / (conv_ms / 1e3) / 1e9,

@@ -23,10 +23,10 @@ unsigned long long stpc::g_launch_count = 0;
 static thread_local std::string g_err;
 
 // pipeline stages timed with CUDA events when profiling is enabled
-enum Stage { ST_INIT, ST_CONVERT, ST_BITMAP, ST_FIT_K, ST_REFIT, ST_FIT_P, ST_PLAN, ST_EMIT,
-             ST_HUFF, ST_PACK, ST_CRC, ST_COUNT };
-static const char* kStageNames[ST_COUNT] = {"init", "convert", "bitmaps", "fit_key", "refit", "fit_p",
-                                            "plan", "emit", "huffman", "pack", "crc"};
+enum Stage { ST_INIT, ST_CONVERT, ST_BITMAP, ST_START_K, ST_FIT_K, ST_REFIT, ST_START_P, ST_FIT_P,
+             ST_PLAN, ST_EMIT, ST_HUFF, ST_PACK, ST_CRC, ST_COUNT };
+static const char* kStageNames[ST_COUNT] = {"init", "convert", "bitmaps", "start_key", "fit_key", "refit",
+                                            "start_p", "fit_p", "plan", "emit", "huffman", "pack", "crc"};
 
 #define CK(x)                                                                         \
     do {                                                                              \
@@ -398,8 +398,10 @@ static int encode_impl(stpc_encoder* e, int G, const void* d_points, const int64
     fa.n_runs = e->n_runs.as<int>();
     fa.cert = e->cert.as<float4>();
     fa.start_ok = e->start_ok.as<uint8_t>();
+    e->mark(ST_START_K, s);
+    launch_start_tiles(fa, s);
     e->mark(ST_FIT_K, s);
-    launch_fit_rows(fa, s);
+    launch_fit_chains(fa, s);
 
     RefitArgs ra;
     ra.best = e->best.as<double>();
@@ -421,12 +423,14 @@ static int encode_impl(stpc_encoder* e, int G, const void* d_points, const int64
     e->mark(ST_REFIT, s);
     launch_refit(ra, s);
 
-    e->mark(ST_FIT_P, s);
+    e->mark(ST_START_P, s);
     if (n > 1) {
         fa.mode = 1;
         fa.n_jobs = G * (n - 1);
-        launch_fit_rows(fa, s);
+        launch_start_tiles(fa, s);
     }
+    e->mark(ST_FIT_P, s);
+    if (n > 1) launch_fit_chains(fa, s);
 
     e->mark(ST_PLAN, s);
     // --- residual stats + plan

@@ -630,6 +630,44 @@ __global__ void __launch_bounds__(FIT_WARPS * 32, 5) fit_pair_kernel(FitArgs A)
                 else done = true;
             }
         }
+        // ---- (1b) pass 2: a growing run extends over temporally covered
+        // (class-1, fully masked) tiles without changing its sums, plane or
+        // verdict; skip the whole stretch at once, certifying the tiles empty
+        if (__any_sync(STPC_FULL, !done && grow && ch.skip1 && crow[t] == 1)) {
+            const bool sk = !done && grow && ch.skip1 && crow[t] == 1;
+            int nt = g.tx;
+            bool found = false;
+            int base = t;
+            while (__any_sync(STPC_FULL, sk && !found && base < g.tx)) {
+                const int j = base + gl;
+                const bool f = sk && !found && j < g.tx && crow[j] != 1;
+                const unsigned mm = (__ballot_sync(STPC_FULL, f) & gmask) >> (sub * 16);
+                if (mm && !found) {
+                    nt = base + __ffs(mm) - 1;
+                    found = true;
+                }
+                base += PG;
+            }
+            if (sk) {
+                for (int tt = t + gl; tt < nt; tt += PG)
+                    ch.cert[CERT_F4 * tt] = make_float4(0.f, 0.f, 0.f, CERT_EMPTY);
+                t = nt;
+                if (t >= g.tx) {  // the run reaches the row end
+                    if (gl == 0) {
+                        rs[n_runs] = (uint16_t)s;
+                        rl[n_runs] = (uint16_t)(g.tx - s);
+                        rabc[3 * n_runs] = (float)a;
+                        rabc[3 * n_runs + 1] = (float)b;
+                        rabc[3 * n_runs + 2] = (float)c;
+                    }
+                    for (int tt = s + gl; tt < g.tx; tt += PG)
+                        if (crow[tt] != 1) crow[tt] = run_cls;
+                    n_runs += 1;
+                    grow = false;
+                    done = true;
+                }
+            }
+        }
         // ---- (2) fold tile t (a start folds from zero)
         const bool live = !done;
         if (live && !grow) acc = 0.0;
@@ -758,13 +796,18 @@ __global__ void __launch_bounds__(FIT_WARPS * 32, 5) fit_pair_kernel(FitArgs A)
     if (cid < n_chains && gl == 0) A.n_runs[slot] = n_runs;
 }
 
-void launch_fit_rows(const FitArgs& a, cudaStream_t s)
+void launch_start_tiles(const FitArgs& a, cudaStream_t s)
+{
+    long long tiles = (long long)a.n_jobs * a.g.ty * a.g.tx;
+    if (tiles <= 0) return;
+    STPC_LAUNCH();
+    start_tiles_kernel<<<(unsigned)((tiles + 255) / 256), 256, 0, s>>>(a);
+}
+
+void launch_fit_chains(const FitArgs& a, cudaStream_t s)
 {
     long long warps = (long long)a.n_jobs * a.g.ty;
     if (warps <= 0) return;
-    long long tiles = warps * a.g.tx;
-    STPC_LAUNCH();
-    start_tiles_kernel<<<(unsigned)((tiles + 255) / 256), 256, 0, s>>>(a);
     STPC_LAUNCH();
     if (a.g.tw * a.g.th <= PG) {
         long long pairs = (warps + 1) / 2;
@@ -772,6 +815,12 @@ void launch_fit_rows(const FitArgs& a, cudaStream_t s)
     } else {
         fit_rows_kernel<<<(unsigned)((warps + FIT_WARPS - 1) / FIT_WARPS), FIT_WARPS * 32, 0, s>>>(a);
     }
+}
+
+void launch_fit_rows(const FitArgs& a, cudaStream_t s)
+{
+    launch_start_tiles(a, s);
+    launch_fit_chains(a, s);
 }
 
 // K3a: one warp per (key-frame chain, P channel); for each run of the chain,

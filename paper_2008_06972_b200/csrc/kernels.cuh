@@ -82,7 +82,9 @@ struct FitArgs {
     float4* cert;       // [F*TY][TX][3] per-tile test certificates (scratch)
     uint8_t* start_ok;  // [F*TY][TX] start verdicts (scratch)
 };
-void launch_fit_rows(const FitArgs& a, cudaStream_t s);
+void launch_fit_rows(const FitArgs& a, cudaStream_t s);  // = start_tiles + fit_chains
+void launch_start_tiles(const FitArgs& a, cudaStream_t s);
+void launch_fit_chains(const FitArgs& a, cudaStream_t s);
 
 struct RefitArgs {
     double* best;  // covered P-frame pixels are overwritten with +inf
