@@ -283,9 +283,144 @@ __device__ bool union_fits(const Chain& ch, const Geometry& g, const Trig& tg, i
 // stores the tile's certificate (whose plane is the start plane).  The
 // chains then skip residual tiles with a byte lookup.
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(256) start_tiles_kernel(FitArgs A)
+// TW x TH > 0: compile-time tile shape (all pixel loads issued up front);
+// 0 x 0: runtime shape.
+// Start verdicts, staged: a block of START_TPB threads owns START_TPB
+// consecutive tiles of one tile-row.  Thread-per-tile pixel reads would put
+// every lane in a different 32-byte sector (the kernel measured L1-wavefront
+// bound), so the block first copies its slab -- rows [v0, v1) x the tiles'
+// columns -- and the column trig factors into shared memory with coalesced
+// loads, tile-major with one double of padding per tile (conflict-free
+// per-thread reads), then each thread folds, solves and tests its own tile.
+constexpr int START_TPB = 128;
+constexpr int START_MAXPX = 16;  // staged path: tiles of up to 16 pixels
+
+template <int TW>
+__global__ void __launch_bounds__(START_TPB) start_tiles_staged_kernel(FitArgs A)
+{
+    constexpr int STRIDE = START_MAXPX + 1;
+    __shared__ double s_r[START_TPB * STRIDE];
+    __shared__ double s_st[START_TPB * (TW + 1)], s_ct[START_TPB * (TW + 1)];  // padded: conflict-free
+    const Geometry& g = A.g;
+    const int th = g.th;
+    const int bpc = (g.tx + START_TPB - 1) / START_TPB;  // blocks per chain
+    const long long cj = blockIdx.x / bpc;                // chain within this pass
+    const int t0 = (int)(blockIdx.x % bpc) * START_TPB;
+    const int job = (int)(cj / g.ty);
+    const int tr = (int)(cj % g.ty);
+    int frame;
+    if (A.mode == 0) {
+        frame = job * A.n_frames_group + A.k;
+    } else {
+        int np = A.n_frames_group - 1;
+        int grp = job / np, i = job % np;
+        frame = grp * A.n_frames_group + (i < A.k ? i : i + 1);
+    }
+    const long long slot = (long long)frame * g.ty + tr;
+    const double* img = A.best + (long long)frame * g.P;
+    const int v0 = tr * th, rows = min(th, g.h - v0);
+    const int U0 = t0 * TW;
+    const int ncol = min(START_TPB * TW, g.w - U0);
+    const double INF = __longlong_as_double(0x7ff0000000000000ll);
+    // coalesced staging: row by row, consecutive threads -> consecutive columns
+    for (int dv = 0; dv < th; ++dv)
+#pragma unroll
+        for (int k = 0; k < TW; ++k) {
+            const int c = k * START_TPB + threadIdx.x;
+            const int tl = c / TW, du = c % TW;
+            double r = INF;
+            if (dv < rows && c < ncol) r = __ldg(img + (long long)(v0 + dv) * g.w + U0 + c);
+            s_r[tl * STRIDE + dv * TW + du] = r;
+        }
+#pragma unroll
+    for (int k = 0; k < TW; ++k) {
+        const int c = k * START_TPB + threadIdx.x;
+        const bool in = c < ncol;
+        const int o = (c / TW) * (TW + 1) + c % TW;
+        s_st[o] = in ? __ldg(A.tg.sin_t + U0 + c) : 0.0;
+        s_ct[o] = in ? __ldg(A.tg.cos_t + U0 + c) : 0.0;
+    }
+    __syncthreads();
+    const int t = t0 + threadIdx.x;
+    if (t >= g.tx) return;
+    uint8_t* sok = A.start_ok + slot * g.tx + t;
+    if (A.mode != 0 && A.cls[slot * g.tx + t] == 1) {
+        *sok = 0;
+        return;
+    }
+    const double* rr = s_r + threadIdx.x * STRIDE;
+    const double* st = s_st + threadIdx.x * (TW + 1);
+    const double* ct = s_ct + threadIdx.x * (TW + 1);
+    const int cols = min(TW, g.w - t * TW);
+    double sm[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+    for (int dv = 0; dv < rows; ++dv) {
+        const double sp = __ldg(A.tg.sin_p + v0 + dv), cp = __ldg(A.tg.cos_p + v0 + dv);
+#pragma unroll
+        for (int du = 0; du < TW; ++du) {
+            const double r = rr[dv * TW + du];
+            if (du >= cols || !isfinite(r)) continue;
+            const double dx = sp * st[du], dy = sp * ct[du], dz = cp;
+            const double x = r * dx, y = r * dy, z = r * dz;
+            sm[0] += y * y; sm[1] += y * z; sm[2] += z * z;
+            sm[3] += y;     sm[4] += z;     sm[5] += x * y;
+            sm[6] += x * z; sm[7] += x;     sm[8] += 1.0;
+        }
+    }
+    double a, b, c;
+    bool ok = sm[8] >= 3.0 && plane_from_sums(sm, A.cond_limit, a, b, c);
+    double m = 1e300, dmin = 1e300, rmin = 1e300, rmax = 0.0;
+    double ylo = 1e300, yhi = -1e300, zlo = 1e300, zhi = -1e300;
+    if (ok) {
+        a = f32_round(a);
+        b = f32_round(b);
+        c = f32_round(c);
+        // verdict and certificate statistics in one pass
+        for (int dv = 0; dv < rows && ok; ++dv) {
+            const double sp = __ldg(A.tg.sin_p + v0 + dv), cp = __ldg(A.tg.cos_p + v0 + dv);
+#pragma unroll
+            for (int du = 0; du < TW; ++du) {
+                const double r = rr[dv * TW + du];
+                if (du >= cols || !isfinite(r)) continue;
+                const double dy = sp * ct[du];
+                const double den = (sp * st[du] + a * dy) + b * cp;
+                const double ad = fabs(den);
+                if (ad < STPC_PARALLEL_EPS) { ok = false; break; }
+                const double r_hat = c / den;
+                if (r_hat <= 0.0 || r_hat > A.r_max || fabs(r - r_hat) > A.tau) { ok = false; break; }
+                m = fmin(m, A.tau - fabs(r - r_hat));
+                dmin = fmin(dmin, ad);
+                rmin = fmin(rmin, r_hat);
+                rmax = fmax(rmax, r_hat);
+                const double yh = r_hat * dy, zh = r_hat * cp;
+                ylo = fmin(ylo, yh);
+                yhi = fmax(yhi, yh);
+                zlo = fmin(zlo, zh);
+                zhi = fmax(zhi, zh);
+            }
+        }
+    }
+    *sok = ok ? 1 : 0;
+    if (!ok) return;
+    float4* ce = A.cert + (slot * g.tx + t) * CERT_F4;
+    ce[0] = make_float4((float)a, (float)b, (float)c, __double2float_rd(fmin(m, 3.0e38)));
+    ce[1] = make_float4(__double2float_rd(fmin(dmin, 3.0e38)), __double2float_rd(fmin(rmin, 3.0e38)),
+                        __double2float_ru(rmax), 0.0f);
+    ce[2] = make_float4(__double2float_rd(ylo), __double2float_ru(yhi), __double2float_rd(zlo),
+                        __double2float_ru(zhi));
+}
+
+#ifndef STPC_START_MINB
+#define STPC_START_MINB 2
+#endif
+#ifndef STPC_START_MINB
+#define STPC_START_MINB 2
+#endif
+template <int TW, int TH>
+__global__ void __launch_bounds__(256, STPC_START_MINB) start_tiles_kernel(FitArgs A)
 {
     const Geometry& g = A.g;
+    const int tw = TW > 0 ? TW : g.tw;
+    const int th = TH > 0 ? TH : g.th;
     const long long n_tiles = (long long)A.n_jobs * g.ty * g.tx;
     const long long id = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (id >= n_tiles) return;
@@ -308,12 +443,35 @@ __global__ void __launch_bounds__(256) start_tiles_kernel(FitArgs A)
         return;
     }
     const double* img = A.best + (long long)frame * g.P;
-    const int v0 = tr * g.th, v1 = min(v0 + g.th, g.h);
-    const int u0 = t * g.tw, u1 = min(u0 + g.tw, g.w);
+    const int v0 = tr * th, v1 = min(v0 + th, g.h);
+    const int u0 = t * tw, u1 = min(u0 + tw, g.w);
+    const double INF = __longlong_as_double(0x7ff0000000000000ll);
+    constexpr int NP = TW * TH;
+    double rr[NP > 0 ? NP : 1];
+    if constexpr (NP > 0) {
+#pragma unroll
+        for (int i = 0; i < NP; ++i) {
+            const int v = v0 + i / TW, u = u0 + i % TW;
+            rr[i] = (v < v1 && u < u1) ? __ldg(img + (long long)v * g.w + u) : INF;
+        }
+    }
+    auto pix = [&](int i, int& v, int& u) {
+        if constexpr (NP > 0) {
+            v = v0 + i / TW;
+            u = u0 + i % TW;
+        } else {
+            v = v0 + i / (u1 - u0);
+            u = u0 + i % (u1 - u0);
+        }
+    };
+    const int npx = NP > 0 ? NP : (v1 - v0) * (u1 - u0);
     double sm[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
-    for (int v = v0; v < v1; ++v)
-        for (int u = u0; u < u1; ++u) {
-            const double r = img[(long long)v * g.w + u];
+#pragma unroll
+    for (int i = 0; i < (NP > 0 ? NP : 1); ++i) {
+        for (int ii = i; ii < (NP > 0 ? i + 1 : npx); ++ii) {
+            int v, u;
+            pix(ii, v, u);
+            const double r = NP > 0 ? rr[ii] : ((v < v1 && u < u1) ? img[(long long)v * g.w + u] : INF);
             if (!isfinite(r)) continue;
             double dx, dy, dz;
             ray_dir(A.tg, v, u, dx, dy, dz);
@@ -322,45 +480,59 @@ __global__ void __launch_bounds__(256) start_tiles_kernel(FitArgs A)
             sm[3] += y;     sm[4] += z;     sm[5] += x * y;
             sm[6] += x * z; sm[7] += x;     sm[8] += 1.0;
         }
+    }
     double a, b, c;
     bool ok = sm[8] >= 3.0 && plane_from_sums(sm, A.cond_limit, a, b, c);
-    double m = 1e300, dmin = 1e300, rmin = 1e300, rmax = 0.0;
-    double ylo = 1e300, yhi = -1e300, zlo = 1e300, zhi = -1e300;
     if (ok) {
         a = f32_round(a);
         b = f32_round(b);
         c = f32_round(c);
-        for (int v = v0; v < v1 && ok; ++v)
-            for (int u = u0; u < u1; ++u) {
-                const double r = img[(long long)v * g.w + u];
+        // verdict first (cheap, early exit); certificate statistics only on a pass
+#pragma unroll
+        for (int i = 0; i < (NP > 0 ? NP : 1); ++i) {
+            for (int ii = i; ii < (NP > 0 ? i + 1 : npx) && ok; ++ii) {
+                int v, u;
+                pix(ii, v, u);
+                const double r = NP > 0 ? rr[ii] : ((v < v1 && u < u1) ? img[(long long)v * g.w + u] : INF);
                 if (!isfinite(r)) continue;
                 double dx, dy, dz;
                 ray_dir(A.tg, v, u, dx, dy, dz);
-                const double den = (dx + a * dy) + b * dz;
-                const double ad = fabs(den);
-                if (ad < STPC_PARALLEL_EPS) { ok = false; break; }
-                const double r_hat = c / den;
-                if (r_hat <= 0.0 || r_hat > A.r_max || fabs(r - r_hat) > A.tau) { ok = false; break; }
-                m = fmin(m, A.tau - fabs(r - r_hat));
-                dmin = fmin(dmin, ad);
-                rmin = fmin(rmin, r_hat);
-                rmax = fmax(rmax, r_hat);
-                const double yh = r_hat * dy, zh = r_hat * dz;
-                ylo = fmin(ylo, yh);
-                yhi = fmax(yhi, yh);
-                zlo = fmin(zlo, zh);
-                zhi = fmax(zhi, zh);
+                if (!pixel_fits(r, dx, dy, dz, a, b, c, A.tau, A.r_max)) ok = false;
             }
+        }
     }
     *sok = ok ? 1 : 0;
-    if (ok) {
-        float4* ce = A.cert + (slot * g.tx + t) * CERT_F4;
-        ce[0] = make_float4((float)a, (float)b, (float)c, __double2float_rd(fmin(m, 3.0e38)));
-        ce[1] = make_float4(__double2float_rd(fmin(dmin, 3.0e38)), __double2float_rd(fmin(rmin, 3.0e38)),
-                            __double2float_ru(rmax), 0.0f);
-        ce[2] = make_float4(__double2float_rd(ylo), __double2float_ru(yhi), __double2float_rd(zlo),
-                            __double2float_ru(zhi));
+    if (!ok) return;
+    double m = 1e300, dmin = 1e300, rmin = 1e300, rmax = 0.0;
+    double ylo = 1e300, yhi = -1e300, zlo = 1e300, zhi = -1e300;
+#pragma unroll
+    for (int i = 0; i < (NP > 0 ? NP : 1); ++i) {
+        for (int ii = i; ii < (NP > 0 ? i + 1 : npx); ++ii) {
+            int v, u;
+            pix(ii, v, u);
+            const double r = NP > 0 ? rr[ii] : ((v < v1 && u < u1) ? img[(long long)v * g.w + u] : INF);
+            if (!isfinite(r)) continue;
+            double dx, dy, dz;
+            ray_dir(A.tg, v, u, dx, dy, dz);
+            const double den = (dx + a * dy) + b * dz;
+            const double r_hat = c / den;
+            m = fmin(m, A.tau - fabs(r - r_hat));
+            dmin = fmin(dmin, fabs(den));
+            rmin = fmin(rmin, r_hat);
+            rmax = fmax(rmax, r_hat);
+            const double yh = r_hat * dy, zh = r_hat * dz;
+            ylo = fmin(ylo, yh);
+            yhi = fmax(yhi, yh);
+            zlo = fmin(zlo, zh);
+            zhi = fmax(zhi, zh);
+        }
     }
+    float4* ce = A.cert + (slot * g.tx + t) * CERT_F4;
+    ce[0] = make_float4((float)a, (float)b, (float)c, __double2float_rd(fmin(m, 3.0e38)));
+    ce[1] = make_float4(__double2float_rd(fmin(dmin, 3.0e38)), __double2float_rd(fmin(rmin, 3.0e38)),
+                        __double2float_ru(rmax), 0.0f);
+    ce[2] = make_float4(__double2float_rd(ylo), __double2float_ru(yhi), __double2float_rd(zlo),
+                        __double2float_ru(zhi));
 }
 
 __device__ __forceinline__ bool solve_round(double acc, double cond_limit, double& a, double& b, double& c)
@@ -801,7 +973,15 @@ void launch_start_tiles(const FitArgs& a, cudaStream_t s)
     long long tiles = (long long)a.n_jobs * a.g.ty * a.g.tx;
     if (tiles <= 0) return;
     STPC_LAUNCH();
-    start_tiles_kernel<<<(unsigned)((tiles + 255) / 256), 256, 0, s>>>(a);
+    const long long chains = (long long)a.n_jobs * a.g.ty;
+    const long long bpc = (a.g.tx + START_TPB - 1) / START_TPB;
+    if (a.g.tw == 4 && a.g.th <= 4) {
+        start_tiles_staged_kernel<4><<<(unsigned)(chains * bpc), START_TPB, 0, s>>>(a);
+    } else if (a.g.tw == 2 && a.g.th <= 8) {
+        start_tiles_staged_kernel<2><<<(unsigned)(chains * bpc), START_TPB, 0, s>>>(a);
+    } else {
+        start_tiles_kernel<0, 0><<<(unsigned)((tiles + 255) / 256), 256, 0, s>>>(a);
+    }
 }
 
 void launch_fit_chains(const FitArgs& a, cudaStream_t s)
