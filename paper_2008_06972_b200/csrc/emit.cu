@@ -63,6 +63,53 @@ __device__ __forceinline__ void word_masks(const Geometry& g, const uint8_t* vb,
     fb = __ballot_sync(STPC_FULL, cls == 2);
 }
 
+
+// Lane-per-word view: the residual / temporal / fallback masks of bitmap word
+// wd restricted to image row [rb, re).  Tile classes are applied per tile span
+// (<= 32/tw + 1 spans per word), not per pixel.
+__device__ __forceinline__ void word_classes(const Geometry& g, const uint8_t* crow, uint32_t valid, long long rb,
+                                             long long re, long long wd, uint32_t& res, uint32_t& tmp, uint32_t& fb)
+{
+    res = tmp = fb = 0;
+    const long long p0 = wd * 32;
+    const int lo = (int)max(0LL, rb - p0), hi = (int)min(32LL, re - p0);
+    if (lo >= hi) return;
+    int u = (int)(p0 + lo - rb);  // column of bit lo
+    int tile = __float2int_rz(((float)u + 0.5f) * __frcp_rn((float)g.tw));
+    {
+        const int r = u - tile * g.tw;
+        tile += r < 0 ? -1 : (r >= g.tw ? 1 : 0);
+    }
+    int bit = lo;
+    while (bit < hi) {
+        const int nb = min(hi - bit, (tile + 1) * g.tw - u);
+        const uint32_t m = (nb >= 32 ? 0xffffffffu : ((1u << nb) - 1u)) << bit;
+        const uint8_t c = crow[tile];
+        if (c == 0) res |= m;
+        else if (c == 1) tmp |= m;
+        else if (c == 2) fb |= m;
+        bit += nb;
+        u += nb;
+        tile += 1;
+    }
+    res &= valid;
+    tmp &= valid;
+    fb &= valid;
+}
+
+__device__ __forceinline__ long long warp_excl_max(long long v, long long ident)
+{
+    const int lane = threadIdx.x & 31;
+    long long inc = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        long long t = __shfl_up_sync(STPC_FULL, inc, o);
+        if (lane >= o) inc = max(inc, t);
+    }
+    long long ex = __shfl_up_sync(STPC_FULL, inc, 1);
+    return lane == 0 ? ident : ex;
+}
+
 // Warp per (frame, row): counts, varint bytes (excluding the row's first
 // delta), first/last residual flat index, coverage counters.
 __global__ void __launch_bounds__(256) rowstats_kernel(PlanArgs A)
@@ -79,29 +126,43 @@ __global__ void __launch_bounds__(256) rowstats_kernel(PlanArgs A)
     const uint8_t* crow = A.cls + ((long long)f * g.ty + v / g.th) * g.tx;
     RowWalk rw = row_walk(g, v);
     int cnt = 0, nesc = 0, vbytes = 0, ntmp = 0, nfb = 0;
-    long long first = -1, last = -1;
-    for (long long wd = rw.w0; wd < rw.w1; ++wd) {
-        uint32_t res, tmp, fb;
-        word_masks(g, vb, crow, rw, wd, v, res, tmp, fb);
-        ntmp += __popc(tmp);
-        nfb += __popc(fb);
-        if (!res) continue;
-        uint32_t esc = load_bits(eb, wd);
-        nesc += __popc(res & esc);
-        // varint length of every residual's delta except the row's first
-        bool mine = (res >> lane) & 1u;
-        int len = 0;
-        if (mine) {
-            uint32_t below = res & ((1u << lane) - 1u);
-            long long idx = wd * 32 + lane;
-            long long prev = below ? wd * 32 + (31 - __clz(below)) : last;
-            if (prev >= 0) len = varint_len((uint32_t)(idx - prev));
+    long long first = -1, last = -1;  // carried across word batches
+    for (long long base = rw.w0; base < rw.w1; base += 32) {
+        const long long wd = base + lane;
+        uint32_t res = 0, tmp = 0, fb = 0, esc = 0;
+        if (wd < rw.w1) {
+            word_classes(g, crow, load_bits(vb, wd), rw.rb, rw.re, wd, res, tmp, fb);
+            if (res) esc = load_bits(eb, wd) & res;
         }
-        for (int o = 16; o > 0; o >>= 1) len += __shfl_xor_sync(STPC_FULL, len, o);
+        const long long wfirst = res ? wd * 32 + (__ffs(res) - 1) : -1;
+        const long long wlast = res ? wd * 32 + (31 - __clz(res)) : -1;
+        // previous residual before this word within the row (or none)
+        long long prev = warp_excl_max(wlast, -1);
+        prev = max(prev, last);
+        int len = 0;
+        if (res) len = (__popc(res) - 1) + (prev >= 0 ? varint_len((uint32_t)(wfirst - prev)) : 0);
+        int c = __popc(res), e = __popc(esc), t1 = __popc(tmp), f2 = __popc(fb);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            len += __shfl_xor_sync(STPC_FULL, len, o);
+            c += __shfl_xor_sync(STPC_FULL, c, o);
+            e += __shfl_xor_sync(STPC_FULL, e, o);
+            t1 += __shfl_xor_sync(STPC_FULL, t1, o);
+            f2 += __shfl_xor_sync(STPC_FULL, f2, o);
+        }
+        // batch first/last
+        const unsigned nz = __ballot_sync(STPC_FULL, res != 0);
+        if (nz) {
+            const long long bf = __shfl_sync(STPC_FULL, wfirst, __ffs(nz) - 1);
+            const long long bl = __shfl_sync(STPC_FULL, wlast, 31 - __clz(nz));
+            if (first < 0) first = bf;
+            last = bl;
+        }
         vbytes += len;
-        if (first < 0) first = wd * 32 + (__ffs(res) - 1);
-        last = wd * 32 + (31 - __clz(res));
-        cnt += __popc(res);
+        cnt += c;
+        nesc += e;
+        ntmp += t1;
+        nfb += f2;
     }
     if (lane == 0) {
         RowStat st;
@@ -370,7 +431,8 @@ __global__ void __launch_bounds__(128) emit_fallback_kernel(EmitArgs E)
     }
 }
 
-// residual rows: warp per (frame, row) with residual pixels
+// residual rows: warp per (frame, row) with residual pixels; lane per bitmap
+// word: offsets by warp scans, each lane writes its word's pixels in flat order
 __global__ void __launch_bounds__(256) emit_residual_kernel(EmitArgs E)
 {
     const PlanArgs& A = E.p;
@@ -396,51 +458,58 @@ __global__ void __launch_bounds__(256) emit_residual_kernel(EmitArgs E)
     const uint8_t* crow = A.cls + (f * g.ty + v / g.th) * g.tx;
     const double* img = E.best + f * g.P;
     RowWalk rw = row_walk(g, v);
-    long long last = ro.prev;
-    for (long long wd = rw.w0; wd < rw.w1; ++wd) {
-        uint32_t res, tmp, fb;
-        word_masks(g, vb, crow, rw, wd, v, res, tmp, fb);
-        if (!res) continue;
-        uint32_t esc = load_bits(eb, wd) & res;
-        bool mine = (res >> lane) & 1u;
-        uint32_t lt = (1u << lane) - 1u;
-        int len = 0;
-        long long idx = wd * 32 + lane;
-        uint32_t delta = 0;
-        if (mine) {
-            uint32_t below = res & lt;
-            long long prev = below ? wd * 32 + (31 - __clz(below)) : last;
-            delta = (uint32_t)(idx - prev);
-            len = varint_len(delta);
+    long long last = ro.prev;  // previous residual of the frame (0 if none)
+    for (long long wbase = rw.w0; wbase < rw.w1; wbase += 32) {
+        const long long wd = wbase + lane;
+        uint32_t res = 0, tmp, fb, esc = 0;
+        if (wd < rw.w1) {
+            word_classes(g, crow, load_bits(vb, wd), rw.rb, rw.re, wd, res, tmp, fb);
+            if (res) esc = load_bits(eb, wd) & res;
         }
-        int inc = warp_incl_scan(len);
-        if (mine) {
-            uint8_t* o = vptr + inc - len;
-            uint32_t d = delta;
-            for (int b = 0; b < len - 1; ++b) {
-                o[b] = (uint8_t)((d & 0x7f) | 0x80);
-                d >>= 7;
+        const long long wfirst = res ? wd * 32 + (__ffs(res) - 1) : -1;
+        const long long wlast = res ? wd * 32 + (31 - __clz(res)) : -1;
+        long long prev = max(warp_excl_max(wlast, -1), last);
+        const int nres = __popc(res), nesc = __popc(esc);
+        const int len = res ? (nres - 1) + varint_len((uint32_t)(wfirst - prev)) : 0;
+        const int vinc = warp_incl_scan(len), cinc = warp_incl_scan(nres), einc = warp_incl_scan(nesc);
+        if (res) {
+            uint8_t* vo = vptr + vinc - len;
+            uint8_t* co = cptr + 2 * (cinc - nres);
+            uint8_t* eo = eptr + 4 * (einc - nesc);
+            uint32_t m = res;
+            while (m) {
+                const int j = __ffs(m) - 1;
+                m &= m - 1;
+                const long long idx = wd * 32 + j;
+                uint32_t d = (uint32_t)(idx - prev);
+                prev = idx;
+                while (d >= 0x80u) {
+                    *vo++ = (uint8_t)((d & 0x7f) | 0x80);
+                    d >>= 7;
+                }
+                *vo++ = (uint8_t)d;
+                const double r = img[idx];
+                uint32_t code = 0xFFFFu;
+                if ((esc >> j) & 1u) {
+                    put_f32(eo, (float)r);
+                    eo += 4;
+                } else {
+                    // rint(r / q) (bitstream.py:178): reciprocal estimate, exact
+                    // IEEE division only when the estimate is near a .5 boundary
+                    const double qa = r * E.inv_quant;
+                    const double fr = qa - floor(qa);
+                    code = fabs(fr - 0.5) > 1e-6 ? (uint32_t)(long long)rint(qa)
+                                                 : (uint32_t)(long long)rint(r / E.range_quant);
+                }
+                put_u16(co, code);
+                co += 2;
             }
-            o[len - 1] = (uint8_t)d;
-            int rank = __popc(res & lt);
-            double r = img[idx];
-            bool e = (esc >> lane) & 1u;
-            uint32_t code = 0xFFFFu;
-            if (!e) {
-                // rint(r / q) (bitstream.py:178): reciprocal estimate, exact
-                // IEEE division only when the estimate is near a .5 boundary
-                const double qa = r * E.inv_quant;
-                const double fr = qa - floor(qa);
-                code = fabs(fr - 0.5) > 1e-6 ? (uint32_t)(long long)rint(qa)
-                                             : (uint32_t)(long long)rint(r / E.range_quant);
-            }
-            put_u16(cptr + 2 * rank, code);
-            if (e) put_f32(eptr + 4 * __popc(esc & lt), (float)r);
         }
-        vptr += __shfl_sync(STPC_FULL, inc, 31);
-        cptr += 2 * __popc(res);
-        eptr += 4 * __popc(esc);
-        last = wd * 32 + (31 - __clz(res));
+        vptr += __shfl_sync(STPC_FULL, vinc, 31);
+        cptr += 2 * __shfl_sync(STPC_FULL, cinc, 31);
+        eptr += 4 * __shfl_sync(STPC_FULL, einc, 31);
+        const unsigned nz = __ballot_sync(STPC_FULL, res != 0);
+        if (nz) last = __shfl_sync(STPC_FULL, wlast, 31 - __clz(nz));
     }
 }
 
