@@ -102,7 +102,7 @@ struct stpc_encoder {
     // frame level
     DevBuf best, vbits, ebits, cls, fstats;
     // chain level
-    DevBuf cert, start_ok;
+    DevBuf cert, start_ok, chain_counter;
     DevBuf run_s, run_len, run_abc, n_runs, ref_ok, ref_c, chain_tbytes, chain_off;
     // plan
     DevBuf rowstat, rowoff, res_cnt, res_vb, res_esc, fb_rows, sec, payload_len, payload_off;
@@ -326,6 +326,7 @@ static int encode_impl(stpc_encoder* e, int G, const void* d_points, const int64
     ENS(e->n_runs, sizeof(int) * F * g.ty);
     ENS(e->cert, sizeof(float4) * 3 * F * TT);
     ENS(e->start_ok, (size_t)F * TT);
+    ENS(e->chain_counter, 64);
     ENS(e->ref_ok, (size_t)G * TT * n);
     ENS(e->ref_c, sizeof(float) * G * TT * n);
     ENS(e->chain_tbytes, sizeof(long long) * G * g.ty);
@@ -398,6 +399,7 @@ static int encode_impl(stpc_encoder* e, int G, const void* d_points, const int64
     fa.n_runs = e->n_runs.as<int>();
     fa.cert = e->cert.as<float4>();
     fa.start_ok = e->start_ok.as<uint8_t>();
+    fa.chain_counter = e->chain_counter.as<unsigned>();
     e->mark(ST_START_K, s);
     launch_start_tiles(fa, s);
     e->mark(ST_FIT_K, s);

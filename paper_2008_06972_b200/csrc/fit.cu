@@ -742,11 +742,39 @@ __global__ void __launch_bounds__(FIT_WARPS * 32, 5) fit_pair_kernel(FitArgs A)
     const int sub = lane >> 4, gl = lane & 15;
     const unsigned gmask = 0xffffu << (sub * 16);
     const long long n_chains = (long long)A.n_jobs * g.ty;
-    const long long cid = ((long long)blockIdx.x * FIT_WARPS + wib) * 2 + sub;
-    bool done = cid >= n_chains;
-    if (__all_sync(STPC_FULL, done)) return;
+    const uint8_t run_cls = A.mode == 0 ? 1 : 2;
+    double* sm = smem[wib][sub];
+    const int kk = gl < 9 ? gl : 8;
+
+    // Work stealing: each half-warp pulls chains from a global counter, so a
+    // half whose chain finished early never idles beside a longer partner.
+    long long cid = -1;
+    bool finished = false;  // no chains left for this half
+    bool done = true;       // current chain complete
     int frame = 0, tr = 0;
-    if (!done) {
+    long long slot = 0;
+    Chain ch;
+    ch.skip1 = A.mode != 0;
+    uint8_t* crow = A.cls;
+    const uint8_t* sok = A.start_ok;
+    uint16_t* rs = A.run_s;
+    uint16_t* rl = A.run_len;
+    float* rabc = A.run_abc;
+    int t = 0, s = 0, n_runs = 0;
+    bool grow = false;
+    double acc = 0.0, a = 0.0, b = 0.0, c = 0.0;
+    int pf_t = -1;
+    double pf_r = 0.0;
+    auto next_chain = [&]() {
+        long long nc = 0;
+        if (gl == 0) nc = (long long)atomicAdd(A.chain_counter, 1u);
+        nc = __shfl_sync(STPC_FULL, nc, sub * 16);
+        cid = nc;
+        if (cid >= n_chains) {
+            finished = true;
+            done = true;
+            return;
+        }
         const int job = (int)(cid / g.ty);
         tr = (int)(cid % g.ty);
         if (A.mode == 0) {
@@ -756,31 +784,28 @@ __global__ void __launch_bounds__(FIT_WARPS * 32, 5) fit_pair_kernel(FitArgs A)
             int grp = job / np, i = job % np;
             frame = grp * A.n_frames_group + (i < A.k ? i : i + 1);
         }
-    }
-    const long long slot = (long long)frame * g.ty + tr;
-    Chain ch;
-    ch.img = A.best + (long long)frame * g.P;
-    uint8_t* crow = A.cls + slot * g.tx;
-    ch.crow = crow;
-    ch.cert = A.cert + slot * g.tx * CERT_F4;
-    ch.skip1 = A.mode != 0;
-    ch.v0 = tr * g.th;
-    ch.rows = min(g.th, g.h - ch.v0);
-    const uint8_t run_cls = A.mode == 0 ? 1 : 2;
-    const uint8_t* sok = A.start_ok + slot * g.tx;
-    double* sm = smem[wib][sub];
-    uint16_t* rs = A.run_s + slot * g.tx;
-    uint16_t* rl = A.run_len + slot * g.tx;
-    float* rabc = A.run_abc + slot * g.tx * 3;
-    const int kk = gl < 9 ? gl : 8;
+        slot = (long long)frame * g.ty + tr;
+        ch.img = A.best + (long long)frame * g.P;
+        crow = A.cls + slot * g.tx;
+        ch.crow = crow;
+        ch.cert = A.cert + slot * g.tx * CERT_F4;
+        ch.v0 = tr * g.th;
+        ch.rows = min(g.th, g.h - ch.v0);
+        sok = A.start_ok + slot * g.tx;
+        rs = A.run_s + slot * g.tx;
+        rl = A.run_len + slot * g.tx;
+        rabc = A.run_abc + slot * g.tx * 3;
+        t = 0;
+        s = 0;
+        n_runs = 0;
+        grow = false;
+        acc = 0.0;
+        pf_t = -1;
+        done = false;
+    };
+    next_chain();
 
-    int t = 0, s = 0, n_runs = 0;
-    bool grow = false;
-    double acc = 0.0, a = 0.0, b = 0.0, c = 0.0;
-    int pf_t = -1;
-    double pf_r = 0.0;
-
-    while (__any_sync(STPC_FULL, !done)) {
+    while (__any_sync(STPC_FULL, !finished)) {
         // ---- (1) chains between runs jump to their next start tile
         const bool scan = !done && !grow;
         {
@@ -964,8 +989,50 @@ __global__ void __launch_bounds__(FIT_WARPS * 32, 5) fit_pair_kernel(FitArgs A)
                 n_runs += 1;
             }
         }
+        // ---- (6) hand-over: a finished chain records its run count and its
+        // half-warp steals the next chain
+        const bool handover = done && !finished;
+        if (handover && gl == 0) A.n_runs[slot] = n_runs;
+        if (__any_sync(STPC_FULL, handover)) {
+            long long nc = 0;
+            if (handover && gl == 0) nc = (long long)atomicAdd(A.chain_counter, 1u);
+            nc = __shfl_sync(STPC_FULL, nc, sub * 16);
+            if (handover) {
+                cid = nc;
+                if (cid >= n_chains) {
+                    finished = true;
+                } else {
+                    const int job = (int)(cid / g.ty);
+                    tr = (int)(cid % g.ty);
+                    if (A.mode == 0) {
+                        frame = job * A.n_frames_group + A.k;
+                    } else {
+                        int np = A.n_frames_group - 1;
+                        int grp = job / np, ii = job % np;
+                        frame = grp * A.n_frames_group + (ii < A.k ? ii : ii + 1);
+                    }
+                    slot = (long long)frame * g.ty + tr;
+                    ch.img = A.best + (long long)frame * g.P;
+                    crow = A.cls + slot * g.tx;
+                    ch.crow = crow;
+                    ch.cert = A.cert + slot * g.tx * CERT_F4;
+                    ch.v0 = tr * g.th;
+                    ch.rows = min(g.th, g.h - ch.v0);
+                    sok = A.start_ok + slot * g.tx;
+                    rs = A.run_s + slot * g.tx;
+                    rl = A.run_len + slot * g.tx;
+                    rabc = A.run_abc + slot * g.tx * 3;
+                    t = 0;
+                    s = 0;
+                    n_runs = 0;
+                    grow = false;
+                    acc = 0.0;
+                    pf_t = -1;
+                    done = false;
+                }
+            }
+        }
     }
-    if (cid < n_chains && gl == 0) A.n_runs[slot] = n_runs;
 }
 
 void launch_start_tiles(const FitArgs& a, cudaStream_t s)
@@ -990,8 +1057,11 @@ void launch_fit_chains(const FitArgs& a, cudaStream_t s)
     if (warps <= 0) return;
     STPC_LAUNCH();
     if (a.g.tw * a.g.th <= PG) {
+        // work-stealing grid: ~5 resident blocks per SM, capped by the chain count
         long long pairs = (warps + 1) / 2;
-        fit_pair_kernel<<<(unsigned)((pairs + FIT_WARPS - 1) / FIT_WARPS), FIT_WARPS * 32, 0, s>>>(a);
+        long long blocks = std::min<long long>((pairs + FIT_WARPS - 1) / FIT_WARPS, 148LL * 5);
+        launch_zero(a.chain_counter, sizeof(unsigned), s);
+        fit_pair_kernel<<<(unsigned)blocks, FIT_WARPS * 32, 0, s>>>(a);
     } else {
         fit_rows_kernel<<<(unsigned)((warps + FIT_WARPS - 1) / FIT_WARPS), FIT_WARPS * 32, 0, s>>>(a);
     }

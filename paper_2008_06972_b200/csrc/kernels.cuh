@@ -81,6 +81,7 @@ struct FitArgs {
     int* n_runs;
     float4* cert;       // [F*TY][TX][3] per-tile test certificates (scratch)
     uint8_t* start_ok;  // [F*TY][TX] start verdicts (scratch)
+    unsigned* chain_counter;  // work-stealing counter (scratch)
 };
 void launch_fit_rows(const FitArgs& a, cudaStream_t s);  // = start_tiles + fit_chains
 void launch_start_tiles(const FitArgs& a, cudaStream_t s);
