@@ -309,3 +309,55 @@ def test_pipelined_host_encode_matches_device_path():
     # spot-check against the oracle
     ocfg_poses = None
     assert ref_blobs[5] == oracle.compress(clouds[15:18], cfg, synth.make_group(505, 3, sensor, n_boxes=5).poses)[0]
+
+
+def _odd_sensor():
+    import math
+
+    from paper_2008_06972_b200 import synth
+
+    return synth.Sensor(333, 13, 2 * math.pi / 333, math.radians(2.1), math.radians(87.0))
+
+
+@pytest.mark.parametrize(
+    "n,k,tile,tau,scale,mutate",
+    [
+        (12, None, (4, 4), 0.1, 1.0, None),   # 2-byte presence masks
+        (3, 0, (3, 3), 0.05, 1.0, None),      # key frame first, 9-pixel tiles
+        (4, 3, (5, 2), 0.2, 1.0, None),       # key frame last, non-square tiles
+        (3, None, (4, 4), 0.1, 3.5, None),    # ranges past u16 quantisation -> escapes, r_max
+        (3, None, (2, 2), 1e-6, 1.0, None),   # everything residual
+        (3, None, (4, 4), 0.1, 1.0, "nan"),   # one frame with no valid points
+    ],
+)
+def test_edge_cases_blob(n, k, tile, tau, scale, mutate):
+    from paper_2008_06972_b200 import AngularResolution, CodecConfig, compress, synth
+
+    sensor = _odd_sensor()
+    grp = synth.make_group(900 + n + tile[0], n, sensor, n_boxes=8)
+    clouds = [c * np.float32(scale) for c in grp.clouds]
+    if mutate == "nan":
+        clouds[0] = np.full_like(clouds[0], np.nan)
+    cfg = CodecConfig(mode="stream", tau=tau, tile_w=tile[0], tile_h=tile[1],
+                      res=AngularResolution(sensor.theta_r, sensor.phi_r), phi_offset=sensor.phi_offset,
+                      w=sensor.w, h=sensor.h, n_frames=n, k_index=k)
+    mine, rep = compress(clouds, cfg, poses=grp.poses)
+    ref, enc = oracle.compress(clouds, cfg, grp.poses)
+    assert mine == ref, _first_divergence(mine, ref)
+    for ch, cov in enumerate(rep.coverage):
+        assert cov["temporal"] + cov["fallback"] + cov["residual"] == cov["valid"]
+    if scale > 1:
+        q = np.concatenate([np.rint(r / cfg.range_quant) for r in enc.residual_r])
+        assert (q >= 0xFFFF).any()  # the escape path was exercised
+
+
+def test_single_mode_f64_input_full_size():
+    """configs[0] through the float64 input path (reference up-casts to f64)."""
+    from paper_2008_06972_b200 import compress, synth
+
+    sensor, n, tile, tau, scene = synth.config_params(1)
+    g = synth.make_group(77, 1, sensor)
+    clouds = [g.clouds[0].astype(np.float64) * 1.0000001]  # not f32-representable
+    cfg = _cfg(sensor, 1, tau, tile)
+    mine, _ = compress(clouds, cfg)
+    assert mine == oracle.compress(clouds, cfg)[0]
