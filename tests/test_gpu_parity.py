@@ -325,7 +325,7 @@ def _odd_sensor():
         (12, None, (4, 4), 0.1, 1.0, None),   # 2-byte presence masks
         (3, 0, (3, 3), 0.05, 1.0, None),      # key frame first, 9-pixel tiles
         (4, 3, (5, 2), 0.2, 1.0, None),       # key frame last, non-square tiles
-        (3, None, (4, 4), 0.1, 8.0, None),    # ranges past u16 quantisation -> escapes, r_max
+        (3, None, (4, 4), 0.1, 20.0, None),   # ranges past u16 quantisation -> escapes, r_max
         (3, None, (2, 2), 1e-6, 1.0, None),   # everything residual
         (3, None, (4, 4), 0.1, 1.0, "nan"),   # one frame with no valid points
     ],
