@@ -12,6 +12,7 @@ test can tell an oracle bug from a host-libm difference.
 
 from __future__ import annotations
 
+import hashlib
 import math
 import os
 import sys
@@ -81,6 +82,10 @@ def compress_case(name, seed, n, tau, tw, th, k=None, sensor=SMALL, f64=False, m
         extra[f"counts{i}"] = np.array([img.stats.rejected_nonfinite, img.stats.dropped_fov,
                                         img.stats.collisions], np.int64)
     extra["fractions"] = np.array([rep.fractions["temporal"], rep.fractions["spatial"], rep.fractions["residual"]])
+    # the reference decoder's output, as exact-bytes digests + point counts
+    dec = stpc.decompress(blob)
+    extra["dec_sha256"] = np.array([hashlib.sha256(np.ascontiguousarray(p).tobytes()).hexdigest() for p in dec])
+    extra["dec_counts"] = np.array([p.shape[0] for p in dec], np.int64)
     save_case(name, clouds, g.poses if n > 1 else None, cfg, blob, extra)
 
 

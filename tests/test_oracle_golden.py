@@ -67,3 +67,19 @@ def test_oracle_pack_and_crc_known_answer():
     assert lens[0] == 1 and lens[1] == 1
     # 0->'0', 1->'1': bits 011010001 -> 0x68 0x80
     assert blob[284:] == bytes([0x68, 0x80])
+
+
+@pytest.mark.parametrize("name", golden_cases())
+def test_oracle_decoder_matches_reference_decompress(name):
+    """The oracle decoder reproduces stpc.decompress bit-for-bit (sha256 of the
+    reference's decoded float64 clouds, stored by make_golden.py)."""
+    import hashlib
+
+    from oracle import decode as odec
+
+    clouds, poses, cfg, blob, z = load_case(name)
+    if not trig_matches_host(z, cfg):
+        pytest.skip("host numpy sin/cos differ from the fixture host's")
+    dec = odec.decompress(blob)
+    assert [p.shape[0] for p in dec] == list(z["dec_counts"])
+    assert [hashlib.sha256(np.ascontiguousarray(p).tobytes()).hexdigest() for p in dec] == list(z["dec_sha256"])
