@@ -128,6 +128,26 @@ int stpc_project(const void* d_points, int32_t points_f64, const int64_t* point_
                  const double* transforms, int32_t w, int32_t h, double theta_r, double phi_r,
                  double phi_offset, double* d_best, int64_t* d_win, int64_t* h_counts, void* stream);
 
+/* Decoder (decompress).  d_blob_off: device int64[n]
+ * blob starts in d_blobs.  stpc_crc32_blobs: zlib CRC-32 of each blob's entropy
+ * payload (bitstream.py:410-411).  stpc_huffman_decode_blobs: raw payload of
+ * each blob into d_out + d_out_off[i] (huffman_decode_kernel, _kernels.py:
+ * 385-417); h_status 0 ok / 1 truncated / 2 invalid code.
+ * stpc_reconstruct_frames: per-tile plane maps (float4 a, b, c, kind; kind 0 =
+ * none) + validity bitmaps + residual pixels -> points (float64 xyz, row-major
+ * per frame, inverse-transformed with d_xf_inv [F][12] = R^-1 | T^-1)
+ * (decode_stream_images temporal.py:293-343, reconstruct_span _kernels.py:
+ * 282-308, unproject range_image.py:214-221).  d_scratch: f64 [F][h*w]. */
+int stpc_crc32_blobs(const uint8_t* d_blobs, const int64_t* d_blob_off, int32_t n, uint32_t* h_crc, void* stream);
+int stpc_huffman_decode_blobs(const uint8_t* d_blobs, const int64_t* d_blob_off, int32_t n, uint8_t* d_out,
+                              const int64_t* d_out_off, int32_t* h_status, void* stream);
+int stpc_reconstruct_frames(int32_t w, int32_t h, int32_t tile_w, int32_t tile_h, const double* d_trig,
+                            int32_t n_frames, const uint8_t* d_vbits, int64_t vstride, const float* d_tile_map,
+                            const int64_t* d_res_flat, const double* d_res_range, const int32_t* d_res_frame,
+                            int64_t n_res, const double* d_xf_inv, double r_max, double* d_scratch,
+                            double* d_points, int64_t points_cap, int64_t* h_frame_counts, int64_t* h_failed,
+                            void* stream);
+
 /* Utilities so FFI callers need no CUDA runtime binding of their own. */
 int stpc_malloc(void** dev_ptr, int64_t bytes);
 int stpc_free(void* dev_ptr);

@@ -22,6 +22,7 @@ from .codec import (
     compress_groups,
     get_encoder,
 )
+from .decode import DecodeReport, decompress, decompress_full, decompress_many
 from .errors import (
     ChecksumError,
     CodecError,

@@ -30,6 +30,7 @@ EXPORTS = [
     "stpc_encoder_buffer", "stpc_project", "stpc_malloc", "stpc_free", "stpc_memcpy_d2h",
     "stpc_memcpy_h2d", "stpc_device_count", "stpc_last_error", "stpc_version",
     "stpc_encoder_profile", "stpc_encoder_stage_ms", "stpc_stage_name", "stpc_launch_count",
+    "stpc_crc32_blobs", "stpc_huffman_decode_blobs", "stpc_reconstruct_frames",
 ]
 
 
@@ -96,6 +97,10 @@ def load(require_device: bool = False):
                 "stpc_encoder_stage_ms": ([P, P, I32], I32),
                 "stpc_stage_name": ([I32], ctypes.c_char_p),
                 "stpc_launch_count": ([], ctypes.c_uint64),
+                "stpc_crc32_blobs": ([P, P, I32, P, P], ctypes.c_int),
+                "stpc_huffman_decode_blobs": ([P, P, I32, P, P, P, P], ctypes.c_int),
+                "stpc_reconstruct_frames": ([I32, I32, I32, I32, P, I32, P, I64, P, P, P, P, I64, P, D, P, P,
+                                             I64, P, ctypes.POINTER(I64), P], ctypes.c_int),
             }
             for name, (args, res) in sig.items():
                 fn = getattr(L, name)

@@ -361,3 +361,63 @@ def test_single_mode_f64_input_full_size():
     cfg = _cfg(sensor, 1, tau, tile)
     mine, _ = compress(clouds, cfg)
     assert mine == oracle.compress(clouds, cfg)[0]
+
+
+# ------------------------------------------------------------------- decoder
+
+
+@pytest.mark.parametrize("name", golden_cases())
+def test_decompress_golden_matches_reference(name):
+    """GPU decompress == reference stpc.decompress (sha256 of the exact float64
+    clouds the reference produced for this fixture)."""
+    import hashlib
+
+    from oracle import decode as odec
+    from paper_2008_06972_b200 import decompress
+
+    clouds, poses, cfg, blob, z = load_case(name)
+    mine = decompress(blob)
+    ref = odec.decompress(blob)
+    assert [p.shape for p in mine] == [p.shape for p in ref]
+    for a, b in zip(mine, ref):
+        assert np.array_equal(a, b)
+    if trig_matches_host(z, cfg):
+        assert [hashlib.sha256(np.ascontiguousarray(p).tobytes()).hexdigest() for p in mine] == list(z["dec_sha256"])
+
+
+@pytest.mark.parametrize("cfg_id", [2, 3])
+def test_decompress_full_size_roundtrip(cfg_id):
+    """configs[1] / configs[2]: compress on the GPU, decompress on the GPU,
+    bit-identical to the oracle decoder; decoded ranges within tau of the
+    input range image on plane pixels and exact (pre-quantisation) otherwise."""
+    from oracle import decode as odec
+    from paper_2008_06972_b200 import compress, decompress_full, synth
+
+    sensor, n, tile, tau, scene = synth.config_params(cfg_id)
+    g = synth.make_group(2000 + cfg_id, n, sensor, **scene)
+    cfg = _cfg(sensor, n, tau, tile)
+    blob, rep = compress(g.clouds, cfg, poses=g.poses)
+    mine, drep = decompress_full(blob)
+    ref = odec.decompress(blob)
+    for a, b in zip(mine, ref):
+        assert a.shape == b.shape and np.array_equal(a, b)
+    assert sum(drep.point_counts) == sum(p.shape[0] for p in ref)
+
+
+def test_decompress_many_batch_and_corruption():
+    from paper_2008_06972_b200 import ChecksumError, DecodeError, compress_groups, decompress_many, synth
+    from oracle import decode as odec
+
+    cfg = _cfg(synth.SENSOR_64, 3, 0.1, 4)
+    groups = [synth.make_group(5000 + i, 3) for i in range(3)]
+    blobs, _ = compress_groups([g.clouds for g in groups], cfg, [g.poses for g in groups])
+    clouds, reps = decompress_many(blobs)
+    for b, cl in zip(blobs, clouds):
+        for a, r in zip(cl, odec.decompress(b)):
+            assert np.array_equal(a, r)
+    bad = bytearray(blobs[0])
+    bad[400] ^= 0x55
+    with pytest.raises(ChecksumError):
+        decompress_many([bytes(bad)])
+    with pytest.raises(DecodeError):
+        decompress_many([blobs[0][:-3]])

@@ -159,3 +159,53 @@ def test_synthetic_scene_shapes_match_baseline():
     assert all(c.dtype == np.float32 and c.shape[1] == 3 for c in g.clouds)
     assert 115_000 < g.clouds[0].shape[0] < 125_000  # ~120k points (BASELINE configs[0])
     assert len(g.poses) == 2
+
+
+@pytest.mark.parametrize("name", ["stream3_4x4", "stream5_2x2", "stream4_8x4_k0", "single_f64_bad", "stream3_empty"])
+def test_decoder_record_parser_matches_oracle(name):
+    """decode._parse (host part of the GPU decoder) on the oracle-decoded
+    payload: tile plane maps and residual pixels agree with the oracle's
+    restatement of deserialize."""
+    import struct
+
+    from oracle import decode as odec
+    from paper_2008_06972_b200 import decode
+
+    clouds, poses, cfg, blob, z = load_case(name)
+    raw_len, enc_len = struct.unpack_from("<QQ", blob, 8)
+    payload = odec.huffman_decode(np.frombuffer(blob, np.uint8, 256, 28), blob[284:284 + enc_len], raw_len)
+    c, xf, vbits, tmap, rflat, rr, rfr = decode._parse(payload)
+    ref = odec.deserialize(blob)
+    assert c == ref.cfg
+    n = c["n_frames"]
+    for ch in range(n):
+        # temporal tiles carry this channel's offset
+        for j, offs in enumerate(ref.t_off):
+            if offs[ch] is not None:
+                a, b, _ = ref.t_abc[j]
+                seg = tmap[ch, ref.t_row[j], ref.t_s[j]:ref.t_s[j] + ref.t_len[j]]
+                assert np.all(seg[:, 3] == 1.0)
+                assert np.all(seg[:, 0] == np.float32(a)) and np.all(seg[:, 2] == np.float32(offs[ch]))
+    got = {int(f[0]): (fl, r) for fl, r, f in zip(rflat, rr, rfr)}
+    for ch in range(n):
+        fl, r = ref.residuals[ch]
+        if fl.size:
+            assert np.array_equal(got[ch][0], fl) and np.array_equal(got[ch][1], r)
+        else:
+            assert ch not in got
+
+
+def test_decoder_rejects_bad_headers():
+    from paper_2008_06972_b200 import MalformedBlobError, TruncatedBlobError, UnknownVersionError
+    from paper_2008_06972_b200.decode import _header
+
+    clouds, poses, cfg, blob, z = load_case("single_4x4")
+    _header(blob)
+    with pytest.raises(TruncatedBlobError):
+        _header(blob[:100])
+    with pytest.raises(MalformedBlobError):
+        _header(b"XXXX" + blob[4:])
+    with pytest.raises(UnknownVersionError):
+        _header(blob[:4] + b"\x02\x00" + blob[6:])
+    with pytest.raises(TruncatedBlobError):
+        _header(blob[:-10])
