@@ -220,5 +220,5 @@ def decompress(blob: bytes) -> List[np.ndarray]:
         R, T = dec.transforms[ch]
         Rinv = R.T
         Tinv = -(R.T @ T)
-        out.append(pts @ Rinv.T + Tinv)
+        out.append(orc.transform(pts, Rinv, Tinv))  # pts @ Rinv.T + Tinv (motion.py:70-72)
     return out

@@ -160,15 +160,20 @@ def poses_to_transforms(poses, k):
     return out
 
 
+def transform(pts: np.ndarray, R, T) -> np.ndarray:
+    """RigidTransform.apply (motion.py:70-72) via orc_transform's FMA chain."""
+    p = np.ascontiguousarray(np.asarray(pts, np.float64).reshape(-1, 3))
+    out = np.empty_like(p)
+    lib().orc_transform(_p(p), p.shape[0], _p(np.ascontiguousarray(R, np.float64)),
+                        _p(np.ascontiguousarray(T, np.float64)), _p(out))
+    return out
+
+
 def convert(cloud: np.ndarray, R, T, cfg: OracleConfig):
     """Transform + project (motion.py:70-72 -> range_image.py:165-211)."""
     pts = np.ascontiguousarray(np.asarray(cloud).reshape(-1, 3))
     n = pts.shape[0]
-    if pts.dtype == np.float32:
-        p64 = np.empty((n, 3), np.float64)
-        lib().orc_transform(_p(pts), n, _p(np.ascontiguousarray(R)), _p(np.ascontiguousarray(T)), _p(p64))
-    else:  # float64 input: same expression in numpy order
-        p64 = np.ascontiguousarray(pts.astype(np.float64) @ np.asarray(R).T + np.asarray(T))
+    p64 = transform(pts, R, T)
     best = np.full(cfg.h * cfg.w, np.inf)
     win = np.full(cfg.h * cfg.w, -1, np.int64)
     counts = np.zeros(3, np.int64)

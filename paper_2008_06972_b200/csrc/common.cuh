@@ -27,6 +27,18 @@ struct Trig {
     const double* cos_p;  // [h]
 };
 
+// One output coordinate of RigidTransform.apply, pts @ R.T + T
+// (motion.py:70-72).  numpy runs the K=3 product through the BLAS dgemm
+// micro-kernel, which accumulates k = 0,1,2 with fused multiply-adds; the + T
+// is a separate numpy add.  For float32 clouds every product is exact, so the
+// FMA chain equals the unfused sum; for float64 clouds it is what decides the
+// bits (pinned by the reference's decompress hashes, tests/golden).
+__device__ __forceinline__ double xform_coord(double x, double y, double z, double r0, double r1, double r2,
+                                              double t)
+{
+    return __fma_rn(z, r2, __fma_rn(y, r1, x * r0)) + t;
+}
+
 __device__ __forceinline__ void ray_dir(const Trig& tg, int v, int u, double& dx, double& dy, double& dz)
 {
     double sp = __ldg(tg.sin_p + v);

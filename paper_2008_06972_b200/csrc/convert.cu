@@ -80,9 +80,9 @@ __device__ __forceinline__ Binned bin_point(double px, double py, double pz, con
 {
     Binned o{0, 0, 0.0, false};
     // ((x*r0 + y*r1) + z*r2) + t, no contraction (-fmad=false)
-    double x = ((px * R[0] + py * R[1]) + pz * R[2]) + T[0];
-    double y = ((px * R[3] + py * R[4]) + pz * R[5]) + T[1];
-    double z = ((px * R[6] + py * R[7]) + pz * R[8]) + T[2];
+    double x = xform_coord(px, py, pz, R[0], R[1], R[2], T[0]);
+    double y = xform_coord(px, py, pz, R[3], R[4], R[5], T[1]);
+    double z = xform_coord(px, py, pz, R[6], R[7], R[8], T[2]);
     if (!(isfinite(x) && isfinite(y) && isfinite(z))) return o;
     double r = sqrt((x * x + y * y) + z * z);
     if (r <= 0.0) return o;
@@ -232,9 +232,9 @@ __global__ void __launch_bounds__(256, 4) convert_kernel(ConvertArgs a, const T*
         long long i = cb + k * 256 + threadIdx.x;
         if (i >= e) continue;
         double qx = (double)px[k], qy = (double)py[k], qz = (double)pz[k];
-        double x = ((qx * xf[0] + qy * xf[1]) + qz * xf[2]) + xf[9];
-        double y = ((qx * xf[3] + qy * xf[4]) + qz * xf[5]) + xf[10];
-        double z = ((qx * xf[6] + qy * xf[7]) + qz * xf[8]) + xf[11];
+        double x = xform_coord(qx, qy, qz, xf[0], xf[1], xf[2], xf[9]);
+        double y = xform_coord(qx, qy, qz, xf[3], xf[4], xf[5], xf[10]);
+        double z = xform_coord(qx, qy, qz, xf[6], xf[7], xf[8], xf[11]);
         if (!(isfinite(x) && isfinite(y) && isfinite(z))) {
             rej += 1;
             continue;
@@ -311,9 +311,9 @@ __global__ void __launch_bounds__(256) convert_overflow_kernel(ConvertArgs a, co
     for (long long i = b + (long long)blockIdx.x * blockDim.x + threadIdx.x; i < e; i += (long long)gridDim.x * blockDim.x) {
         const T* p = pts + 3 * i;
         double px = (double)p[0], py = (double)p[1], pz = (double)p[2];
-        double x = ((px * xf[0] + py * xf[1]) + pz * xf[2]) + xf[9];
-        double y = ((px * xf[3] + py * xf[4]) + pz * xf[5]) + xf[10];
-        double z = ((px * xf[6] + py * xf[7]) + pz * xf[8]) + xf[11];
+        double x = xform_coord(px, py, pz, xf[0], xf[1], xf[2], xf[9]);
+        double y = xform_coord(px, py, pz, xf[3], xf[4], xf[5], xf[10]);
+        double z = xform_coord(px, py, pz, xf[6], xf[7], xf[8], xf[11]);
         if (!(isfinite(x) && isfinite(y) && isfinite(z))) continue;
         double r = sqrt((x * x + y * y) + z * z);
         long long u, v;

@@ -209,7 +209,7 @@ __global__ void count_points_kernel(const double* out_r, long long P, int* blk_c
 }
 
 // points = r * d in row-major pixel order per frame, then p' = R^-1 p + T^-1
-// with ((x r0 + y r1) + z r2) + t (motion.py:70-72 on the inverse transform).
+// with fma(z, r2, fma(y, r1, x r0)) + t (motion.py:70-72 on the inverse transform).
 __global__ void unproject_kernel(Geometry g, Trig tg, const double* out_r, const long long* blk_off,
                                  const double* xf_inv, double* pts)
 {
@@ -232,9 +232,13 @@ __global__ void unproject_kernel(Geometry g, Trig tg, const double* out_r, const
     const double r = out_r[i];
     const double x = r * dx, y = r * dy, z = r * dz;
     const double* R = xf_inv + 12 * f;
-    pts[3 * o] = ((x * R[0] + y * R[1]) + z * R[2]) + R[9];
-    pts[3 * o + 1] = ((x * R[3] + y * R[4]) + z * R[5]) + R[10];
-    pts[3 * o + 2] = ((x * R[6] + y * R[7]) + z * R[8]) + R[11];
+    // numpy's pts @ Rinv.T is a K=3 dgemm: the BLAS micro-kernel accumulates
+    // k = 0,1,2 with fused multiply-adds (checked bit-for-bit against the
+    // reference's decompress output, tests/golden dec_sha256); + T is a
+    // separate add.  -fmad=false keeps every other op unfused.
+    pts[3 * o] = xform_coord(x, y, z, R[0], R[1], R[2], R[9]);
+    pts[3 * o + 1] = xform_coord(x, y, z, R[3], R[4], R[5], R[10]);
+    pts[3 * o + 2] = xform_coord(x, y, z, R[6], R[7], R[8], R[11]);
 }
 
 }  // namespace stpc

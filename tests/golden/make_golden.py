@@ -99,6 +99,13 @@ def with_bad_points(clouds):
     return out
 
 
+def with_f64_jitter(clouds):
+    """float64 clouds that are not float32-representable: the transform's
+    products are inexact, so the BLAS FMA contraction shows in the bits."""
+    rng = np.random.default_rng(7)
+    return [c * (1.0 + rng.uniform(-1e-6, 1e-6, c.shape)) for c in clouds]
+
+
 def with_empty_frame(clouds):
     out = list(clouds)
     out[0] = np.zeros((0, 3), np.float32)
@@ -149,13 +156,23 @@ def projection_cases():
     print("projection", list(cases))
 
 
+CASES = {
+    "single_4x4": lambda: compress_case("single_4x4", 101, 1, 0.1, 4, 4),
+    "stream3_4x4": lambda: compress_case("stream3_4x4", 102, 3, 0.1, 4, 4),
+    "stream5_2x2": lambda: compress_case("stream5_2x2", 103, 5, 0.2, 2, 2),
+    "stream4_8x4_k0": lambda: compress_case("stream4_8x4_k0", 104, 4, 0.05, 8, 5, k=0),
+    "single_f64_bad": lambda: compress_case("single_f64_bad", 105, 1, 0.1, 4, 4, f64=True, mutate=with_bad_points),
+    "stream3_empty": lambda: compress_case("stream3_empty", 106, 3, 0.1, 4, 4, mutate=with_empty_frame),
+    "stream6_16x16": lambda: compress_case("stream6_16x16", 107, 6, 0.02, 16, 16),
+    "stream4_f64": lambda: compress_case("stream4_f64", 108, 4, 0.1, 4, 4, f64=True, mutate=with_f64_jitter),
+}
+
 if __name__ == "__main__":
-    projection_cases()
-    huffman_cases()
-    compress_case("single_4x4", 101, 1, 0.1, 4, 4)
-    compress_case("stream3_4x4", 102, 3, 0.1, 4, 4)
-    compress_case("stream5_2x2", 103, 5, 0.2, 2, 2)
-    compress_case("stream4_8x4_k0", 104, 4, 0.05, 8, 5, k=0)
-    compress_case("single_f64_bad", 105, 1, 0.1, 4, 4, f64=True, mutate=with_bad_points)
-    compress_case("stream3_empty", 106, 3, 0.1, 4, 4, mutate=with_empty_frame)
-    compress_case("stream6_16x16", 107, 6, 0.02, 16, 16)
+    # python tests/golden/make_golden.py [case ...]   (no args: everything)
+    only = sys.argv[1:]
+    if not only:
+        projection_cases()
+        huffman_cases()
+    for name, fn in CASES.items():
+        if not only or name in only:
+            fn()
