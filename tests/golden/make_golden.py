@@ -156,6 +156,36 @@ def projection_cases():
     print("projection", list(cases))
 
 
+def imu_case(name, seed, n, tau, tw, th, sensor=SMALL):
+    """compress() through the IMU path (motion.py:119-207): a 200 Hz trace with
+    a gap, reference frame_transforms stored as the case's poses (the key is
+    identity, so poses_to_transforms on them is an exact no-op) plus the trace."""
+    g = synth.make_group(seed, n, sensor)
+    rng = np.random.default_rng(seed)
+    t = np.round(np.arange(0.0, 0.1 * n + 0.05, 0.005), 6)
+    t = np.delete(t, [40, 41, 42])  # a gap > 2x nominal (logged, not an error)
+    accel = rng.normal([0.8, 0.1, 0.0], 0.3, (t.size, 3))
+    gyro = rng.normal([0.0, 0.0, 0.15], 0.02, (t.size, 3))
+    imu = [stpc.ImuSample(t=float(a), accel=b, gyro=c) for a, b, c in zip(t, accel, gyro)]
+    frame_times = [0.013 + 0.1 * i for i in range(n)]
+    v0 = np.array([9.5, 0.2, 0.0])
+    cfg = ref_cfg(sensor, n, tau, tw, th, None)
+    blob, rep = stpc.compress(g.clouds, cfg, imu_samples=imu, frame_times=frame_times, v0=v0)
+    ts = stpc.frame_transforms(imu, frame_times, cfg.k_index, v0)
+    dec = stpc.decompress(blob)
+    extra = dict(fractions=np.array([rep.fractions["temporal"], rep.fractions["spatial"], rep.fractions["residual"]]),
+                 imu_t=t, imu_accel=accel, imu_gyro=gyro, frame_times=np.array(frame_times), v0=v0,
+                 dec_sha256=np.array([hashlib.sha256(np.ascontiguousarray(p).tobytes()).hexdigest() for p in dec]),
+                 dec_counts=np.array([p.shape[0] for p in dec], np.int64))
+    for i, (c, tr) in enumerate(zip(g.clouds, [x.round_f32() for x in ts])):
+        img, win = ref_project(tr.apply(c), cfg.res, cfg.w, cfg.h, cfg.phi_offset, return_indices=True)
+        extra[f"ranges{i}"] = img.ranges
+        extra[f"win{i}"] = win.astype(np.int32)
+        extra[f"counts{i}"] = np.array([img.stats.rejected_nonfinite, img.stats.dropped_fov,
+                                        img.stats.collisions], np.int64)
+    save_case(name, list(g.clouds), [(x.R, x.T) for x in ts], cfg, blob, extra)
+
+
 CASES = {
     "single_4x4": lambda: compress_case("single_4x4", 101, 1, 0.1, 4, 4),
     "stream3_4x4": lambda: compress_case("stream3_4x4", 102, 3, 0.1, 4, 4),
@@ -164,6 +194,7 @@ CASES = {
     "single_f64_bad": lambda: compress_case("single_f64_bad", 105, 1, 0.1, 4, 4, f64=True, mutate=with_bad_points),
     "stream3_empty": lambda: compress_case("stream3_empty", 106, 3, 0.1, 4, 4, mutate=with_empty_frame),
     "stream6_16x16": lambda: compress_case("stream6_16x16", 107, 6, 0.02, 16, 16),
+    "stream5_imu": lambda: imu_case("stream5_imu", 109, 5, 0.1, 4, 4),
     "stream4_f64": lambda: compress_case("stream4_f64", 108, 4, 0.1, 4, 4, f64=True, mutate=with_f64_jitter),
 }
 

@@ -177,6 +177,17 @@ def test_golden_blob(name):
         assert (rep.fractions["temporal"], rep.fractions["spatial"], rep.fractions["residual"]) == tuple(fr)
 
 
+def test_golden_blob_imu_path():
+    """compress(imu_samples=, frame_times=, v0=) == the reference's blob
+    (IMU alignment on the host, then the device path)."""
+    from paper_2008_06972_b200 import ImuSample, compress
+
+    clouds, poses, cfg, blob, z = load_case("stream5_imu")
+    imu = [ImuSample(t=float(t), accel=a, gyro=g) for t, a, g in zip(z["imu_t"], z["imu_accel"], z["imu_gyro"])]
+    mine, rep = compress(clouds, cfg, imu_samples=imu, frame_times=list(z["frame_times"]), v0=z["v0"])
+    assert mine == (blob if trig_matches_host(z, cfg) else oracle.compress(clouds, cfg, poses)[0])
+
+
 def _cfg(sensor, n, tau, tile):
     from paper_2008_06972_b200 import AngularResolution, CodecConfig
 

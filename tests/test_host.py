@@ -209,3 +209,39 @@ def test_decoder_rejects_bad_headers():
         _header(blob[:4] + b"\x02\x00" + blob[6:])
     with pytest.raises(TruncatedBlobError):
         _header(blob[:-10])
+
+
+def _imu_of(z):
+    from paper_2008_06972_b200 import ImuSample
+
+    return [ImuSample(t=float(t), accel=a, gyro=g) for t, a, g in zip(z["imu_t"], z["imu_accel"], z["imu_gyro"])]
+
+
+def test_imu_frame_transforms_match_reference_bits():
+    """frame_transforms (motion.py:169-207) over a gapped 200 Hz trace equals
+    the reference's output bit-for-bit (stored as the fixture's poses)."""
+    from paper_2008_06972_b200 import frame_transforms
+
+    clouds, poses, cfg, blob, z = load_case("stream5_imu")
+    ts = frame_transforms(_imu_of(z), list(z["frame_times"]), cfg.k_index, z["v0"])
+    for t, (R, T) in zip(ts, poses):
+        assert np.array_equal(t.R, R) and np.array_equal(t.T, T)
+
+
+def test_imu_errors_mirror_reference():
+    from paper_2008_06972_b200 import ImuCoverageError, frame_transforms, integrate_imu
+
+    clouds, poses, cfg, blob, z = load_case("stream5_imu")
+    imu = _imu_of(z)
+    with pytest.raises(ImuCoverageError):
+        integrate_imu(imu, -1.0, 0.1)
+    with pytest.raises(ImuCoverageError):
+        integrate_imu([], 0.0, 0.1)
+    with pytest.raises(ValueError):
+        integrate_imu(imu, 0.2, 0.1)
+    with pytest.raises(ValueError):
+        frame_transforms(imu, [0.1, 0.1], 0)
+    with pytest.raises(ValueError):
+        frame_transforms(imu, [0.1, 0.2], 2)
+    d, a, v = integrate_imu(imu, 0.1, 0.1, z["v0"])
+    assert not d.any() and not a.any() and np.array_equal(v, z["v0"])
