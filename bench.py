@@ -50,6 +50,8 @@ def parse():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--stages", action="store_true", help="print per-stage ms to stderr")
+    ap.add_argument("--no-decode", action="store_true", help="skip the decompress measurement")
+    ap.add_argument("--decode-e2e-groups", type=int, default=128)
     return ap.parse_args()
 
 
@@ -210,6 +212,88 @@ def cpu_pool_rate(sample, cfg, n, seconds, cores):
     return done * n / dt, done, dt
 
 
+_DEC_SAMPLE = None
+
+
+def _dec_job(i):
+    from oracle import decode as odec
+
+    return sum(c.shape[0] for c in odec.decompress(_DEC_SAMPLE[i]))
+
+
+def cpu_decode_rate(blobs, n, seconds, cores):
+    """Frames/s of the oracle decoder (numpy + C restatement of
+    stpc.decompress) over a bounded sample, all host cores."""
+    import concurrent.futures as cf
+    import multiprocessing as mp
+
+    from oracle import oracle
+
+    global _DEC_SAMPLE
+    oracle.build()
+    _DEC_SAMPLE = list(blobs)
+    t0 = time.perf_counter()
+    done = 0
+    with cf.ProcessPoolExecutor(max_workers=cores, mp_context=mp.get_context("fork")) as ex:
+        while True:
+            list(ex.map(_dec_job, [(done + j) % len(blobs) for j in range(cores)]))
+            done += cores
+            if time.perf_counter() - t0 >= seconds:
+                break
+    dt = time.perf_counter() - t0
+    return done * n / dt, done, dt
+
+
+def measure_decode(args, L, enc, G, n, rank, world, cpu_ok):
+    """decompress of this step's blobs: device-resident
+    blobs -> points left in HBM (value), and end to end through
+    decompress_many from host bytes to float64 numpy clouds (e2e)."""
+    import torch
+
+    from paper_2008_06972_b200.decode import Decoder, decompress_many
+
+    dec = Decoder()
+    off_b, len_b = enc.blob_layout()
+    dptr = L.stpc_result_device_blobs(enc.handle)
+    offs = np.ascontiguousarray(off_b[:G + 1], np.int64)
+    for _ in range(max(args.warmup, 1)):
+        dec.decode(dptr, offs, True, keep_on_device=True)
+    torch.cuda.synchronize()
+    launches0 = L.stpc_launch_count()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        _, reps, errs = dec.decode(dptr, offs, True, keep_on_device=True)
+    dt = (time.perf_counter() - t0) / max(args.steps, 1)
+    launches = int(L.stpc_launch_count() - launches0) // max(args.steps, 1)
+    assert not errs, errs
+    pts = sum(sum(r.point_counts) for r in reps)
+    out = {"metric": "frames/sec decompressed", "value": G * n / dt, "unit": "frames/s", "ms_per_step": dt * 1e3,
+           "groups": G, "mpoints_per_s": pts / dt / 1e6, "gpu_launches_per_step": launches,
+           "timing": "host wall clock around the synchronous decoder call (blobs resident in HBM, "
+                     "points left in HBM)"}
+    # end to end: host blob bytes -> numpy clouds
+    Ge = min(G, args.decode_e2e_groups)
+    arena = np.empty(int(off_b[Ge]), np.uint8)
+    L.stpc_memcpy_d2h(arena.ctypes.data, dptr, arena.nbytes)
+    blobs = [arena[off_b[i]:off_b[i] + len_b[i]].tobytes() for i in range(Ge)]
+    del dec
+    decompress_many(blobs)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        clouds, _ = decompress_many(blobs)
+    et = (time.perf_counter() - t0) / max(args.steps, 1)
+    npts = sum(c.shape[0] for cl in clouds for c in cl)
+    out["e2e"] = {"value": Ge * n / et, "unit": "frames/s", "ms_per_step": et * 1e3, "groups": Ge,
+                  "h2d_bytes_per_step": int(sum(len(b) for b in blobs)), "d2h_bytes_per_step": int(24 * npts)}
+    if cpu_ok and rank == 0 and world == 1:
+        cores = host_cores()
+        rate, done, cdt = cpu_decode_rate(blobs[:max(cores, 8)], n, args.cpu_seconds / 2, cores)
+        out["cpu_baseline"] = {"value": rate, "unit": "frames/s", "cores": cores, "kind": "port",
+                               "sample": f"{done} blobs ({done * n} frames) of this workload through the "
+                                         f"numpy/C oracle decoder in {cdt:.1f} s, ProcessPool x{cores}"}
+    return out
+
+
 def host_cores():
     try:
         return len(os.sched_getaffinity(0))
@@ -339,6 +423,14 @@ def main():
     stage_ms = stage_ms[:ns] / max(args.steps, 1)
     L.stpc_encoder_profile(enc.handle, 0)
 
+    decode = None
+    if not args.no_decode:
+        try:
+            decode = measure_decode(args, L, enc, G, n, rank, world, not args.no_cpu)
+        except Exception as exc:  # never let the decoder leg kill the encoder line
+            decode = {"error": repr(exc)[:300]}
+    torch.cuda.empty_cache()
+
     off_b, len_b = enc.blob_layout()
     raw = enc.payload_lengths()
     blob_bytes = int(len_b.sum())
@@ -442,6 +534,7 @@ def main():
             "e2e": e2e, "roofline": roofline, "cpu_baseline": cpu, "clocks": clk,
             "gpu_launches": launches,
             "stage_ms": {nm: round(float(v), 4) for nm, v in zip(names, stage_ms)},
+            "decode": decode,
             "impl": "b200",
         }
         print(json.dumps(line))

@@ -20,6 +20,8 @@
  *                        huffman_encode_kernel _kernels.py:363-382, zlib.crc32)
  * stpc_project         project(..., return_indices=True) (range_image.py:165-211)
  *                        fused with RigidTransform.apply (motion.py:70-72)
+ * stpc_decoder_*       decompress (bitstream.py:605-631): deserialize,
+ *                        decode_stream_images, unproject (see below)
  */
 #ifndef STPC_B200_H
 #define STPC_B200_H
@@ -128,25 +130,58 @@ int stpc_project(const void* d_points, int32_t points_f64, const int64_t* point_
                  const double* transforms, int32_t w, int32_t h, double theta_r, double phi_r,
                  double phi_offset, double* d_best, int64_t* d_win, int64_t* h_counts, void* stream);
 
-/* Decoder (decompress).  d_blob_off: device int64[n]
- * blob starts in d_blobs.  stpc_crc32_blobs: zlib CRC-32 of each blob's entropy
- * payload (bitstream.py:410-411).  stpc_huffman_decode_blobs: raw payload of
- * each blob into d_out + d_out_off[i] (huffman_decode_kernel, _kernels.py:
- * 385-417); h_status 0 ok / 1 truncated / 2 invalid code.
- * stpc_reconstruct_frames: per-tile plane maps (float4 a, b, c, kind; kind 0 =
- * none) + validity bitmaps + residual pixels -> points (float64 xyz, row-major
- * per frame, inverse-transformed with d_xf_inv [F][12] = R^-1 | T^-1)
- * (decode_stream_images temporal.py:293-343, reconstruct_span _kernels.py:
- * 282-308, unproject range_image.py:214-221).  d_scratch: f64 [F][h*w]. */
-int stpc_crc32_blobs(const uint8_t* d_blobs, const int64_t* d_blob_off, int32_t n, uint32_t* h_crc, void* stream);
-int stpc_huffman_decode_blobs(const uint8_t* d_blobs, const int64_t* d_blob_off, int32_t n, uint8_t* d_out,
-                              const int64_t* d_out_off, int32_t* h_status, void* stream);
-int stpc_reconstruct_frames(int32_t w, int32_t h, int32_t tile_w, int32_t tile_h, const double* d_trig,
-                            int32_t n_frames, const uint8_t* d_vbits, int64_t vstride, const float* d_tile_map,
-                            const int64_t* d_res_flat, const double* d_res_range, const int32_t* d_res_frame,
-                            int64_t n_res, const double* d_xf_inv, double r_max, double* d_scratch,
-                            double* d_points, int64_t points_cap, int64_t* h_frame_counts, int64_t* h_failed,
-                            void* stream);
+/* Decoder (decompress / decompress_full, bitstream.py:605-631; SURVEY.md
+ * §8(f) rank 3), batched over blobs, all on the GPU:
+ *
+ * stpc_decoder_load    replaces deserialize's header checks (bitstream.py:
+ *                        398-409), zlib.crc32 (:410-411), decode_tables and
+ *                        huffman.decode_bytes (huffman.py:80-137,
+ *                        huffman_decode_kernel _kernels.py:385-417).  blobs:
+ *                        host or device bytes, blob i at [offsets[i],
+ *                        offsets[i+1]).  status[i]: STPC_DEC_* of the first
+ *                        failing check, in the reference's order.
+ * stpc_decoder_heads   first head_cap bytes of each raw payload (config block
+ *                        + float32 transforms, bitstream.py:413-426) for the
+ *                        host-side config checks.
+ * stpc_decoder_frames  replaces the record sections of deserialize (:428-519),
+ *                        decode_stream_images (temporal.py:293-343) and
+ *                        reconstruct_span (_kernels.py:282-308) for the loaded
+ *                        blobs sel[0..m) sharing one configuration; trig tables
+ *                        as for the encoder; xf_inv: double[m*n][12]
+ *                        R^-1 | T^-1 (RigidTransform.inverse, motion.py:78-79).
+ *                        frame_counts[m*n]: points per frame; status[m]: 0 or
+ *                        (reader position << 8 | order << 4 | STPC_DEC_*) of
+ *                        the first structural error; failed[m]: failed
+ *                        reconstructions (DecodeReport).
+ * stpc_decoder_points  unproject (range_image.py:214-221) + inverse transform
+ *                        (motion.py:70-72): float64 xyz of every frame of the
+ *                        last stpc_decoder_frames, concatenated, into dst (host
+ *                        or device, capacity cap_points points); dst NULL with
+ *                        dst_on_device = 1 keeps them in the decoder's own
+ *                        device buffer (stpc_decoder_device_points). */
+#define STPC_DEC_TRUNCATED 1 /* TruncatedBlobError */
+#define STPC_DEC_MALFORMED 2 /* MalformedBlobError */
+#define STPC_DEC_CHECKSUM 3  /* ChecksumError */
+#define STPC_DEC_VERSION 4   /* UnknownVersionError */
+
+typedef struct stpc_decode_geom {
+    int32_t w, h, tile_w, tile_h, n_frames, k_index;
+    double range_quant, r_max;
+} stpc_decode_geom;
+
+typedef struct stpc_decoder stpc_decoder;
+int stpc_decoder_create(stpc_decoder** out);
+void stpc_decoder_destroy(stpc_decoder* dec);
+int stpc_decoder_load(stpc_decoder* dec, const uint8_t* blobs, int32_t blobs_on_device, const int64_t* offsets,
+                      int32_t n, int32_t* status, void* stream);
+int stpc_decoder_heads(stpc_decoder* dec, int32_t head_cap, uint8_t* h_heads, int64_t* h_raw_len, void* stream);
+int stpc_decoder_frames(stpc_decoder* dec, const stpc_decode_geom* geom, const int32_t* sel, int32_t m,
+                        const double* sin_theta, const double* cos_theta, const double* sin_phi,
+                        const double* cos_phi, const double* xf_inv, int64_t* frame_counts, int64_t* status,
+                        int64_t* failed, void* stream);
+int64_t stpc_decoder_total_points(const stpc_decoder* dec);
+int stpc_decoder_points(stpc_decoder* dec, double* dst, int32_t dst_on_device, int64_t cap_points, void* stream);
+const double* stpc_decoder_device_points(const stpc_decoder* dec);
 
 /* Utilities so FFI callers need no CUDA runtime binding of their own. */
 int stpc_malloc(void** dev_ptr, int64_t bytes);

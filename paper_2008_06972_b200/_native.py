@@ -30,12 +30,22 @@ EXPORTS = [
     "stpc_encoder_buffer", "stpc_project", "stpc_malloc", "stpc_free", "stpc_memcpy_d2h",
     "stpc_memcpy_h2d", "stpc_device_count", "stpc_last_error", "stpc_version",
     "stpc_encoder_profile", "stpc_encoder_stage_ms", "stpc_stage_name", "stpc_launch_count",
-    "stpc_crc32_blobs", "stpc_huffman_decode_blobs", "stpc_reconstruct_frames",
+    "stpc_decoder_create", "stpc_decoder_destroy", "stpc_decoder_load", "stpc_decoder_heads",
+    "stpc_decoder_frames", "stpc_decoder_total_points", "stpc_decoder_points",
+    "stpc_decoder_device_points",
 ]
+
+# stpc_decoder_* status kinds
+DEC_TRUNCATED, DEC_MALFORMED, DEC_CHECKSUM, DEC_VERSION = 1, 2, 3, 4
 
 
 class NativeUnavailable(CodecError):
     """libstpc_b200 is not built or no CUDA device is present (no CPU fallback)."""
+
+
+class StpcDecodeGeom(ctypes.Structure):
+    _fields_ = [(name, ctypes.c_int32) for name in ("w", "h", "tile_w", "tile_h", "n_frames", "k_index")] + [
+        ("range_quant", ctypes.c_double), ("r_max", ctypes.c_double)]
 
 
 class StpcConfig(ctypes.Structure):
@@ -97,10 +107,15 @@ def load(require_device: bool = False):
                 "stpc_encoder_stage_ms": ([P, P, I32], I32),
                 "stpc_stage_name": ([I32], ctypes.c_char_p),
                 "stpc_launch_count": ([], ctypes.c_uint64),
-                "stpc_crc32_blobs": ([P, P, I32, P, P], ctypes.c_int),
-                "stpc_huffman_decode_blobs": ([P, P, I32, P, P, P, P], ctypes.c_int),
-                "stpc_reconstruct_frames": ([I32, I32, I32, I32, P, I32, P, I64, P, P, P, P, I64, P, D, P, P,
-                                             I64, P, ctypes.POINTER(I64), P], ctypes.c_int),
+                "stpc_decoder_create": ([ctypes.POINTER(P)], ctypes.c_int),
+                "stpc_decoder_destroy": ([P], None),
+                "stpc_decoder_load": ([P, P, I32, P, I32, P, P], ctypes.c_int),
+                "stpc_decoder_heads": ([P, I32, P, P, P], ctypes.c_int),
+                "stpc_decoder_frames": ([P, ctypes.POINTER(StpcDecodeGeom), P, I32, P, P, P, P, P, P, P, P, P],
+                                        ctypes.c_int),
+                "stpc_decoder_total_points": ([P], I64),
+                "stpc_decoder_points": ([P, P, I32, I64, P], ctypes.c_int),
+                "stpc_decoder_device_points": ([P], P),
             }
             for name, (args, res) in sig.items():
                 fn = getattr(L, name)

@@ -1,23 +1,96 @@
-// Decoder kernels: the device side of decompress().
+// Decoder: the device side of decompress().
 //
-// Replaces the heavy loops of the reference decoder
-// (/root/reference/pkg/src/stpc/bitstream.py:388-519, 605-631):
-//   * zlib.crc32 of the entropy payload (:410-411)       -> crc_blob_kernel
-//   * huffman_decode_kernel (_kernels.py:385-417)       -> huff_decode_kernel
-//   * decode_stream_images + reconstruct_span
-//     (temporal.py:293-343, _kernels.py:282-308)        -> reconstruct_kernel
-//   * unproject (range_image.py:214-221) + the inverse
-//     frame transform (motion.py:78-79, 70-72)          -> unproject_kernel
-// Record-level parsing (runs, fallback rows, residual varints: O(records))
-// stays in the host mirror (decode.py), which builds per-tile plane maps.
+// Replaces the reference decoder (/root/reference/pkg/src/stpc/bitstream.py:
+// 388-519, 605-631) end to end on the GPU, batched over blobs:
+//
+//   phase 1  stpc_decoder_load     header + code-table checks (host, :398-409,
+//                                  huffman.py:80-104), zlib.crc32 (:410-411)
+//                                  -> crc_blob_kernel, canonical Huffman decode
+//                                  (huffman.py:121-137, _kernels.py:385-417)
+//                                  -> huff_decode_kernel
+//   phase 2  stpc_decoder_frames   record sections of deserialize (:428-519)
+//                                  -> parse_kernel (validation + per-tile plane
+//                                  maps + residual section bounds);
+//                                  decode_stream_images (temporal.py:293-343)
+//                                  with reconstruct_span (_kernels.py:282-308)
+//                                  -> reconstruct_kernel, residual_kernel;
+//                                  point counts -> count/scan kernels
+//   phase 3  stpc_decoder_points   unproject (range_image.py:214-221) + the
+//                                  inverse frame transform (motion.py:78-79,
+//                                  70-72) -> unproject_kernel
+//
+// Structural errors carry a key (reader position << 8 | order << 4 | kind);
+// the smallest key per blob is the error the reference's sequential reader
+// (_Reader, bitstream.py:333-353) raises first.
+#include <algorithm>
+#include <cstring>
+#include <string>
 #include <vector>
 
 #include "kernels.cuh"
+#include "runtime.cuh"
 #include "../../include/stpc_b200.h"
 
 namespace stpc {
 
-__device__ __forceinline__ unsigned int dec_multmodp(unsigned int a, unsigned int b)
+constexpr unsigned long long DEC_NONE = ~0ull;
+// "no point" marker of the range scratch: a signalling NaN whose low mantissa
+// bit is set, which neither a float32 escape range widened to float64 (low 29
+// bits zero) nor a reconstructed range (positive, finite) can produce.
+constexpr long long DEC_NOPT = 0x7ff4000000000001ll;
+constexpr int DEC_HEADER = 284;
+
+struct DecGeom {
+    int w, h, tw, th, tx, ty, n, k, pm;
+    long long P, nb;
+    long long bits_off;  // 57 + 48 n: first validity bitmap
+    long long runs_off;  // bits_off + n nb: temporal run count
+    double quant, r_max;
+};
+
+struct ResSec {
+    long long pos_var;   // first varint byte
+    long long cnt;       // residual pixels
+    long long pos_code;  // u16 codes
+    long long pos_esc;   // f32 escape ranges
+};
+
+__device__ __forceinline__ unsigned dec_u8(const uint8_t* p) { return __ldg(p); }
+__device__ __forceinline__ unsigned dec_u16(const uint8_t* p) { return dec_u8(p) | (dec_u8(p + 1) << 8); }
+__device__ __forceinline__ unsigned dec_u32(const uint8_t* p) { return dec_u16(p) | (dec_u16(p + 2) << 16); }
+__device__ __forceinline__ float dec_f32(const uint8_t* p) { return __uint_as_float(dec_u32(p)); }
+__device__ __forceinline__ unsigned long long dec_key(long long pos, int order, int kind)
+{
+    return ((unsigned long long)pos << 8) | ((unsigned)order << 4) | (unsigned)kind;
+}
+
+// ---------------------------------------------------------------- block scans
+
+template <int NT>
+__device__ __forceinline__ long long block_excl_scan(long long v, long long& total)
+{
+    __shared__ long long ws[NT / 32];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    long long x = v;
+    for (int o = 1; o < 32; o <<= 1) {
+        const long long t = __shfl_up_sync(STPC_FULL, x, o);
+        if (lane >= o) x += t;
+    }
+    if (lane == 31) ws[wid] = x;
+    __syncthreads();
+    long long before = 0, tot = 0;
+    for (int w = 0; w < NT / 32; ++w) {
+        if (w < wid) before += ws[w];
+        tot += ws[w];
+    }
+    __syncthreads();
+    total = tot;
+    return before + x - v;
+}
+
+// ---------------------------------------------------------------- CRC-32
+
+__host__ __device__ __forceinline__ unsigned int dec_multmodp(unsigned int a, unsigned int b)
 {
     unsigned int m = 1u << 31, p = 0;
     for (;;) {
@@ -31,7 +104,7 @@ __device__ __forceinline__ unsigned int dec_multmodp(unsigned int a, unsigned in
     return p;
 }
 
-__device__ __forceinline__ unsigned int dec_x8nmodp(unsigned long long nbytes)
+__host__ __device__ __forceinline__ unsigned int dec_x8nmodp(unsigned long long nbytes)
 {
     unsigned int p = 1u << 31, sq = 1u << 23;
     while (nbytes) {
@@ -42,127 +115,782 @@ __device__ __forceinline__ unsigned int dec_x8nmodp(unsigned long long nbytes)
     return p;
 }
 
-// block per blob: threads CRC 1 KB pieces of the encoded payload, thread 0
-// combines them in order (a few hundred pieces per blob).
+constexpr int DC_PIECE = 128;                   // bytes per thread
+constexpr int DC_CHUNK = 256 * DC_PIECE;          // bytes per block pass
+
+struct DecCrcK {
+    unsigned int lvl[8];  // x^(8 * DC_PIECE * 2^l) mod P, l = 0..7
+    unsigned int chunk;   // x^(8 * DC_CHUNK)
+};
+
+// Block per blob.  Each pass stages a 32 KB chunk of the entropy payload in
+// shared memory (coalesced 32-bit loads from the aligned base), every thread
+// folds a 128-byte piece with the byte table, and the pieces are combined
+// in order by a shuffle tree (crc(A|B) = x^(8|B|) crc(A) ^ crc(B) for the
+// zero-initialised register).  A short last chunk is end-aligned in its
+// frame: leading zero bytes leave a zero register unchanged.  crc_bad =
+// (zlib.crc32(encoded) != header CRC), bitstream.py:410-411.
 __global__ void __launch_bounds__(256) crc_blob_kernel(const uint8_t* blobs, const long long* blob_off,
-                                                       unsigned int* crc_out)
+                                                       const int* skip, DecCrcK K, int* crc_bad)
 {
+    if (skip[blockIdx.x]) return;
     __shared__ unsigned int tab[256];
-    __shared__ unsigned int part[256];
-    for (int i = threadIdx.x; i < 256; i += blockDim.x) {
-        unsigned int c = i;
+    __shared__ unsigned int stage[DC_CHUNK / 4 + 2];
+    __shared__ unsigned int wpart[8];
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    {
+        unsigned int c = tid;
         for (int k = 0; k < 8; ++k) c = c & 1 ? (c >> 1) ^ 0xedb88320u : c >> 1;
-        tab[i] = c;
+        tab[tid] = c;
     }
-    __syncthreads();
     const uint8_t* blob = blobs + blob_off[blockIdx.x];
     unsigned long long enc_len = 0;
     for (int b = 0; b < 8; ++b) enc_len |= (unsigned long long)blob[16 + b] << (8 * b);
-    const uint8_t* enc = blob + 284;
-    const long long piece = 1024;
-    const long long npieces = ((long long)enc_len + piece - 1) / piece;
+    const unsigned int want = dec_u32(blob + 24);
+    const uint8_t* enc = blob + DEC_HEADER;
+    const unsigned long long addr = (unsigned long long)enc;
+    const int mis = (int)(addr & 3);
+    const unsigned int* wbase = (const unsigned int*)(addr - mis);
+    const long long last_byte = mis + (long long)enc_len - 1;  // relative to wbase
     unsigned int raw = 0;
-    for (long long base = 0; base < npieces; base += 256) {
-        const long long pi = base + threadIdx.x;
-        unsigned int c = 0;
-        if (pi < npieces) {
-            const long long e = min((pi + 1) * piece, (long long)enc_len);
-            for (long long i = pi * piece; i < e; ++i) c = tab[(c ^ enc[i]) & 0xff] ^ (c >> 8);
-        }
-        part[threadIdx.x] = c;
+    for (long long base = 0; base < (long long)enc_len; base += DC_CHUNK) {
+        const long long nb = min((long long)DC_CHUNK, (long long)enc_len - base);
+        const long long w0 = (mis + base) >> 2;
+        const long long w1 = (mis + base + nb - 1) >> 2;
         __syncthreads();
-        if (threadIdx.x == 0) {
-            const unsigned int X = dec_x8nmodp(piece);
-            for (int t = 0; t < 256 && base + t < npieces; ++t) {
-                const long long len = min(piece, (long long)enc_len - (base + t) * piece);
-                raw = dec_multmodp(len == piece ? X : dec_x8nmodp(len), raw) ^ part[t];
+        for (long long i = tid; w0 + i <= w1; i += 256) {
+            const long long w = w0 + i;
+            unsigned int v;
+            if (4 * w + 3 <= last_byte) {
+                v = __ldg(wbase + w);
+            } else {  // the stream's last word: no read past its final byte
+                v = 0;
+                const uint8_t* bp = (const uint8_t*)wbase + 4 * w;
+                for (int k = 0; k < 4 && 4 * w + k <= last_byte; ++k) v |= (unsigned)dec_u8(bp + k) << (8 * k);
             }
+            stage[i] = v;
         }
         __syncthreads();
+        // piece tid covers frame bytes [tid*128, +128); frame byte f is stream
+        // byte base + f - (DC_CHUNK - nb); earlier frame bytes are zeros
+        const long long lead = DC_CHUNK - nb;
+        const uint8_t* sb = (const uint8_t*)stage + ((mis + base) - 4 * w0);
+        unsigned int c = 0;
+        const long long f0 = (long long)tid * DC_PIECE;
+        for (int i = 0; i < DC_PIECE; ++i) {
+            const long long f = f0 + i;
+            if (f < lead) continue;
+            c = tab[(c ^ sb[f - lead]) & 0xff] ^ (c >> 8);
+        }
+        for (int l = 0; l < 5; ++l) {
+            const unsigned int other = __shfl_down_sync(STPC_FULL, c, 1 << l);
+            if ((lane & ((2 << l) - 1)) == 0) c = dec_multmodp(K.lvl[l], c) ^ other;
+        }
+        if (lane == 0) wpart[wid] = c;
+        __syncthreads();
+        if (tid == 0) {
+            unsigned int ch = 0;
+            for (int w = 0; w < 8; ++w) ch = dec_multmodp(K.lvl[5], ch) ^ wpart[w];
+            raw = dec_multmodp(nb == DC_CHUNK ? K.chunk : dec_x8nmodp((unsigned long long)nb), raw) ^ ch;
+        }
     }
-    if (threadIdx.x == 0)
-        crc_out[blockIdx.x] = ~(raw ^ dec_multmodp(dec_x8nmodp(enc_len), 0xffffffffu));
+    if (tid == 0) {
+        const unsigned int crc = ~(raw ^ dec_multmodp(dec_x8nmodp(enc_len), 0xffffffffu));
+        crc_bad[blockIdx.x] = crc != want;
+    }
 }
 
-// One thread per blob: bit-serial canonical Huffman decode with the
-// reference's per-length first-code search (batches decode many blobs in
-// parallel).  status: 0 ok, 1 out of bits, 2 bad code.
-__global__ void huff_decode_kernel(const uint8_t* blobs, const long long* blob_off, int n, uint8_t* out,
-                                   const long long* out_off, int* status)
-{
-    const int bi = blockIdx.x * blockDim.x + threadIdx.x;
-    if (bi >= n) return;
-    const uint8_t* blob = blobs + blob_off[bi];
-    unsigned long long raw_len = 0, enc_len = 0;
-    for (int b = 0; b < 8; ++b) {
-        raw_len |= (unsigned long long)blob[8 + b] << (8 * b);
-        enc_len |= (unsigned long long)blob[16 + b] << (8 * b);
-    }
-    const uint8_t* lens = blob + 28;
-    const uint8_t* enc = blob + 284;
-    // canonical tables (huffman.py:80-104)
-    int count[33] = {0};
-    for (int s = 0; s < 256; ++s) count[lens[s]] += 1;
-    count[0] = 0;
-    unsigned int first[33], index[33];
-    unsigned int code = 0, idx = 0;
-    for (int l = 1; l <= 32; ++l) {
-        first[l] = code;
-        index[l] = idx;
-        code = (code + count[l]) << 1;
-        idx += count[l];
-    }
-    uint8_t sym_sorted[256];
+// ---------------------------------------------------------------- Huffman
+
+constexpr int HD_THREADS = 256;
+constexpr int HD_SUB = 4;                     // sub-segments per thread
+constexpr int HD_NSEG = HD_THREADS * HD_SUB;  // sub-segments per blob (max)
+constexpr int HD_LUT = 12;                    // first-level table bits
+constexpr long long HD_SEG_MIN = 2048;        // bits per sub-segment (min)
+
+struct HuffDev {
+    unsigned short lut[1 << HD_LUT];  // (len << 8) | symbol; 0 = longer code
+    unsigned long long first[33];
+    int count[33];
+    int index[33];
+    unsigned char sym[256];
+};
+
+// Bit reader over aligned 64-bit words (big-endian bit order), with a
+// four-word register ring: the load for word i+3 is issued when word i
+// becomes current, so ~190 bits of decoding cover its HBM latency.  Words
+// past the end of the stream read as zero (never outside the blob: the
+// aligned base only reaches back into the blob header).
+struct BitRd {
+    const unsigned long long* words;
+    long long wmax, wi, pos, total;
+    unsigned long long w0, w1, w2, w3;
+    int off;
+    __device__ __forceinline__ unsigned long long ld(long long i) const
     {
-        int fill[33];
-        for (int l = 1; l <= 32; ++l) fill[l] = index[l];
-        for (int s = 0; s < 256; ++s)
-            if (lens[s]) sym_sorted[fill[lens[s]]++] = (uint8_t)s;
+        if (i > wmax) return 0ull;
+        const unsigned long long x = __ldg(words + i);
+        return ((unsigned long long)__byte_perm((unsigned)x, 0, 0x0123) << 32) |
+               __byte_perm((unsigned)(x >> 32), 0, 0x0123);
     }
-    uint8_t* o = out + out_off[bi];
-    const unsigned long long total_bits = enc_len * 8;
-    unsigned long long bitpos = 0;
-    int st = 0;
-    for (unsigned long long i = 0; i < raw_len; ++i) {
-        unsigned int c = 0;
-        int l = 0;
-        for (;;) {
-            if (bitpos >= total_bits) { st = 1; break; }
-            const unsigned int bit = (enc[bitpos >> 3] >> (7 - (bitpos & 7))) & 1u;
-            ++bitpos;
-            c = (c << 1) | bit;
-            ++l;
-            if (l > 32) { st = 2; break; }
-            if (count[l] > 0 && c - first[l] < (unsigned)count[l]) {
-                o[i] = sym_sorted[index[l] + (c - first[l])];
+    __device__ __forceinline__ void init(const uint8_t* e, long long elen, long long start)
+    {
+        const unsigned long long a = (unsigned long long)e;
+        const int mis = (int)(a & 7);
+        words = (const unsigned long long*)(a - mis);
+        wmax = elen > 0 ? (mis + elen - 1) / 8 : -1;
+        const long long sb = start + 8ll * mis;
+        wi = sb >> 6;
+        off = (int)(sb & 63);
+        w0 = ld(wi);
+        w1 = ld(wi + 1);
+        w2 = ld(wi + 2);
+        w3 = ld(wi + 3);
+        pos = start;
+        total = elen * 8;
+    }
+    __device__ __forceinline__ unsigned peek32() const
+    {
+        const unsigned long long v = off ? (w0 << off) | (w1 >> (64 - off)) : w0;
+        return (unsigned)(v >> 32);
+    }
+    // branch-free advance (selects + one predicated load) so a warp's lanes
+    // stay converged through the decode loop
+    __device__ __forceinline__ void skip(int len)
+    {
+        off += len;
+        pos += len;
+        const bool sh = off >= 64;
+        unsigned long long nw = 0;
+        if (sh && wi + 4 <= wmax) nw = __ldg(words + wi + 4);
+        nw = ((unsigned long long)__byte_perm((unsigned)nw, 0, 0x0123) << 32) |
+             __byte_perm((unsigned)(nw >> 32), 0, 0x0123);
+        w0 = sh ? w1 : w0;
+        w1 = sh ? w2 : w1;
+        w2 = sh ? w3 : w2;
+        w3 = sh ? nw : w3;
+        wi += sh ? 1 : 0;
+        off -= sh ? 64 : 0;
+    }
+};
+
+// codes longer than the first-level table (rare): canonical first-code search
+// over lengths HD_LUT+1..32 (huffman_decode_kernel's per-length test)
+__device__ __noinline__ int huff_long(const HuffDev& T, unsigned w, int& sym)
+{
+    for (int l = HD_LUT + 1; l <= 32; ++l) {
+        if (T.count[l]) {
+            const unsigned long long c = (unsigned long long)w >> (32 - l);
+            if (c >= T.first[l] && c - T.first[l] < (unsigned long long)T.count[l]) {
+                sym = T.sym[T.index[l] + (int)(c - T.first[l])];
+                return l;
+            }
+        }
+    }
+    return 0;
+}
+
+// One canonical symbol; the same answers as the reference's bit-serial loop:
+// 0 ok; 1 the stream ends inside the symbol (or fewer than 33 bits remain
+// with no match); 2 no code matches within 32 bits and >= 33 bits remain.
+// Straight-line apart from the rare long-code call (no early exits).
+__device__ __forceinline__ int huff_step(const HuffDev& T, BitRd& r, int& sym)
+{
+    const unsigned w = r.peek32();
+    const unsigned e = T.lut[w >> (32 - HD_LUT)];
+    int len = (int)(e >> 8);
+    sym = (int)(e & 0xff);
+    if (len == 0) len = huff_long(T, w, sym);
+    const bool fits = len != 0 && r.pos + len <= r.total;
+    const int rc = fits ? 0 : (len == 0 && r.total - r.pos >= 33 ? 2 : 1);
+    r.skip(fits ? len : 0);
+    return rc;
+}
+
+// Block per blob.  The bitstream is cut into <= 1024 sub-segments (4 per
+// thread).  Round 1: each thread parses its sub-segments in sequence from the
+// nominal start of its first one (a guess: it may sit inside a codeword).
+// Later rounds: a thread whose first start differs from where its left
+// neighbour's parse ended re-parses from that end, sub-segment by
+// sub-segment, until its new parse reaches a sub-segment end of the old one
+// (canonical codes resynchronise within a few symbols), after which the old
+// counts stand.  Converged starts are exact by induction from bit 0; a final
+// pass writes the symbols at scanned offsets.
+__global__ void __launch_bounds__(HD_THREADS) huff_decode_kernel(const uint8_t* blobs, const long long* blob_off,
+                                                                 const int* skip, uint8_t* raw,
+                                                                 const long long* raw_off, int* status)
+{
+    const int b = blockIdx.x;
+    if (skip[b]) return;
+    __shared__ HuffDev T;
+    __shared__ long long s_st[HD_NSEG], s_en[HD_NSEG];
+    __shared__ int s_cnt[HD_NSEG];
+    __shared__ unsigned char s_err[HD_NSEG];
+    __shared__ unsigned char s_len[256];
+    __shared__ long long s_errpos;
+    const int tid = threadIdx.x;
+    const uint8_t* blob = blobs + blob_off[b];
+    unsigned long long raw_len = 0, enc_len = 0;
+    for (int i = 0; i < 8; ++i) {
+        raw_len |= (unsigned long long)blob[8 + i] << (8 * i);
+        enc_len |= (unsigned long long)blob[16 + i] << (8 * i);
+    }
+    if (raw_len == 0) {
+        if (tid == 0) status[b] = 0;
+        return;
+    }
+    // canonical tables (huffman.py:80-104); the host has checked the lengths
+    for (int i = tid; i < (1 << HD_LUT); i += HD_THREADS) T.lut[i] = 0;
+    if (tid < 33) T.count[tid] = 0;
+    s_len[tid] = blob[28 + tid];
+    if (tid == 0) s_errpos = 0x7fffffffffffffffll;
+    __syncthreads();
+    if (s_len[tid]) atomicAdd(&T.count[s_len[tid]], 1);
+    __syncthreads();
+    if (tid == 0) {
+        unsigned long long code = 0;
+        int idx = 0;
+        T.first[0] = 0;
+        T.index[0] = 0;
+        for (int l = 1; l <= 32; ++l) {
+            T.first[l] = code;
+            T.index[l] = idx;
+            code = (code + (unsigned long long)T.count[l]) << 1;
+            idx += T.count[l];
+        }
+    }
+    __syncthreads();
+    {
+        const int l = s_len[tid];
+        if (l) {
+            int rank = T.index[l];
+            for (int s = 0; s < 256; ++s) rank += (s < tid) & (s_len[s] == l);
+            T.sym[rank] = (unsigned char)tid;
+            if (l <= HD_LUT) {
+                const unsigned long long code = T.first[l] + (unsigned long long)(rank - T.index[l]);
+                const int lo = (int)(code << (HD_LUT - l)), span = 1 << (HD_LUT - l);
+                for (int i = 0; i < span; ++i) T.lut[lo + i] = (unsigned short)((l << 8) | tid);
+            }
+        }
+    }
+    __syncthreads();
+
+    const uint8_t* enc = blob + DEC_HEADER;
+    const long long total = (long long)enc_len * 8;
+    long long nseg = (total + HD_SEG_MIN - 1) / HD_SEG_MIN;
+    nseg = nseg < 1 ? 1 : (nseg > HD_NSEG ? HD_NSEG : nseg);
+    const long long seg = total > 0 ? (total + nseg - 1) / nseg : 0;
+    const int t0 = tid * HD_SUB;
+    const int t1 = (int)min((long long)t0 + HD_SUB, nseg);
+    auto nominal_end = [&](int t) -> long long { return t == nseg - 1 ? total : min((t + 1) * seg, total); };
+    // Parse one sub-segment per lane, all 32 lanes of the warp together: the
+    // vote in the loop condition keeps the warp converged every step (a
+    // plain per-lane loop lets the lanes drift apart and run one at a time).
+    auto parse_sub = [&](bool active, int t, long long start, long long& end, int& cnt) -> int {
+        BitRd r;
+        r.init(enc, (long long)enc_len, active ? start : 0);
+        const long long stop = active ? nominal_end(t) : 0;
+        int c = 0, rc = 0;
+        bool go = active && r.pos < stop;
+        while (__any_sync(STPC_FULL, go)) {
+            if (go) {
+                int sym;
+                rc = huff_step(T, r, sym);
+                if (rc) {
+                    go = false;
+                } else {
+                    ++c;
+                    go = r.pos < stop;
+                }
+            }
+        }
+        end = r.pos;
+        cnt = c;
+        return rc;
+    };
+
+    // round 1 (warp-uniform trip count; __syncwarp re-converges the lanes
+    // before every sub-segment so the 32 parses run in lock-step)
+    {
+        long long pos = t0 < nseg ? min(t0 * seg, total) : total;
+        bool dead = false;
+        for (int k = 0; k < HD_SUB; ++k) {
+            __syncwarp();
+            const int t = t0 + k;
+            const bool act = t < t1 && !dead;
+            long long e;
+            int c;
+            const int rc = parse_sub(act, t, pos, e, c);
+            if (t < t1) {
+                s_st[t] = pos;
+                if (dead) {
+                    s_en[t] = pos;
+                    s_cnt[t] = 0;
+                    s_err[t] = 3;
+                } else {
+                    s_en[t] = e;
+                    s_cnt[t] = c;
+                    s_err[t] = (unsigned char)rc;
+                    pos = e;
+                    dead = rc == 2;
+                }
+            }
+        }
+    }
+    __syncthreads();  // round-1 ends must be visible before any thread reads its neighbour's
+    // correction rounds
+    for (;;) {
+        long long want = -1;
+        if (t0 > 0 && t0 < nseg && s_err[t0 - 1] == 0 && s_en[t0 - 1] != s_st[t0]) want = s_en[t0 - 1];
+        __syncthreads();
+        long long pos = want;
+        bool live = want >= 0, dead = false;
+        for (int k = 0; k < HD_SUB; ++k) {
+            __syncwarp();
+            const int t = t0 + k;
+            const bool act = live && t < t1 && !dead;
+            long long e;
+            int c;
+            const int rc = parse_sub(act, t, pos, e, c);
+            if (live && t < t1) {
+                if (dead) {
+                    s_st[t] = pos;
+                    s_en[t] = pos;
+                    s_cnt[t] = 0;
+                    s_err[t] = 3;
+                } else {
+                    const long long old_en = s_en[t];
+                    const int old_err = s_err[t];
+                    s_st[t] = pos;
+                    s_en[t] = e;
+                    s_cnt[t] = c;
+                    s_err[t] = (unsigned char)rc;
+                    if (rc == 2) dead = true;
+                    else if (rc == 0 && old_err == 0 && e == old_en) live = false;  // resynchronised
+                    else pos = e;
+                }
+            }
+        }
+        if (!__syncthreads_or(want >= 0)) break;
+    }
+
+    // symbol offsets; the first invalid code (in parse order) and the total
+    long long mine = 0;
+    for (int t = t0; t < t1; ++t) mine += s_cnt[t];
+    long long tot;
+    const long long base = block_excl_scan<HD_THREADS>(mine, tot);
+    {
+        long long o = base;
+        for (int t = t0; t < t1; ++t) {
+            if (s_err[t] == 2) {
+                atomicMin((unsigned long long*)&s_errpos, (unsigned long long)(o + s_cnt[t]));
                 break;
             }
+            o += s_cnt[t];
         }
-        if (st) break;
     }
-    status[bi] = st;
+    __syncthreads();
+    const long long errpos = s_errpos;
+    if (errpos < (long long)raw_len) {
+        if (tid == 0) status[b] = 2;
+        return;
+    }
+    if (tot < (long long)raw_len) {
+        if (tid == 0) status[b] = 1;
+        return;
+    }
+    // write pass (warp-synchronous like parse_sub)
+    uint8_t* out = raw + raw_off[b];
+    long long o = base;
+    for (int k = 0; k < HD_SUB; ++k) {
+        const int t = t0 + k;
+        const bool act = t < t1 && o < (long long)raw_len;
+        BitRd r;
+        r.init(enc, (long long)enc_len, act ? s_st[t] : 0);
+        const int c = act ? (int)min((long long)s_cnt[t], (long long)raw_len - o) : 0;
+        int i = 0;
+        bool go = i < c;
+        while (__any_sync(STPC_FULL, go)) {
+            if (go) {
+                int sym;
+                huff_step(T, r, sym);
+                out[o + i] = (uint8_t)sym;
+                go = ++i < c;
+            }
+        }
+        if (t < t1) o += s_cnt[t];
+    }
+    if (tid == 0) status[b] = 0;
 }
 
-// Per pixel of every frame: plane reconstruction from the per-tile plane map
-// (kind 1 = temporal run with this channel's offset, kind 2 = fallback run
-// over the channel's remaining pixels), exactly reconstruct_span's
-// arithmetic; then residual pixels override.  out_r: +inf = no point.
-__global__ void reconstruct_kernel(Geometry g, Trig tg, int n_frames, const uint8_t* vbits, long long vstride,
-                                   const float4* tmap, const double* r_max_p, double* out_r,
-                                   unsigned long long* failed)
+// the 284-byte header of every blob (shorter blobs: what there is, zero-padded)
+__global__ void blob_headers_kernel(const uint8_t* blobs, const long long* blob_off, const long long* blob_len,
+                                    uint8_t* out)
 {
-    const long long P = g.P;
-    const long long total = (long long)n_frames * P;
-    const double r_max = *r_max_p;
-    unsigned int nfail = 0;
-    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total;
-         i += (long long)gridDim.x * blockDim.x) {
-        const long long f = i / P, p = i - f * P;
-        const int v = (int)(p / g.w), u = (int)(p - (long long)v * g.w);
-        const bool valid = (vbits[f * vstride + (p >> 3)] >> (7 - (p & 7))) & 1u;
-        double r = __longlong_as_double(0x7ff0000000000000ll);
+    const int b = blockIdx.x;
+    const long long n = min((long long)DEC_HEADER, blob_len[b]);
+    for (int i = threadIdx.x; i < DEC_HEADER; i += blockDim.x)
+        out[(long long)b * DEC_HEADER + i] = i < n ? blobs[blob_off[b] + i] : 0;
+}
+
+// first min(raw_len, cap) bytes of every raw payload (config + transforms)
+__global__ void heads_kernel(const uint8_t* raw, const long long* raw_off, const long long* raw_len,
+                             const int* ok, int cap, uint8_t* heads)
+{
+    const int b = blockIdx.x;
+    const long long n = ok[b] ? min((long long)cap, raw_len[b]) : 0;
+    for (int i = threadIdx.x; i < cap; i += blockDim.x)
+        heads[(long long)b * cap + i] = i < n ? raw[raw_off[b] + i] : 0;
+}
+
+// ---------------------------------------------------------------- records
+
+constexpr int PK_THREADS = 256;
+constexpr int PK_BATCH = 1024;
+constexpr int PK_WIN = 16384;  // staged bytes of the run section
+
+// Block per blob: validates the record sections in the reference's reading
+// order and turns them into per-(frame, tile) plane maps (a, b, c, kind:
+// 1 temporal run with this frame's offset, 2 fallback run, 0 none) plus the
+// bounds of each frame's residual section.  The variable-length records are
+// walked by one thread (a record's size depends on its presence mask) in
+// batches that the block then expands in parallel; residual varints are
+// scanned block-parallel (terminator bytes < 0x80).
+__global__ void __launch_bounds__(PK_THREADS) parse_kernel(DecGeom G, const uint8_t* raw, const long long* raw_off,
+                                                           const long long* raw_len, const int* sel, float4* tmap,
+                                                           ResSec* res, unsigned long long* pstat)
+{
+    const int j = blockIdx.x;
+    const int b = sel[j];
+    const uint8_t* p = raw + raw_off[b];
+    const long long len = raw_len[b];
+    const int tid = threadIdx.x;
+    __shared__ unsigned long long st;
+    __shared__ long long recs[PK_BATCH];
+    __shared__ int fch[PK_BATCH], frow[PK_BATCH], fnr[PK_BATCH];
+    __shared__ unsigned win32[PK_WIN / 4];
+    __shared__ int s_nrec, s_done;
+    __shared__ long long s_pos, s_cnt, s_end, s_left;
+    __shared__ int s_ch;
+    __shared__ unsigned long long s_flat;
+    __shared__ int s_dbad, s_vbad;
+    if (tid == 0) st = DEC_NONE;
+    float4* tm = tmap + (long long)j * G.n * G.ty * G.tx;
+    const long long ntile = (long long)G.n * G.ty * G.tx;
+    for (long long i = tid; i < ntile; i += PK_THREADS) tm[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+    __syncthreads();
+    auto fail = [&](long long pos, int order, int kind) { atomicMin(&st, dec_key(pos, order, kind)); };
+
+    // bitmaps (n takes of nb bytes) and the run count
+    if (tid == 0) {
+        if (len < G.runs_off) {
+            fail(G.bits_off + (len - G.bits_off) / G.nb * G.nb, 0, STPC_DEC_TRUNCATED);
+        } else if (G.runs_off + 4 > len) {
+            fail(G.runs_off, 0, STPC_DEC_TRUNCATED);
+        } else {
+            s_cnt = dec_u32(p + G.runs_off);
+            s_pos = G.runs_off + 4;
+        }
+    }
+    if (__syncthreads_or(tid == 0 && st != DEC_NONE)) goto finish;
+
+    // temporal runs: <HHH fff> + presence mask + f32 per present non-key frame
+    {
+        const long long n_runs = s_cnt;
+        long long done = 0;
+        while (done < n_runs) {
+            // stage the next window of the run section (coalesced; raw
+            // payloads are 16-byte aligned in the arena)
+            const long long wbase = s_pos & ~3ll;
+            {
+                const long long wl = min((long long)PK_WIN, len - wbase);
+                const unsigned* src = (const unsigned*)(p + wbase);
+                for (long long i = tid; 4 * i < wl; i += PK_THREADS) win32[i] = __ldg(src + i);
+            }
+            __syncthreads();
+            if (tid == 0) {
+                const uint8_t* win = (const uint8_t*)win32;
+                auto wb = [&](long long x) -> unsigned { return x - wbase < PK_WIN ? win[x - wbase] : dec_u8(p + x); };
+                int c = 0;
+                long long q = s_pos;
+                while (c < PK_BATCH && done + c < n_runs) {
+                    if (c > 0 && q + 18 + G.pm > wbase + PK_WIN) break;  // restage
+                    if (q + 18 > len) {
+                        fail(q, 0, STPC_DEC_TRUNCATED);
+                        break;
+                    }
+                    recs[c++] = q;
+                    if (q + 18 + G.pm > len) {
+                        fail(q + 18, 1, STPC_DEC_TRUNCATED);
+                        break;
+                    }
+                    int present = 0;
+                    for (int i = 0; i < G.pm; ++i) {
+                        unsigned m = wb(q + 18 + i);
+                        const int valid_bits = min(8, G.n - 8 * i);
+                        if (valid_bits < 8) m &= (1u << valid_bits) - 1u;
+                        present += __popc(m);
+                    }
+                    const int kbit = (wb(q + 18 + (G.k >> 3)) >> (G.k & 7)) & 1;
+                    const long long size = 18 + G.pm + 4ll * (present - kbit);
+                    if (q + size > len) {
+                        const long long o0 = q + 18 + G.pm;
+                        fail(o0 + (len - o0) / 4 * 4, 0, STPC_DEC_TRUNCATED);
+                        break;
+                    }
+                    q += size;
+                }
+                s_nrec = c;
+                s_pos = q;
+            }
+            __syncthreads();
+            const int c = s_nrec;
+            for (int r = tid; r < c; r += PK_THREADS) {
+                const long long q = recs[r];
+                const int row = (int)dec_u16(p + q), s = (int)dec_u16(p + q + 2), ln = (int)dec_u16(p + q + 4);
+                if (row >= G.ty || ln < 1 || s + ln > G.tx) {
+                    fail(q + 18, 0, STPC_DEC_MALFORMED);
+                    continue;
+                }
+                if (q + 18 + G.pm > len) continue;
+                const float a = dec_f32(p + q + 6), bb = dec_f32(p + q + 10), cc = dec_f32(p + q + 14);
+                long long o = q + 18 + G.pm;
+                bool havek = false, trunc = false;
+                for (int ch = 0; ch < G.n; ++ch) {
+                    if (!((dec_u8(p + q + 18 + (ch >> 3)) >> (ch & 7)) & 1)) continue;
+                    float off;
+                    if (ch == G.k) {
+                        off = cc;
+                        havek = true;
+                    } else {
+                        if (o + 4 > len) {
+                            trunc = true;
+                            break;
+                        }
+                        off = dec_f32(p + o);
+                        o += 4;
+                    }
+                    float4* dst = tm + ((long long)ch * G.ty + row) * G.tx;
+                    for (int t = s; t < s + ln; ++t) dst[t] = make_float4(a, bb, off, 1.f);
+                }
+                if (!trunc && !havek) fail(o, 0, STPC_DEC_MALFORMED);
+            }
+            done += c;
+            if (__syncthreads_or(st != DEC_NONE)) goto finish;
+        }
+    }
+
+    // fallback rows per frame: <I> rows, each <HH> + nr x <HH fff>
+    if (tid == 0) {
+        s_ch = 0;
+        s_left = 0;
+        s_done = 0;
+    }
+    __syncthreads();
+    for (;;) {
+        if (tid == 0) {
+            int c = 0;
+            long long q = s_pos;
+            while (c < PK_BATCH) {
+                if (s_left == 0) {
+                    if (s_ch == G.n) {
+                        s_done = 1;
+                        break;
+                    }
+                    if (q + 4 > len) {
+                        fail(q, 0, STPC_DEC_TRUNCATED);
+                        break;
+                    }
+                    const long long nrows = dec_u32(p + q);
+                    q += 4;
+                    if (nrows > G.ty) {
+                        fail(q, 0, STPC_DEC_MALFORMED);
+                        break;
+                    }
+                    s_left = nrows;
+                    ++s_ch;
+                    continue;
+                }
+                if (q + 4 > len) {
+                    fail(q, 0, STPC_DEC_TRUNCATED);
+                    break;
+                }
+                const int row = (int)dec_u16(p + q), nr = (int)dec_u16(p + q + 2);
+                q += 4;
+                if (row >= G.ty || nr > G.tx) {
+                    fail(q, 0, STPC_DEC_MALFORMED);
+                    break;
+                }
+                if (q + 16ll * nr > len) {
+                    const int avail = (int)((len - q) / 16);
+                    fch[c] = s_ch - 1;
+                    frow[c] = row;
+                    fnr[c] = avail;
+                    recs[c++] = q;
+                    fail(q + 16ll * avail, 0, STPC_DEC_TRUNCATED);
+                    break;
+                }
+                fch[c] = s_ch - 1;
+                frow[c] = row;
+                fnr[c] = nr;
+                recs[c++] = q;
+                q += 16ll * nr;
+                --s_left;
+            }
+            s_nrec = c;
+            s_pos = q;
+        }
+        __syncthreads();
+        const int c = s_nrec;
+        const int lane = tid & 31, wid = tid >> 5;
+        for (int r = wid; r < c; r += PK_THREADS / 32) {
+            float4* dst = tm + ((long long)fch[r] * G.ty + frow[r]) * G.tx;
+            for (int i = lane; i < fnr[r]; i += 32) {
+                const long long rp = recs[r] + 16ll * i;
+                const int s = (int)dec_u16(p + rp), ln = (int)dec_u16(p + rp + 2);
+                if (ln < 1 || s + ln > G.tx) {
+                    fail(rp + 16, 0, STPC_DEC_MALFORMED);
+                    continue;
+                }
+                const float4 v = make_float4(dec_f32(p + rp + 4), dec_f32(p + rp + 8), dec_f32(p + rp + 12), 2.f);
+                for (int t = s; t < s + ln; ++t)
+                    if (dst[t].w != 1.f) dst[t] = v;  // temporal coverage wins (remaining mask)
+            }
+        }
+        if (__syncthreads_or(st != DEC_NONE)) goto finish;
+        if (s_done) break;
+        __syncthreads();
+    }
+
+    // residual sections per frame
+    for (int ch = 0; ch < G.n; ++ch) {
+        ResSec* rs = res + (long long)j * G.n + ch;
+        if (tid == 0) {
+            const long long q = s_pos;
+            if (q + 4 > len) {
+                fail(q, 0, STPC_DEC_TRUNCATED);
+            } else {
+                const long long cnt = dec_u32(p + q);
+                s_pos = q + 4;
+                s_cnt = cnt;
+                if (cnt > G.P) fail(q + 4, 0, STPC_DEC_MALFORMED);
+                if (cnt == 0) *rs = ResSec{q + 4, 0, q + 4, q + 4};
+            }
+            s_end = -1;
+            s_flat = 0;
+            s_dbad = 0;
+            s_vbad = 0;
+        }
+        if (__syncthreads_or(st != DEC_NONE)) goto finish;
+        const long long cnt = s_cnt;
+        if (cnt == 0) continue;
+        // varints: value i ends at the i-th byte < 0x80 (varint_decode_kernel
+        // _kernels.py:435-459); deltas checked as bitstream.py:494-498
+        const long long base = s_pos;
+        long long found = 0;
+        for (long long chunk = base;; chunk += 4 * PK_THREADS) {
+            const long long x0 = chunk + 4ll * tid;
+            int nt = 0;
+            for (int i = 0; i < 4; ++i)
+                if (x0 + i < len && dec_u8(p + x0 + i) < 128) ++nt;
+            long long tot;
+            long long vi = found + block_excl_scan<PK_THREADS>(nt, tot);
+            unsigned long long dsum = 0;
+            for (int i = 0; i < 4; ++i) {
+                const long long x = x0 + i;
+                if (x >= len) break;
+                if (dec_u8(p + x) >= 128) continue;
+                if (vi < cnt) {
+                    long long y = x;
+                    while (y > base && dec_u8(p + y - 1) >= 128 && x - y < 9) --y;
+                    unsigned long long v = 0;
+                    for (long long z = y; z <= x; ++z)
+                        v |= (unsigned long long)(dec_u8(p + z) & 0x7f) << (7 * (z - y));
+                    const long long dlt = (long long)v;
+                    if ((vi == 0 ? dlt < 0 : dlt < 1) || dlt > G.P) s_dbad = 1;
+                    else dsum += (unsigned long long)dlt;
+                    if (vi == cnt - 1) s_end = x + 1;
+                }
+                ++vi;
+            }
+            if (dsum) atomicAdd(&s_flat, dsum);
+            __syncthreads();
+            const long long end = s_end;
+            const long long lim = end >= 0 ? end : len;
+            // an 11th byte of one value: ten continuation bytes in a row (shift > 63)
+            for (int i = 0; i < 4; ++i) {
+                const long long x = x0 + i;
+                if (x >= lim || x - 9 < base || dec_u8(p + x) < 128) continue;
+                bool all = true;
+                for (int dd = 1; dd <= 9 && all; ++dd) all = dec_u8(p + x - dd) >= 128;
+                if (all) s_vbad = 1;
+            }
+            found += tot;
+            if (__syncthreads_or(end >= 0 || chunk + 4 * PK_THREADS >= len)) break;
+        }
+        if (tid == 0) {
+            const long long end = s_end;
+            if (end < 0 || s_vbad) {
+                fail(base, 1, STPC_DEC_TRUNCATED);
+            } else if (s_dbad) {
+                fail(end, 1, STPC_DEC_MALFORMED);
+            } else if ((long long)s_flat >= G.P) {
+                fail(end, 2, STPC_DEC_MALFORMED);
+            } else if (end + 2 * cnt > len) {
+                fail(end, 3, STPC_DEC_TRUNCATED);
+            } else if (end + 2 * cnt + 4 > len) {
+                fail(end + 2 * cnt, 0, STPC_DEC_TRUNCATED);
+            } else {
+                const long long n_esc = dec_u32(p + end + 2 * cnt);
+                const long long pe = end + 2 * cnt + 4;
+                if (pe + 4 * n_esc > len) {
+                    fail(pe + (len - pe) / 4 * 4, 0, STPC_DEC_TRUNCATED);
+                } else {
+                    *rs = ResSec{base, cnt, end, pe};
+                    s_pos = pe + 4 * n_esc;
+                    s_cnt = n_esc;
+                }
+            }
+        }
+        if (__syncthreads_or(st != DEC_NONE)) goto finish;
+        {
+            // escape count (bitstream.py:499-501)
+            const long long pc = res[(long long)j * G.n + ch].pos_code;
+            int ne = 0;
+            for (long long i = tid; i < cnt; i += PK_THREADS) ne += dec_u16(p + pc + 2 * i) == 0xFFFFu;
+            long long tot;
+            block_excl_scan<PK_THREADS>(ne, tot);
+            if (tid == 0 && tot != s_cnt) fail(s_pos, 0, STPC_DEC_MALFORMED);
+        }
+        if (__syncthreads_or(st != DEC_NONE)) goto finish;
+    }
+    if (tid == 0 && s_pos != len) fail(s_pos, 0, STPC_DEC_MALFORMED);  // trailing bytes
+
+finish:
+    __syncthreads();
+    if (tid == 0) pstat[j] = st;
+}
+
+// Per pixel of every frame: plane reconstruction from the tile map, exactly
+// reconstruct_span's arithmetic; failures counted per blob.  Grid (blocks per
+// frame, frames).  out_r: DEC_NOPT = no point.
+__global__ void __launch_bounds__(1024) reconstruct_kernel(DecGeom G, Trig tg, const uint8_t* raw,
+                                                           const long long* raw_off, const int* sel,
+                                                           const float4* tmap, const unsigned long long* pstat,
+                                                           double* out_r, unsigned long long* failed)
+{
+    const long long f = blockIdx.y;
+    const int j = (int)(f / G.n), ch = (int)(f - (long long)j * G.n);
+    if (pstat[j] != DEC_NONE) return;
+    const long long pix = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    int nfail = 0;
+    if (pix < G.P) {
+        const uint8_t* vb = raw + raw_off[sel[j]] + G.bits_off + (long long)ch * G.nb;
+        const bool valid = (dec_u8(vb + (pix >> 3)) >> (7 - (pix & 7))) & 1u;
+        long long r = DEC_NOPT;
         if (valid) {
-            const float4 pl = tmap[(f * g.ty + v / g.th) * g.tx + u / g.tw];
+            const int v = (int)(pix / G.w), u = (int)(pix - (long long)v * G.w);
+            const float4 pl = tmap[(f * G.ty + v / G.th) * G.tx + u / G.tw];
             if (pl.w != 0.0f) {
                 double dx, dy, dz;
                 ray_dir(tg, v, u, dx, dy, dz);
@@ -171,32 +899,89 @@ __global__ void reconstruct_kernel(Geometry g, Trig tg, int n_frames, const uint
                     ++nfail;
                 } else {
                     const double r_hat = (double)pl.z / den;
-                    if (r_hat <= 0.0 || r_hat > r_max) ++nfail;
-                    else r = r_hat;
+                    if (r_hat <= 0.0 || r_hat > G.r_max) ++nfail;
+                    else r = __double_as_longlong(r_hat);
                 }
             }
         }
-        out_r[i] = r;
+        out_r[f * G.P + pix] = __longlong_as_double(r);
     }
     for (int o = 16; o > 0; o >>= 1) nfail += __shfl_xor_sync(STPC_FULL, nfail, o);
-    if ((threadIdx.x & 31) == 0 && nfail) atomicAdd(failed, (unsigned long long)nfail);
+    if ((threadIdx.x & 31) == 0 && nfail) atomicAdd(failed + j, (unsigned long long)nfail);
 }
 
-__global__ void residual_scatter_kernel(const long long* flat, const double* ranges, long long n, long long P,
-                                        const int* frame_of, double* out_r)
+// Residual pixels override (rng_out[vs, us] = ranges, temporal.py:336-338):
+// block per (frame, blob); the same terminator scan as parse_kernel, with
+// block scans carrying value index, pixel index (cumsum of deltas) and escape
+// rank across 1 KB chunks.  The section was validated by parse_kernel.
+__global__ void __launch_bounds__(PK_THREADS) residual_kernel(DecGeom G, const uint8_t* raw, const long long* raw_off,
+                                                              const int* sel, const ResSec* res,
+                                                              const unsigned long long* pstat, double* out_r)
 {
-    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-         i += (long long)gridDim.x * blockDim.x)
-        out_r[(long long)frame_of[i] * P + flat[i]] = ranges[i];
+    const int ch = blockIdx.x, j = blockIdx.y;
+    if (pstat[j] != DEC_NONE) return;
+    const ResSec rs = res[(long long)j * G.n + ch];
+    if (rs.cnt == 0) return;
+    const uint8_t* p = raw + raw_off[sel[j]];
+    double* dst = out_r + ((long long)j * G.n + ch) * G.P;
+    const int tid = threadIdx.x;
+    long long c_idx = 0, c_flat = 0, c_esc = 0;
+    for (long long chunk = rs.pos_var; chunk < rs.pos_code; chunk += 4 * PK_THREADS) {
+        const long long x0 = chunk + 4ll * tid;
+        long long dv[4];
+        int term[4];
+        int nv = 0;
+        long long dsum = 0;
+        int ne = 0;
+        for (int i = 0; i < 4; ++i) {
+            const long long x = x0 + i;
+            term[i] = 0;
+            if (x >= rs.pos_code || dec_u8(p + x) >= 128) continue;
+            long long y = x;
+            while (y > rs.pos_var && dec_u8(p + y - 1) >= 128) --y;
+            unsigned long long v = 0;
+            for (long long z = y; z <= x; ++z) v |= (unsigned long long)(dec_u8(p + z) & 0x7f) << (7 * (z - y));
+            dv[i] = (long long)v;
+            term[i] = 1;
+            ++nv;
+            dsum += (long long)v;
+        }
+        long long t_idx, t_flat, t_esc;
+        const long long b_idx = c_idx + block_excl_scan<PK_THREADS>(nv, t_idx);
+        const long long b_flat = c_flat + block_excl_scan<PK_THREADS>(dsum, t_flat);
+        // escape flags need the value index, so count them after the index scan
+        {
+            long long vi = b_idx;
+            for (int i = 0; i < 4; ++i)
+                if (term[i]) ne += dec_u16(p + rs.pos_code + 2 * vi++) == 0xFFFFu;
+        }
+        const long long b_esc = c_esc + block_excl_scan<PK_THREADS>(ne, t_esc);
+        long long vi = b_idx, flat = b_flat, ei = b_esc;
+        for (int i = 0; i < 4; ++i) {
+            if (!term[i]) continue;
+            flat += dv[i];
+            const unsigned code = dec_u16(p + rs.pos_code + 2 * vi);
+            double r;
+            if (code == 0xFFFFu) r = (double)dec_f32(p + rs.pos_esc + 4 * ei++);
+            else r = (double)code * G.quant;
+            if (flat >= 0 && flat < G.P) dst[flat] = r;
+            ++vi;
+        }
+        c_idx += t_idx;
+        c_flat += t_flat;
+        c_esc += t_esc;
+    }
 }
 
-// count points per (frame, 1024-pixel block) -- grid (blocks per frame,
-// frames) so blocks never straddle frames -- for the row-major compaction
-__global__ void count_points_kernel(const double* out_r, long long P, int* blk_count)
+// points per (frame, 1024-pixel block); blocks never straddle frames
+__global__ void __launch_bounds__(1024) count_points_kernel(DecGeom G, const double* out_r,
+                                                            const unsigned long long* pstat, int* blk_count)
 {
-    const long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    const long long i = (long long)blockIdx.y * P + p;
-    const bool have = p < P && isfinite(out_r[i]);
+    const long long f = blockIdx.y;
+    const int j = (int)(f / G.n);
+    const long long pix = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    const bool have = pstat[j] == DEC_NONE && pix < G.P &&
+                      __double_as_longlong(out_r[f * G.P + pix]) != DEC_NOPT;
     const unsigned m = __ballot_sync(STPC_FULL, have);
     __shared__ int ws[32];
     if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5] = __popc(m);
@@ -204,19 +989,60 @@ __global__ void count_points_kernel(const double* out_r, long long P, int* blk_c
     if (threadIdx.x == 0) {
         int t = 0;
         for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += ws[w];
-        blk_count[(long long)blockIdx.y * gridDim.x + blockIdx.x] = t;
+        blk_count[f * gridDim.x + blockIdx.x] = t;
     }
 }
 
-// points = r * d in row-major pixel order per frame, then p' = R^-1 p + T^-1
-// with fma(z, r2, fma(y, r1, x r0)) + t (motion.py:70-72 on the inverse transform).
-__global__ void unproject_kernel(Geometry g, Trig tg, const double* out_r, const long long* blk_off,
-                                 const double* xf_inv, double* pts)
+// warp per frame: exclusive scan of its block counts in place + frame total
+__global__ void frame_scan_kernel(int* blk_count, long long bpf, long long F, long long* frame_count)
 {
-    const long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    const long long f = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (f >= F) return;
+    const int lane = threadIdx.x & 31;
+    int* c = blk_count + f * bpf;
+    int carry = 0;
+    for (long long i0 = 0; i0 < bpf; i0 += 32) {
+        const long long i = i0 + lane;
+        const int v = i < bpf ? c[i] : 0;
+        int x = v;
+        for (int o = 1; o < 32; o <<= 1) {
+            const int t = __shfl_up_sync(STPC_FULL, x, o);
+            if (lane >= o) x += t;
+        }
+        if (i < bpf) c[i] = carry + x - v;
+        carry += __shfl_sync(STPC_FULL, x, 31);
+    }
+    if (lane == 0) frame_count[f] = carry;
+}
+
+// single block: exclusive scan over the frame totals
+__global__ void __launch_bounds__(1024) frame_offset_kernel(const long long* frame_count, long long F,
+                                                            long long* frame_off)
+{
+    long long carry = 0;
+    for (long long i0 = 0; i0 < F; i0 += 1024) {
+        const long long i = i0 + threadIdx.x;
+        const long long v = i < F ? frame_count[i] : 0;
+        long long tot;
+        const long long e = block_excl_scan<1024>(v, tot);
+        if (i < F) frame_off[i] = carry + e;
+        carry += tot;
+    }
+}
+
+// points = r * d in row-major pixel order per frame, then
+// p' = R^-1 p + T^-1 as fma(z, r2, fma(y, r1, x r0)) + t (xform_coord)
+__global__ void __launch_bounds__(1024) unproject_kernel(DecGeom G, Trig tg, const double* out_r,
+                                                         const unsigned long long* pstat, const int* blk_off,
+                                                         const long long* frame_off, const double* xf_inv,
+                                                         double* pts)
+{
     const long long f = blockIdx.y;
-    const long long i = f * g.P + p;
-    const bool have = p < g.P && isfinite(out_r[i]);
+    const int j = (int)(f / G.n);
+    if (pstat[j] != DEC_NONE) return;
+    const long long pix = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    const long long i = f * G.P + pix;
+    const bool have = pix < G.P && __double_as_longlong(out_r[i]) != DEC_NOPT;
     const unsigned m = __ballot_sync(STPC_FULL, have);
     __shared__ int ws[32];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -225,17 +1051,14 @@ __global__ void unproject_kernel(Geometry g, Trig tg, const double* out_r, const
     int before = 0;
     for (int w = 0; w < wid; ++w) before += ws[w];
     if (!have) return;
-    const long long o = blk_off[f * gridDim.x + blockIdx.x] + before + __popc(m & ((1u << lane) - 1u));
-    const int v = (int)(p / g.w), u = (int)(p - (long long)v * g.w);
+    const long long o = frame_off[f] + blk_off[f * gridDim.x + blockIdx.x] + before +
+                        __popc(m & ((1u << lane) - 1u));
+    const int v = (int)(pix / G.w), u = (int)(pix - (long long)v * G.w);
     double dx, dy, dz;
     ray_dir(tg, v, u, dx, dy, dz);
     const double r = out_r[i];
     const double x = r * dx, y = r * dy, z = r * dz;
     const double* R = xf_inv + 12 * f;
-    // numpy's pts @ Rinv.T is a K=3 dgemm: the BLAS micro-kernel accumulates
-    // k = 0,1,2 with fused multiply-adds (checked bit-for-bit against the
-    // reference's decompress output, tests/golden dec_sha256); + T is a
-    // separate add.  -fmad=false keeps every other op unfused.
     pts[3 * o] = xform_coord(x, y, z, R[0], R[1], R[2], R[9]);
     pts[3 * o + 1] = xform_coord(x, y, z, R[3], R[4], R[5], R[10]);
     pts[3 * o + 2] = xform_coord(x, y, z, R[6], R[7], R[8], R[11]);
@@ -245,107 +1068,323 @@ __global__ void unproject_kernel(Geometry g, Trig tg, const double* out_r, const
 
 using namespace stpc;
 
+#define DCK(x)                                                                        \
+    do {                                                                              \
+        cudaError_t e_ = (x);                                                         \
+        if (e_ != cudaSuccess) {                                                      \
+            set_last_error(std::string(#x) + ": " + cudaGetErrorString(e_));          \
+            return STPC_ERR_CUDA;                                                     \
+        }                                                                             \
+    } while (0)
+#define DRET(x)                  \
+    do {                         \
+        int r_ = (x);            \
+        if (r_) return r_;       \
+    } while (0)
+
+struct stpc_decoder {
+    // phase 1
+    int n = 0;
+    std::vector<long long> raw_len, raw_off;
+    std::vector<int> ok;
+    const uint8_t* d_blob_base = nullptr;
+    DevBuf blobs, boff, skip, raw, roff, rlen, crcbad, hstat, okdev, heads;
+    // phase 2
+    int m = 0;
+    DecGeom G{};
+    long long F = 0, bpf = 0, total = 0;
+    DevBuf sel, tmap, res, pstat, outr, trig, xfi, blkcnt, fcnt, foff, failed, pts;
+    std::vector<unsigned long long> h_pstat;
+    const double* last_points = nullptr;
+};
+
+namespace {
+
+// header checks of deserialize in the reference's order (bitstream.py:398-409)
+int check_header(const uint8_t* hdr, long long blob_len, long long& raw_len, long long& enc_len)
+{
+    if (blob_len < DEC_HEADER) return STPC_DEC_TRUNCATED;
+    if (std::memcmp(hdr, "STPC", 4) != 0) return STPC_DEC_MALFORMED;
+    const unsigned version = hdr[4] | (hdr[5] << 8);
+    if (version != 1) return STPC_DEC_VERSION;
+    unsigned long long rl = 0, el = 0;
+    for (int i = 0; i < 8; ++i) {
+        rl |= (unsigned long long)hdr[8 + i] << (8 * i);
+        el |= (unsigned long long)hdr[16 + i] << (8 * i);
+    }
+    if (rl > (1ull << 30)) return STPC_DEC_MALFORMED;
+    if (el > (unsigned long long)(blob_len - DEC_HEADER)) return STPC_DEC_TRUNCATED;
+    raw_len = (long long)rl;
+    enc_len = (long long)el;
+    return 0;
+}
+
+// decode_tables (huffman.py:80-104) checks; only consulted when raw_len > 0
+int check_table(const uint8_t* lens)
+{
+    long long count[33] = {0};
+    int nsym = 0;
+    for (int s = 0; s < 256; ++s) {
+        if (lens[s] > 32) return STPC_DEC_MALFORMED;
+        if (lens[s]) {
+            ++count[lens[s]];
+            ++nsym;
+        }
+    }
+    unsigned long long code = 0;
+    for (int l = 1; l <= 32; ++l) {
+        if (code + (unsigned long long)count[l] > (1ull << l)) return STPC_DEC_MALFORMED;
+        code = (code + (unsigned long long)count[l]) << 1;
+    }
+    if (nsym == 0) return STPC_DEC_MALFORMED;
+    return 0;
+}
+
+}  // namespace
+
 extern "C" {
 
-int stpc_crc32_blobs(const uint8_t* d_blobs, const int64_t* d_blob_off, int32_t n, uint32_t* h_crc, void* stream)
+int stpc_decoder_create(stpc_decoder** out)
 {
-    if (n < 1 || !d_blobs || !d_blob_off || !h_crc) return STPC_ERR_ARG;
-    cudaStream_t s = (cudaStream_t)stream;
-    unsigned int* d_crc = nullptr;
-    if (cudaMalloc(&d_crc, sizeof(unsigned) * n) != cudaSuccess) return STPC_ERR_NOMEM;
-    STPC_LAUNCH();
-    crc_blob_kernel<<<n, 256, 0, s>>>(d_blobs, (const long long*)d_blob_off, d_crc);
-    cudaError_t e = cudaMemcpyAsync(h_crc, d_crc, sizeof(unsigned) * n, cudaMemcpyDeviceToHost, s);
-    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
-    cudaFree(d_crc);
-    return e == cudaSuccess ? STPC_OK : STPC_ERR_CUDA;
+    if (!out) return STPC_ERR_ARG;
+    *out = new stpc_decoder();
+    return STPC_OK;
 }
 
-int stpc_huffman_decode_blobs(const uint8_t* d_blobs, const int64_t* d_blob_off, int32_t n, uint8_t* d_out,
-                              const int64_t* d_out_off, int32_t* h_status, void* stream)
-{
-    if (n < 1 || !d_blobs || !d_out || !h_status) return STPC_ERR_ARG;
-    cudaStream_t s = (cudaStream_t)stream;
-    int* d_st = nullptr;
-    if (cudaMalloc(&d_st, sizeof(int) * n) != cudaSuccess) return STPC_ERR_NOMEM;
-    STPC_LAUNCH();
-    huff_decode_kernel<<<(n + 63) / 64, 64, 0, s>>>(d_blobs, (const long long*)d_blob_off, n, d_out,
-                                                     (const long long*)d_out_off, d_st);
-    cudaError_t e = cudaMemcpyAsync(h_status, d_st, sizeof(int) * n, cudaMemcpyDeviceToHost, s);
-    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
-    cudaFree(d_st);
-    return e == cudaSuccess ? STPC_OK : STPC_ERR_CUDA;
-}
+void stpc_decoder_destroy(stpc_decoder* d) { delete d; }
 
-int stpc_reconstruct_frames(int32_t w, int32_t h, int32_t tile_w, int32_t tile_h, const double* d_trig,
-                            int32_t n_frames, const uint8_t* d_vbits, int64_t vstride, const float* d_tile_map,
-                            const int64_t* d_res_flat, const double* d_res_range, const int32_t* d_res_frame,
-                            int64_t n_res, const double* d_xf_inv, double r_max, double* d_scratch,
-                            double* d_points, int64_t points_cap, int64_t* h_frame_counts, int64_t* h_failed,
-                            void* stream)
+int stpc_decoder_load(stpc_decoder* d, const uint8_t* blobs, int32_t blobs_on_device, const int64_t* offsets,
+                      int32_t n, int32_t* status, void* stream)
 {
-    if (n_frames < 1 || w < 1 || h < 1 || !d_trig || !d_vbits || !d_tile_map || !d_scratch || !h_frame_counts)
-        return STPC_ERR_ARG;
+    if (!d || !blobs || !offsets || !status || n < 1) return STPC_ERR_ARG;
     cudaStream_t s = (cudaStream_t)stream;
-    Geometry g{};
-    g.w = w;
-    g.h = h;
-    g.tw = tile_w;
-    g.th = tile_h;
-    g.tx = (w + tile_w - 1) / tile_w;
-    g.ty = (h + tile_h - 1) / tile_h;
-    g.P = (long long)w * h;
-    Trig tg;
-    tg.sin_t = d_trig;
-    tg.cos_t = d_trig + w;
-    tg.sin_p = d_trig + 2 * w;
-    tg.cos_p = d_trig + 2 * w + h;
-    const long long bpf = (g.P + 1023) / 1024;  // blocks per frame
-    const long long nblk = bpf * n_frames;
-    void* tmp = nullptr;
-    const size_t tmp_bytes = 16 + sizeof(int) * nblk + 8 + sizeof(long long) * nblk;
-    if (cudaMalloc(&tmp, tmp_bytes) != cudaSuccess) return STPC_ERR_NOMEM;
-    unsigned long long* d_failed = (unsigned long long*)tmp;
-    double* d_rmax = (double*)(d_failed + 1);
-    int* d_cnt = (int*)(d_rmax + 1);
-    long long* d_off = (long long*)(((uintptr_t)(d_cnt + nblk) + 7) & ~(uintptr_t)7);
-    cudaError_t e = cudaMemsetAsync(d_failed, 0, sizeof(unsigned long long), s);
-    if (e == cudaSuccess) e = cudaMemcpyAsync(d_rmax, &r_max, sizeof(double), cudaMemcpyHostToDevice, s);
-    STPC_LAUNCH();
-    reconstruct_kernel<<<148 * 8, 256, 0, s>>>(g, tg, n_frames, d_vbits, vstride, (const float4*)d_tile_map,
-                                                d_rmax, d_scratch, d_failed);
-    if (n_res > 0) {
+    d->n = n;
+    d->m = 0;
+    const long long arena = offsets[n];
+    // headers (on the host already, or a small gather)
+    std::vector<uint8_t> hdr((size_t)n * DEC_HEADER, 0);
+    if (blobs_on_device) {
+        std::vector<long long> blen(n);
+        for (int i = 0; i < n; ++i) blen[i] = offsets[i + 1] - offsets[i];
+        DRET(d->boff.ensure(sizeof(long long) * 2 * n));
+        DRET(d->heads.ensure((size_t)n * DEC_HEADER));
+        DCK(cudaMemcpyAsync(d->boff.p, offsets, sizeof(long long) * n, cudaMemcpyHostToDevice, s));
+        DCK(cudaMemcpyAsync(d->boff.as<long long>() + n, blen.data(), sizeof(long long) * n, cudaMemcpyHostToDevice,
+                            s));
         STPC_LAUNCH();
-        residual_scatter_kernel<<<148 * 4, 256, 0, s>>>((const long long*)d_res_flat, d_res_range, n_res, g.P,
-                                                         d_res_frame, d_scratch);
+        blob_headers_kernel<<<n, 128, 0, s>>>(blobs, d->boff.as<long long>(), d->boff.as<long long>() + n,
+                                              d->heads.as<uint8_t>());
+        DCK(cudaGetLastError());
+        DCK(cudaMemcpyAsync(hdr.data(), d->heads.p, (size_t)n * DEC_HEADER, cudaMemcpyDeviceToHost, s));
+        DCK(cudaStreamSynchronize(s));
+    } else {
+        for (int i = 0; i < n; ++i) {
+            const long long len = std::min<long long>(offsets[i + 1] - offsets[i], DEC_HEADER);
+            if (len > 0) std::memcpy(hdr.data() + (size_t)i * DEC_HEADER, blobs + offsets[i], len);
+        }
     }
+    d->raw_len.assign(n, 0);
+    d->raw_off.assign(n + 1, 0);
+    d->ok.assign(n, 0);
+    std::vector<int> pre(n, 0), skip(n, 1), table(n, 0);
+    long long ro = 0;
+    for (int i = 0; i < n; ++i) {
+        long long rl = 0, el = 0;
+        const uint8_t* h = hdr.data() + (size_t)i * DEC_HEADER;
+        pre[i] = check_header(h, offsets[i + 1] - offsets[i], rl, el);
+        d->raw_off[i] = ro;
+        if (!pre[i]) {
+            d->raw_len[i] = rl;
+            table[i] = rl > 0 ? check_table(h + 28) : 0;
+            skip[i] = 0;
+            ro += (rl + 15) / 16 * 16;
+        }
+    }
+    d->raw_off[n] = ro;
+    // device buffers
+    if (blobs_on_device) {
+        d->d_blob_base = blobs;
+    } else {
+        DRET(d->blobs.ensure(std::max<long long>(arena, 1)));
+        DCK(cudaMemcpyAsync(d->blobs.p, blobs, arena, cudaMemcpyHostToDevice, s));
+        d->d_blob_base = d->blobs.as<uint8_t>();
+    }
+    // per-blob tables for the CRC/Huffman kernels: skip = header or table error
+    std::vector<int> skip_huff(n);
+    for (int i = 0; i < n; ++i) skip_huff[i] = skip[i] || table[i];
+    DRET(d->boff.ensure(sizeof(long long) * 2 * n));
+    DRET(d->skip.ensure(sizeof(int) * 2 * n));
+    DRET(d->roff.ensure(sizeof(long long) * (n + 1)));
+    DRET(d->rlen.ensure(sizeof(long long) * n));
+    DRET(d->crcbad.ensure(sizeof(int) * 2 * n));
+    DRET(d->raw.ensure(std::max<long long>(ro, 16)));
+    DCK(cudaMemcpyAsync(d->boff.p, offsets, sizeof(long long) * n, cudaMemcpyHostToDevice, s));
+    DCK(cudaMemcpyAsync(d->skip.p, skip.data(), sizeof(int) * n, cudaMemcpyHostToDevice, s));
+    DCK(cudaMemcpyAsync(d->skip.as<int>() + n, skip_huff.data(), sizeof(int) * n, cudaMemcpyHostToDevice, s));
+    DCK(cudaMemcpyAsync(d->roff.p, d->raw_off.data(), sizeof(long long) * (n + 1), cudaMemcpyHostToDevice, s));
+    DCK(cudaMemcpyAsync(d->rlen.p, d->raw_len.data(), sizeof(long long) * n, cudaMemcpyHostToDevice, s));
+    DCK(cudaMemsetAsync(d->crcbad.p, 0, sizeof(int) * 2 * n, s));
+    DecCrcK ck;
+    for (int l = 0; l < 8; ++l) ck.lvl[l] = dec_x8nmodp((unsigned long long)DC_PIECE << l);
+    ck.chunk = dec_x8nmodp((unsigned long long)DC_CHUNK);
     STPC_LAUNCH();
-    count_points_kernel<<<dim3((unsigned)bpf, (unsigned)n_frames), 1024, 0, s>>>(d_scratch, g.P, d_cnt);
-    std::vector<int> hc(nblk);
-    std::vector<long long> ho(nblk + 1);
-    if (e == cudaSuccess) e = cudaMemcpyAsync(hc.data(), d_cnt, sizeof(int) * nblk, cudaMemcpyDeviceToHost, s);
-    unsigned long long hfail = 0;
-    if (e == cudaSuccess) e = cudaMemcpyAsync(&hfail, d_failed, sizeof(hfail), cudaMemcpyDeviceToHost, s);
-    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
-    if (e != cudaSuccess) {
-        cudaFree(tmp);
-        return STPC_ERR_CUDA;
+    crc_blob_kernel<<<n, 256, 0, s>>>(d->d_blob_base, d->boff.as<long long>(), d->skip.as<int>(), ck,
+                                      d->crcbad.as<int>());
+    STPC_LAUNCH();
+    huff_decode_kernel<<<n, HD_THREADS, 0, s>>>(d->d_blob_base, d->boff.as<long long>(), d->skip.as<int>() + n,
+                                                d->raw.as<uint8_t>(), d->roff.as<long long>(),
+                                                d->crcbad.as<int>() + n);
+    DCK(cudaGetLastError());
+    std::vector<int> res(2 * (size_t)n);
+    DCK(cudaMemcpyAsync(res.data(), d->crcbad.p, sizeof(int) * 2 * n, cudaMemcpyDeviceToHost, s));
+    DCK(cudaStreamSynchronize(s));
+    for (int i = 0; i < n; ++i) {
+        int st = pre[i];
+        if (!st && res[i]) st = STPC_DEC_CHECKSUM;
+        if (!st && table[i]) st = table[i];
+        if (!st && res[n + i]) st = res[n + i] == 1 ? STPC_DEC_TRUNCATED : STPC_DEC_MALFORMED;
+        status[i] = st;
+        d->ok[i] = st == 0;
     }
-    ho[0] = 0;
-    for (long long b = 0; b < nblk; ++b) ho[b + 1] = ho[b] + hc[b];
-    for (int f = 0; f < n_frames; ++f) h_frame_counts[f] = ho[(long long)(f + 1) * bpf] - ho[(long long)f * bpf];
-    if (ho[nblk] > points_cap || (!d_points && ho[nblk] > 0)) {
-        cudaFree(tmp);
+    DRET(d->okdev.ensure(sizeof(int) * n));
+    DCK(cudaMemcpyAsync(d->okdev.p, d->ok.data(), sizeof(int) * n, cudaMemcpyHostToDevice, s));
+    return STPC_OK;
+}
+
+int stpc_decoder_heads(stpc_decoder* d, int32_t head_cap, uint8_t* h_heads, int64_t* h_raw_len, void* stream)
+{
+    if (!d || d->n < 1 || head_cap < 1 || !h_heads) return STPC_ERR_ARG;
+    cudaStream_t s = (cudaStream_t)stream;
+    DRET(d->heads.ensure((size_t)d->n * head_cap));
+    STPC_LAUNCH();
+    heads_kernel<<<d->n, 256, 0, s>>>(d->raw.as<uint8_t>(), d->roff.as<long long>(), d->rlen.as<long long>(),
+                                      d->okdev.as<int>(), head_cap, d->heads.as<uint8_t>());
+    DCK(cudaGetLastError());
+    DCK(cudaMemcpyAsync(h_heads, d->heads.p, (size_t)d->n * head_cap, cudaMemcpyDeviceToHost, s));
+    DCK(cudaStreamSynchronize(s));
+    if (h_raw_len)
+        for (int i = 0; i < d->n; ++i) h_raw_len[i] = d->raw_len[i];
+    return STPC_OK;
+}
+
+int stpc_decoder_frames(stpc_decoder* d, const stpc_decode_geom* g, const int32_t* sel, int32_t m,
+                        const double* sin_theta, const double* cos_theta, const double* sin_phi,
+                        const double* cos_phi, const double* xf_inv, int64_t* frame_counts, int64_t* status,
+                        int64_t* failed, void* stream)
+{
+    if (!d || !g || !sel || m < 1 || !sin_theta || !cos_theta || !sin_phi || !cos_phi || !xf_inv ||
+        !frame_counts || !status || !failed)
         return STPC_ERR_ARG;
-    }
-    e = cudaMemcpyAsync(d_off, ho.data(), sizeof(long long) * nblk, cudaMemcpyHostToDevice, s);
+    if (g->w < 1 || g->h < 1 || g->tile_w < 1 || g->tile_h < 1 || g->n_frames < 1 || g->k_index < 0 ||
+        g->k_index >= g->n_frames)
+        return STPC_ERR_ARG;
+    for (int j = 0; j < m; ++j)
+        if (sel[j] < 0 || sel[j] >= d->n || !d->ok[sel[j]]) return STPC_ERR_ARG;
+    cudaStream_t s = (cudaStream_t)stream;
+    DecGeom& G = d->G;
+    G.w = g->w;
+    G.h = g->h;
+    G.tw = g->tile_w;
+    G.th = g->tile_h;
+    G.tx = (g->w + g->tile_w - 1) / g->tile_w;
+    G.ty = (g->h + g->tile_h - 1) / g->tile_h;
+    G.n = g->n_frames;
+    G.k = g->k_index;
+    G.pm = (g->n_frames + 7) / 8;
+    G.P = (long long)g->w * g->h;
+    G.nb = (G.P + 7) / 8;
+    G.bits_off = 57 + 48ll * G.n;
+    G.runs_off = G.bits_off + (long long)G.n * G.nb;
+    G.quant = g->range_quant;
+    G.r_max = g->r_max;
+    d->m = m;
+    d->F = (long long)m * G.n;
+    d->bpf = (G.P + 1023) / 1024;
+    const long long F = d->F, bpf = d->bpf;
+    DRET(d->sel.ensure(sizeof(int) * m));
+    DRET(d->tmap.ensure(sizeof(float4) * F * G.ty * G.tx));
+    DRET(d->res.ensure(sizeof(ResSec) * F));
+    DRET(d->pstat.ensure(sizeof(unsigned long long) * m));
+    DRET(d->outr.ensure(sizeof(double) * F * G.P));
+    DRET(d->trig.ensure(sizeof(double) * 2 * (G.w + G.h)));
+    DRET(d->xfi.ensure(sizeof(double) * 12 * F));
+    DRET(d->blkcnt.ensure(sizeof(int) * F * bpf));
+    DRET(d->fcnt.ensure(sizeof(long long) * F));
+    DRET(d->foff.ensure(sizeof(long long) * F));
+    DRET(d->failed.ensure(sizeof(unsigned long long) * m));
+    DCK(cudaMemcpyAsync(d->sel.p, sel, sizeof(int) * m, cudaMemcpyHostToDevice, s));
+    double* tr = d->trig.as<double>();
+    DCK(cudaMemcpyAsync(tr, sin_theta, sizeof(double) * G.w, cudaMemcpyHostToDevice, s));
+    DCK(cudaMemcpyAsync(tr + G.w, cos_theta, sizeof(double) * G.w, cudaMemcpyHostToDevice, s));
+    DCK(cudaMemcpyAsync(tr + 2 * G.w, sin_phi, sizeof(double) * G.h, cudaMemcpyHostToDevice, s));
+    DCK(cudaMemcpyAsync(tr + 2 * G.w + G.h, cos_phi, sizeof(double) * G.h, cudaMemcpyHostToDevice, s));
+    DCK(cudaMemcpyAsync(d->xfi.p, xf_inv, sizeof(double) * 12 * F, cudaMemcpyHostToDevice, s));
+    DCK(cudaMemsetAsync(d->failed.p, 0, sizeof(unsigned long long) * m, s));
+    Trig tg{tr, tr + G.w, tr + 2 * G.w, tr + 2 * G.w + G.h};
+    const uint8_t* raw = d->raw.as<uint8_t>();
+    const long long* roff = d->roff.as<long long>();
+    const unsigned long long* pst = d->pstat.as<unsigned long long>();
     STPC_LAUNCH();
-    unproject_kernel<<<dim3((unsigned)bpf, (unsigned)n_frames), 1024, 0, s>>>(g, tg, d_scratch, d_off, d_xf_inv,
-                                                                              d_points);
-    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
-    cudaFree(tmp);
-    if (h_failed) *h_failed = (int64_t)hfail;
-    return e == cudaSuccess ? STPC_OK : STPC_ERR_CUDA;
+    parse_kernel<<<m, PK_THREADS, 0, s>>>(G, raw, roff, d->rlen.as<long long>(), d->sel.as<int>(),
+                                          d->tmap.as<float4>(), d->res.as<ResSec>(),
+                                          d->pstat.as<unsigned long long>());
+    const dim3 fg((unsigned)bpf, (unsigned)F);
+    STPC_LAUNCH();
+    reconstruct_kernel<<<fg, 1024, 0, s>>>(G, tg, raw, roff, d->sel.as<int>(), d->tmap.as<float4>(), pst,
+                                           d->outr.as<double>(), d->failed.as<unsigned long long>());
+    STPC_LAUNCH();
+    residual_kernel<<<dim3((unsigned)G.n, (unsigned)m), PK_THREADS, 0, s>>>(G, raw, roff, d->sel.as<int>(),
+                                                                            d->res.as<ResSec>(), pst,
+                                                                            d->outr.as<double>());
+    STPC_LAUNCH();
+    count_points_kernel<<<fg, 1024, 0, s>>>(G, d->outr.as<double>(), pst, d->blkcnt.as<int>());
+    STPC_LAUNCH();
+    frame_scan_kernel<<<(unsigned)((F + 7) / 8), 256, 0, s>>>(d->blkcnt.as<int>(), bpf, F, d->fcnt.as<long long>());
+    STPC_LAUNCH();
+    frame_offset_kernel<<<1, 1024, 0, s>>>(d->fcnt.as<long long>(), F, d->foff.as<long long>());
+    DCK(cudaGetLastError());
+    d->h_pstat.resize(m);
+    std::vector<unsigned long long> hf(m);
+    DCK(cudaMemcpyAsync(frame_counts, d->fcnt.p, sizeof(long long) * F, cudaMemcpyDeviceToHost, s));
+    DCK(cudaMemcpyAsync(d->h_pstat.data(), d->pstat.p, sizeof(unsigned long long) * m, cudaMemcpyDeviceToHost, s));
+    DCK(cudaMemcpyAsync(hf.data(), d->failed.p, sizeof(unsigned long long) * m, cudaMemcpyDeviceToHost, s));
+    DCK(cudaStreamSynchronize(s));
+    d->total = 0;
+    for (int j = 0; j < m; ++j) {
+        status[j] = d->h_pstat[j] == DEC_NONE ? 0 : (int64_t)d->h_pstat[j];
+        failed[j] = (int64_t)hf[j];
+    }
+    for (long long f = 0; f < F; ++f) d->total += frame_counts[f];
+    return STPC_OK;
+}
+
+int64_t stpc_decoder_total_points(const stpc_decoder* d) { return d ? d->total : -1; }
+
+const double* stpc_decoder_device_points(const stpc_decoder* d) { return d ? d->last_points : nullptr; }
+
+int stpc_decoder_points(stpc_decoder* d, double* dst, int32_t dst_on_device, int64_t cap_points, void* stream)
+{
+    if (!d || d->m < 1 || (!dst && !dst_on_device && d->total > 0) || (dst && cap_points < d->total))
+        return STPC_ERR_ARG;
+    cudaStream_t s = (cudaStream_t)stream;
+    double* out = dst;
+    if (!dst_on_device || !dst) {
+        DRET(d->pts.ensure(sizeof(double) * 3 * std::max<long long>(d->total, 1)));
+        out = d->pts.as<double>();
+    }
+    Trig tg;
+    const double* tr = d->trig.as<double>();
+    tg = Trig{tr, tr + d->G.w, tr + 2 * d->G.w, tr + 2 * d->G.w + d->G.h};
+    STPC_LAUNCH();
+    unproject_kernel<<<dim3((unsigned)d->bpf, (unsigned)d->F), 1024, 0, s>>>(
+        d->G, tg, d->outr.as<double>(), d->pstat.as<unsigned long long>(), d->blkcnt.as<int>(),
+        d->foff.as<long long>(), d->xfi.as<double>(), out);
+    DCK(cudaGetLastError());
+    if (!dst_on_device && d->total > 0)
+        DCK(cudaMemcpyAsync(dst, out, sizeof(double) * 3 * d->total, cudaMemcpyDeviceToHost, s));
+    d->last_points = out;
+    DCK(cudaStreamSynchronize(s));
+    return STPC_OK;
 }
 
 }  // extern "C"

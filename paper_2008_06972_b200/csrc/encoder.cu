@@ -15,12 +15,14 @@
 #include <algorithm>
 
 #include "kernels.cuh"
+#include "runtime.cuh"
 #include "../../include/stpc_b200.h"
 
 using namespace stpc;
 
 unsigned long long stpc::g_launch_count = 0;
 static thread_local std::string g_err;
+void stpc::set_last_error(const std::string& msg) { g_err = msg; }
 
 // pipeline stages timed with CUDA events when profiling is enabled
 enum Stage { ST_INIT, ST_CONVERT, ST_BITMAP, ST_START_K, ST_FIT_K, ST_REFIT, ST_START_P, ST_FIT_P,
@@ -37,57 +39,6 @@ static const char* kStageNames[ST_COUNT] = {"init", "convert", "bitmaps", "start
         }                                                                             \
     } while (0)
 
-namespace {
-
-struct DevBuf {
-    void* p = nullptr;
-    size_t cap = 0;
-    int ensure(size_t need)
-    {
-        if (need <= cap) return 0;
-        if (p) cudaFree(p);
-        p = nullptr;
-        cap = 0;
-        size_t c = need + need / 8 + 256;
-        if (cudaMalloc(&p, c) != cudaSuccess) {
-            g_err = "cudaMalloc failed (" + std::to_string(c) + " bytes)";
-            return STPC_ERR_NOMEM;
-        }
-        cap = c;
-        return 0;
-    }
-    template <class T> T* as() const { return reinterpret_cast<T*>(p); }
-    ~DevBuf()
-    {
-        if (p) cudaFree(p);
-    }
-};
-
-struct HostBuf {
-    void* p = nullptr;
-    size_t cap = 0;
-    int ensure(size_t need)
-    {
-        if (need <= cap) return 0;
-        if (p) cudaFreeHost(p);
-        p = nullptr;
-        cap = 0;
-        size_t c = need + need / 8 + 256;
-        if (cudaMallocHost(&p, c) != cudaSuccess) {
-            g_err = "cudaMallocHost failed";
-            return STPC_ERR_NOMEM;
-        }
-        cap = c;
-        return 0;
-    }
-    template <class T> T* as() const { return reinterpret_cast<T*>(p); }
-    ~HostBuf()
-    {
-        if (p) cudaFreeHost(p);
-    }
-};
-
-}  // namespace
 
 struct stpc_encoder {
     stpc_config cfg;

@@ -1,0 +1,64 @@
+// Host-side runtime helpers shared by the encoder and decoder contexts:
+// grow-only device / pinned-host workspaces and the thread-local error text
+// behind stpc_last_error().
+#pragma once
+#include <string>
+
+#include <cuda_runtime.h>
+
+#include "../../include/stpc_b200.h"
+
+namespace stpc {
+
+void set_last_error(const std::string& msg);
+
+struct DevBuf {
+    void* p = nullptr;
+    size_t cap = 0;
+    int ensure(size_t need)
+    {
+        if (need <= cap) return 0;
+        if (p) cudaFree(p);
+        p = nullptr;
+        cap = 0;
+        size_t c = need + need / 8 + 256;
+        if (cudaMalloc(&p, c) != cudaSuccess) {
+            set_last_error("cudaMalloc failed (" + std::to_string(c) + " bytes)");
+            return STPC_ERR_NOMEM;
+        }
+        cap = c;
+        return 0;
+    }
+    template <class T> T* as() const { return reinterpret_cast<T*>(p); }
+    ~DevBuf()
+    {
+        if (p) cudaFree(p);
+    }
+};
+
+struct HostBuf {
+    void* p = nullptr;
+    size_t cap = 0;
+    int ensure(size_t need)
+    {
+        if (need <= cap) return 0;
+        if (p) cudaFreeHost(p);
+        p = nullptr;
+        cap = 0;
+        size_t c = need + need / 8 + 256;
+        if (cudaMallocHost(&p, c) != cudaSuccess) {
+            set_last_error("cudaMallocHost failed");
+            return STPC_ERR_NOMEM;
+        }
+        cap = c;
+        return 0;
+    }
+    template <class T> T* as() const { return reinterpret_cast<T*>(p); }
+    ~HostBuf()
+    {
+        if (p) cudaFreeHost(p);
+    }
+};
+
+
+}  // namespace stpc

@@ -1,44 +1,67 @@
 """Drop-in ``decompress`` / ``decompress_full``.
 
-Mirrors /root/reference/pkg/src/stpc/bitstream.py:605-631 (and the checks of
-``deserialize`` :388-519) with the heavy work on the GPU (libstpc_b200):
-CRC-32 and Huffman decoding of the entropy payload, plane reconstruction of
-every pixel, residual scatter, unprojection and the inverse frame transform.
-The host parses the record sections (O(runs + rows), vectorised numpy for
-the residual varints) into per-tile plane maps.  ``decompress_many`` decodes
-a batch of blobs that share one configuration in one device pass.
+Mirrors /root/reference/pkg/src/stpc/bitstream.py:605-631 with every heavy
+step on the GPU (libstpc_b200, csrc/decode.cu): header / code-table checks,
+CRC-32, canonical Huffman decoding, the record sections of ``deserialize``
+(:388-519), plane reconstruction (``decode_stream_images`` temporal.py:293-343,
+``reconstruct_span`` _kernels.py:282-308), residual pixels, ``unproject``
+(range_image.py:214-221) and the inverse frame transform (motion.py:70-79).
+The host reads only the 57-byte config block and the float32 transforms of
+each blob (``_parse_config`` :356-385 checks, ``RigidTransform`` validation)
+and computes ``R^-1 | T^-1`` with the reference's numpy expressions.
+
+``decompress_many`` decodes a batch of blobs in one device pass per distinct
+configuration; errors are raised for the first failing blob, with the
+exception type the reference raises for it.
 """
 
 from __future__ import annotations
 
 import ctypes
 import struct
+import time
 from dataclasses import dataclass
-from typing import Dict, List, Sequence, Tuple
+from typing import Dict, List, Optional, Sequence, Tuple
 
 import numpy as np
 
 from . import _native
 from .errors import ChecksumError, MalformedBlobError, TruncatedBlobError, UnknownVersionError
-from .geometry import DEFAULT_R_MAX, ray_trig_tables
+from .geometry import DEFAULT_R_MAX, RigidTransform, ray_trig_tables
 
 MAGIC = b"STPC"
 HEADER = 284
 MAX_RAW_LEN = 1 << 30  # bitstream.py:82
-MAX_PIXELS = 1 << 26
-MAX_FRAMES = 4096
-_CFG = struct.Struct("<Bd HH ddd II HH d")
+MAX_PIXELS = 1 << 26  # :83
+MAX_FRAMES = 4096  # :84
+_CFG = struct.Struct("<Bd HH ddd II HH d")  # bitstream.py:154-173
+_HEAD_FRAMES = 16  # transforms fetched with the config in the first pass
+
+_KIND = {
+    _native.DEC_TRUNCATED: TruncatedBlobError,
+    _native.DEC_MALFORMED: MalformedBlobError,
+    _native.DEC_CHECKSUM: ChecksumError,
+    _native.DEC_VERSION: UnknownVersionError,
+}
+_LOAD_MSG = {
+    _native.DEC_TRUNCATED: "blob or entropy payload truncated",
+    _native.DEC_MALFORMED: "malformed header, code table or entropy payload",
+    _native.DEC_CHECKSUM: "payload CRC-32 mismatch",
+    _native.DEC_VERSION: "format version not supported",
+}
 
 
 @dataclass
 class DecodeReport:
+    """bitstream.py:143-146."""
+
     point_counts: List[int]
     failed_reconstructions: int
     timings: Dict[str, float]
 
 
 def _header(blob: bytes):
-    """bitstream.py:398-411 header checks (CRC is verified on the GPU)."""
+    """bitstream.py:398-409 header checks (also run natively by stpc_decoder_load)."""
     if len(blob) < HEADER:
         raise TruncatedBlobError(f"blob of {len(blob)} bytes is shorter than the header")
     magic, version, _r, raw_len, enc_len, crc = struct.unpack_from("<4sHHQQI", blob, 0)
@@ -53,37 +76,11 @@ def _header(blob: bytes):
     return raw_len, enc_len, crc
 
 
-def _varints(buf: np.ndarray, pos: int, count: int) -> Tuple[np.ndarray, int]:
-    """Vectorised LEB128 decode of `count` values at buf[pos:] (varint_decode_kernel)."""
-    seg = buf[pos:pos + 10 * count]
-    term = np.flatnonzero(seg < 128)
-    if term.size < count:
-        raise TruncatedBlobError("residual index varints ran past payload")
-    end = int(term[count - 1]) + 1
-    seg = seg[:end].astype(np.int64)
-    starts = np.concatenate(([0], term[:count - 1] + 1))
-    group = np.zeros(end, np.int64)
-    group[starts[1:]] = 1
-    group = np.cumsum(group)
-    shift = 7 * (np.arange(end) - starts[group])
-    if shift.max(initial=0) > 63:
-        raise TruncatedBlobError("overlong varint")
-    vals = np.add.reduceat((seg & 0x7F) << shift, starts)
-    return vals, pos + end
-
-
-def _parse(payload: bytes):
-    """Structure of one raw payload (bitstream.py:413-519)."""
-    buf = np.frombuffer(payload, np.uint8)
-    pos = 0
-
-    def need(nbytes):
-        if nbytes < 0 or pos + nbytes > len(payload):
-            raise TruncatedBlobError(f"payload ends at byte {len(payload)}, needed {pos + nbytes}")
-
-    need(_CFG.size)
-    (mode, tau, tw, th, theta_r, phi_r, phi_off, w, h, n, k, quant) = _CFG.unpack_from(payload, 0)
-    pos = _CFG.size
+def _config(head: bytes, raw_len: int) -> dict:
+    """_parse_config (bitstream.py:356-385) on the first bytes of a raw payload."""
+    if raw_len < _CFG.size:
+        raise TruncatedBlobError(f"payload ends at byte {raw_len}, needed {_CFG.size}")
+    (mode, tau, tw, th, theta_r, phi_r, phi_off, w, h, n, k, quant) = _CFG.unpack_from(head, 0)
     if mode not in (0, 1):
         raise MalformedBlobError(f"unknown mode code {mode}")
     if not all(np.isfinite([tau, theta_r, phi_r, phi_off, quant])):
@@ -94,234 +91,231 @@ def _parse(payload: bytes):
         raise MalformedBlobError(f"image size {w}x{h} outside supported range")
     if n < 1 or n > MAX_FRAMES:
         raise MalformedBlobError(f"frame count {n} outside supported range")
-    if tw < 1 or th < 1 or not 0 <= k < n or (mode == 0 and n != 1):
-        raise MalformedBlobError("inconsistent config")
-    cfg = dict(mode=mode, tau=tau, tile_w=tw, tile_h=th, theta_r=theta_r, phi_r=phi_r, phi_offset=phi_off,
-               w=w, h=h, n_frames=n, k_index=k, range_quant=quant)
-    tx, ty = -(-w // tw), -(-h // th)
-    need(48 * n)
-    xf = np.frombuffer(payload, "<f4", 12 * n, pos).astype(np.float64).reshape(n, 12)
-    pos += 48 * n
-    nb = (w * h + 7) // 8
-    need(nb * n)
-    vbits = buf[pos:pos + nb * n].reshape(n, nb)
-    pos += nb * n
-    # per-tile plane maps: float4 (a, b, c, kind) per (channel, tile)
-    tmap = np.zeros((n, ty, tx, 4), np.float32)
-    pm = (n + 7) // 8
-    need(4)
-    (n_runs,) = struct.unpack_from("<I", payload, pos)
-    pos += 4
-    runs = []
-    for _ in range(n_runs):
-        need(18 + pm)
-        row, s, ln, a, b, c = struct.unpack_from("<HHHfff", payload, pos)
-        pos += 18
-        if row >= ty or ln < 1 or s + ln > tx:
-            raise MalformedBlobError("temporal run outside tile grid")
-        bits = payload[pos:pos + pm]
-        pos += pm
-        offs = []
-        for ch in range(n):
-            if bits[ch >> 3] & (1 << (ch & 7)):
-                if ch == k:
-                    offs.append((ch, c))
-                else:
-                    need(4)
-                    offs.append((ch, struct.unpack_from("<f", payload, pos)[0]))
-                    pos += 4
-        if not any(ch == k for ch, _ in offs):
-            raise MalformedBlobError("temporal run missing key-frame offset")
-        runs.append((row, s, ln, a, b, offs))
-    fb = []
-    for ch in range(n):
-        need(4)
-        (nrows,) = struct.unpack_from("<I", payload, pos)
-        pos += 4
-        if nrows > ty:
-            raise MalformedBlobError("more fallback rows than tile rows")
-        for _ in range(nrows):
-            need(4)
-            row, nr = struct.unpack_from("<HH", payload, pos)
-            pos += 4
-            if row >= ty or nr > tx:
-                raise MalformedBlobError("fallback row outside tile grid")
-            need(16 * nr)
-            rec = np.frombuffer(payload, dtype=[("s", "<u2"), ("l", "<u2"), ("abc", "<f4", 3)], count=nr, offset=pos)
-            pos += 16 * nr
-            if nr and (np.any(rec["l"] < 1) or np.any(rec["s"].astype(np.int64) + rec["l"] > tx)):
-                raise MalformedBlobError("fallback run outside tile grid")
-            fb.append((ch, row, rec))
-    # fallback first (kind 2), temporal overrides (kind 1): temporal coverage wins
-    for ch, row, rec in fb:
-        for s, ln, abc in zip(rec["s"], rec["l"], rec["abc"]):
-            tmap[ch, row, s:s + ln] = (abc[0], abc[1], abc[2], 2.0)
-    for row, s, ln, a, b, offs in runs:
-        for ch, cc in offs:
-            tmap[ch, row, s:s + ln] = (a, b, cc, 1.0)
-    res_flat, res_r, res_f = [], [], []
-    for ch in range(n):
-        need(4)
-        (cnt,) = struct.unpack_from("<I", payload, pos)
-        pos += 4
-        if cnt > w * h:
-            raise MalformedBlobError("residual count exceeds pixel count")
-        if cnt == 0:
-            continue
-        deltas, pos = _varints(buf, pos, cnt)
-        if deltas[0] < 0 or np.any(deltas[1:] < 1) or np.any(deltas > w * h):
-            raise MalformedBlobError("residual pixel deltas out of range")
-        flat = np.cumsum(deltas)
-        if flat[-1] >= w * h:
-            raise MalformedBlobError("residual pixel indices not strictly increasing")
-        need(2 * cnt + 4)
-        codes = np.frombuffer(payload, "<u2", cnt, pos).astype(np.int64)
-        pos += 2 * cnt
-        (n_esc,) = struct.unpack_from("<I", payload, pos)
-        pos += 4
-        need(4 * n_esc)
-        esc = np.frombuffer(payload, "<f4", n_esc, pos).astype(np.float64)
-        pos += 4 * n_esc
-        emask = codes == 0xFFFF
-        if int(np.count_nonzero(emask)) != n_esc:
-            raise MalformedBlobError("escape count mismatch in residual section")
-        ranges = codes.astype(np.float64) * quant
-        ranges[emask] = esc
-        res_flat.append(flat)
-        res_r.append(ranges)
-        res_f.append(np.full(cnt, ch, np.int32))
-    if pos != len(payload):
-        raise MalformedBlobError(f"{len(payload) - pos} trailing payload bytes")
-    return cfg, xf, vbits, tmap, res_flat, res_r, res_f
+    if tw < 1 or th < 1:
+        raise MalformedBlobError("tile dimensions must be >= 1")
+    if not 0 <= k < n:
+        raise MalformedBlobError("k_index out of range")
+    if mode == 0 and n != 1:
+        raise MalformedBlobError("single-frame blob with multiple frames")
+    return dict(mode=mode, tau=tau, tile_w=tw, tile_h=th, theta_r=theta_r, phi_r=phi_r, phi_offset=phi_off,
+                w=w, h=h, n_frames=n, k_index=k, range_quant=quant)
 
 
-def _inverse_rows(xf: np.ndarray) -> np.ndarray:
-    """R^-1 | T^-1 per frame with the reference's numpy expressions (motion.py:78-79)."""
-    out = np.empty_like(xf)
-    for i, row in enumerate(xf):
-        R = row[:9].reshape(3, 3)
-        T = row[9:]
-        out[i, :9] = R.T.reshape(9)
-        out[i, 9:] = -(R.T @ T)
+def _transforms(head: bytes, raw_len: int, n: int) -> np.ndarray:
+    """The float32 transform block (bitstream.py:420-426) as R^-1 | T^-1 rows,
+    validated like RigidTransform(...) and inverted with motion.py:78-79's
+    expressions."""
+    end = _CFG.size + 48 * n
+    if raw_len < end:
+        raise TruncatedBlobError(f"payload ends at byte {raw_len}, needed {end}")
+    block = np.frombuffer(head, "<f4", 12 * n, _CFG.size).astype(np.float64).reshape(n, 12)
+    out = np.empty((n, 12))
+    for i in range(n):
+        try:
+            t = RigidTransform(block[i, :9].reshape(3, 3), block[i, 9:])
+        except ValueError as exc:
+            raise MalformedBlobError(f"transform {i}: {exc}") from exc
+        inv = t.inverse()
+        out[i, :9] = inv.R.reshape(9)
+        out[i, 9:] = inv.T
     return out
 
 
+def _transforms_batch(heads: np.ndarray, raw_len: np.ndarray, idxs: List[int], n: int
+                      ) -> Tuple[Dict[int, np.ndarray], Dict[int, Exception]]:
+    """_transforms for many blobs with one frame count, vectorised: the
+    RigidTransform checks (motion.py:52-62: allclose(R.T @ R, I, atol=1e-6),
+    isclose(det R, 1, atol=1e-6)) on the stacked matrices, and the inverse
+    R.T | -(R.T @ T) by one batched matmul -- bit-identical to the per-frame
+    numpy expressions (R and T are float32-exact, so every product is exact
+    and numpy's K=3 sums run left to right either way; checked in
+    tests/test_host.py).  Frames whose orthonormality residual lies within
+    1e-12 of the tolerance, or hold non-finite values, are re-checked with
+    the per-frame reference expression."""
+    from .geometry import ORTHONORMAL_ATOL
+
+    good: Dict[int, np.ndarray] = {}
+    errors: Dict[int, Exception] = {}
+    end = _CFG.size + 48 * n
+    ok = [i for i in idxs if raw_len[i] >= end]
+    for i in idxs:
+        if raw_len[i] < end:
+            errors[i] = TruncatedBlobError(f"payload ends at byte {int(raw_len[i])}, needed {end}")
+    if not ok:
+        return good, errors
+    blk = np.ascontiguousarray(heads[ok, _CFG.size:end]).view("<f4").astype(np.float64).reshape(len(ok), n, 12)
+    R = blk[:, :, :9].reshape(-1, 3, 3)
+    T = blk[:, :, 9:].reshape(-1, 3)
+    Rt = np.transpose(R, (0, 2, 1))
+    eye = np.eye(3)
+    with np.errstate(all="ignore"):
+        M = np.matmul(Rt, R)
+        dev = np.abs(M - eye)
+        thr = ORTHONORMAL_ATOL + 1e-5 * eye  # allclose: atol + rtol * |b|
+        orth = np.all(dev <= thr, axis=(1, 2))
+        near = np.any(np.abs(dev - thr) < 1e-12, axis=(1, 2)) | ~np.all(np.isfinite(R), axis=(1, 2))
+        det = np.linalg.det(R)
+        detok = np.abs(det - 1.0) <= ORTHONORMAL_ATOL + 1e-5
+        Tinv = -np.matmul(Rt, T[:, :, None])[:, :, 0]
+    for f in np.flatnonzero(near):
+        orth[f] = np.allclose(R[f].T @ R[f], eye, atol=ORTHONORMAL_ATOL)
+    rows = np.concatenate([Rt.reshape(-1, 9), Tinv], axis=1).reshape(len(ok), n, 12)
+    valid = (orth & detok).reshape(len(ok), n)
+    for j, i in enumerate(ok):
+        if valid[j].all():
+            good[i] = rows[j]
+            continue
+        f = int(np.flatnonzero(~valid[j])[0])
+        why = "R is not orthonormal" if not orth.reshape(len(ok), n)[j, f] else "R must be a proper rotation (det +1)"
+        errors[i] = MalformedBlobError(f"transform {f}: {why}")
+    return good, errors
+
+
+class Decoder:
+    """One native decoder context (device workspace reused across calls)."""
+
+    def __init__(self):
+        self.L = _native.load(require_device=True)
+        h = ctypes.c_void_p()
+        _native.check(self.L.stpc_decoder_create(ctypes.byref(h)))
+        self.h = h
+
+    def __del__(self):
+        if getattr(self, "h", None) and self.L is not None:
+            self.L.stpc_decoder_destroy(self.h)
+            self.h = None
+
+    def decode(self, blobs_ptr: int, offsets: np.ndarray, on_device: bool, stream: Optional[int] = None,
+               keep_on_device: bool = False) -> Tuple[List, List, Dict[int, Exception]]:
+        """Decode n blobs at blobs_ptr[offsets[i]:offsets[i+1]] (host or device).
+        Returns (clouds per blob or None, reports, {blob index: exception}).
+        keep_on_device: leave the points in the decoder's device buffer
+        (clouds are then None; reports carry the per-frame counts)."""
+        L = self.L
+        n = offsets.size - 1
+        offsets = np.ascontiguousarray(offsets, np.int64)
+        t0 = time.perf_counter()
+        status = np.zeros(n, np.int32)
+        _native.check(L.stpc_decoder_load(self.h, blobs_ptr, int(on_device), offsets.ctypes.data, n,
+                                          status.ctypes.data, stream))
+        errors: Dict[int, Exception] = {}
+        for i in np.flatnonzero(status):
+            errors[int(i)] = _KIND[int(status[i])](_LOAD_MSG[int(status[i])])
+        raw_len = np.zeros(n, np.int64)
+        cap = _CFG.size + 48 * _HEAD_FRAMES
+        heads = np.zeros((n, cap), np.uint8)
+        _native.check(L.stpc_decoder_heads(self.h, cap, heads.ctypes.data, raw_len.ctypes.data, stream))
+        cfgs: Dict[int, dict] = {}
+        for i in range(n):
+            if i in errors:
+                continue
+            try:
+                cfgs[i] = _config(heads[i].tobytes(), int(raw_len[i]))
+            except Exception as exc:  # noqa: BLE001 -- reported per blob
+                errors[i] = exc
+        need = max([c["n_frames"] for c in cfgs.values()], default=0)
+        if need > _HEAD_FRAMES:
+            cap = _CFG.size + 48 * need
+            heads = np.zeros((n, cap), np.uint8)
+            _native.check(L.stpc_decoder_heads(self.h, cap, heads.ctypes.data, raw_len.ctypes.data, stream))
+        xf_inv: Dict[int, np.ndarray] = {}
+        by_n: Dict[int, List[int]] = {}
+        for i, c in cfgs.items():
+            by_n.setdefault(c["n_frames"], []).append(i)
+        for nf, idxs in by_n.items():
+            good, bad = _transforms_batch(heads, raw_len, idxs, nf)
+            xf_inv.update(good)
+            for i, exc in bad.items():
+                errors[i] = exc
+                del cfgs[i]
+        t1 = time.perf_counter()
+        groups: Dict[bytes, List[int]] = {}
+        for i in cfgs:
+            groups.setdefault(heads[i, :_CFG.size].tobytes(), []).append(i)
+        clouds: List[Optional[List[np.ndarray]]] = [None] * n
+        reports: List[Optional[DecodeReport]] = [None] * n
+        t_frames = t_points = 0.0
+        for idxs in groups.values():
+            ta = time.perf_counter()
+            c = cfgs[idxs[0]]
+            nf = c["n_frames"]
+            m = len(idxs)
+            geom = _native.StpcDecodeGeom(c["w"], c["h"], c["tile_w"], c["tile_h"], nf, c["k_index"],
+                                          c["range_quant"], DEFAULT_R_MAX)
+            st, ct, sp, cp = (np.ascontiguousarray(a) for a in
+                              ray_trig_tables(c["w"], c["h"], c["theta_r"], c["phi_r"], c["phi_offset"]))
+            sel = np.asarray(idxs, np.int32)
+            xfi = np.ascontiguousarray(np.concatenate([xf_inv[i] for i in idxs]))
+            counts = np.zeros(m * nf, np.int64)
+            pstat = np.zeros(m, np.int64)
+            failed = np.zeros(m, np.int64)
+            _native.check(L.stpc_decoder_frames(
+                self.h, ctypes.byref(geom), sel.ctypes.data, m, st.ctypes.data, ct.ctypes.data, sp.ctypes.data,
+                cp.ctypes.data, xfi.ctypes.data, counts.ctypes.data, pstat.ctypes.data, failed.ctypes.data,
+                stream))
+            tb = time.perf_counter()
+            total = int(L.stpc_decoder_total_points(self.h))
+            if keep_on_device:
+                pts = None
+                _native.check(L.stpc_decoder_points(self.h, None, 1, 0, stream))
+            else:
+                pts = np.empty((total, 3))
+                _native.check(L.stpc_decoder_points(self.h, pts.ctypes.data, 0, total, stream))
+            tc = time.perf_counter()
+            t_frames += tb - ta
+            t_points += tc - tb
+            bounds = np.concatenate(([0], np.cumsum(counts)))
+            for jj, i in enumerate(idxs):
+                if pstat[jj]:
+                    kind = int(pstat[jj]) & 0xF
+                    errors[i] = _KIND[kind](f"structural error at payload byte {int(pstat[jj]) >> 8}")
+                    continue
+                if pts is not None:
+                    clouds[i] = [pts[bounds[jj * nf + ch]:bounds[jj * nf + ch + 1]] for ch in range(nf)]
+                reports[i] = DecodeReport(point_counts=[int(x) for x in counts[jj * nf:(jj + 1) * nf]],
+                                          failed_reconstructions=int(failed[jj]), timings={})
+        timings = {"deserialize": (t1 - t0) + t_frames, "reconstruct": t_points}
+        for r in reports:
+            if r is not None:
+                r.timings = dict(timings)
+        return clouds, reports, errors
+
+
+_decoders: Dict[int, Decoder] = {}
+
+
+def get_decoder() -> Decoder:
+    import threading
+
+    key = threading.get_ident()
+    if key not in _decoders:
+        _decoders[key] = Decoder()
+    return _decoders[key]
+
+
 def decompress_many(blobs: Sequence[bytes]) -> Tuple[List[List[np.ndarray]], List[DecodeReport]]:
-    """Decode a batch of blobs (one device pass per distinct configuration)."""
-    import time
-
-    L = _native.load(require_device=True)
-    t0 = time.perf_counter()
-    heads = [_header(b) for b in blobs]
-    off = np.zeros(len(blobs) + 1, np.int64)
-    off[1:] = np.cumsum([(len(b) + 15) // 16 * 16 for b in blobs])
-    arena = np.zeros(int(off[-1]), np.uint8)
-    for b, o in zip(blobs, off[:-1]):
-        arena[o:o + len(b)] = np.frombuffer(b, np.uint8)
-    raw_off = np.zeros(len(blobs) + 1, np.int64)
-    raw_off[1:] = np.cumsum([(h[0] + 15) // 16 * 16 for h in heads])
-    dev = _Dev(L)
-    d_blobs = dev.put(arena)
-    d_off = dev.put(off[:-1])
-    crc = np.zeros(len(blobs), np.uint32)
-    _native.check(L.stpc_crc32_blobs(d_blobs, d_off, len(blobs), crc.ctypes.data, None))
-    for h, c in zip(heads, crc):
-        if int(c) != h[2]:
-            raise ChecksumError("payload CRC-32 mismatch")
-    d_raw = dev.alloc(max(int(raw_off[-1]), 1))
-    d_roff = dev.put(raw_off[:-1])
-    st = np.zeros(len(blobs), np.int32)
-    _native.check(L.stpc_huffman_decode_blobs(d_blobs, d_off, len(blobs), d_raw, d_roff, st.ctypes.data, None))
-    if np.any(st == 1):
-        raise TruncatedBlobError("entropy payload ended mid-symbol")
-    if np.any(st != 0):
-        raise MalformedBlobError("invalid Huffman code in payload")
-    raw = np.empty(int(raw_off[-1]), np.uint8)
-    _native.check(L.stpc_memcpy_d2h(raw.ctypes.data, d_raw, raw.nbytes))
-    t1 = time.perf_counter()
-    parsed = [_parse(raw[o:o + h[0]].tobytes()) for o, h in zip(raw_off[:-1], heads)]
-    t2 = time.perf_counter()
-    clouds_all: List[List[np.ndarray]] = [None] * len(blobs)  # type: ignore
-    reports: List[DecodeReport] = [None] * len(blobs)  # type: ignore
-    by_cfg: Dict[tuple, List[int]] = {}
-    for i, p in enumerate(parsed):
-        by_cfg.setdefault(tuple(sorted(p[0].items())), []).append(i)
-    for key, idxs in by_cfg.items():
-        cfg = dict(key)
-        n, w, h = cfg["n_frames"], cfg["w"], cfg["h"]
-        F = n * len(idxs)
-        tabs = ray_trig_tables(w, h, cfg["theta_r"], cfg["phi_r"], cfg["phi_offset"])
-        trig = np.concatenate(tabs)
-        vbits = np.concatenate([parsed[i][2] for i in idxs]).reshape(F, -1)
-        tmap = np.concatenate([parsed[i][3] for i in idxs]).reshape(F, -1, 4)
-        xf_inv = np.concatenate([_inverse_rows(parsed[i][1]) for i in idxs])
-        flats, rngs, frames = [], [], []
-        for j, i in enumerate(idxs):
-            for fl, rr, ff in zip(parsed[i][4], parsed[i][5], parsed[i][6]):
-                flats.append(fl)
-                rngs.append(rr)
-                frames.append(ff + j * n)
-        res_flat = np.concatenate(flats) if flats else np.zeros(1, np.int64)
-        res_r = np.concatenate(rngs) if rngs else np.zeros(1)
-        res_f = np.concatenate(frames) if frames else np.zeros(1, np.int32)
-        n_res = int(sum(x.size for x in flats))
-        cap = int(np.unpackbits(vbits, axis=1).sum()) + 1
-        d_trig, d_vb, d_tm = dev.put(trig), dev.put(np.ascontiguousarray(vbits)), dev.put(np.ascontiguousarray(tmap))
-        d_rf, d_rr, d_rfr = dev.put(res_flat), dev.put(res_r), dev.put(res_f.astype(np.int32))
-        d_xi = dev.put(xf_inv)
-        d_scr = dev.alloc(8 * F * w * h)
-        d_pts = dev.alloc(24 * cap)
-        counts = np.zeros(F, np.int64)
-        failed = ctypes.c_int64()
-        _native.check(L.stpc_reconstruct_frames(
-            w, h, cfg["tile_w"], cfg["tile_h"], d_trig, F, d_vb, vbits.shape[1], d_tm, d_rf, d_rr, d_rfr,
-            n_res, d_xi, DEFAULT_R_MAX, d_scr, d_pts, cap, counts.ctypes.data, ctypes.byref(failed), None))
-        pts = np.empty((int(counts.sum()), 3))
-        _native.check(L.stpc_memcpy_d2h(pts.ctypes.data, d_pts, pts.nbytes))
-        bounds = np.concatenate(([0], np.cumsum(counts)))
-        for j, i in enumerate(idxs):
-            clouds_all[i] = [pts[bounds[j * n + c]:bounds[j * n + c + 1]] for c in range(n)]
-            reports[i] = DecodeReport(point_counts=[int(x) for x in counts[j * n:(j + 1) * n]],
-                                      failed_reconstructions=int(failed.value) if len(idxs) == 1 else -1,
-                                      timings={})
-    t3 = time.perf_counter()
-    for r in reports:
-        r.timings = {"entropy": t1 - t0, "parse": t2 - t1, "reconstruct": t3 - t2}
-    dev.free_all()
-    return clouds_all, reports
+    """Decode a batch of blobs (one device pass per distinct configuration).
+    Raises the reference's exception for the first blob that fails."""
+    dec = get_decoder()
+    sizes = np.array([len(b) for b in blobs], np.int64)
+    offsets = np.zeros(len(blobs) + 1, np.int64)
+    offsets[1:] = np.cumsum(sizes)
+    arena = np.frombuffer(b"".join(blobs), np.uint8) if len(blobs) else np.zeros(0, np.uint8)
+    if arena.size == 0:
+        arena = np.zeros(1, np.uint8)
+    clouds, reports, errors = dec.decode(arena.ctypes.data, offsets, on_device=False)
+    if errors:
+        raise errors[min(errors)]
+    return clouds, reports  # type: ignore[return-value]
 
 
-def decompress_full(blob: bytes):
+def decompress_full(blob: bytes) -> Tuple[List[np.ndarray], DecodeReport]:
+    """Drop-in for stpc.decompress_full (bitstream.py:605-625)."""
     clouds, reps = decompress_many([blob])
     return clouds[0], reps[0]
 
 
 def decompress(blob: bytes) -> List[np.ndarray]:
-    """Drop-in for stpc.decompress: one (N, 3) float64 cloud per frame."""
+    """Drop-in for stpc.decompress (bitstream.py:628-631): one (N, 3) float64
+    cloud per frame, in each frame's own coordinates."""
     return decompress_full(blob)[0]
-
-
-class _Dev:
-    """Scoped device allocations through the C-ABI."""
-
-    def __init__(self, L):
-        self.L = L
-        self.ptrs = []
-
-    def alloc(self, nbytes):
-        p = ctypes.c_void_p()
-        _native.check(self.L.stpc_malloc(ctypes.byref(p), int(max(nbytes, 1))))
-        self.ptrs.append(p)
-        return p
-
-    def put(self, arr):
-        arr = np.ascontiguousarray(arr)
-        p = self.alloc(arr.nbytes)
-        if arr.nbytes:
-            _native.check(self.L.stpc_memcpy_h2d(p, arr.ctypes.data, arr.nbytes))
-        return p
-
-    def free_all(self):
-        for p in self.ptrs:
-            self.L.stpc_free(p)
-        self.ptrs = []

@@ -186,6 +186,221 @@ def imu_case(name, seed, n, tau, tw, th, sensor=SMALL):
     save_case(name, list(g.clouds), [(x.R, x.T) for x in ts], cfg, blob, extra)
 
 
+# ----------------------------------------------------------- decoder errors
+
+
+def _wrap(payload: bytes, lengths=None, encoded=None, raw_len=None, crc=None, magic=b"STPC", version=1):
+    """Entropy-code a raw payload the way serialize does (bitstream.py:279-289)."""
+    import struct
+    import zlib
+
+    if lengths is None:
+        lengths, encoded = ref_huffman.encode_bytes(payload)
+    lengths = np.asarray(lengths, np.uint8)
+    raw_len = len(payload) if raw_len is None else raw_len
+    crc = zlib.crc32(encoded) & 0xFFFFFFFF if crc is None else crc
+    return struct.pack("<4sHHQQI", magic, version, 0, raw_len, len(encoded), crc) + lengths.tobytes() + encoded
+
+
+def _varint(vals):
+    out = bytearray()
+    for v in vals:
+        v = int(v)
+        while v >= 128:
+            out.append((v & 0x7F) | 0x80)
+            v >>= 7
+        out.append(v)
+    return bytes(out)
+
+
+def _layout(pl: bytes):
+    """Byte positions of every section of a raw payload (bitstream.py:193-278)."""
+    import struct
+
+    (mode, tau, tw, th, tr, pr, po, w, h, n, k, q) = struct.unpack_from("<Bd HH ddd II HH d", pl, 0)
+    tx, ty, nb, pm = -(-w // tw), -(-h // th), (w * h + 7) // 8, (n + 7) // 8
+    L = dict(n=n, k=k, tx=tx, ty=ty, P=w * h, bits=57 + 48 * n, runs=[], fb=[], res=[])
+    pos = 57 + 48 * n + n * nb
+    L["nruns"] = pos
+    (nr,) = struct.unpack_from("<I", pl, pos)
+    pos += 4
+    for _ in range(nr):
+        mask = pl[pos + 18:pos + 18 + pm]
+        present = [ch for ch in range(n) if mask[ch >> 3] & (1 << (ch & 7))]
+        extra = len([c for c in present if c != k])
+        L["runs"].append(dict(pos=pos, extra=extra, present=present))
+        pos += 18 + pm + 4 * extra
+    for ch in range(n):
+        pc = pos
+        (nrows,) = struct.unpack_from("<I", pl, pos)
+        pos += 4
+        rows = []
+        for _ in range(nrows):
+            row, nrr = struct.unpack_from("<HH", pl, pos)
+            rows.append(dict(pos=pos, nr=nrr, runs=pos + 4))
+            pos += 4 + 16 * nrr
+        L["fb"].append(dict(pos=pc, rows=rows))
+    for ch in range(n):
+        pc = pos
+        (cnt,) = struct.unpack_from("<I", pl, pos)
+        pos += 4
+        if cnt == 0:
+            L["res"].append(dict(pos=pc, cnt=0))
+            continue
+        var = pos
+        vals = []
+        for _ in range(cnt):
+            v = sh = 0
+            while True:
+                b = pl[pos]
+                pos += 1
+                v |= (b & 0x7F) << sh
+                if b < 128:
+                    break
+                sh += 7
+            vals.append(v)
+        code = pos
+        pos += 2 * cnt
+        (ne,) = struct.unpack_from("<I", pl, pos)
+        L["res"].append(dict(pos=pc, cnt=cnt, var=var, deltas=vals, code=code, nesc=pos, esc=pos + 4, n_esc=ne))
+        pos += 4 + 4 * ne
+    L["end"] = pos
+    assert pos == len(pl)
+    return L
+
+
+def decode_error_cases():
+    """Corrupted blobs and the exception the reference's decompress raises for
+    each (tests/test_gpu_parity.py::test_decode_errors_match_reference)."""
+    import struct
+
+    g = synth.make_group(301, 3, SMALL)
+    import dataclasses
+
+    cfg = dataclasses.replace(ref_cfg(SMALL, 3, 0.1, 4, 4), range_quant=0.0003)  # ranges > 19.7 m escape
+    poses = [RigidTransform(R=R, T=T) for R, T in g.poses]
+    blob, _ = stpc.compress(g.clouds, cfg, poses=poses)
+    enc, _ = stpc.bitstream.deserialize(blob)
+    raw_len, enc_len = struct.unpack_from("<QQ", blob, 8)
+    pl = stpc.huffman.decode_bytes(np.frombuffer(blob, np.uint8, 256, 28), blob[284:284 + enc_len], raw_len)
+    L = _layout(pl)
+    n, k, tx, ty, P = L["n"], L["k"], L["tx"], L["ty"], L["P"]
+    run_x = next(r for r in L["runs"] if r["extra"] > 0)
+    fb_ch = next(c for c in range(n) if L["fb"][c]["rows"])
+    fb_row = L["fb"][fb_ch]["rows"][0]
+    res_ch = next(c for c in range(n) if L["res"][c]["cnt"] > 3 and L["res"][c]["n_esc"] > 0)
+    R = L["res"][res_ch]
+    print("layout: runs", len(L["runs"]), "fb rows", sum(len(f["rows"]) for f in L["fb"]),
+          "res", [r["cnt"] for r in L["res"]], "esc", [r.get("n_esc", 0) for r in L["res"]])
+
+    def put(b, off, fmt, *v):
+        b = bytearray(b)
+        struct.pack_into(fmt, b, off, *v)
+        return bytes(b)
+
+    def one_byte_delta(r):
+        # index i > 0 of a one-byte varint
+        pos = r["var"]
+        for i, d in enumerate(r["deltas"]):
+            ln = len(_varint([d]))
+            if i > 0 and ln == 1:
+                return pos
+            pos += ln
+        raise AssertionError
+
+    def with_deltas(b, r, deltas):
+        return b[:r["var"]] + _varint(deltas) + b[r["code"]:]
+
+    pcases = {
+        "ok": pl,
+        "trunc_config": pl[:30],
+        "trunc_transforms": pl[:57 + 10],
+        "trunc_bitmaps": pl[:L["bits"] + 5],
+        "trunc_nruns": pl[:L["nruns"] + 2],
+        "trunc_run_header": pl[:run_x["pos"] + 10],
+        "trunc_run_mask": pl[:run_x["pos"] + 18],
+        "trunc_run_offsets": pl[:run_x["pos"] + 19 + 2],
+        "trunc_fb_count": pl[:L["fb"][0]["pos"] + 2],
+        "trunc_fb_row": pl[:fb_row["pos"] + 2],
+        "trunc_fb_runs": pl[:fb_row["runs"] + 8],
+        "trunc_res_count": pl[:L["res"][0]["pos"] + 3],
+        "trunc_varints": pl[:R["var"] + 2],
+        "trunc_codes": pl[:R["code"] + 3],
+        "trunc_nesc": pl[:R["nesc"] + 1],
+        "trunc_escapes": pl[:R["esc"] + 2],
+        "trailing_bytes": pl + b"\x00\x00",
+        "cfg_mode": put(pl, 0, "<B", 7),
+        "cfg_tau_neg": put(pl, 1, "<d", -1.0),
+        "cfg_tau_nan": put(pl, 1, "<d", float("nan")),
+        "cfg_tile0": put(pl, 9, "<H", 0),
+        "cfg_frames0": put(pl, 45, "<H", 0),
+        "cfg_k_oob": put(pl, 47, "<H", n),
+        "cfg_single_multi": put(pl, 0, "<B", 0),
+        "cfg_huge_image": put(pl, 37, "<II", 70000, 1000),
+        "xf_not_orthonormal": put(pl, 57 + 48, "<f", 2.0),
+        "xf_nan": put(pl, 57 + 48 + 36, "<f", float("nan")),
+        "run_row_oob": put(pl, run_x["pos"], "<H", ty),
+        "run_len0": put(pl, run_x["pos"] + 4, "<H", 0),
+        "run_span_oob": put(pl, run_x["pos"] + 2, "<H", tx - 1),
+        "run_no_key": put(pl, run_x["pos"] + 18, "<B", pl[run_x["pos"] + 18] & ~(1 << k)),
+        "fb_nrows_oob": put(pl, L["fb"][fb_ch]["pos"], "<I", ty + 1),
+        "fb_row_oob": put(pl, fb_row["pos"], "<H", ty),
+        "fb_nr_oob": put(pl, fb_row["pos"] + 2, "<H", tx + 1),
+        "fb_run_len0": put(pl, fb_row["runs"] + 2, "<H", 0),
+        "fb_run_span_oob": put(pl, fb_row["runs"], "<H", tx),
+        "res_count_oob": put(pl, R["pos"], "<I", P + 1),
+        "res_delta_zero": put(pl, one_byte_delta(R), "<B", 0),
+        "res_overlong_varint": pl[:R["var"]] + b"\x80" * 11 + pl[R["var"] + 11:],
+        "res_flat_oob": with_deltas(pl, R, [R["deltas"][0] + P] + R["deltas"][1:]),
+        "res_delta_too_big": with_deltas(pl, R, R["deltas"][:1] + [P + 1] + R["deltas"][2:]),
+        "res_escape_mismatch": put(pl, R["nesc"], "<I", R["n_esc"] - 1)[:R["esc"] + 4 * (R["n_esc"] - 1)]
+        + pl[R["esc"] + 4 * R["n_esc"]:],
+        # two errors: the reference reports the first in reading order
+        "two_run_len0_then_trunc": put(pl, run_x["pos"] + 4, "<H", 0)[:R["code"] + 1],
+        "two_row_oob_mask_trunc": put(pl, run_x["pos"], "<H", ty)[:run_x["pos"] + 18],
+        "two_delta_zero_then_trunc_codes": put(pl, one_byte_delta(R), "<B", 0)[:R["code"] + 3],
+        "two_fb_oob_then_trailing": put(pl, fb_row["pos"], "<H", ty) + b"\x01",
+        "two_no_key_then_res_oob": put(put(pl, run_x["pos"] + 18, "<B", pl[run_x["pos"] + 18] & ~(1 << k)),
+                                       R["pos"], "<I", P + 1),
+    }
+    blobs = {name: _wrap(b) for name, b in pcases.items()}
+    # header / code table / entropy-stage cases
+    lens, encd = ref_huffman.encode_bytes(pl)
+    blobs["hdr_short"] = blob[:100]
+    blobs["hdr_magic"] = b"XTPC" + blob[4:]
+    blobs["hdr_version"] = blob[:4] + b"\x02\x00" + blob[6:]
+    blobs["hdr_raw_cap"] = put(blob, 8, "<Q", (1 << 30) + 1)
+    blobs["hdr_enc_past_end"] = blob[:-10]
+    blobs["hdr_crc"] = put(blob, 24, "<I", (struct.unpack_from("<I", blob, 24)[0] ^ 1))
+    bad = np.array(lens, np.uint8)
+    bad[np.flatnonzero(bad)[0]] = 33
+    blobs["table_len33"] = _wrap(pl, bad, encd)
+    blobs["table_overflow"] = _wrap(pl, np.ones(256, np.uint8), encd)
+    blobs["table_empty"] = _wrap(pl, np.zeros(256, np.uint8), encd)
+    blobs["raw_len0"] = _wrap(b"", np.zeros(256, np.uint8), b"", raw_len=0)
+    one = np.zeros(256, np.uint8)
+    one[65] = 1
+    blobs["huff_invalid_code"] = _wrap(b"", one, b"\x00\xff\xff\xff\xff\xff\xff\xff", raw_len=20)
+    blobs["huff_invalid_after_end"] = _wrap(b"", one, b"\x00\x00\xff\xff\xff\xff\xff\xff", raw_len=16)
+    blobs["huff_truncated"] = _wrap(b"", one, b"\x00\x00", raw_len=40)
+    blobs["huff_short_tail"] = _wrap(b"", one, b"\x00\x00\xff\xff", raw_len=20)
+    names, expect, data = [], [], []
+    for name, b in blobs.items():
+        try:
+            stpc.decompress(b)
+            exc = "ok"
+        except Exception as e:  # noqa: BLE001
+            exc = type(e).__name__
+        names.append(name)
+        expect.append(exc)
+        data.append(np.frombuffer(b, np.uint8))
+        print(f"  {name:34s} {exc}")
+    off = np.zeros(len(data) + 1, np.int64)
+    off[1:] = np.cumsum([d.size for d in data])
+    np.savez_compressed(os.path.join(HERE, "decode_errors.npz"), names=np.array(names), expect=np.array(expect),
+                        blobs=np.concatenate(data), offsets=off)
+
+
 CASES = {
     "single_4x4": lambda: compress_case("single_4x4", 101, 1, 0.1, 4, 4),
     "stream3_4x4": lambda: compress_case("stream3_4x4", 102, 3, 0.1, 4, 4),
@@ -204,6 +419,8 @@ if __name__ == "__main__":
     if not only:
         projection_cases()
         huffman_cases()
+    if not only or "decode_errors" in only:
+        decode_error_cases()
     for name, fn in CASES.items():
         if not only or name in only:
             fn()

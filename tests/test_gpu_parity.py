@@ -432,3 +432,49 @@ def test_decompress_many_batch_and_corruption():
         decompress_many([bytes(bad)])
     with pytest.raises(DecodeError):
         decompress_many([blobs[0][:-3]])
+
+
+def test_decode_errors_match_reference():
+    """Corrupt blobs (tests/golden/decode_errors.npz, labelled by the
+    reference's own decompress): the GPU decoder raises the same exception
+    class, including which of two errors comes first in reading order; the
+    valid ones decode bit-identically to the oracle decoder."""
+    from conftest import ROOT
+    from oracle import decode as odec
+    from paper_2008_06972_b200 import decompress
+
+    z = np.load(os.path.join(ROOT, "tests", "golden", "decode_errors.npz"))
+    off = z["offsets"]
+    bad = []
+    for i, (name, expect) in enumerate(zip(z["names"], z["expect"])):
+        blob = z["blobs"][off[i]:off[i + 1]].tobytes()
+        try:
+            out = decompress(blob)
+            got = "ok"
+        except Exception as exc:  # noqa: BLE001
+            got = type(exc).__name__
+        if got != str(expect):
+            bad.append((str(name), str(expect), got))
+            continue
+        if got == "ok":
+            for a, b in zip(out, odec.decompress(blob)):
+                assert np.array_equal(a, b, equal_nan=True), name
+    assert not bad, bad
+
+
+def test_decompress_many_mixed_batch_reports_first_error():
+    """A batch with a corrupt blob in the middle raises that blob's error;
+    the same blobs without it decode like one-at-a-time calls."""
+    from conftest import ROOT
+    from paper_2008_06972_b200 import MalformedBlobError, decompress, decompress_many
+
+    z = np.load(os.path.join(ROOT, "tests", "golden", "decode_errors.npz"))
+    off = z["offsets"]
+    blobs = {str(nm): z["blobs"][off[i]:off[i + 1]].tobytes() for i, nm in enumerate(z["names"])}
+    good = [load_case(n)[3] for n in ("stream3_4x4", "single_4x4", "stream5_2x2", "stream3_4x4")]
+    with pytest.raises(MalformedBlobError):
+        decompress_many(good[:2] + [blobs["run_len0"]] + good[2:])
+    clouds, reps = decompress_many(good)
+    for b, cl in zip(good, clouds):
+        for a, r in zip(cl, decompress(b)):
+            assert np.array_equal(a, r)

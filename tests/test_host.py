@@ -161,38 +161,43 @@ def test_synthetic_scene_shapes_match_baseline():
     assert len(g.poses) == 2
 
 
-@pytest.mark.parametrize("name", ["stream3_4x4", "stream5_2x2", "stream4_8x4_k0", "single_f64_bad", "stream3_empty"])
-def test_decoder_record_parser_matches_oracle(name):
-    """decode._parse (host part of the GPU decoder) on the oracle-decoded
-    payload: tile plane maps and residual pixels agree with the oracle's
-    restatement of deserialize."""
+def _decode_error_cases():
+    z = np.load(os.path.join(ROOT, "tests", "golden", "decode_errors.npz"))
+    off = z["offsets"]
+    return [(str(nm), str(ex), z["blobs"][off[i]:off[i + 1]].tobytes())
+            for i, (nm, ex) in enumerate(zip(z["names"], z["expect"]))]
+
+
+def test_decoder_host_checks_match_reference():
+    """The checks the host side of the GPU decoder makes itself -- header
+    (bitstream.py:398-409), config block (_parse_config :356-385) and the
+    transform block (:420-426) -- raise the reference's exception class on
+    the reference-labelled corrupt blobs they decide."""
     import struct
 
     from oracle import decode as odec
     from paper_2008_06972_b200 import decode
 
-    clouds, poses, cfg, blob, z = load_case(name)
-    raw_len, enc_len = struct.unpack_from("<QQ", blob, 8)
-    payload = odec.huffman_decode(np.frombuffer(blob, np.uint8, 256, 28), blob[284:284 + enc_len], raw_len)
-    c, xf, vbits, tmap, rflat, rr, rfr = decode._parse(payload)
-    ref = odec.deserialize(blob)
-    assert c == ref.cfg
-    n = c["n_frames"]
-    for ch in range(n):
-        # temporal tiles carry this channel's offset
-        for j, offs in enumerate(ref.t_off):
-            if offs[ch] is not None:
-                a, b, _ = ref.t_abc[j]
-                seg = tmap[ch, ref.t_row[j], ref.t_s[j]:ref.t_s[j] + ref.t_len[j]]
-                assert np.all(seg[:, 3] == 1.0)
-                assert np.all(seg[:, 0] == np.float32(a)) and np.all(seg[:, 2] == np.float32(offs[ch]))
-    got = {int(f[0]): (fl, r) for fl, r, f in zip(rflat, rr, rfr)}
-    for ch in range(n):
-        fl, r = ref.residuals[ch]
-        if fl.size:
-            assert np.array_equal(got[ch][0], fl) and np.array_equal(got[ch][1], r)
-        else:
-            assert ch not in got
+    checked = 0
+    for name, expect, blob in _decode_error_cases():
+        if name.startswith("hdr_") and name != "hdr_crc":
+            with pytest.raises(Exception) as ei:
+                decode._header(blob)
+            assert type(ei.value).__name__ == expect, name
+            checked += 1
+        elif name.startswith(("cfg_", "xf_", "trunc_config", "trunc_transforms")):
+            raw_len, enc_len = struct.unpack_from("<QQ", blob, 8)
+            pl = odec.huffman_decode(np.frombuffer(blob, np.uint8, 256, 28), blob[284:284 + enc_len], raw_len)
+            got = "ok"
+            try:
+                c = decode._config(pl[:57].ljust(57, b"\0"), len(pl))
+                decode._transforms(pl[:57 + 48 * c["n_frames"]].ljust(57 + 48 * c["n_frames"], b"\0"), len(pl),
+                                   c["n_frames"])
+            except Exception as exc:  # noqa: BLE001
+                got = type(exc).__name__
+            assert got == expect, name
+            checked += 1
+    assert checked >= 15
 
 
 def test_decoder_rejects_bad_headers():
@@ -245,3 +250,38 @@ def test_imu_errors_mirror_reference():
         frame_transforms(imu, [0.1, 0.2], 2)
     d, a, v = integrate_imu(imu, 0.1, 0.1, z["v0"])
     assert not d.any() and not a.any() and np.array_equal(v, z["v0"])
+
+
+def test_decoder_batched_transforms_equal_per_frame_reference_expressions():
+    """_transforms_batch (vectorised RigidTransform checks + inverse) gives the
+    bits and errors of the per-frame reference expressions (_transforms)."""
+    from paper_2008_06972_b200 import decode as D
+
+    rng = np.random.default_rng(3)
+    B, n = 64, 8
+    heads = np.zeros((B, 57 + 48 * 16), np.uint8)
+    for i in range(B):
+        q = rng.normal(size=(n, 4))
+        q /= np.linalg.norm(q, axis=1, keepdims=True)
+        w, x, y, z = q.T
+        R = np.stack([1 - 2 * (y * y + z * z), 2 * (x * y - z * w), 2 * (x * z + y * w),
+                      2 * (x * y + z * w), 1 - 2 * (x * x + z * z), 2 * (y * z - x * w),
+                      2 * (x * z - y * w), 2 * (y * z + x * w), 1 - 2 * (x * x + y * y)], 1)
+        T = rng.normal(size=(n, 3)) * 30
+        heads[i, 57:57 + 48 * n] = np.concatenate([R, T], 1).astype("<f4").view(np.uint8).reshape(-1)
+    f32 = lambda v: np.frombuffer(np.float32(v).tobytes(), np.uint8)  # noqa: E731
+    heads[5, 57 + 96:57 + 100] = f32(2.0)
+    heads[9, 57 + 48 + 36:57 + 48 + 40] = f32(np.nan)
+    heads[11, 57 + 144:57 + 148] = f32(np.inf)
+    heads[13, 57:57 + 36] = np.diag([1.0, 1.0, -1.0]).reshape(9).astype("<f4").view(np.uint8)
+    raw_len = np.full(B, 10 ** 6, np.int64)
+    raw_len[7] = 100
+    good, bad = D._transforms_batch(heads, raw_len, list(range(B)), n)
+    assert sorted(bad) == [5, 7, 11, 13]
+    for i in range(B):
+        try:
+            ref = D._transforms(heads[i].tobytes(), int(raw_len[i]), n)
+        except Exception as exc:  # noqa: BLE001
+            assert type(bad[i]) is type(exc) and str(bad[i]) == str(exc)
+            continue
+        assert np.array_equal(good[i], ref, equal_nan=True)
