@@ -41,11 +41,14 @@ def needs_build() -> bool:
     return any(os.path.getmtime(p) > t for p in deps())
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not needs_build():
+def build(force: bool = False, verbose: bool = False, out: str = None, defines=()) -> str:
+    """out/defines: tuning variants (e.g. build_variants/, -DSTPC_PAIR_MINB=6),
+    loaded through the STPC_B200_LIB override; the product is LIB."""
+    out = out or LIB
+    if out == LIB and not force and not needs_build():
         return LIB
     nvcc = os.environ.get("NVCC", "nvcc")
-    cmd = [nvcc, *NVCC_FLAGS, "-I", os.path.join(ROOT, "include"), "-o", LIB, *sources()]
+    cmd = [nvcc, *NVCC_FLAGS, *defines, "-I", os.path.join(ROOT, "include"), "-o", out, *sources()]
     if verbose:
         print(" ".join(cmd), file=sys.stderr)
     subprocess.check_call(cmd)
@@ -53,4 +56,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
 
 
 if __name__ == "__main__":
-    build(force="--force" in sys.argv, verbose=True)
+    args = sys.argv[1:]
+    out = None
+    if "--out" in args:
+        out = args[args.index("--out") + 1]
+    build(force="--force" in args, verbose=True, out=out, defines=[a for a in args if a.startswith("-D")])

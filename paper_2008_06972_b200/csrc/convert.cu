@@ -142,11 +142,11 @@ __device__ __forceinline__ void warp_add_stats(long long* fs, int rej, int drop,
 // [1e-15, 1e15]) go to the exact fp64 path.  Returns false when undecided.
 constexpr double FAST_MARGIN = 1e-5;
 
-// atan2 for the fast path: odd minimax-style polynomial of degree 13 in
-// t = min/max (max error 3.2e-7 rad in float32 FMA evaluation, measured on
-// 2M points), reflections in double.  With the f32 input rounding the angle
-// is within ~1.3e-6 rad of the true one -- 8x inside FAST_MARGIN.
-__device__ __forceinline__ double fast_atan2(float y, float x)
+// atan2 for the fast path, entirely in fp32: odd minimax-style polynomial of
+// degree 13 in t = min/max (max error 3.2e-7 rad in float32 FMA evaluation,
+// measured on 2M points) and float reflections (pi/2, pi rounded to float:
+// <= 9e-8 rad each, plus half-ulp roundings <= 1.2e-7 rad per step).
+__device__ __forceinline__ float fast_atan2f(float y, float x)
 {
     const float ax = fabsf(x), ay = fabsf(y);
     const float mx = fmaxf(ax, ay), mn = fminf(ax, ay);
@@ -159,33 +159,38 @@ __device__ __forceinline__ double fast_atan2(float y, float x)
     p = __fmaf_rn(p, s2, 0.19807815551757812f);
     p = __fmaf_rn(p, s2, -0.3331736922264099f);
     p = __fmaf_rn(p, s2, 0.9999961256980896f);
-    double r = (double)p * (double)t;
-    if (ay > ax) r = 1.5707963267948966 - r;
-    if (x < 0.0f) r = 3.141592653589793 - r;
-    if (y < 0.0f) r = -r;
-    return r;
+    float r = p * t;
+    r = ay > ax ? 1.57079637f - r : r;
+    r = x < 0.0f ? 3.14159274f - r : r;
+    return y < 0.0f ? -r : r;
 }
 
-__device__ __forceinline__ bool fast_bin(double x, double y, double z, const Geometry& g, double inv_tr,
-                                         double inv_pr, long long& u, long long& v)
+// Error budget of the fp32 decision (in bins of the azimuth; elevation is
+// analogous and smaller): angle error <= 3.2e-7 (polynomial) + 1.2e-7 (input
+// rounding of x, y, z to float) + 5e-7 (reflections, + 2 pi wrap) rad, and
+// qu = th * inv_tr in float adds a relative 1.2e-7, i.e. <= 2 pi * 1.2e-7 *
+// inv_tr bins.  Total < 2.75e-6 * inv_tr bins against a margin of
+// FAST_MARGIN * inv_tr = 1e-5 * inv_tr bins: 3.6x headroom at any resolution.
+__device__ __forceinline__ bool fast_bin(double x, double y, double z, const Geometry& g, float inv_tr,
+                                         float inv_pr, float phi_off, int& u, int& v)
 {
     const float xf = (float)x, yf = (float)y, zf = (float)z;
     const float mxy = fmaxf(fabsf(xf), fabsf(yf));
     const float mall = fmaxf(mxy, fabsf(zf));
     // keep squares and ratios in float range; degenerate directions go exact
     if (!(mall < 1e15f && mxy > 1e-30f)) return false;
-    double th = fast_atan2(xf, yf);
-    if (th < 0.0) th += 2.0 * 3.141592653589793;
-    const double qu = th * inv_tr;
-    const double ph = fast_atan2(sqrtf(xf * xf + yf * yf), zf);
-    const double qv = (ph - g.phi_offset) * inv_pr;
-    const double flu = floor(qu), flv = floor(qv);
-    const double fu = qu - flu, fv = qv - flv;
-    const double mu = FAST_MARGIN * inv_tr, mv = FAST_MARGIN * inv_pr;
-    if (fu < mu || fu > 1.0 - mu || fv < mv || fv > 1.0 - mv) return false;
-    const long long uq = (long long)flu;  // qu >= 0
-    u = uq < g.w ? uq : uq % (long long)g.w;
-    v = (long long)flv;
+    float th = fast_atan2f(xf, yf);
+    th = th < 0.0f ? th + 6.28318548f : th;
+    const float qu = th * inv_tr;
+    const float ph = fast_atan2f(sqrtf(xf * xf + yf * yf), zf);
+    const float qv = (ph - phi_off) * inv_pr;
+    const float flu = floorf(qu), flv = floorf(qv);
+    const float fu = qu - flu, fv = qv - flv;
+    const float mu = (float)FAST_MARGIN * inv_tr, mv = (float)FAST_MARGIN * inv_pr;
+    if (fu < mu || fu > 1.0f - mu || fv < mv || fv > 1.0f - mv) return false;
+    const int uq = (int)flu;  // 0 <= qu <= w (th <= 2 pi)
+    u = uq >= g.w ? uq - g.w : uq;
+    v = (int)flv;
     return true;
 }
 
@@ -225,7 +230,8 @@ __global__ void __launch_bounds__(256, 4) convert_kernel(ConvertArgs a, const T*
     }
     __syncthreads();
     unsigned long long* best = a.best + (long long)f * a.g.P;
-    const double inv_tr = 1.0 / a.g.theta_r, inv_pr = 1.0 / a.g.phi_r;
+    const float inv_tr = (float)(1.0 / a.g.theta_r), inv_pr = (float)(1.0 / a.g.phi_r);
+    const float phi_off = (float)a.g.phi_offset;
     int rej = 0, drop = 0, kept = 0;
 #pragma unroll
     for (int k = 0; k < K; ++k) {
@@ -240,15 +246,15 @@ __global__ void __launch_bounds__(256, 4) convert_kernel(ConvertArgs a, const T*
             continue;
         }
         double r = sqrt((x * x + y * y) + z * z);
-        long long u, v;
+        int u, v;
         if (r <= 0.0) {
             rej += 1;
-        } else if (isfinite(r) && fast_bin(x, y, z, a.g, inv_tr, inv_pr, u, v)) {
+        } else if (isfinite(r) && fast_bin(x, y, z, a.g, inv_tr, inv_pr, phi_off, u, v)) {
             if (v < 0 || v >= a.g.h) {
                 drop += 1;
             } else {
                 kept += 1;
-                atomicMin(best + v * (long long)a.g.w + u, (unsigned long long)__double_as_longlong(r));
+                atomicMin(best + (v * a.g.w + u), (unsigned long long)__double_as_longlong(r));
             }
         } else {  // undecided: block-local queue
             int slot = atomicAdd(&q_n, 1);
@@ -307,7 +313,8 @@ __global__ void __launch_bounds__(256) convert_overflow_kernel(ConvertArgs a, co
     const int f = blockIdx.y;
     const long long b = a.pt_off[f], e = a.pt_off[f + 1];
     const double* xf = a.xf + 12 * f;
-    const double inv_tr = 1.0 / a.g.theta_r, inv_pr = 1.0 / a.g.phi_r;
+    const float inv_tr = (float)(1.0 / a.g.theta_r), inv_pr = (float)(1.0 / a.g.phi_r);
+    const float phi_off = (float)a.g.phi_offset;
     for (long long i = b + (long long)blockIdx.x * blockDim.x + threadIdx.x; i < e; i += (long long)gridDim.x * blockDim.x) {
         const T* p = pts + 3 * i;
         double px = (double)p[0], py = (double)p[1], pz = (double)p[2];
@@ -316,8 +323,8 @@ __global__ void __launch_bounds__(256) convert_overflow_kernel(ConvertArgs a, co
         double z = xform_coord(px, py, pz, xf[6], xf[7], xf[8], xf[11]);
         if (!(isfinite(x) && isfinite(y) && isfinite(z))) continue;
         double r = sqrt((x * x + y * y) + z * z);
-        long long u, v;
-        if (r <= 0.0 || (isfinite(r) && fast_bin(x, y, z, a.g, inv_tr, inv_pr, u, v))) continue;
+        int u, v;
+        if (r <= 0.0 || (isfinite(r) && fast_bin(x, y, z, a.g, inv_tr, inv_pr, phi_off, u, v))) continue;
         exact_point(a, px, py, pz, f);
     }
 }

@@ -733,7 +733,10 @@ __device__ bool test_tile_pair(bool active, const Chain& ch, const Geometry& g, 
     return pass;
 }
 
-__global__ void __launch_bounds__(FIT_WARPS * 32, 5) fit_pair_kernel(FitArgs A)
+#ifndef STPC_PAIR_MINB
+#define STPC_PAIR_MINB 5
+#endif
+__global__ void __launch_bounds__(FIT_WARPS * 32, STPC_PAIR_MINB) fit_pair_kernel(FitArgs A)
 {
     __shared__ double smem[FIT_WARPS][2][PG * 9];
     const Geometry& g = A.g;
@@ -1057,9 +1060,9 @@ void launch_fit_chains(const FitArgs& a, cudaStream_t s)
     if (warps <= 0) return;
     STPC_LAUNCH();
     if (a.g.tw * a.g.th <= PG) {
-        // work-stealing grid: ~5 resident blocks per SM, capped by the chain count
+        // work-stealing grid: STPC_PAIR_MINB resident blocks per SM, capped by the chain count
         long long pairs = (warps + 1) / 2;
-        long long blocks = std::min<long long>((pairs + FIT_WARPS - 1) / FIT_WARPS, 148LL * 5);
+        long long blocks = std::min<long long>((pairs + FIT_WARPS - 1) / FIT_WARPS, 148LL * STPC_PAIR_MINB);
         launch_zero(a.chain_counter, sizeof(unsigned), s);
         fit_pair_kernel<<<(unsigned)blocks, FIT_WARPS * 32, 0, s>>>(a);
     } else {
