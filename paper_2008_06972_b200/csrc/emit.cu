@@ -431,13 +431,18 @@ __global__ void __launch_bounds__(128) emit_fallback_kernel(EmitArgs E)
     }
 }
 
-// residual rows: warp per (frame, row) with residual pixels; lane per bitmap
-// word: offsets by warp scans, each lane writes its word's pixels in flat order
+// residual rows: warp per (frame, row) with residual pixels.  Lane per bitmap
+// word for the class masks (32 words at a time), then the emission is
+// transposed to lane per pixel, one word at a time: the previous residual
+// index comes from the word mask, varint offsets from a warp scan and code /
+// escape slots from popcounts, so every byte, code, escape store and range
+// load of the warp is coalesced.
 __global__ void __launch_bounds__(256) emit_residual_kernel(EmitArgs E)
 {
     const PlanArgs& A = E.p;
     const Geometry& g = A.g;
     const int lane = threadIdx.x & 31;
+    const unsigned lt = (1u << lane) - 1u;
     const long long wid = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
     const long long F = (long long)A.n_groups * A.n;
     if (wid >= F * g.h) return;
@@ -466,33 +471,31 @@ __global__ void __launch_bounds__(256) emit_residual_kernel(EmitArgs E)
             word_classes(g, crow, load_bits(vb, wd), rw.rb, rw.re, wd, res, tmp, fb);
             if (res) esc = load_bits(eb, wd) & res;
         }
-        const long long wfirst = res ? wd * 32 + (__ffs(res) - 1) : -1;
-        const long long wlast = res ? wd * 32 + (31 - __clz(res)) : -1;
-        long long prev = max(warp_excl_max(wlast, -1), last);
-        const int nres = __popc(res), nesc = __popc(esc);
-        const int len = res ? (nres - 1) + varint_len((uint32_t)(wfirst - prev)) : 0;
-        const int vinc = warp_incl_scan(len), cinc = warp_incl_scan(nres), einc = warp_incl_scan(nesc);
-        if (res) {
-            uint8_t* vo = vptr + vinc - len;
-            uint8_t* co = cptr + 2 * (cinc - nres);
-            uint8_t* eo = eptr + 4 * (einc - nesc);
-            uint32_t m = res;
-            while (m) {
-                const int j = __ffs(m) - 1;
-                m &= m - 1;
-                const long long idx = wd * 32 + j;
-                uint32_t d = (uint32_t)(idx - prev);
-                prev = idx;
+        unsigned todo = __ballot_sync(STPC_FULL, res != 0);
+        while (todo) {
+            const int j = __ffs(todo) - 1;
+            todo &= todo - 1;
+            const uint32_t m = __shfl_sync(STPC_FULL, res, j);
+            const uint32_t em = __shfl_sync(STPC_FULL, esc, j);
+            const long long w0px = (wbase + j) * 32;
+            const bool has = (m >> lane) & 1u;
+            const uint32_t below = m & lt;
+            const long long prev = below ? w0px + (31 - __clz(below)) : last;
+            const long long idx = w0px + lane;
+            uint32_t d = (uint32_t)(idx - prev);
+            const int len = has ? varint_len(d) : 0;
+            const int vinc = warp_incl_scan(len);
+            if (has) {
+                uint8_t* vo = vptr + (vinc - len);
                 while (d >= 0x80u) {
                     *vo++ = (uint8_t)((d & 0x7f) | 0x80);
                     d >>= 7;
                 }
-                *vo++ = (uint8_t)d;
+                *vo = (uint8_t)d;
                 const double r = img[idx];
                 uint32_t code = 0xFFFFu;
-                if ((esc >> j) & 1u) {
-                    put_f32(eo, (float)r);
-                    eo += 4;
+                if ((em >> lane) & 1u) {
+                    put_f32(eptr + 4 * __popc(em & lt), (float)r);
                 } else {
                     // rint(r / q) (bitstream.py:178): reciprocal estimate, exact
                     // IEEE division only when the estimate is near a .5 boundary
@@ -501,15 +504,13 @@ __global__ void __launch_bounds__(256) emit_residual_kernel(EmitArgs E)
                     code = fabs(fr - 0.5) > 1e-6 ? (uint32_t)(long long)rint(qa)
                                                  : (uint32_t)(long long)rint(r / E.range_quant);
                 }
-                put_u16(co, code);
-                co += 2;
+                put_u16(cptr + 2 * __popc(below), code);
             }
+            vptr += __shfl_sync(STPC_FULL, vinc, 31);
+            cptr += 2 * __popc(m);
+            eptr += 4 * __popc(em);
+            last = w0px + (31 - __clz(m));
         }
-        vptr += __shfl_sync(STPC_FULL, vinc, 31);
-        cptr += 2 * __shfl_sync(STPC_FULL, cinc, 31);
-        eptr += 4 * __shfl_sync(STPC_FULL, einc, 31);
-        const unsigned nz = __ballot_sync(STPC_FULL, res != 0);
-        if (nz) last = __shfl_sync(STPC_FULL, wlast, 31 - __clz(nz));
     }
 }
 
