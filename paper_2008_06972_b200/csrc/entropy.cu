@@ -213,84 +213,80 @@ __global__ void __launch_bounds__(PACK_THREADS) pack_write_kernel(EntropyArgs E)
     __shared__ uint8_t lens[256];
     __shared__ unsigned int codes[256];
     __shared__ unsigned int buf[PACK_CHUNK + 2];  // 32 bits per byte worst case
-    __shared__ long long wsum[PACK_THREADS / 32];
+    __shared__ int wsum[PACK_THREADS / 32];
     lens[threadIdx.x] = E.lens[grp * 256 + threadIdx.x];
     codes[threadIdx.x] = E.codes[grp * 256 + threadIdx.x];
-    for (int i = threadIdx.x; i < PACK_CHUNK + 2; i += PACK_THREADS) buf[i] = 0;
     __syncthreads();
     const uint8_t* p = E.payload + E.payload_off[grp];
     const long long O = E.chunk_bits[(long long)grp * E.max_chunks + c];  // chunk's first bit
     const int lead = (int)(O & 31);
-    // each thread owns PACK_PER_THREAD consecutive bytes
+    // each thread owns PACK_PER_THREAD consecutive bytes (a chunk holds at
+    // most 4096 * 32 bits: 32-bit counts throughout)
     const long long tb = b + (long long)threadIdx.x * PACK_PER_THREAD;
-    uint8_t sym[PACK_PER_THREAD];
-    int mybits = 0;
-    if (tb + PACK_PER_THREAD <= e) {  // 16-byte aligned (payload offsets are 16-aligned)
+    const int nq = (int)max(0LL, min((long long)PACK_PER_THREAD, e - tb));
+    uint32_t wv[4] = {0u, 0u, 0u, 0u};
+    if (nq == PACK_PER_THREAD) {  // 16-byte aligned (payload offsets are 16-aligned)
         const uint4 v4 = *reinterpret_cast<const uint4*>(p + tb);
-        const uint32_t wv[4] = {v4.x, v4.y, v4.z, v4.w};
-#pragma unroll
-        for (int q = 0; q < PACK_PER_THREAD; ++q) {
-            sym[q] = (uint8_t)(wv[q >> 2] >> (8 * (q & 3)));
-            mybits += lens[sym[q]];
-        }
+        wv[0] = v4.x;
+        wv[1] = v4.y;
+        wv[2] = v4.z;
+        wv[3] = v4.w;
     } else {
-#pragma unroll
-        for (int q = 0; q < PACK_PER_THREAD; ++q) {
-            long long i = tb + q;
-            sym[q] = i < e ? p[i] : 0;
-            mybits += i < e ? lens[sym[q]] : 0;
-        }
+        for (int q = 0; q < nq; ++q) wv[q >> 2] |= (uint32_t)p[tb + q] << (8 * (q & 3));
     }
-    long long inc = warp_incl_scan_ll(mybits);
+    int mybits = 0;
+#pragma unroll
+    for (int q = 0; q < PACK_PER_THREAD; ++q)
+        mybits += q < nq ? lens[(wv[q >> 2] >> (8 * (q & 3))) & 0xff] : 0;
+    const int inc = warp_incl_scan(mybits);
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     if (lane == 31) wsum[wid] = inc;
     __syncthreads();
-    long long wbase = 0;
-    for (int w = 0; w < wid; ++w) wbase += wsum[w];
-    long long pos = lead + wbase + inc - mybits;  // bit position in buf
-    // Assemble this thread's bits into whole big-endian words: words strictly
-    // inside [pos, pos + mybits) belong to this thread alone (plain stores);
-    // only the first and last word can be shared with a neighbour (atomicOr).
-    {
-        const int w0 = (int)(pos >> 5);
-        int fill = (int)(pos & 31);  // bits already occupied in the current word
-        int wi = w0;
+    int wbase = 0, total = 0;
+#pragma unroll
+    for (int w = 0; w < PACK_THREADS / 32; ++w) {
+        const int x = wsum[w];
+        wbase += w < wid ? x : 0;
+        total += x;
+    }
+    // zero only the words this chunk fills (~6 bits per byte, not the
+    // 32-bit worst case the buffer is sized for)
+    const int nwords = (lead + total + 31) >> 5;
+    for (int i = threadIdx.x; i < nwords + 1; i += PACK_THREADS) buf[i] = 0;
+    __syncthreads();
+    // Big-endian word assembly: the accumulator starts with `fill` zero bits
+    // (the neighbour's share of the first word); a code is <= 32 bits and
+    // fewer than 32 bits are pending, so each symbol emits at most one word.
+    // Words strictly inside this thread's bits are plain stores; the first
+    // and the last can be shared with a neighbour (atomicOr).
+    if (nq > 0) {
+        const int pos = lead + wbase + inc - mybits;
+        int wi = pos >> 5;
+        const int w0 = wi;
         unsigned long long acc = 0;
-        int nacc = 0;
-        unsigned int cur = 0;
+        int nacc = pos & 31;
 #pragma unroll
         for (int q = 0; q < PACK_PER_THREAD; ++q) {
-            long long i = tb + q;
-            if (i >= e) break;
-            const int l = lens[sym[q]];
-            acc = (acc << l) | codes[sym[q]];
-            nacc += l;
-            while (fill + nacc >= 32) {
-                const int k = 32 - fill;
-                const unsigned int bits = (unsigned int)(acc >> (nacc - k)) & (k == 32 ? 0xffffffffu : ((1u << k) - 1u));
-                nacc -= k;
-                acc &= (nacc ? ((1ull << nacc) - 1ull) : 0ull);
-                cur |= bits;
-                if (wi == w0) atomicOr(&buf[wi], cur);
-                else buf[wi] = cur;
-                wi += 1;
-                fill = 0;
-                cur = 0;
+            if (q < nq) {
+                const unsigned s = (wv[q >> 2] >> (8 * (q & 3))) & 0xff;
+                const int l = lens[s];
+                acc = (acc << l) | codes[s];
+                nacc += l;
+                if (nacc >= 32) {
+                    nacc -= 32;
+                    const unsigned int word = (unsigned int)(acc >> nacc);
+                    if (wi == w0) atomicOr(&buf[wi], word);
+                    else buf[wi] = word;
+                    ++wi;
+                }
             }
         }
-        if (nacc > 0) {
-            cur |= (unsigned int)(acc << (32 - fill - nacc));
-            atomicOr(&buf[wi], cur);
-        }
+        if (nacc > 0) atomicOr(&buf[wi], (unsigned int)(acc << (32 - nacc)));
     }
     __syncthreads();
-    long long total = 0;
-    for (int w = 0; w < PACK_THREADS / 32; ++w) total += wsum[w];
-    const int nwords = (int)((lead + total + 31) >> 5);
     unsigned int* gw = reinterpret_cast<unsigned int*>(E.blobs + E.blob_off[grp] + HDR) + (O >> 5);
     for (int i = threadIdx.x; i < nwords; i += PACK_THREADS) {
-        unsigned int be = buf[i];
-        unsigned int le = __byte_perm(be, 0, 0x0123);
+        const unsigned int le = __byte_perm(buf[i], 0, 0x0123);
         if (i == 0 || i == nwords - 1) {
             if (le) atomicOr(gw + i, le);
         } else {
@@ -345,25 +341,40 @@ __device__ __forceinline__ unsigned int x8nmodp(unsigned long long nbytes)
 }
 
 // slice-by-4 tables for the reflected CRC (T[0] is the classic byte table)
-__device__ __forceinline__ void crc_tables4(unsigned int (*T)[256])
+// Slice-by-4 CRC-32 tables (zlib polynomial), built at compile time and
+// copied into shared memory per block with coalesced loads.
+struct CrcTab4 {
+    unsigned int t[4][256];
+};
+constexpr CrcTab4 make_crc_tab4()
 {
-    for (int i = threadIdx.x; i < 256; i += blockDim.x) {
+    CrcTab4 r{};
+    for (unsigned int i = 0; i < 256; ++i) {
         unsigned int c = i;
-        for (int k = 0; k < 8; ++k) c = c & 1 ? (c >> 1) ^ 0xedb88320u : c >> 1;
-        T[0][i] = c;
+        for (int k = 0; k < 8; ++k) c = (c & 1u) ? (c >> 1) ^ 0xedb88320u : c >> 1;
+        r.t[0][i] = c;
     }
-    __syncthreads();
-    for (int i = threadIdx.x; i < 256; i += blockDim.x) {
-        unsigned int c = T[0][i];
+    for (unsigned int i = 0; i < 256; ++i) {
+        unsigned int c = r.t[0][i];
         for (int k = 1; k < 4; ++k) {
-            c = (c >> 8) ^ T[0][c & 0xff];
-            T[k][i] = c;
+            c = (c >> 8) ^ r.t[0][c & 0xff];
+            r.t[k][i] = c;
         }
     }
+    return r;
+}
+__device__ const CrcTab4 kCrcTab4 = make_crc_tab4();
+
+__device__ __forceinline__ void crc_tables4(unsigned int (*T)[256])
+{
+    const unsigned int* src = &kCrcTab4.t[0][0];
+    unsigned int* dst = &T[0][0];
+    for (int i = threadIdx.x; i < 1024; i += blockDim.x) dst[i] = __ldg(src + i);
     __syncthreads();
 }
 
-constexpr int CRC_WARPS = 4;
+constexpr int CRC_WARPS = 8;
+constexpr int CRC_SEGS_PER_WARP = 4;  // segments per warp (amortises the table copy)
 
 // grid (segments / CRC_WARPS, groups): warp w of block x handles segment
 // x*CRC_WARPS + w = 32 pieces of 256 B of the encoded payload, counted from
@@ -371,41 +382,59 @@ constexpr int CRC_WARPS = 4;
 // in by crc_finish).  The last segment's pieces are end-aligned in the
 // 32-slot tree: the missing leading slots act as a zero prefix, which leaves
 // an init-0 CRC register unchanged.
+// Each lane folds one 256-byte piece; the warp stages the pieces through
+// shared memory in 4 rounds of 64 bytes per piece (two pieces per load
+// instruction, every sector fully used) into a padded [32][17] word tile, so
+// the lane-per-piece fold reads conflict-free shared memory instead of
+// 256-byte-strided global words.
+constexpr int CRC_SUB = 64;  // bytes per piece per staging round
 __global__ void __launch_bounds__(CRC_WARPS * 32) crc_segment_kernel(EntropyArgs E, CrcConsts K)
 {
     __shared__ unsigned int T[4][256];
+    __shared__ unsigned int stg[CRC_WARPS][32][CRC_SUB / 4 + 1];
     crc_tables4(T);
     const int grp = blockIdx.y;
-    const int lane = threadIdx.x & 31;
-    const long long sgi = (long long)blockIdx.x * CRC_WARPS + (threadIdx.x >> 5);
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const long long L = E.enc_len[grp];
     const long long npieces = L / CRC_PIECE;
     const long long nseg = (npieces + 31) / 32;
-    if (sgi >= nseg) return;
-    const long long first = sgi * 32;
-    const int np = (int)min(32LL, npieces - first);
-    const int slot_piece = lane - (32 - np);  // end-aligned
-    const uint8_t* enc = E.blobs + E.blob_off[grp] + HDR;  // 4-byte aligned
-    unsigned int crc = 0;
-    if (slot_piece >= 0) {
-        const uint32_t* w = reinterpret_cast<const uint32_t*>(enc + (first + slot_piece) * CRC_PIECE);
-#pragma unroll 8
-        for (int i = 0; i < CRC_PIECE / 4; ++i) {
-            const unsigned int x = crc ^ __ldg(w + i);
-            crc = T[3][x & 0xff] ^ T[2][(x >> 8) & 0xff] ^ T[1][(x >> 16) & 0xff] ^ T[0][x >> 24];
-        }
-    }
-    // tree: level l merges blocks of 2^l pieces (256 * 2^l bytes)
+    const uint32_t* enc = reinterpret_cast<const uint32_t*>(E.blobs + E.blob_off[grp] + HDR);  // 4-byte aligned
+    unsigned int (*tile)[CRC_SUB / 4 + 1] = stg[wib];
+    for (int rep = 0; rep < CRC_SEGS_PER_WARP; ++rep) {
+        const long long sgi = ((long long)blockIdx.x * CRC_SEGS_PER_WARP + rep) * CRC_WARPS + wib;
+        if (sgi >= nseg) return;
+        const long long first = sgi * 32;
+        const int np = (int)min(32LL, npieces - first);
+        const int slot_piece = lane - (32 - np);  // end-aligned
+        unsigned int crc = 0;
+        for (int r = 0; r < CRC_PIECE / CRC_SUB; ++r) {
 #pragma unroll
-    for (int l = 0; l < 5; ++l) {
-        const unsigned int right = __shfl_down_sync(STPC_FULL, crc, 1 << l);
-        if ((lane & ((2 << l) - 1)) == 0) crc = multmodp(K.x256[l], crc) ^ right;
+            for (int it = 0; it < CRC_SUB / 4; ++it) {  // 32 pieces x 16 words, 2 pieces per load
+                const int widx = it * 32 + lane;
+                const int k = widx >> 4, wd = widx & 15;
+                const int pk = k - (32 - np);
+                tile[k][wd] = pk >= 0 ? __ldg(enc + ((first + pk) * CRC_PIECE + r * CRC_SUB) / 4 + wd) : 0u;
+            }
+            __syncwarp();
+            if (slot_piece >= 0) {
+#pragma unroll
+                for (int i = 0; i < CRC_SUB / 4; ++i) {
+                    const unsigned int x = crc ^ tile[lane][i];
+                    crc = T[3][x & 0xff] ^ T[2][(x >> 8) & 0xff] ^ T[1][(x >> 16) & 0xff] ^ T[0][x >> 24];
+                }
+            }
+            __syncwarp();
+        }
+        // tree: level l merges blocks of 2^l pieces (256 * 2^l bytes)
+#pragma unroll
+        for (int l = 0; l < 5; ++l) {
+            const unsigned int right = __shfl_down_sync(STPC_FULL, crc, 1 << l);
+            if ((lane & ((2 << l) - 1)) == 0) crc = multmodp(K.x256[l], crc) ^ right;
+        }
+        if (lane == 0) E.seg_crc[(long long)grp * E.max_segs + sgi] = crc;
     }
-    if (lane == 0) E.seg_crc[(long long)grp * E.max_segs + sgi] = crc;
 }
 
-// block per group: combine segments (each 8 KB, the last end-aligned), fold
-// in the tail, apply the 0xFFFFFFFF init/xorout, write the header.
 __global__ void crc_finish_kernel(EntropyArgs E, CrcConsts K)
 {
     const int grp = blockIdx.x;
@@ -479,7 +508,8 @@ void launch_crc(const EntropyArgs& E, cudaStream_t s)
     K.seg = h_x8nmodp(32ull * CRC_PIECE);
     if (E.max_segs > 0) {
         STPC_LAUNCH();
-        crc_segment_kernel<<<dim3((E.max_segs + CRC_WARPS - 1) / CRC_WARPS, E.G), CRC_WARPS * 32, 0, s>>>(E, K);
+        const long long per_block = (long long)CRC_WARPS * CRC_SEGS_PER_WARP;
+        crc_segment_kernel<<<dim3((unsigned)((E.max_segs + per_block - 1) / per_block), E.G), CRC_WARPS * 32, 0, s>>>(E, K);
     }
     STPC_LAUNCH();
     crc_finish_kernel<<<E.G, 64, 0, s>>>(E, K);
