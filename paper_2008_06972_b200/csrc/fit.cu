@@ -352,18 +352,22 @@ __global__ void __launch_bounds__(START_TPB) start_tiles_staged_kernel(FitArgs A
     const double* st = s_st + threadIdx.x * (TW + 1);
     const double* ct = s_ct + threadIdx.x * (TW + 1);
     const int cols = min(TW, g.w - t * TW);
+    // Branch-free ordered fold: an invalid pixel (or a column past the image
+    // edge) contributes +0.0 to every sum, which is exact -- a running sum
+    // that starts at +0.0 never becomes -0.0 -- so the lanes of a warp stay
+    // converged through data-dependent validity.
     double sm[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
     for (int dv = 0; dv < rows; ++dv) {
         const double sp = __ldg(A.tg.sin_p + v0 + dv), cp = __ldg(A.tg.cos_p + v0 + dv);
 #pragma unroll
         for (int du = 0; du < TW; ++du) {
             const double r = rr[dv * TW + du];
-            if (du >= cols || !isfinite(r)) continue;
+            const bool valid = du < cols && isfinite(r);
             const double dx = sp * st[du], dy = sp * ct[du], dz = cp;
-            const double x = r * dx, y = r * dy, z = r * dz;
+            const double x = valid ? r * dx : 0.0, y = valid ? r * dy : 0.0, z = valid ? r * dz : 0.0;
             sm[0] += y * y; sm[1] += y * z; sm[2] += z * z;
             sm[3] += y;     sm[4] += z;     sm[5] += x * y;
-            sm[6] += x * z; sm[7] += x;     sm[8] += 1.0;
+            sm[6] += x * z; sm[7] += x;     sm[8] += valid ? 1.0 : 0.0;
         }
     }
     double a, b, c;
@@ -374,28 +378,33 @@ __global__ void __launch_bounds__(START_TPB) start_tiles_staged_kernel(FitArgs A
         a = f32_round(a);
         b = f32_round(b);
         c = f32_round(c);
-        // verdict and certificate statistics in one pass
-        for (int dv = 0; dv < rows && ok; ++dv) {
+        // verdict and certificate statistics in one branch-free pass: the
+        // verdict is the AND over valid pixels (the reference's early return
+        // gives the same answer); masked pixels leave every statistic alone
+        for (int dv = 0; dv < rows; ++dv) {
             const double sp = __ldg(A.tg.sin_p + v0 + dv), cp = __ldg(A.tg.cos_p + v0 + dv);
 #pragma unroll
             for (int du = 0; du < TW; ++du) {
                 const double r = rr[dv * TW + du];
-                if (du >= cols || !isfinite(r)) continue;
+                const bool valid = du < cols && isfinite(r);
                 const double dy = sp * ct[du];
                 const double den = (sp * st[du] + a * dy) + b * cp;
                 const double ad = fabs(den);
-                if (ad < STPC_PARALLEL_EPS) { ok = false; break; }
-                const double r_hat = c / den;
-                if (r_hat <= 0.0 || r_hat > A.r_max || fabs(r - r_hat) > A.tau) { ok = false; break; }
-                m = fmin(m, A.tau - fabs(r - r_hat));
-                dmin = fmin(dmin, ad);
-                rmin = fmin(rmin, r_hat);
-                rmax = fmax(rmax, r_hat);
+                const bool par = ad < STPC_PARALLEL_EPS;
+                const double r_hat = c / (par ? 1.0 : den);
+                const double err = fabs(r - r_hat);
+                const bool bad = par || r_hat <= 0.0 || r_hat > A.r_max || err > A.tau;
+                ok = ok && !(valid && bad);
+                const bool use = valid && !bad;
                 const double yh = r_hat * dy, zh = r_hat * cp;
-                ylo = fmin(ylo, yh);
-                yhi = fmax(yhi, yh);
-                zlo = fmin(zlo, zh);
-                zhi = fmax(zhi, zh);
+                m = use ? fmin(m, A.tau - err) : m;
+                dmin = use ? fmin(dmin, ad) : dmin;
+                rmin = use ? fmin(rmin, r_hat) : rmin;
+                rmax = use ? fmax(rmax, r_hat) : rmax;
+                ylo = use ? fmin(ylo, yh) : ylo;
+                yhi = use ? fmax(yhi, yh) : yhi;
+                zlo = use ? fmin(zlo, zh) : zlo;
+                zhi = use ? fmax(zhi, zh) : zhi;
             }
         }
     }
@@ -409,9 +418,6 @@ __global__ void __launch_bounds__(START_TPB) start_tiles_staged_kernel(FitArgs A
                         __double2float_ru(zhi));
 }
 
-#ifndef STPC_START_MINB
-#define STPC_START_MINB 2
-#endif
 #ifndef STPC_START_MINB
 #define STPC_START_MINB 2
 #endif
