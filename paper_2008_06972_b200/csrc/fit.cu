@@ -742,6 +742,26 @@ __device__ bool test_tile_pair(bool active, const Chain& ch, const Geometry& g, 
 #ifndef STPC_PAIR_MINB
 #define STPC_PAIR_MINB 5
 #endif
+#ifdef STPC_FIT_STATS
+// diagnostic build only (tools/fit_stats.py): chain-step counters
+__device__ unsigned long long g_fit_stats[8];
+#define FIT_STAT(i, pred)                                                               \
+    do {                                                                                \
+        const unsigned m_ = __ballot_sync(STPC_FULL, (pred));                          \
+        if ((threadIdx.x & 31) == 0 && m_) atomicAdd(&g_fit_stats[i], (unsigned long long)__popc(m_)); \
+    } while (0)
+extern "C" int stpc_debug_fit_stats(unsigned long long* out)
+{
+    return cudaMemcpyFromSymbol(out, g_fit_stats, sizeof(g_fit_stats)) == cudaSuccess ? 0 : 1;
+}
+extern "C" int stpc_debug_fit_stats_reset()
+{
+    unsigned long long z[8] = {0};
+    return cudaMemcpyToSymbol(g_fit_stats, z, sizeof(z)) == cudaSuccess ? 0 : 1;
+}
+#else
+#define FIT_STAT(i, pred) ((void)0)
+#endif
 __global__ void __launch_bounds__(FIT_WARPS * 32, STPC_PAIR_MINB) fit_pair_kernel(FitArgs A)
 {
     __shared__ double smem[FIT_WARPS][2][PG * 9];
@@ -926,6 +946,9 @@ __global__ void __launch_bounds__(FIT_WARPS * 32, STPC_PAIR_MINB) fit_pair_kerne
             pf_t = t + 1;
         }
         // ---- (3) solve: starts (verdict known ok) and growing chains with new pixels
+        FIT_STAT(0, live && gl == 0);                      // chain steps
+        FIT_STAT(1, live && !grow && gl == 0);             // start steps
+        FIT_STAT(2, live && grow && cnt == 0 && gl == 0);  // empty growth steps
         const bool need = live && (!grow || cnt > 0);
         double na = 0.0, nb = 0.0, nc = 0.0;
         bool ok = false;
@@ -945,10 +968,14 @@ __global__ void __launch_bounds__(FIT_WARPS * 32, STPC_PAIR_MINB) fit_pair_kerne
         bool pass = false;
         if (__any_sync(STPC_FULL, testing)) {
             pass = test_tile_pair(testing, ch, g, A.tg, t, na, nb, nc, A.tau, A.r_max);
+            FIT_STAT(5, testing && gl == 0);        // growth tests
+            FIT_STAT(6, testing && pass && gl == 0);  // growth tests passed (new tile)
             int base = s;
             while (__any_sync(STPC_FULL, pass && base < t)) {
                 const int j = base + gl;
                 const bool weak = pass && j < t && !cert_holds(ch.cert, j, na, nb, nc, A.r_max);
+                FIT_STAT(3, pass && j < t);  // certificate checks
+                FIT_STAT(4, weak);           // weak certificates -> full re-test
                 unsigned wm = (__ballot_sync(STPC_FULL, weak) & gmask) >> (sub * 16);
                 while (__any_sync(STPC_FULL, pass && wm != 0)) {
                     const bool act = pass && wm != 0;
