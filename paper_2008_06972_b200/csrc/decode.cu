@@ -25,6 +25,7 @@
 #include <algorithm>
 #include <cstring>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "kernels.cuh"
@@ -1096,9 +1097,37 @@ struct stpc_decoder {
     DevBuf sel, tmap, res, pstat, outr, trig, xfi, blkcnt, fcnt, foff, failed, pts;
     std::vector<unsigned long long> h_pstat;
     const double* last_points = nullptr;
+    // host output path: pinned double buffer + copy threads
+    HostBuf stage[2];
+    cudaEvent_t ev[2] = {nullptr, nullptr};
+    ~stpc_decoder()
+    {
+        for (auto& e : ev)
+            if (e) cudaEventDestroy(e);
+    }
 };
 
 namespace {
+
+// memcpy with the destination's page faults spread over host threads (a
+// fresh numpy array is first touched here)
+void parallel_memcpy(uint8_t* dst, const uint8_t* src, size_t n)
+{
+    const size_t min_part = 8u << 20;
+    unsigned nt = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+    nt = (unsigned)std::max<size_t>(1, std::min<size_t>(nt, n / min_part));
+    if (nt <= 1) {
+        std::memcpy(dst, src, n);
+        return;
+    }
+    std::vector<std::thread> th;
+    const size_t part = (n + nt - 1) / nt;
+    for (unsigned t = 0; t < nt; ++t) {
+        const size_t b = t * part, e = std::min(n, b + part);
+        if (b < e) th.emplace_back([=] { std::memcpy(dst + b, src + b, e - b); });
+    }
+    for (auto& x : th) x.join();
+}
 
 // header checks of deserialize in the reference's order (bitstream.py:398-409)
 int check_header(const uint8_t* hdr, long long blob_len, long long& raw_len, long long& enc_len)
@@ -1380,8 +1409,30 @@ int stpc_decoder_points(stpc_decoder* d, double* dst, int32_t dst_on_device, int
         d->G, tg, d->outr.as<double>(), d->pstat.as<unsigned long long>(), d->blkcnt.as<int>(),
         d->foff.as<long long>(), d->xfi.as<double>(), out);
     DCK(cudaGetLastError());
-    if (!dst_on_device && d->total > 0)
-        DCK(cudaMemcpyAsync(dst, out, sizeof(double) * 3 * d->total, cudaMemcpyDeviceToHost, s));
+    if (!dst_on_device && d->total > 0) {
+        // D2H through two pinned 128 MB stages; the copy of chunk k into the
+        // caller's (pageable) array overlaps the D2H of chunk k+1
+        const size_t total_bytes = sizeof(double) * 3 * (size_t)d->total;
+        const size_t CH = 128u << 20;
+        const size_t nch = (total_bytes + CH - 1) / CH;
+        for (int i = 0; i < 2; ++i) {
+            DRET(d->stage[i].ensure(std::min(CH, total_bytes)));
+            if (!d->ev[i]) DCK(cudaEventCreateWithFlags(&d->ev[i], cudaEventDisableTiming));
+        }
+        auto issue = [&](size_t k) -> cudaError_t {
+            const size_t o = k * CH, n = std::min(CH, total_bytes - o);
+            cudaError_t e = cudaMemcpyAsync(d->stage[k & 1].p, (const uint8_t*)out + o, n, cudaMemcpyDeviceToHost, s);
+            if (e == cudaSuccess) e = cudaEventRecord(d->ev[k & 1], s);
+            return e;
+        };
+        DCK(issue(0));
+        for (size_t k = 0; k < nch; ++k) {
+            DCK(cudaEventSynchronize(d->ev[k & 1]));
+            if (k + 1 < nch) DCK(issue(k + 1));
+            const size_t o = k * CH, n = std::min(CH, total_bytes - o);
+            parallel_memcpy((uint8_t*)dst + o, d->stage[k & 1].as<uint8_t>(), n);
+        }
+    }
     d->last_points = out;
     DCK(cudaStreamSynchronize(s));
     return STPC_OK;
