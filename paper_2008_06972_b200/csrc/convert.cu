@@ -14,6 +14,8 @@
 // computes the same minimum independent of thread order; the optional second
 // pass resolves the winning index with an atomicMin over indices whose range
 // equals the minimum (identical to "first index wins").
+#include <cstring>
+
 #include "kernels.cuh"
 #include "dd.cuh"
 
@@ -424,11 +426,37 @@ void launch_convert_win(const ConvertArgs& a, int max_pts, cudaStream_t s)
     win_finalize_kernel<<<blocks, 256, 0, s>>>(a.win, a.best, n);
 }
 
+// Escape test without a division: rint(r / q) outside [1, 0xFFFF)
+// (bitstream.py:176-182) <=> fl(r / q) <= 0.5 or fl(r / q) > 65534.5 (round
+// half to even: rint(0.5) = 0, rint(65534.5) = 65534).  fl(r / q) is
+// monotonic in r for q > 0, so both sets are half-lines in r, bounded by the
+// largest doubles t_lo / t_hi with fl(t / q) <= 0.5 / <= 65534.5, found once
+// on the host by bisection over the bit patterns with IEEE division.
+static double largest_r_with_quot_le(double q, double x)
+{
+    unsigned long long lo = 0, hi = 0x7ff0000000000000ull;  // [+0, +inf]
+    while (hi - lo > 1) {
+        const unsigned long long mid = lo + (hi - lo) / 2;
+        double r;
+        std::memcpy(&r, &mid, 8);
+        if (r / q <= x) lo = mid;
+        else hi = mid;
+    }
+    double r;
+    std::memcpy(&r, &lo, 8);
+    return r;
+}
+
+void escape_thresholds(double range_quant, double& t_lo, double& t_hi)
+{
+    t_lo = largest_r_with_quot_le(range_quant, 0.5);
+    t_hi = largest_r_with_quot_le(range_quant, 65534.5);
+}
+
 // One warp per 32 bitmap words (1024 pixels) of one frame: ballot the
 // validity / escape predicates and store packbits-ordered words.
-// Escape: rint(r / range_quant) outside [1, 0xFFFF) (bitstream.py:176-182).
 __global__ void __launch_bounds__(256) bitmap_kernel(const double* __restrict__ best, Geometry g,
-                                                     double quant, uint8_t* vbits, uint8_t* ebits,
+                                                     double t_lo, double t_hi, uint8_t* vbits, uint8_t* ebits,
                                                      long long* fstats)
 {
     const int f = blockIdx.y;
@@ -439,20 +467,18 @@ __global__ void __launch_bounds__(256) bitmap_kernel(const double* __restrict__ 
     const double* img = best + (long long)f * g.P;
     uint32_t my_v = 0, my_e = 0;
     int nvalid = 0;
+#pragma unroll 8
     for (int i = 0; i < 32; ++i) {
-        long long pix = (wbase + i) * 32 + lane;
-        bool valid = false, esc = false;
-        if (pix < g.P) {
-            double r = img[pix];
-            valid = isfinite(r);
-            if (valid) {
-                double q = rint(r / quant);
-                esc = (q < 1.0) || (q >= 65535.0);
-            }
+        const long long pix = (wbase + i) * 32 + lane;
+        const double r = pix < g.P ? __ldg(img + pix) : __longlong_as_double(0x7ff0000000000000ll);
+        const bool valid = isfinite(r);
+        const bool esc = valid && (r <= t_lo || r > t_hi);
+        const uint32_t mv = __ballot_sync(STPC_FULL, valid);
+        const uint32_t me = __ballot_sync(STPC_FULL, esc);
+        if (lane == i) {
+            my_v = mv;
+            my_e = me;
         }
-        uint32_t mv = __ballot_sync(STPC_FULL, valid);
-        uint32_t me = __ballot_sync(STPC_FULL, esc);
-        if (lane == i) { my_v = mv; my_e = me; }
         nvalid += __popc(mv);
     }
     if (wbase + lane < words) {
@@ -467,11 +493,13 @@ void launch_bitmaps(const double* best, int n_frames, const Geometry& g, double 
                     uint8_t* vbits, uint8_t* ebits, long long* fstats, cudaStream_t s)
 {
     if (n_frames <= 0) return;
+    double t_lo, t_hi;
+    escape_thresholds(range_quant, t_lo, t_hi);
     long long words = g.pbs / 4;
     long long warps = (words + 31) / 32;
     dim3 grid((unsigned)((warps + 7) / 8), n_frames);
     STPC_LAUNCH();
-    bitmap_kernel<<<grid, 256, 0, s>>>(best, g, range_quant, vbits, ebits, fstats);
+    bitmap_kernel<<<grid, 256, 0, s>>>(best, g, t_lo, t_hi, vbits, ebits, fstats);
 }
 
 }  // namespace stpc
