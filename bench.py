@@ -303,12 +303,14 @@ def host_cores():
 
 # ------------------------------------------------------------------- roofline
 
-def algorithmic_bytes(stage, cfg, n, G, npts):
-    """SURVEY.md §8(d) per-unit figures x the units one launch processes."""
+def algorithmic_bytes(stage, cfg, n, G, npts, raw_bytes=0, blob_bytes=0):
+    """SURVEY.md §8(d) per-unit figures x the units one launch processes
+    (bytes a kernel must move at minimum; +inf fills, atomics and padding are
+    not algorithmic)."""
     P = cfg.w * cfg.h
     F = G * n
     if stage == "convert":
-        return 12 * npts + 8 * P * F + P / 8 * F
+        return 12 * npts + 8 * P * F
     if stage in ("fit_key", "start_key"):
         return G * (8 * P + P / 8)
     if stage in ("fit_p", "start_p"):
@@ -317,6 +319,14 @@ def algorithmic_bytes(stage, cfg, n, G, npts):
         return G * (n - 1) * (8 * P + P / 8)
     if stage == "bitmaps":
         return F * (8 * P + 2 * P / 8)
+    if stage == "emit":  # K3c compaction: read ranges + masks, write the raw payload
+        return F * (8 * P + P / 8) + raw_bytes
+    if stage == "huffman":  # histogram of the raw payload
+        return raw_bytes
+    if stage == "pack":  # raw payload read twice (bit counts, packing), packed stream written
+        return 2 * raw_bytes + blob_bytes
+    if stage == "crc":
+        return blob_bytes
     return None
 
 
@@ -343,6 +353,23 @@ def ncu_traffic(stage, args, G):
                 "traffic_source": "profiles/r1_ncu_full_1024groups.json (ncu --set full, same workload)"}
     except Exception:
         return {"traffic": None}
+
+
+def fit_utilisation(args, G):
+    """SM / FP64-pipe utilisation of the fitting kernel (BASELINE asks for it
+    instead of an HBM fraction) from the committed ncu capture."""
+    if args.config != 4 or G != 1024 or args.tile or args.tau:
+        return None
+    try:
+        rows = [r for r in json.load(open(os.path.join(ROOT, "profiles", "r1_ncu_full_1024groups.json")))
+                if r["kernel"] == "fit_pair_kernel"]
+        r = rows[-1]
+        return {"kernel": "fit_pair_kernel (P frames)", "sm_throughput_pct": r["sm_throughput_pct"],
+                "fp64_pipe_pct": r["fp64_pipe_pct"], "ipc": r["ipc"],
+                "achieved_occupancy_pct": r["achieved_occupancy_pct"],
+                "source": "profiles/r1_ncu_full_1024groups.json (ncu --set full)"}
+    except Exception:
+        return None
 
 
 def main():
@@ -500,10 +527,19 @@ def main():
                 "peak_source": peak_src, "unit": "GB/s", "traffic": None}
     roofline["frac"] = roofline["achieved"] / peak if roofline["achieved"] else None
     roofline.update(ncu_traffic(dom, args, G))
-    conv_ms = float(stage_ms[names.index("convert")])
-    conv_ab = algorithmic_bytes("convert", cfg, n, G, npts)
-    roofline["convert"] = {"ms": conv_ms, "achieved": conv_ab / (conv_ms / 1e3) / 1e9,
-                           "frac": conv_ab / (conv_ms / 1e3) / 1e9 / peak}
+    # per-stage achieved fraction of the HBM roofline (BASELINE: "per-kernel
+    # achieved fraction"; conversion and compaction called out)
+    stages = {}
+    for nm, v in zip(names, stage_ms):
+        b = algorithmic_bytes(nm, cfg, n, G, npts, int(raw.sum()), blob_bytes)
+        if b and v > 0:
+            gbs = b / (float(v) / 1e3) / 1e9
+            stages[nm] = {"ms": round(float(v), 4), "algorithmic_GB": round(b / 1e9, 3), "achieved": round(gbs, 1),
+                          "frac": round(gbs / peak, 4)}
+    roofline["stages"] = stages
+    roofline["convert"] = stages.get("convert")
+    roofline["compaction"] = stages.get("emit")
+    roofline["fit_utilisation"] = fit_utilisation(args, G)
 
     # ---------------- CPU baseline (rank 0, N=1)
     cpu = None
