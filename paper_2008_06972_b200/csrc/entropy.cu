@@ -12,26 +12,42 @@ namespace stpc {
 
 // ---------------------------------------------------------------- histogram
 // grid (chunks, groups); 256-bin shared histogram per block.
+// Byte histogram of the raw payload (np.bincount, huffman.py:112): 64 KB per
+// block read as 16-byte vectors; 16 private sub-histograms (per warp x lane
+// parity) keep same-bin collisions of the skewed payload bytes low.
+constexpr int HIST_CHUNK = 65536;
 __global__ void __launch_bounds__(256) histogram_kernel(EntropyArgs E)
 {
-    __shared__ unsigned int h[256];
+    __shared__ unsigned int h[16][256];
     const int grp = blockIdx.y;
-    h[threadIdx.x] = 0;
+    for (int i = threadIdx.x; i < 16 * 256; i += 256) (&h[0][0])[i] = 0;
     __syncthreads();
     const long long len = E.payload_len[grp];
-    const uint8_t* p = E.payload + E.payload_off[grp];
-    const long long chunk = 16384;
-    long long b = (long long)blockIdx.x * chunk;
-    long long e = min(b + chunk, len);
-    for (long long i = b + threadIdx.x; i < e; i += blockDim.x) atomicAdd(&h[p[i]], 1u);
+    const uint8_t* p = E.payload + E.payload_off[grp];  // 16-byte aligned
+    const long long b = (long long)blockIdx.x * HIST_CHUNK;
+    const long long e = min(b + HIST_CHUNK, len);
+    unsigned int* hh = h[((threadIdx.x >> 5) << 1) | (threadIdx.x & 1)];
+    for (long long i = b + 16LL * threadIdx.x; i < e; i += 16LL * 256) {
+        if (i + 16 <= e) {
+            const uint4 v = *reinterpret_cast<const uint4*>(p + i);
+            const unsigned w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+            for (int q = 0; q < 16; ++q) atomicAdd(&hh[(w[q >> 2] >> (8 * (q & 3))) & 0xff], 1u);
+        } else {
+            for (long long j = i; j < e; ++j) atomicAdd(&hh[p[j]], 1u);
+        }
+    }
     __syncthreads();
-    if (h[threadIdx.x]) atomicAdd(&E.hist[grp * 256 + threadIdx.x], h[threadIdx.x]);
+    unsigned int t = 0;
+#pragma unroll
+    for (int k = 0; k < 16; ++k) t += h[k][threadIdx.x];
+    if (t) atomicAdd(&E.hist[grp * 256 + threadIdx.x], t);
 }
 
 void launch_histogram(const EntropyArgs& E, int max_payload, cudaStream_t s)
 {
     if (E.G <= 0) return;
-    dim3 grid((max_payload + 16383) / 16384 > 0 ? (max_payload + 16383) / 16384 : 1, E.G);
+    dim3 grid((max_payload + HIST_CHUNK - 1) / HIST_CHUNK > 0 ? (max_payload + HIST_CHUNK - 1) / HIST_CHUNK : 1, E.G);
     STPC_LAUNCH();
     histogram_kernel<<<grid, 256, 0, s>>>(E);
 }
