@@ -339,17 +339,37 @@ __global__ void emit_header_kernel(EmitArgs E)
 }
 
 // validity bitmaps: frame bytes [0, PB) copied into the payload
-__global__ void emit_bitmaps_kernel(EmitArgs E)
+// Validity bitmaps into the payload (packbits, bitstream.py:219-220): block
+// per frame; the destination sits at an arbitrary byte offset, so head and
+// tail bytes are stored singly and every aligned 32-bit destination word is
+// assembled from two source words by a funnel shift.
+__global__ void __launch_bounds__(256) emit_bitmaps_kernel(EmitArgs E)
 {
     const PlanArgs& A = E.p;
     const Geometry& g = A.g;
-    const int f = blockIdx.y;
+    const int f = blockIdx.x;
     const int grp = f / A.n, i = f % A.n;
     const long long PB = (g.P + 7) / 8;
     uint8_t* out = E.payload + A.payload_off[grp] + 57 + 48LL * A.n + PB * i;
-    const uint8_t* src = A.vbits + (long long)f * g.pbs;
-    for (long long b = (long long)blockIdx.x * blockDim.x + threadIdx.x; b < PB; b += (long long)gridDim.x * blockDim.x)
-        out[b] = src[b];
+    const uint8_t* src = A.vbits + (long long)f * g.pbs;  // 4-byte aligned, pbs % 4 == 0
+    const uint32_t* src32 = reinterpret_cast<const uint32_t*>(src);
+    const long long nsw = g.pbs / 4;
+    const int head = (int)((4 - ((unsigned long long)out & 3)) & 3);
+    if (head > PB) {
+        for (long long b = threadIdx.x; b < PB; b += blockDim.x) out[b] = src[b];
+        return;
+    }
+    if (threadIdx.x < head) out[threadIdx.x] = src[threadIdx.x];
+    const long long nw = (PB - head) / 4;
+    uint32_t* dst32 = reinterpret_cast<uint32_t*>(out + head);
+    const int sh = 8 * head;
+    for (long long j = threadIdx.x; j < nw; j += blockDim.x) {
+        const long long sw = (head + 4 * j) >> 2;  // head < 4: source word holding the first byte
+        const uint32_t lo = __ldg(src32 + sw);
+        const uint32_t hi = sw + 1 < nsw ? __ldg(src32 + sw + 1) : 0u;
+        dst32[j] = sh ? __funnelshift_r(lo, hi, sh) : lo;
+    }
+    for (long long b = head + 4 * nw + threadIdx.x; b < PB; b += blockDim.x) out[b] = src[b];
 }
 
 // temporal runs: warp per key chain
@@ -522,9 +542,8 @@ void launch_emit(const EmitArgs& E, cudaStream_t s)
     const long long F = (long long)A.n_groups * A.n;
     STPC_LAUNCH();
     emit_header_kernel<<<A.n_groups, 128, 0, s>>>(E);
-    long long PB = (g.P + 7) / 8;
     STPC_LAUNCH();
-    emit_bitmaps_kernel<<<dim3((unsigned)std::min<long long>((PB + 255) / 256, 64), (unsigned)F), 256, 0, s>>>(E);
+    emit_bitmaps_kernel<<<(unsigned)F, 256, 0, s>>>(E);
     long long kwarps = (long long)A.n_groups * g.ty;
     STPC_LAUNCH();
     emit_temporal_kernel<<<(unsigned)((kwarps + 3) / 4), 128, 0, s>>>(E);
