@@ -188,8 +188,18 @@ __global__ void __launch_bounds__(PACK_THREADS) pack_count_kernel(EntropyArgs E)
     lens[threadIdx.x] = E.lens[grp * 256 + threadIdx.x];
     __syncthreads();
     const uint8_t* p = E.payload + E.payload_off[grp];
+    // the same 16-byte-per-thread layout as pack_write (vector loads)
+    const long long tb = b + (long long)threadIdx.x * PACK_PER_THREAD;
+    const int nq = (int)max(0LL, min((long long)PACK_PER_THREAD, e - tb));
     long long bits = 0;
-    for (long long i = b + threadIdx.x; i < e; i += PACK_THREADS) bits += lens[p[i]];
+    if (nq == PACK_PER_THREAD) {
+        const uint4 v4 = *reinterpret_cast<const uint4*>(p + tb);
+        const uint32_t wv[4] = {v4.x, v4.y, v4.z, v4.w};
+#pragma unroll
+        for (int q = 0; q < PACK_PER_THREAD; ++q) bits += lens[(wv[q >> 2] >> (8 * (q & 3))) & 0xff];
+    } else {
+        for (int q = 0; q < nq; ++q) bits += lens[p[tb + q]];
+    }
     for (int o = 16; o > 0; o >>= 1) bits += __shfl_xor_sync(STPC_FULL, bits, o);
     __shared__ long long ws[PACK_THREADS / 32];
     if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5] = bits;
