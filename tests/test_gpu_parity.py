@@ -362,6 +362,43 @@ def test_edge_cases_blob(n, k, tile, tau, scale, mutate):
         assert (q >= 0xFFFF).any()  # the escape path was exercised
 
 
+@pytest.mark.parametrize("seed", range(12))
+def test_fuzz_small_configs_blob(seed):
+    """Seeded random small configurations -- odd sensor sizes and resolutions,
+    tiles from 1x1 to 7x6 (both fit kernels), k anywhere, 1..12 frames, tau
+    from tight to loose, coarse and fine quantisation, float64 clouds -- GPU
+    blob == oracle blob byte for byte, and the GPU decoder inverts it exactly
+    like the oracle decoder."""
+    from oracle import decode as odec
+    from paper_2008_06972_b200 import AngularResolution, CodecConfig, compress, decompress, synth
+
+    rng = np.random.default_rng(7000 + seed)
+    w = int(rng.integers(40, 400))
+    h = int(rng.integers(4, 40))
+    sensor = synth.Sensor(w, h, 2 * np.pi / w * float(rng.uniform(0.5, 1.0)), float(rng.uniform(0.01, 0.06)),
+                          float(rng.uniform(1.2, 1.7)))
+    n = int(rng.integers(1, 13))
+    tw, th = int(rng.integers(1, 8)), int(rng.integers(1, 7))
+    tau = float(rng.choice([0.005, 0.02, 0.1, 0.3, 1.0]))
+    quant = float(rng.choice([0.001, 0.0005, 0.01, 0.05]))
+    grp = synth.make_group(7100 + seed, n, sensor, n_boxes=int(rng.integers(2, 30)),
+                           noise=float(rng.uniform(0.0, 0.05)), dropout=float(rng.uniform(0.0, 0.3)))
+    clouds = list(grp.clouds)
+    if seed % 4 == 3:
+        clouds = [c.astype(np.float64) * (1.0 + 1e-7) for c in clouds]
+    mode = "single" if n == 1 else "stream"
+    k = None if n == 1 else int(rng.integers(0, n))
+    cfg = CodecConfig(mode=mode, tau=tau, tile_w=tw, tile_h=th, res=AngularResolution(sensor.theta_r, sensor.phi_r),
+                      phi_offset=sensor.phi_offset, w=sensor.w, h=sensor.h, n_frames=n, k_index=k,
+                      range_quant=quant)
+    poses = grp.poses if n > 1 else None
+    mine, rep = compress(clouds, cfg, poses=poses)
+    ref, _ = oracle.compress(clouds, cfg, poses)
+    assert mine == ref, (seed, _first_divergence(mine, ref))
+    for a, b in zip(decompress(mine), odec.decompress(mine)):
+        assert np.array_equal(a, b)
+
+
 def test_single_mode_f64_input_full_size():
     """configs[0] through the float64 input path (reference up-casts to f64)."""
     from paper_2008_06972_b200 import compress, synth
