@@ -85,7 +85,7 @@ int stpc_encode_device(stpc_encoder* enc, int32_t n_groups, const void* d_points
 
 /* End-to-end variant from host memory: H2D of the points (pinned memory
  * recommended), encode, D2H of every blob into h_out (capacity out_cap).
- * Batches of >= 64 groups are pipelined in 8 chunks: the H2D of chunk c+1
+ * Batches of >= 64 groups are pipelined in 8 chunks (16 from 128 groups): the H2D of chunk c+1
  * overlaps the encode and blob D2H of chunk c; stpc_result_blobs then gives
  * offsets into h_out and stpc_result_device_blobs returns NULL. */
 int stpc_encode_host(stpc_encoder* enc, int32_t n_groups, const void* h_points,
