@@ -285,9 +285,11 @@ def test_fit_intermediates_match_oracle():
             assert np.array_equal(abc[ch, tr, :m].astype(np.float64), a)
 
 
-def test_pipelined_host_encode_matches_device_path():
+@pytest.mark.parametrize("G", [70, 131])
+def test_pipelined_host_encode_matches_device_path(G):
     """stpc_encode_host with >= 64 groups overlaps H2D with compute in 8
-    chunks; every blob and frame statistic must equal the one-shot result."""
+    chunks (16 from 128 groups; 131 leaves a short and an empty chunk);
+    every blob and frame statistic must equal the one-shot result."""
     import math
 
     from paper_2008_06972_b200 import AngularResolution, CodecConfig, Encoder, synth
@@ -296,7 +298,6 @@ def test_pipelined_host_encode_matches_device_path():
     cfg = CodecConfig(mode="stream", tau=0.1, tile_w=4, tile_h=4,
                       res=AngularResolution(sensor.theta_r, sensor.phi_r), phi_offset=sensor.phi_offset,
                       w=sensor.w, h=sensor.h, n_frames=3)
-    G = 70
     from paper_2008_06972_b200.geometry import poses_to_transforms
 
     clouds, xf = [], []
