@@ -277,18 +277,18 @@ struct BitRd {
 
 // codes longer than the first-level table (rare): canonical first-code search
 // over lengths HD_LUT+1..32 (huffman_decode_kernel's per-length test)
-__device__ __noinline__ int huff_long(const HuffDev& T, unsigned w, int& sym)
+__device__ __noinline__ unsigned huff_long(const HuffDev& T, unsigned w)
 {
+    // returns (len << 8) | symbol, 0 when no code matches (by value: a
+    // reference argument would force the caller's symbol through local memory)
     for (int l = HD_LUT + 1; l <= 32; ++l) {
         if (T.count[l]) {
             const unsigned long long c = (unsigned long long)w >> (32 - l);
-            if (c >= T.first[l] && c - T.first[l] < (unsigned long long)T.count[l]) {
-                sym = T.sym[T.index[l] + (int)(c - T.first[l])];
-                return l;
-            }
+            if (c >= T.first[l] && c - T.first[l] < (unsigned long long)T.count[l])
+                return ((unsigned)l << 8) | T.sym[T.index[l] + (int)(c - T.first[l])];
         }
     }
-    return 0;
+    return 0u;
 }
 
 // One canonical symbol; the same answers as the reference's bit-serial loop:
@@ -298,15 +298,82 @@ __device__ __noinline__ int huff_long(const HuffDev& T, unsigned w, int& sym)
 __device__ __forceinline__ int huff_step(const HuffDev& T, BitRd& r, int& sym)
 {
     const unsigned w = r.peek32();
-    const unsigned e = T.lut[w >> (32 - HD_LUT)];
-    int len = (int)(e >> 8);
+    unsigned e = T.lut[w >> (32 - HD_LUT)];
+    if (e == 0) e = huff_long(T, w);
+    const int len = (int)(e >> 8);
     sym = (int)(e & 0xff);
-    if (len == 0) len = huff_long(T, w, sym);
     const bool fits = len != 0 && r.pos + len <= r.total;
     const int rc = fits ? 0 : (len == 0 && r.total - r.pos >= 33 ? 2 : 1);
     r.skip(fits ? len : 0);
     return rc;
 }
+
+// Lean reader for the decode loops: a 64-bit MSB-aligned window refilled by
+// one 32-bit big-endian word whenever fewer than 32 bits remain (one word
+// prefetched ahead); positions are 32-bit offsets from the start of the
+// sub-segment, so the per-symbol work stays in 32-bit integer ops.
+struct BitRd2 {
+    const uint32_t* words;
+    long long wlast, wi;
+    unsigned long long cur;
+    int nb, used, avail;
+    uint32_t nxt;
+    __device__ __forceinline__ uint32_t ldw(long long i) const
+    {
+        return i <= wlast ? __byte_perm(__ldg(words + i), 0, 0x0123) : 0u;
+    }
+    __device__ __forceinline__ void init(const uint8_t* e, long long elen, long long start)
+    {
+        const unsigned long long a = (unsigned long long)e;
+        const int mis = (int)(a & 3);
+        words = (const uint32_t*)(a - mis);
+        wlast = elen > 0 ? (mis + elen - 1) / 4 : -1;
+        const long long sb = start + 8ll * mis;
+        const long long w = sb >> 5;
+        const int o = (int)(sb & 31);
+        cur = (((unsigned long long)ldw(w) << 32) | ldw(w + 1)) << o;
+        nb = 64 - o;
+        nxt = ldw(w + 2);
+        wi = w + 3;
+        used = 0;
+        avail = (int)min(elen * 8 - start, (long long)0x7fffffff);
+    }
+};
+
+// One symbol; returns whether it fit (the caller derives the reference's
+// 1 / 2 status from the last `len` once, after its loop).
+__device__ __forceinline__ bool huff_step2(const HuffDev& T, BitRd2& r, int& sym, int& len)
+{
+    const unsigned w = (unsigned)(r.cur >> 32);
+    unsigned e = T.lut[w >> (32 - HD_LUT)];
+    if (e == 0) e = huff_long(T, w);
+    len = (int)(e >> 8);
+    sym = (int)(e & 0xff);
+    const bool fits = len != 0 && len <= r.avail - r.used;
+    if (fits) {
+        r.cur <<= len;
+        r.nb -= len;
+        r.used += len;
+        if (r.nb < 32) {
+            r.cur |= (unsigned long long)r.nxt << (32 - r.nb);
+            r.nb += 32;
+            r.nxt = r.ldw(r.wi);
+            ++r.wi;
+        }
+    }
+    return fits;
+}
+
+#ifdef STPC_HUFF_STATS
+__device__ unsigned long long g_huff_stats[8];
+extern "C" int stpc_debug_huff_stats(unsigned long long* out)
+{
+    return cudaMemcpyFromSymbol(out, g_huff_stats, sizeof(g_huff_stats)) == cudaSuccess ? 0 : 1;
+}
+#define HUFF_STAT(i, v) atomicAdd(&g_huff_stats[i], (unsigned long long)(v))
+#else
+#define HUFF_STAT(i, v) ((void)0)
+#endif
 
 // Block per blob.  The bitstream is cut into <= 1024 sub-segments (4 per
 // thread).  Round 1: each thread parses its sub-segments in sequence from the
@@ -388,26 +455,24 @@ __global__ void __launch_bounds__(HD_THREADS) huff_decode_kernel(const uint8_t* 
     // vote in the loop condition keeps the warp converged every step (a
     // plain per-lane loop lets the lanes drift apart and run one at a time).
     auto parse_sub = [&](bool active, int t, long long start, long long& end, int& cnt) -> int {
-        BitRd r;
+        BitRd2 r;
         r.init(enc, (long long)enc_len, active ? start : 0);
-        const long long stop = active ? nominal_end(t) : 0;
-        int c = 0, rc = 0;
-        bool go = active && r.pos < stop;
+        const int need = active ? (int)(nominal_end(t) - start) : 0;
+        int c = 0, len = 1;
+        bool fits = true;
+        bool go = active && need > 0;
         while (__any_sync(STPC_FULL, go)) {
             if (go) {
                 int sym;
-                rc = huff_step(T, r, sym);
-                if (rc) {
-                    go = false;
-                } else {
-                    ++c;
-                    go = r.pos < stop;
-                }
+                fits = huff_step2(T, r, sym, len);
+                c += fits ? 1 : 0;
+                go = fits && r.used < need;
             }
         }
-        end = r.pos;
+        end = start + r.used;
         cnt = c;
-        return rc;
+        if (active) HUFF_STAT(0, c);  // symbols parsed (all rounds)
+        return fits ? 0 : (len == 0 && r.avail - r.used >= 33 ? 2 : 1);
     };
 
     // round 1 (warp-uniform trip count; __syncwarp re-converges the lanes
@@ -472,6 +537,8 @@ __global__ void __launch_bounds__(HD_THREADS) huff_decode_kernel(const uint8_t* 
                 }
             }
         }
+        if (tid == 0) HUFF_STAT(1, 1);  // correction rounds
+        if (want >= 0) HUFF_STAT(2, 1);  // corrected threads
         if (!__syncthreads_or(want >= 0)) break;
     }
 
@@ -506,15 +573,15 @@ __global__ void __launch_bounds__(HD_THREADS) huff_decode_kernel(const uint8_t* 
     for (int k = 0; k < HD_SUB; ++k) {
         const int t = t0 + k;
         const bool act = t < t1 && o < (long long)raw_len;
-        BitRd r;
+        BitRd2 r;
         r.init(enc, (long long)enc_len, act ? s_st[t] : 0);
         const int c = act ? (int)min((long long)s_cnt[t], (long long)raw_len - o) : 0;
         int i = 0;
         bool go = i < c;
         while (__any_sync(STPC_FULL, go)) {
             if (go) {
-                int sym;
-                huff_step(T, r, sym);
+                int sym, len;
+                huff_step2(T, r, sym, len);
                 out[o + i] = (uint8_t)sym;
                 go = ++i < c;
             }
