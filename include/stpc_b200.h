@@ -140,6 +140,9 @@ int stpc_project(const void* d_points, int32_t points_f64, const int64_t* point_
  *                        host or device bytes, blob i at [offsets[i],
  *                        offsets[i+1]).  status[i]: STPC_DEC_* of the first
  *                        failing check, in the reference's order.
+ * stpc_decoder_load_gather  the same from n separate host buffers (blob i at
+ *                        blobs[i], lengths[i] bytes): gathered into pinned
+ *                        staging by host threads, one H2D.
  * stpc_decoder_heads   first head_cap bytes of each raw payload (config block
  *                        + float32 transforms, bitstream.py:413-426) for the
  *                        host-side config checks.
@@ -174,6 +177,8 @@ int stpc_decoder_create(stpc_decoder** out);
 void stpc_decoder_destroy(stpc_decoder* dec);
 int stpc_decoder_load(stpc_decoder* dec, const uint8_t* blobs, int32_t blobs_on_device, const int64_t* offsets,
                       int32_t n, int32_t* status, void* stream);
+int stpc_decoder_load_gather(stpc_decoder* dec, const uint8_t* const* blobs, const int64_t* lengths, int32_t n,
+                             int32_t* status, void* stream);
 int stpc_decoder_heads(stpc_decoder* dec, int32_t head_cap, uint8_t* h_heads, int64_t* h_raw_len, void* stream);
 int stpc_decoder_frames(stpc_decoder* dec, const stpc_decode_geom* geom, const int32_t* sel, int32_t m,
                         const double* sin_theta, const double* cos_theta, const double* sin_phi,

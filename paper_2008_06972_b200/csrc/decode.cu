@@ -1166,6 +1166,7 @@ struct stpc_decoder {
     const double* last_points = nullptr;
     // host output path: pinned double buffer + copy threads
     HostBuf stage[2];
+    HostBuf stage_in;  // gathered host blobs (stpc_decoder_load_gather)
     cudaEvent_t ev[2] = {nullptr, nullptr};
     ~stpc_decoder()
     {
@@ -1249,10 +1250,15 @@ int stpc_decoder_create(stpc_decoder** out)
 
 void stpc_decoder_destroy(stpc_decoder* d) { delete d; }
 
-int stpc_decoder_load(stpc_decoder* d, const uint8_t* blobs, int32_t blobs_on_device, const int64_t* offsets,
-                      int32_t n, int32_t* status, void* stream)
+}  // extern "C"
+
+// Phase 1 body.  Blob i starts at offsets[i]; its length is lengths[i] when
+// given (gathered, padded layout) else offsets[i+1] - offsets[i].
+static int decoder_load_impl(stpc_decoder* d, const uint8_t* blobs, int32_t blobs_on_device, const int64_t* offsets,
+                             const int64_t* lengths, int32_t n, int32_t* status, void* stream)
 {
     if (!d || !blobs || !offsets || !status || n < 1) return STPC_ERR_ARG;
+    auto blen_of = [&](int i) -> long long { return lengths ? lengths[i] : offsets[i + 1] - offsets[i]; };
     cudaStream_t s = (cudaStream_t)stream;
     d->n = n;
     d->m = 0;
@@ -1261,7 +1267,7 @@ int stpc_decoder_load(stpc_decoder* d, const uint8_t* blobs, int32_t blobs_on_de
     std::vector<uint8_t> hdr((size_t)n * DEC_HEADER, 0);
     if (blobs_on_device) {
         std::vector<long long> blen(n);
-        for (int i = 0; i < n; ++i) blen[i] = offsets[i + 1] - offsets[i];
+        for (int i = 0; i < n; ++i) blen[i] = blen_of(i);
         DRET(d->boff.ensure(sizeof(long long) * 2 * n));
         DRET(d->heads.ensure((size_t)n * DEC_HEADER));
         DCK(cudaMemcpyAsync(d->boff.p, offsets, sizeof(long long) * n, cudaMemcpyHostToDevice, s));
@@ -1275,7 +1281,7 @@ int stpc_decoder_load(stpc_decoder* d, const uint8_t* blobs, int32_t blobs_on_de
         DCK(cudaStreamSynchronize(s));
     } else {
         for (int i = 0; i < n; ++i) {
-            const long long len = std::min<long long>(offsets[i + 1] - offsets[i], DEC_HEADER);
+            const long long len = std::min<long long>(blen_of(i), DEC_HEADER);
             if (len > 0) std::memcpy(hdr.data() + (size_t)i * DEC_HEADER, blobs + offsets[i], len);
         }
     }
@@ -1287,7 +1293,7 @@ int stpc_decoder_load(stpc_decoder* d, const uint8_t* blobs, int32_t blobs_on_de
     for (int i = 0; i < n; ++i) {
         long long rl = 0, el = 0;
         const uint8_t* h = hdr.data() + (size_t)i * DEC_HEADER;
-        pre[i] = check_header(h, offsets[i + 1] - offsets[i], rl, el);
+        pre[i] = check_header(h, blen_of(i), rl, el);
         d->raw_off[i] = ro;
         if (!pre[i]) {
             d->raw_len[i] = rl;
@@ -1345,6 +1351,42 @@ int stpc_decoder_load(stpc_decoder* d, const uint8_t* blobs, int32_t blobs_on_de
     DRET(d->okdev.ensure(sizeof(int) * n));
     DCK(cudaMemcpyAsync(d->okdev.p, d->ok.data(), sizeof(int) * n, cudaMemcpyHostToDevice, s));
     return STPC_OK;
+}
+
+extern "C" {
+
+int stpc_decoder_load(stpc_decoder* d, const uint8_t* blobs, int32_t blobs_on_device, const int64_t* offsets,
+                      int32_t n, int32_t* status, void* stream)
+{
+    return decoder_load_impl(d, blobs, blobs_on_device, offsets, nullptr, n, status, stream);
+}
+
+int stpc_decoder_load_gather(stpc_decoder* d, const uint8_t* const* blobs, const int64_t* lengths, int32_t n,
+                             int32_t* status, void* stream)
+{
+    if (!d || !blobs || !lengths || !status || n < 1) return STPC_ERR_ARG;
+    std::vector<int64_t> off(n + 1, 0);
+    for (int i = 0; i < n; ++i) {
+        if (lengths[i] < 0 || (!blobs[i] && lengths[i] > 0)) return STPC_ERR_ARG;
+        off[i + 1] = off[i] + (lengths[i] + 15) / 16 * 16;
+    }
+    DRET(d->stage_in.ensure((size_t)std::max<int64_t>(off[n], 16)));
+    uint8_t* dst = d->stage_in.as<uint8_t>();
+    // threads over contiguous runs of blobs; each blob's tail pad is zeroed
+    const unsigned nt = std::max(1u, std::min(16u, std::min((unsigned)n, std::thread::hardware_concurrency())));
+    std::vector<std::thread> th;
+    for (unsigned t = 0; t < nt; ++t) {
+        th.emplace_back([&, t] {
+            for (int i = (int)((long long)n * t / nt); i < (int)((long long)n * (t + 1) / nt); ++i) {
+                if (lengths[i] > 0) std::memcpy(dst + off[i], blobs[i], (size_t)lengths[i]);
+                std::memset(dst + off[i] + lengths[i], 0, (size_t)(off[i + 1] - off[i] - lengths[i]));
+            }
+        });
+    }
+    for (auto& x : th) x.join();
+    // blob i occupies [off[i], off[i] + lengths[i]) of the pinned arena: the
+    // H2D of the whole arena runs at pinned speed, headers are read in place
+    return decoder_load_impl(d, dst, 0, off.data(), lengths, n, status, stream);
 }
 
 int stpc_decoder_heads(stpc_decoder* d, int32_t head_cap, uint8_t* h_heads, int64_t* h_raw_len, void* stream)

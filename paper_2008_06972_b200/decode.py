@@ -186,18 +186,29 @@ class Decoder:
             self.h = None
 
     def decode(self, blobs_ptr: int, offsets: np.ndarray, on_device: bool, stream: Optional[int] = None,
-               keep_on_device: bool = False) -> Tuple[List, List, Dict[int, Exception]]:
-        """Decode n blobs at blobs_ptr[offsets[i]:offsets[i+1]] (host or device).
+               keep_on_device: bool = False, host_blobs: Optional[Sequence[bytes]] = None
+               ) -> Tuple[List, List, Dict[int, Exception]]:
+        """Decode n blobs at blobs_ptr[offsets[i]:offsets[i+1]] (host or device),
+        or the separate host buffers `host_blobs` (gathered natively, no join).
         Returns (clouds per blob or None, reports, {blob index: exception}).
         keep_on_device: leave the points in the decoder's device buffer
         (clouds are then None; reports carry the per-frame counts)."""
         L = self.L
-        n = offsets.size - 1
-        offsets = np.ascontiguousarray(offsets, np.int64)
         t0 = time.perf_counter()
-        status = np.zeros(n, np.int32)
-        _native.check(L.stpc_decoder_load(self.h, blobs_ptr, int(on_device), offsets.ctypes.data, n,
-                                          status.ctypes.data, stream))
+        if host_blobs is not None:
+            n = len(host_blobs)
+            keep = [b if isinstance(b, bytes) else bytes(b) for b in host_blobs]
+            ptrs = (ctypes.c_void_p * n)(*[ctypes.cast(ctypes.c_char_p(b), ctypes.c_void_p).value for b in keep])
+            lens = np.array([len(b) for b in keep], np.int64)
+            status = np.zeros(n, np.int32)
+            _native.check(L.stpc_decoder_load_gather(self.h, ptrs, lens.ctypes.data, n, status.ctypes.data, stream))
+            del keep
+        else:
+            n = offsets.size - 1
+            offsets = np.ascontiguousarray(offsets, np.int64)
+            status = np.zeros(n, np.int32)
+            _native.check(L.stpc_decoder_load(self.h, blobs_ptr, int(on_device), offsets.ctypes.data, n,
+                                              status.ctypes.data, stream))
         errors: Dict[int, Exception] = {}
         for i in np.flatnonzero(status):
             errors[int(i)] = _KIND[int(status[i])](_LOAD_MSG[int(status[i])])
@@ -297,13 +308,9 @@ def decompress_many(blobs: Sequence[bytes]) -> Tuple[List[List[np.ndarray]], Lis
     """Decode a batch of blobs (one device pass per distinct configuration).
     Raises the reference's exception for the first blob that fails."""
     dec = get_decoder()
-    sizes = np.array([len(b) for b in blobs], np.int64)
-    offsets = np.zeros(len(blobs) + 1, np.int64)
-    offsets[1:] = np.cumsum(sizes)
-    arena = np.frombuffer(b"".join(blobs), np.uint8) if len(blobs) else np.zeros(0, np.uint8)
-    if arena.size == 0:
-        arena = np.zeros(1, np.uint8)
-    clouds, reports, errors = dec.decode(arena.ctypes.data, offsets, on_device=False)
+    if not len(blobs):
+        return [], []
+    clouds, reports, errors = dec.decode(0, None, False, host_blobs=blobs)
     if errors:
         raise errors[min(errors)]
     return clouds, reports  # type: ignore[return-value]
