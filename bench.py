@@ -509,8 +509,6 @@ def main():
                "d2h_bytes_per_step": int(off2[-1] + 8 * (3 * G + 2))}
 
     # ---------------- roofline of the dominant stage
-    from paper_2008_06972_b200.codec import MODE_SINGLE  # noqa: F401
-
     peaks = {}
     try:
         peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))

@@ -217,64 +217,6 @@ struct HuffDev {
     unsigned char sym[256];
 };
 
-// Bit reader over aligned 64-bit words (big-endian bit order), with a
-// four-word register ring: the load for word i+3 is issued when word i
-// becomes current, so ~190 bits of decoding cover its HBM latency.  Words
-// past the end of the stream read as zero (never outside the blob: the
-// aligned base only reaches back into the blob header).
-struct BitRd {
-    const unsigned long long* words;
-    long long wmax, wi, pos, total;
-    unsigned long long w0, w1, w2, w3;
-    int off;
-    __device__ __forceinline__ unsigned long long ld(long long i) const
-    {
-        if (i > wmax) return 0ull;
-        const unsigned long long x = __ldg(words + i);
-        return ((unsigned long long)__byte_perm((unsigned)x, 0, 0x0123) << 32) |
-               __byte_perm((unsigned)(x >> 32), 0, 0x0123);
-    }
-    __device__ __forceinline__ void init(const uint8_t* e, long long elen, long long start)
-    {
-        const unsigned long long a = (unsigned long long)e;
-        const int mis = (int)(a & 7);
-        words = (const unsigned long long*)(a - mis);
-        wmax = elen > 0 ? (mis + elen - 1) / 8 : -1;
-        const long long sb = start + 8ll * mis;
-        wi = sb >> 6;
-        off = (int)(sb & 63);
-        w0 = ld(wi);
-        w1 = ld(wi + 1);
-        w2 = ld(wi + 2);
-        w3 = ld(wi + 3);
-        pos = start;
-        total = elen * 8;
-    }
-    __device__ __forceinline__ unsigned peek32() const
-    {
-        const unsigned long long v = off ? (w0 << off) | (w1 >> (64 - off)) : w0;
-        return (unsigned)(v >> 32);
-    }
-    // branch-free advance (selects + one predicated load) so a warp's lanes
-    // stay converged through the decode loop
-    __device__ __forceinline__ void skip(int len)
-    {
-        off += len;
-        pos += len;
-        const bool sh = off >= 64;
-        unsigned long long nw = 0;
-        if (sh && wi + 4 <= wmax) nw = __ldg(words + wi + 4);
-        nw = ((unsigned long long)__byte_perm((unsigned)nw, 0, 0x0123) << 32) |
-             __byte_perm((unsigned)(nw >> 32), 0, 0x0123);
-        w0 = sh ? w1 : w0;
-        w1 = sh ? w2 : w1;
-        w2 = sh ? w3 : w2;
-        w3 = sh ? nw : w3;
-        wi += sh ? 1 : 0;
-        off -= sh ? 64 : 0;
-    }
-};
-
 // codes longer than the first-level table (rare): canonical first-code search
 // over lengths HD_LUT+1..32 (huffman_decode_kernel's per-length test)
 __device__ __noinline__ unsigned huff_long(const HuffDev& T, unsigned w)
@@ -291,28 +233,11 @@ __device__ __noinline__ unsigned huff_long(const HuffDev& T, unsigned w)
     return 0u;
 }
 
-// One canonical symbol; the same answers as the reference's bit-serial loop:
-// 0 ok; 1 the stream ends inside the symbol (or fewer than 33 bits remain
-// with no match); 2 no code matches within 32 bits and >= 33 bits remain.
-// Straight-line apart from the rare long-code call (no early exits).
-__device__ __forceinline__ int huff_step(const HuffDev& T, BitRd& r, int& sym)
-{
-    const unsigned w = r.peek32();
-    unsigned e = T.lut[w >> (32 - HD_LUT)];
-    if (e == 0) e = huff_long(T, w);
-    const int len = (int)(e >> 8);
-    sym = (int)(e & 0xff);
-    const bool fits = len != 0 && r.pos + len <= r.total;
-    const int rc = fits ? 0 : (len == 0 && r.total - r.pos >= 33 ? 2 : 1);
-    r.skip(fits ? len : 0);
-    return rc;
-}
-
 // Lean reader for the decode loops: a 64-bit MSB-aligned window refilled by
 // one 32-bit big-endian word whenever fewer than 32 bits remain (one word
 // prefetched ahead); positions are 32-bit offsets from the start of the
 // sub-segment, so the per-symbol work stays in 32-bit integer ops.
-struct BitRd2 {
+struct BitRd {
     const uint32_t* words;
     long long wlast, wi;
     unsigned long long cur;
@@ -342,7 +267,7 @@ struct BitRd2 {
 
 // One symbol; returns whether it fit (the caller derives the reference's
 // 1 / 2 status from the last `len` once, after its loop).
-__device__ __forceinline__ bool huff_step2(const HuffDev& T, BitRd2& r, int& sym, int& len)
+__device__ __forceinline__ bool huff_step(const HuffDev& T, BitRd& r, int& sym, int& len)
 {
     const unsigned w = (unsigned)(r.cur >> 32);
     unsigned e = T.lut[w >> (32 - HD_LUT)];
@@ -455,7 +380,7 @@ __global__ void __launch_bounds__(HD_THREADS) huff_decode_kernel(const uint8_t* 
     // vote in the loop condition keeps the warp converged every step (a
     // plain per-lane loop lets the lanes drift apart and run one at a time).
     auto parse_sub = [&](bool active, int t, long long start, long long& end, int& cnt) -> int {
-        BitRd2 r;
+        BitRd r;
         r.init(enc, (long long)enc_len, active ? start : 0);
         const int need = active ? (int)(nominal_end(t) - start) : 0;
         int c = 0, len = 1;
@@ -464,7 +389,7 @@ __global__ void __launch_bounds__(HD_THREADS) huff_decode_kernel(const uint8_t* 
         while (__any_sync(STPC_FULL, go)) {
             if (go) {
                 int sym;
-                fits = huff_step2(T, r, sym, len);
+                fits = huff_step(T, r, sym, len);
                 c += fits ? 1 : 0;
                 go = fits && r.used < need;
             }
@@ -573,7 +498,7 @@ __global__ void __launch_bounds__(HD_THREADS) huff_decode_kernel(const uint8_t* 
     for (int k = 0; k < HD_SUB; ++k) {
         const int t = t0 + k;
         const bool act = t < t1 && o < (long long)raw_len;
-        BitRd2 r;
+        BitRd r;
         r.init(enc, (long long)enc_len, act ? s_st[t] : 0);
         const int c = act ? (int)min((long long)s_cnt[t], (long long)raw_len - o) : 0;
         int i = 0;
@@ -581,7 +506,7 @@ __global__ void __launch_bounds__(HD_THREADS) huff_decode_kernel(const uint8_t* 
         while (__any_sync(STPC_FULL, go)) {
             if (go) {
                 int sym, len;
-                huff_step2(T, r, sym, len);
+                huff_step(T, r, sym, len);
                 out[o + i] = (uint8_t)sym;
                 go = ++i < c;
             }
