@@ -1116,7 +1116,10 @@ void launch_fit_rows(const FitArgs& a, cudaStream_t s)
 // and poison the channel's pixels there (+inf) for pass 2.  A second tiny
 // kernel sizes each chain's temporal records (18 B + presence bits + 4 B per
 // present P channel, bitstream.py:222-245).
-__global__ void __launch_bounds__(128) refit_kernel(RefitArgs A)
+#ifndef STPC_REFIT_MINB
+#define STPC_REFIT_MINB 10  // measured: unbounded 5.74 ms, 10 -> 5.66, 16 -> 5.65 (latency-bound; more warps beat a few spills)
+#endif
+__global__ void __launch_bounds__(128, STPC_REFIT_MINB) refit_kernel(RefitArgs A)
 {
     __shared__ double smem[4][32];
     const Geometry& g = A.g;
