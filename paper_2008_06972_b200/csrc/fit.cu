@@ -296,7 +296,10 @@ constexpr int START_TPB = 128;
 constexpr int START_MAXPX = 16;  // staged path: tiles of up to 16 pixels
 
 template <int TW>
-__global__ void __launch_bounds__(START_TPB) start_tiles_staged_kernel(FitArgs A)
+#ifndef STPC_STAGED_MINB
+#define STPC_STAGED_MINB 8  // measured (start_p): 1 -> 5.92 ms, 6 -> 5.62, 8 -> 5.43
+#endif
+__global__ void __launch_bounds__(START_TPB, STPC_STAGED_MINB) start_tiles_staged_kernel(FitArgs A)
 {
     constexpr int STRIDE = START_MAXPX + 1;
     __shared__ double s_r[START_TPB * STRIDE];
