@@ -202,7 +202,10 @@ template <> struct PPT<double> { static constexpr int value = 4; };
 
 // grid: (x = chunks of 256*PPT points of a frame, y = frame)
 template <class T>
-__global__ void __launch_bounds__(256, 4) convert_kernel(ConvertArgs a, const T* pts)
+#ifndef STPC_CONVERT_MINB
+#define STPC_CONVERT_MINB 4
+#endif
+__global__ void __launch_bounds__(256, STPC_CONVERT_MINB) convert_kernel(ConvertArgs a, const T* pts)
 {
     constexpr int K = PPT<T>::value;
     constexpr int CH = 256 * K;

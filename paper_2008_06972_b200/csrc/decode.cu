@@ -309,7 +309,10 @@ extern "C" int stpc_debug_huff_stats(unsigned long long* out)
 // (canonical codes resynchronise within a few symbols), after which the old
 // counts stand.  Converged starts are exact by induction from bit 0; a final
 // pass writes the symbols at scanned offsets.
-__global__ void __launch_bounds__(HD_THREADS) huff_decode_kernel(const uint8_t* blobs, const long long* blob_off,
+#ifndef STPC_HUFF_MINB
+#define STPC_HUFF_MINB 8  // measured (load = crc + huffman, 1024 blobs): 1 -> 27.7 ms, 8 -> 26.0
+#endif
+__global__ void __launch_bounds__(HD_THREADS, STPC_HUFF_MINB) huff_decode_kernel(const uint8_t* blobs, const long long* blob_off,
                                                                  const int* skip, uint8_t* raw,
                                                                  const long long* raw_off, int* status)
 {
@@ -549,7 +552,10 @@ constexpr int PK_WIN = 16384;  // staged bytes of the run section
 // walked by one thread (a record's size depends on its presence mask) in
 // batches that the block then expands in parallel; residual varints are
 // scanned block-parallel (terminator bytes < 0x80).
-__global__ void __launch_bounds__(PK_THREADS) parse_kernel(DecGeom G, const uint8_t* raw, const long long* raw_off,
+#ifndef STPC_PARSE_MINB
+#define STPC_PARSE_MINB 6  // measured (frames phase): 1 -> 35.5 ms, 6 -> 31.7, 8 -> 32.7
+#endif
+__global__ void __launch_bounds__(PK_THREADS, STPC_PARSE_MINB) parse_kernel(DecGeom G, const uint8_t* raw, const long long* raw_off,
                                                            const long long* raw_len, const int* sel, float4* tmap,
                                                            ResSec* res, unsigned long long* pstat)
 {
