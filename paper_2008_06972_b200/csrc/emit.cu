@@ -112,7 +112,10 @@ __device__ __forceinline__ long long warp_excl_max(long long v, long long ident)
 
 // Warp per (frame, row): counts, varint bytes (excluding the row's first
 // delta), first/last residual flat index, coverage counters.
-__global__ void __launch_bounds__(256) rowstats_kernel(PlanArgs A)
+#ifndef STPC_ROWSTATS_MINB
+#define STPC_ROWSTATS_MINB 1
+#endif
+__global__ void __launch_bounds__(256, STPC_ROWSTATS_MINB) rowstats_kernel(PlanArgs A)
 {
     const Geometry& g = A.g;
     const int lane = threadIdx.x & 31;
