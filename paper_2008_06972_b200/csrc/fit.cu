@@ -743,7 +743,7 @@ __device__ bool test_tile_pair(bool active, const Chain& ch, const Geometry& g, 
 }
 
 #ifndef STPC_PAIR_MINB
-#define STPC_PAIR_MINB 5
+#define STPC_PAIR_MINB 8  // measured (fit_p): 5 -> 28.5 ms, 6 -> 29.1, 7 -> 26.5, 8 -> 26.3, 10 -> 29.8 (more chains in flight beat the spills)
 #endif
 #ifdef STPC_FIT_STATS
 // diagnostic build only (tools/fit_stats.py): chain-step counters
