@@ -332,7 +332,7 @@ def algorithmic_bytes(stage, cfg, n, G, npts, raw_bytes=0, blob_bytes=0):
 
 # stage -> (kernel name in the ncu capture, which of its launches)
 _NCU_KERNEL = {"fit_p": ("fit_pair_kernel", -1), "fit_key": ("fit_pair_kernel", 0),
-               "convert": ("void convert_kernel<float>", 0)}
+               "convert": ("void convert_kernel<float>", 0), "emit": ("emit_residual_kernel", 0)}
 
 
 def ncu_traffic(stage, args, G):
@@ -537,6 +537,9 @@ def main():
     roofline["stages"] = stages
     roofline["convert"] = stages.get("convert")
     roofline["compaction"] = stages.get("emit")
+    if roofline["compaction"]:
+        roofline["compaction"] = dict(roofline["compaction"], **ncu_traffic("emit", args, G),
+                                      kernel="emit_residual_kernel (traffic); stage time covers all emit kernels")
     roofline["fit_utilisation"] = fit_utilisation(args, G)
 
     # ---------------- CPU baseline (rank 0, N=1)
