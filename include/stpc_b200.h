@@ -92,6 +92,12 @@ int stpc_encode_host(stpc_encoder* enc, int32_t n_groups, const void* h_points,
                      const int64_t* point_offsets, const double* transforms, uint8_t* h_out,
                      int64_t out_cap, void* stream);
 
+/* Make `stream` wait for the encoder's pending side-stream work (the +inf
+ * prefill of the next call's range grid, which overlaps the entropy stage of
+ * the last call).  Timing code calls it before its closing event so that a
+ * window of K calls contains exactly K prefills. */
+int stpc_encoder_wait(stpc_encoder* enc, void* stream);
+
 /* Results of the last encode. offsets: int64[G+1] (blob start in the arena;
  * offsets[G] = arena bytes), lengths: int64[G]. */
 int32_t stpc_result_groups(const stpc_encoder* enc);

@@ -50,8 +50,15 @@ struct stpc_encoder {
     DevBuf pts, pt_off, xf;
     DevBuf q_count, q_idx, q_frame;  // convert's exact-path queue
     HostBuf h_stage;  // pinned staging: pt_off | xf
-    // frame level
-    DevBuf best, vbits, ebits, cls, fstats;
+    // frame level.  The range grid is double-buffered: the pack kernel of a
+    // call (which runs after the last reader of its grid) also +inf-fills the
+    // other buffer with background stores, so the next call starts on a
+    // prefilled grid; the last call's grid stays readable (STPC_BUF_BEST).
+    DevBuf best2[2];
+    int best_cur = 0, best_last = 0;
+    long long best_filled[2] = {0, 0};  // +inf-filled elements (valid once ev_fill[i] completes)
+    cudaEvent_t ev_fill[2] = {};
+    DevBuf vbits, ebits, cls, fstats;
     // chain level
     DevBuf cert, start_ok, chain_counter;
     DevBuf run_s, run_len, run_abc, n_runs, ref_ok, ref_c, chain_tbytes, chain_off;
@@ -85,6 +92,8 @@ struct stpc_encoder {
             if (ev_done[i]) cudaEventDestroy(ev_done[i]);
         }
         if (copy_stream) cudaStreamDestroy(copy_stream);
+        for (auto& x : ev_fill)
+            if (x) cudaEventDestroy(x);
     }
     void mark(int st, cudaStream_t s)
     {
@@ -266,7 +275,13 @@ static int encode_impl(stpc_encoder* e, int G, const void* d_points, const int64
         dev_xf = e->xf.as<double>();
     }
     // --- workspace
-    ENS(e->best, sizeof(double) * F * g.P);
+    const int bi = e->best_cur;
+    DevBuf& best = e->best2[bi];
+    {
+        void* before = best.p;
+        ENS(best, sizeof(double) * F * g.P);
+        if (best.p != before) e->best_filled[bi] = 0;
+    }
     ENS(e->vbits, (size_t)F * g.pbs);
     ENS(e->ebits, (size_t)F * g.pbs);
     ENS(e->cls, (size_t)F * TT);
@@ -300,7 +315,12 @@ static int encode_impl(stpc_encoder* e, int G, const void* d_points, const int64
 
     launch_zero(e->fstats.p, sizeof(long long) * F * FS_COUNT, s);
     launch_zero(e->cls.p, (long long)F * TT, s);
-    launch_fill_u64(e->best.as<unsigned long long>(), 0x7ff0000000000000ull, F * g.P, s);
+    if (e->best_filled[bi] >= F * g.P) {
+        CK(cudaStreamWaitEvent(s, e->ev_fill[bi], 0));  // prefilled during the previous call's entropy stage
+    } else {
+        launch_fill_u64(best.as<unsigned long long>(), 0x7ff0000000000000ull, F * g.P, s);
+    }
+    e->best_filled[bi] = 0;  // consumed by this call
 
     e->mark(ST_CONVERT, s);
     // --- K1
@@ -311,7 +331,7 @@ static int encode_impl(stpc_encoder* e, int G, const void* d_points, const int64
     ca.xf = dev_xf;
     ca.n_frames = (int)F;
     ca.g = g;
-    ca.best = e->best.as<unsigned long long>();
+    ca.best = best.as<unsigned long long>();
     ca.win = nullptr;
     ca.fstats = e->fstats.as<long long>();
     {
@@ -327,13 +347,13 @@ static int encode_impl(stpc_encoder* e, int G, const void* d_points, const int64
     }
     launch_convert(ca, (int)max_pts, s);
     e->mark(ST_BITMAP, s);
-    launch_bitmaps(e->best.as<double>(), (int)F, g, e->cfg.range_quant, e->vbits.as<uint8_t>(),
+    launch_bitmaps(best.as<double>(), (int)F, g, e->cfg.range_quant, e->vbits.as<uint8_t>(),
                    e->ebits.as<uint8_t>(), e->fstats.as<long long>(), s);
 
     // --- K2 / K3a / K3b
     Trig tg = trig_of(e);
     FitArgs fa;
-    fa.best = e->best.as<double>();
+    fa.best = best.as<double>();
     fa.tg = tg;
     fa.g = g;
     fa.tau = e->cfg.tau;
@@ -357,7 +377,7 @@ static int encode_impl(stpc_encoder* e, int G, const void* d_points, const int64
     launch_fit_chains(fa, s);
 
     RefitArgs ra;
-    ra.best = e->best.as<double>();
+    ra.best = best.as<double>();
     ra.tg = tg;
     ra.g = g;
     ra.tau = fa.tau;
@@ -437,12 +457,22 @@ static int encode_impl(stpc_encoder* e, int G, const void* d_points, const int64
     ea.ref_c = ra.ref_c;
     ea.payload = e->payload.as<uint8_t>();
     launch_emit(ea, s);
-
     e->mark(ST_HUFF, s);
     // --- entropy stage
     EntropyArgs en;
     en.G = G;
     en.payload = ea.payload;
+    // this call's grid is dead after emit (the entropy stage never reads it):
+    // the pack blocks +inf-fill the other buffer for the next call
+    const int nb = 1 - bi;
+    DevBuf& nxt_best = e->best2[nb];
+    {
+        void* before = nxt_best.p;
+        ENS(nxt_best, sizeof(double) * F * g.P);
+        if (nxt_best.p != before) e->best_filled[nb] = 0;
+    }
+    en.prefill = nxt_best.as<unsigned long long>();
+    en.prefill_n = (F * g.P + 1) / 2 * 2;
     en.payload_off = pa.payload_off;
     en.payload_len = pa.payload_len;
     en.hist = e->hist.as<unsigned>();
@@ -473,6 +503,11 @@ static int encode_impl(stpc_encoder* e, int G, const void* d_points, const int64
     launch_zero(en.blobs, blob_total, s);
     e->mark(ST_PACK, s);
     launch_pack(en, s);
+    if (!e->ev_fill[0]) for (auto& x : e->ev_fill) CK(cudaEventCreateWithFlags(&x, cudaEventDisableTiming));
+    CK(cudaEventRecord(e->ev_fill[nb], s));
+    e->best_filled[nb] = en.max_chunks > 0 ? F * g.P : 0;  // pack ran: the next grid is +inf
+    e->best_last = bi;
+    e->best_cur = nb;
     e->mark(ST_CRC, s);
     launch_crc(en, s);
     CK(cudaGetLastError());
@@ -680,6 +715,14 @@ int stpc_encode_host(stpc_encoder* enc, int32_t n_groups, const void* h_points,
     return STPC_OK;
 }
 
+int stpc_encoder_wait(stpc_encoder* enc, void* stream)
+{
+    if (!enc) return STPC_ERR_ARG;
+    cudaStream_t s = (cudaStream_t)stream;
+    if (enc->ev_fill[enc->best_cur]) CK(cudaStreamWaitEvent(s, enc->ev_fill[enc->best_cur], 0));
+    return STPC_OK;
+}
+
 int32_t stpc_result_groups(const stpc_encoder* enc) { return enc ? enc->G : 0; }
 
 int stpc_result_blobs(const stpc_encoder* enc, int64_t* offsets, int64_t* lengths)
@@ -741,7 +784,7 @@ int stpc_encoder_buffer(const stpc_encoder* enc, int32_t which, void** dev_ptr, 
     if (!enc || !dev_ptr) return STPC_ERR_ARG;
     const DevBuf* b = nullptr;
     switch (which) {
-    case STPC_BUF_BEST: b = &enc->best; break;
+    case STPC_BUF_BEST: b = &enc->best2[enc->best_last]; break;
     case STPC_BUF_CLS: b = &enc->cls; break;
     case STPC_BUF_RUN_S: b = &enc->run_s; break;
     case STPC_BUF_RUN_LEN: b = &enc->run_len; break;

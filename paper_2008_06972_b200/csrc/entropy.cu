@@ -236,6 +236,15 @@ __global__ void pack_scan_kernel(EntropyArgs E)
 __global__ void __launch_bounds__(PACK_THREADS, STPC_PACK_MINB) pack_write_kernel(EntropyArgs E)
 {
     const int grp = blockIdx.y, c = blockIdx.x;
+    if (E.prefill) {  // this block's slice of the next grid's +inf fill (16-byte stores)
+        const long long nblk = (long long)gridDim.x * gridDim.y;
+        const long long bid = (long long)blockIdx.y * gridDim.x + blockIdx.x;
+        const long long n2 = E.prefill_n / 2;
+        const long long per = (n2 + nblk - 1) / nblk;
+        ulonglong2* dst = reinterpret_cast<ulonglong2*>(E.prefill);
+        const ulonglong2 inf2 = make_ulonglong2(0x7ff0000000000000ull, 0x7ff0000000000000ull);
+        for (long long i = bid * per + threadIdx.x; i < min(n2, (bid + 1) * per); i += PACK_THREADS) dst[i] = inf2;
+    }
     long long b, e;
     chunk_range(E, grp, c, b, e);
     if (b >= e) return;

@@ -168,6 +168,10 @@ struct EntropyArgs {
     long long* chunk_bits;         // [G][max_chunks]
     unsigned int* seg_crc;         // [G][max_segs]
     int max_chunks, max_segs;
+    // +inf prefill of the next call's range grid, spread over the pack
+    // blocks (background stores behind the instruction-bound packing)
+    unsigned long long* prefill = nullptr;
+    long long prefill_n = 0;  // u64 elements (even)
 };
 constexpr int PACK_CHUNK = 4096;  // payload bytes per pack block
 constexpr int CRC_PIECE = 256;    // bytes per CRC thread
