@@ -174,7 +174,7 @@ __device__ __forceinline__ float fast_atan2f(float y, float x)
 // inv_tr bins.  Total < 2.75e-6 * inv_tr bins against a margin of
 // FAST_MARGIN * inv_tr = 1e-5 * inv_tr bins: 3.6x headroom at any resolution.
 __device__ __forceinline__ bool fast_bin(double x, double y, double z, const Geometry& g, float inv_tr,
-                                         float inv_pr, float phi_off, int& u, int& v)
+                                         float inv_pr, float phi_off, float mu, float mv, int& u, int& v)
 {
     const float xf = (float)x, yf = (float)y, zf = (float)z;
     const float mxy = fmaxf(fabsf(xf), fabsf(yf));
@@ -188,7 +188,6 @@ __device__ __forceinline__ bool fast_bin(double x, double y, double z, const Geo
     const float qv = (ph - phi_off) * inv_pr;
     const float flu = floorf(qu), flv = floorf(qv);
     const float fu = qu - flu, fv = qv - flv;
-    const float mu = (float)FAST_MARGIN * inv_tr, mv = (float)FAST_MARGIN * inv_pr;
     if (fu < mu || fu > 1.0f - mu || fv < mv || fv > 1.0f - mv) return false;
     const int uq = (int)flu;  // 0 <= qu <= w (th <= 2 pi)
     u = uq >= g.w ? uq - g.w : uq;
@@ -235,8 +234,6 @@ __global__ void __launch_bounds__(256, STPC_CONVERT_MINB) convert_kernel(Convert
     }
     __syncthreads();
     unsigned long long* best = a.best + (long long)f * a.g.P;
-    const float inv_tr = (float)(1.0 / a.g.theta_r), inv_pr = (float)(1.0 / a.g.phi_r);
-    const float phi_off = (float)a.g.phi_offset;
     int rej = 0, drop = 0, kept = 0;
 #pragma unroll
     for (int k = 0; k < K; ++k) {
@@ -254,7 +251,7 @@ __global__ void __launch_bounds__(256, STPC_CONVERT_MINB) convert_kernel(Convert
         int u, v;
         if (r <= 0.0) {
             rej += 1;
-        } else if (isfinite(r) && fast_bin(x, y, z, a.g, inv_tr, inv_pr, phi_off, u, v)) {
+        } else if (isfinite(r) && fast_bin(x, y, z, a.g, a.inv_tr, a.inv_pr, a.phi_off, a.mu, a.mv, u, v)) {
             if (v < 0 || v >= a.g.h) {
                 drop += 1;
             } else {
@@ -318,8 +315,6 @@ __global__ void __launch_bounds__(256) convert_overflow_kernel(ConvertArgs a, co
     const int f = blockIdx.y;
     const long long b = a.pt_off[f], e = a.pt_off[f + 1];
     const double* xf = a.xf + 12 * f;
-    const float inv_tr = (float)(1.0 / a.g.theta_r), inv_pr = (float)(1.0 / a.g.phi_r);
-    const float phi_off = (float)a.g.phi_offset;
     for (long long i = b + (long long)blockIdx.x * blockDim.x + threadIdx.x; i < e; i += (long long)gridDim.x * blockDim.x) {
         const T* p = pts + 3 * i;
         double px = (double)p[0], py = (double)p[1], pz = (double)p[2];
@@ -329,7 +324,8 @@ __global__ void __launch_bounds__(256) convert_overflow_kernel(ConvertArgs a, co
         if (!(isfinite(x) && isfinite(y) && isfinite(z))) continue;
         double r = sqrt((x * x + y * y) + z * z);
         int u, v;
-        if (r <= 0.0 || (isfinite(r) && fast_bin(x, y, z, a.g, inv_tr, inv_pr, phi_off, u, v))) continue;
+        if (r <= 0.0 || (isfinite(r) && fast_bin(x, y, z, a.g, a.inv_tr, a.inv_pr, a.phi_off, a.mu, a.mv, u, v)))
+            continue;
         exact_point(a, px, py, pz, f);
     }
 }
@@ -393,9 +389,15 @@ static dim3 chunk_grid(int max_pts, int n_frames)
     return dim3(bx < 1 ? 1 : bx, n_frames);
 }
 
-void launch_convert(const ConvertArgs& a, int max_pts, cudaStream_t s)
+void launch_convert(const ConvertArgs& a0, int max_pts, cudaStream_t s)
 {
-    if (a.n_frames <= 0) return;
+    if (a0.n_frames <= 0) return;
+    ConvertArgs a = a0;
+    a.inv_tr = (float)(1.0 / a.g.theta_r);
+    a.inv_pr = (float)(1.0 / a.g.phi_r);
+    a.phi_off = (float)a.g.phi_offset;
+    a.mu = (float)FAST_MARGIN * a.inv_tr;
+    a.mv = (float)FAST_MARGIN * a.inv_pr;
     launch_zero(a.q_count, sizeof(unsigned long long), s);
     STPC_LAUNCH();
     if (a.pts_f64)

@@ -57,6 +57,8 @@ struct ConvertArgs {
     long long* q_idx;
     int* q_frame;
     long long q_cap;
+    // fp32 fast-path constants, set by launch_convert
+    float inv_tr = 0.f, inv_pr = 0.f, phi_off = 0.f, mu = 0.f, mv = 0.f;
 };
 
 void launch_fill_u64(unsigned long long* p, unsigned long long v, long long n, cudaStream_t s);
