@@ -92,6 +92,16 @@ int stpc_encode_host(stpc_encoder* enc, int32_t n_groups, const void* h_points,
                      const int64_t* point_offsets, const double* transforms, uint8_t* h_out,
                      int64_t out_cap, void* stream);
 
+/* Host encode from per-frame arrays (no concatenation on the caller's side):
+ * frame f's xyz at frame_points[f] (float32, or float64 if cfg.points_f64),
+ * frame_counts[f] points.  Frames are gathered by host threads into pinned
+ * staging per pipeline chunk (overlapping the previous chunk's H2D and
+ * encode); blobs land in the encoder's own pinned arena
+ * (stpc_result_host_blobs / stpc_result_copy_blobs). */
+int stpc_encode_host_gather(stpc_encoder* enc, int32_t n_groups, const void* const* frame_points,
+                            const int64_t* frame_counts, const double* transforms, void* stream);
+const uint8_t* stpc_result_host_blobs(const stpc_encoder* enc);
+
 /* Make `stream` wait for the encoder's pending side-stream work (the +inf
  * prefill of the next call's range grid, which overlaps the entropy stage of
  * the last call).  Timing code calls it before its closing event so that a

@@ -25,6 +25,7 @@ STPC_NSTAT = 9
 # every symbol include/stpc_b200.h declares
 EXPORTS = [
     "stpc_encoder_create", "stpc_encoder_destroy", "stpc_encode_device", "stpc_encode_host", "stpc_encoder_wait",
+    "stpc_encode_host_gather", "stpc_result_host_blobs",
     "stpc_result_groups", "stpc_result_blobs", "stpc_result_device_blobs",
     "stpc_result_copy_blobs", "stpc_result_frame_stats", "stpc_result_payload_lengths",
     "stpc_encoder_buffer", "stpc_project", "stpc_malloc", "stpc_free", "stpc_memcpy_d2h",
@@ -109,6 +110,8 @@ def load(require_device: bool = False):
                 "stpc_stage_name": ([I32], ctypes.c_char_p),
                 "stpc_launch_count": ([], ctypes.c_uint64),
                 "stpc_encoder_wait": ([P, P], ctypes.c_int),
+                "stpc_encode_host_gather": ([P, I32, P, P, P, P], ctypes.c_int),
+                "stpc_result_host_blobs": ([P], P),
                 "stpc_decoder_create": ([ctypes.POINTER(P)], ctypes.c_int),
                 "stpc_decoder_destroy": ([P], None),
                 "stpc_decoder_load": ([P, P, I32, P, I32, P, P], ctypes.c_int),

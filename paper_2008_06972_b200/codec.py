@@ -33,6 +33,7 @@ from .geometry import (
     AngularResolution,
     RigidTransform,
     frame_transforms,
+    poses_to_transform_rows,
     poses_to_transforms,
     ray_trig_tables,
 )
@@ -167,6 +168,17 @@ class Encoder:
         _native.check(self._L.stpc_encode_host(self._h, n_groups, points.ctypes.data, off.ctypes.data,
                                                xf.ctypes.data, out_ptr, cap, stream))
 
+    def encode_host_gather(self, n_groups: int, frames: Sequence[np.ndarray], transforms: np.ndarray,
+                           stream: int = 0) -> None:
+        """Per-frame host arrays (contiguous (N, 3) of the encoder's dtype):
+        gathered natively into pinned staging, pipelined with the encode."""
+        n = len(frames)
+        ptrs = (ctypes.c_void_p * max(n, 1))(*[a.ctypes.data if a.size else None for a in frames])
+        counts = np.array([a.shape[0] if a.size else 0 for a in frames], np.int64)
+        xf = np.ascontiguousarray(transforms, dtype=np.float64)
+        _native.check(self._L.stpc_encode_host_gather(self._h, n_groups, ptrs, counts.ctypes.data,
+                                                      xf.ctypes.data, stream))
+
     # -- results -------------------------------------------------------------
     def blob_layout(self) -> Tuple[np.ndarray, np.ndarray]:
         G = self._L.stpc_result_groups(self._h)
@@ -177,6 +189,9 @@ class Encoder:
 
     def blobs(self, arena: Optional[np.ndarray] = None) -> List[bytes]:
         off, ln = self.blob_layout()
+        host = self._L.stpc_result_host_blobs(self._h) if arena is None else None
+        if host:  # blobs already in the encoder's pinned arena: one copy per blob
+            return [ctypes.string_at(host + int(o), int(n)) for o, n in zip(off[:-1], ln)]
         if arena is None:
             arena = np.empty(int(off[-1]), np.uint8)
             _native.check(self._L.stpc_result_copy_blobs(self._h, arena.ctypes.data, arena.nbytes, None))
@@ -258,6 +273,24 @@ def _stack_points(clouds) -> Tuple[np.ndarray, np.ndarray, bool, List[int]]:
     return np.ascontiguousarray(pts), off, f64, counts
 
 
+def _frame_arrays(clouds) -> Tuple[List[np.ndarray], bool, List[int]]:
+    """Per-frame contiguous (N, 3) arrays of one dtype (float32, or float64
+    when any frame is not float32 -- the reference up-casts to float64),
+    without concatenating them."""
+    arrs = [np.asarray(c) for c in clouds]
+    counts = []
+    f64 = False
+    for a in arrs:
+        if a.size and (a.ndim != 2 or a.shape[1] != 3):
+            raise ValueError("cloud must be an (N, 3) array")
+        counts.append(0 if a.size == 0 else a.shape[0])
+        if a.size and a.dtype != np.float32:
+            f64 = True
+    dt = np.float64 if f64 else np.float32
+    frames = [np.ascontiguousarray(a.reshape(-1, 3), dtype=dt) for a in arrs]
+    return frames, f64, counts
+
+
 def _reports(cfg: CodecConfig, stats: np.ndarray, blobs: List[bytes], counts_per_group, timings) -> List[EncodeReport]:
     n = cfg.n_frames
     out = []
@@ -296,18 +329,24 @@ def compress_groups(groups: Sequence[Sequence[np.ndarray]], cfg: CodecConfig,
     """Encode many independent groups in one device pass; one blob per group,
     each byte-identical to ``compress(group, cfg, poses=poses[g])``."""
     t0 = time.perf_counter()
-    xf = []
-    for g, clouds in enumerate(groups):
+    for clouds in groups:
         if len(clouds) != cfg.n_frames:
             raise DataError(f"config expects {cfg.n_frames} frames, got {len(clouds)}")
-        ts = _transforms_for(cfg, None if poses is None else poses[g], None, None, None)
-        xf.extend(t.row12() for t in ts)
-    xf = np.asarray(xf, np.float64).reshape(-1, 12)
+    if cfg.n_frames > 1 and poses is not None and len(groups):
+        if len(poses) != len(groups) or any(len(p) != cfg.n_frames for p in poses):
+            raise DataError("need one pose per frame")
+        xf = poses_to_transform_rows(poses, cfg.k_index)  # batched, same bits as per group
+    else:
+        xf = []
+        for g, clouds in enumerate(groups):
+            ts = _transforms_for(cfg, None if poses is None else poses[g], None, None, None)
+            xf.extend(t.row12() for t in ts)
+        xf = np.asarray(xf, np.float64).reshape(-1, 12)
     t1 = time.perf_counter()
-    pts, off, f64, counts = _stack_points([c for grp in groups for c in grp])
+    frames, f64, counts = _frame_arrays([c for grp in groups for c in grp])
     enc = get_encoder(cfg, f64)
     with enc.lock:
-        enc.encode_host(len(groups), pts, off, xf)
+        enc.encode_host_gather(len(groups), frames, xf)
         blobs = enc.blobs()
         stats = enc.frame_stats()
     t2 = time.perf_counter()

@@ -11,6 +11,7 @@
 #include <chrono>
 #include <cstring>
 #include <string>
+#include <thread>
 #include <vector>
 #include <algorithm>
 
@@ -76,6 +77,9 @@ struct stpc_encoder {
     cudaStream_t copy_stream = nullptr;
     cudaEvent_t ev_h2d[2] = {}, ev_done[2] = {};
     bool host_result = false;            // last result assembled on the host
+    HostBuf gstage[2];                   // pinned gather staging (stpc_encode_host_gather)
+    HostBuf hout;                        // encoder-owned pinned blob arena (gather path)
+    bool own_host_blobs = false;         // last host result lives in hout
     std::vector<long long> acc_payload;  // per group raw payload lengths
     HostBuf acc_stats;                   // pinned [F][FS_COUNT]
     // profiling
@@ -558,11 +562,38 @@ int stpc_encode_device(stpc_encoder* enc, int32_t n_groups, const void* d_points
     return encode_impl(enc, n_groups, d_points, (const int64_t*)point_offsets, transforms, (cudaStream_t)stream);
 }
 
-int stpc_encode_host(stpc_encoder* enc, int32_t n_groups, const void* h_points,
-                     const int64_t* point_offsets, const double* transforms, uint8_t* h_out,
-                     int64_t out_cap, void* stream)
+}  // extern "C"
+
+// copy frames [f0, f1) (host pointers fptrs[f], counts from the offsets) to
+// dst in order, frames spread over host threads
+static void gather_frames(char* dst, const void* const* fptrs, const int64_t* point_offsets, long long f0,
+                          long long f1, size_t esz)
 {
-    if (!enc || n_groups < 1 || !point_offsets || !transforms) {
+    const long long nf = f1 - f0;
+    if (nf <= 0) return;
+    const unsigned nt = (unsigned)std::max<long long>(1, std::min<long long>(
+        std::min<long long>(16, std::max(1u, std::thread::hardware_concurrency())), nf));
+    std::vector<std::thread> th;
+    for (unsigned t = 0; t < nt; ++t) {
+        th.emplace_back([=] {
+            for (long long f = f0 + nf * t / nt; f < f0 + nf * (t + 1) / nt; ++f) {
+                const long long cnt = point_offsets[f + 1] - point_offsets[f];
+                if (cnt > 0)
+                    memcpy(dst + esz * 3 * (point_offsets[f] - point_offsets[f0]), fptrs[f], esz * 3 * (size_t)cnt);
+            }
+        });
+    }
+    for (auto& x : th) x.join();
+}
+
+// Host-memory encode.  Points come from one contiguous buffer (hp) or from
+// per-frame pointers (fptrs, gathered into pinned staging).  Blobs go to
+// h_out, or (own_out) to the encoder's pinned arena, or stay on the device.
+static int encode_host_impl(stpc_encoder* enc, int32_t n_groups, const char* hp, const void* const* fptrs,
+                            const int64_t* point_offsets, const double* transforms, uint8_t* h_out,
+                            int64_t out_cap, void* stream, bool own_out)
+{
+    if (!enc || n_groups < 1 || !point_offsets || !transforms || (!hp && !fptrs)) {
         g_err = "invalid arguments";
         return STPC_ERR_ARG;
     }
@@ -570,7 +601,7 @@ int stpc_encode_host(stpc_encoder* enc, int32_t n_groups, const void* h_points,
     const int n = enc->n;
     const long long F = (long long)n_groups * n;
     const size_t esz = enc->cfg.points_f64 ? sizeof(double) : sizeof(float);
-    const char* hp = (const char*)h_points;
+    enc->own_host_blobs = false;
     // Small batches: one H2D + encode + D2H.
     // measured on the bench workload (1024 groups): 8 chunks 232.5 ms,
     // 16: 227.7, 24: 226.8, 32: 239.4 -- the tail (last chunk's encode + blob
@@ -579,12 +610,16 @@ int stpc_encode_host(stpc_encoder* enc, int32_t n_groups, const void* h_points,
     if (n_chunks > 1 && getenv("STPC_PIPE_CHUNKS")) {  // tuning knob
         n_chunks = std::max(2, std::min(atoi(getenv("STPC_PIPE_CHUNKS")), n_groups / 8));
     }
-    if (n_chunks == 1 || !h_out) {
+    if (n_chunks == 1 || (!h_out && !own_out)) {
         long long npts = point_offsets[F] - point_offsets[0];
         ENS(enc->pts, esz * 3 * std::max<long long>(npts, 1));
-        if (npts > 0)
-            CK(cudaMemcpyAsync(enc->pts.p, hp + esz * 3 * point_offsets[0], esz * 3 * npts,
-                               cudaMemcpyHostToDevice, s));
+        const char* src = hp ? hp + esz * 3 * point_offsets[0] : nullptr;
+        if (!hp) {
+            ENS(enc->gstage[0], esz * 3 * std::max<long long>(npts, 1));
+            gather_frames(enc->gstage[0].as<char>(), fptrs, point_offsets, 0, F, esz);
+            src = enc->gstage[0].as<char>();
+        }
+        if (npts > 0) CK(cudaMemcpyAsync(enc->pts.p, src, esz * 3 * npts, cudaMemcpyHostToDevice, s));
         std::vector<int64_t> off(point_offsets, point_offsets + F + 1);
         for (auto& o : off) o -= point_offsets[0];
         int rc = encode_impl(enc, n_groups, enc->pts.p, off.data(), transforms, s);
@@ -635,16 +670,49 @@ int stpc_encode_host(stpc_encoder* enc, int32_t n_groups, const void* h_points,
         CK(cudaStreamSynchronize(s));
     }
     std::vector<long long> blob_off(n_groups + 1, 0), enc_len(n_groups, 0), payload(n_groups, 0);
+    // gather (per-frame mode): host threads copy chunk c into pinned stage
+    // c&1 once that stage's previous H2D (chunk c-2) has drained; runs on a
+    // helper thread one chunk ahead, concurrently with encode_impl(c - 1)
+    if (!hp) {
+        ENS(enc->gstage[0], esz * 3 * max_pts);
+        ENS(enc->gstage[1], esz * 3 * max_pts);
+    }
+    auto gather = [&](int c) -> int {
+        const int b = c & 1;
+        const int g0 = c * gc, g1 = std::min(n_groups, g0 + gc);
+        if (c >= 2 && cudaEventSynchronize(enc->ev_h2d[b]) != cudaSuccess) return STPC_ERR_CUDA;
+        auto gt0 = std::chrono::steady_clock::now();
+        gather_frames(enc->gstage[b].as<char>(), fptrs, point_offsets, (long long)g0 * n, (long long)g1 * n, esz);
+        if (getenv("STPC_PIPE_TRACE"))
+            fprintf(stderr, "host: gather(%d) %.2f ms\n", c,
+                    std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - gt0).count());
+        return STPC_OK;
+    };
     auto h2d = [&](int c) -> int {
         const int b = c & 1;
         const int g0 = c * gc, g1 = std::min(n_groups, g0 + gc);
         const long long p0 = point_offsets[(long long)g0 * n], p1 = point_offsets[(long long)g1 * n];
         CK(cudaStreamWaitEvent(enc->copy_stream, enc->ev_done[b], 0));
+        const char* src = hp ? hp + esz * 3 * p0 : enc->gstage[b].as<char>();
         if (p1 > p0)
-            CK(cudaMemcpyAsync(enc->pts2[b].p, hp + esz * 3 * p0, esz * 3 * (p1 - p0), cudaMemcpyHostToDevice,
+            CK(cudaMemcpyAsync(enc->pts2[b].p, src, esz * 3 * (p1 - p0), cudaMemcpyHostToDevice,
                                enc->copy_stream));
         CK(cudaEventRecord(enc->ev_h2d[b], enc->copy_stream));
         return STPC_OK;
+    };
+    auto chunk_ok = [&](int c) { return c < n_chunks && c * gc < n_groups; };
+    std::thread helper;
+    int helper_rc = STPC_OK;
+    struct JoinGuard {
+        std::thread& t;
+        ~JoinGuard()
+        {
+            if (t.joinable()) t.join();
+        }
+    } join_guard{helper};
+    auto join_helper = [&]() -> int {
+        if (helper.joinable()) helper.join();
+        return helper_rc;
     };
     // optional timeline (STPC_PIPE_TRACE=1): per chunk H2D end / encode end
     const bool trace = getenv("STPC_PIPE_TRACE") != nullptr;
@@ -654,17 +722,28 @@ int stpc_encode_host(stpc_encoder* enc, int32_t n_groups, const void* h_points,
         cudaEventCreate(&t0);
         cudaEventRecord(t0, s);
     }
+    if (!hp) {
+        int grc = gather(0);
+        if (grc) return grc;
+    }
     int rc = h2d(0);
     if (rc) return rc;
     if (trace) { tev.emplace_back(); cudaEventCreate(&tev.back()); cudaEventRecord(tev.back(), enc->copy_stream); }
+    if (!hp && chunk_ok(1)) helper = std::thread([&] { helper_rc = gather(1); });
     long long out_pos = 0;
+    if (own_out) ENS(enc->hout, (size_t)(esz * 3 * (point_offsets[F] - point_offsets[0]) / 6 + (1 << 20)));
     for (int c = 0; c < n_chunks; ++c) {
         const int g0 = c * gc, g1 = std::min(n_groups, g0 + gc);
         if (g0 >= g1) break;
         const int b = c & 1;
-        if (c + 1 < n_chunks && (c + 1) * gc < n_groups) {
+        if (chunk_ok(c + 1)) {
             auto hA = std::chrono::steady_clock::now();
+            if (!hp) {
+                rc = join_helper();
+                if (rc) return rc;
+            }
             rc = h2d(c + 1);
+            if (!hp && !rc && chunk_ok(c + 2)) helper = std::thread([&, cc = c + 2] { helper_rc = gather(cc); });
             if (trace)
                 fprintf(stderr, "host: h2d(%d) enqueue took %.2f ms\n", c + 1,
                         std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - hA).count());
@@ -681,11 +760,21 @@ int stpc_encode_host(stpc_encoder* enc, int32_t n_groups, const void* h_points,
         CK(cudaEventRecord(enc->ev_done[b], s));
         if (trace) { tev.emplace_back(); cudaEventCreate(&tev.back()); cudaEventRecord(tev.back(), s); }
         const long long total = enc->h_blob_off[g1 - g0];
-        if (out_pos + total > out_cap) {
+        if (own_out && out_pos + total > (long long)enc->hout.cap) {
+            // grow the encoder's arena, keeping the blobs already copied
+            CK(cudaStreamSynchronize(s));
+            HostBuf bigger;
+            if (bigger.ensure((size_t)((out_pos + total) * 3 / 2 + (1 << 20)))) return STPC_ERR_NOMEM;
+            if (out_pos > 0) memcpy(bigger.p, enc->hout.p, (size_t)out_pos);
+            std::swap(bigger.p, enc->hout.p);
+            std::swap(bigger.cap, enc->hout.cap);
+        }
+        uint8_t* out_base = own_out ? enc->hout.as<uint8_t>() : h_out;
+        if (!own_out && out_pos + total > out_cap) {
             g_err = "output buffer too small";
             return STPC_ERR_ARG;
         }
-        if (total > 0) CK(cudaMemcpyAsync(h_out + out_pos, enc->blobs.p, (size_t)total, cudaMemcpyDeviceToHost, s));
+        if (total > 0) CK(cudaMemcpyAsync(out_base + out_pos, enc->blobs.p, (size_t)total, cudaMemcpyDeviceToHost, s));
         CK(cudaMemcpyAsync(enc->acc_stats.as<long long>() + FS_COUNT * f0, enc->fstats.p,
                            sizeof(long long) * FS_COUNT * (f1 - f0), cudaMemcpyDeviceToHost, s));
         for (int i = 0; i < g1 - g0; ++i) {
@@ -712,7 +801,46 @@ int stpc_encode_host(stpc_encoder* enc, int32_t n_groups, const void* h_points,
     enc->h_enc_len = enc_len;
     enc->h_payload_len = payload;
     enc->host_result = true;
+    enc->own_host_blobs = own_out;
     return STPC_OK;
+}
+
+extern "C" {
+
+int stpc_encode_host(stpc_encoder* enc, int32_t n_groups, const void* h_points,
+                     const int64_t* point_offsets, const double* transforms, uint8_t* h_out,
+                     int64_t out_cap, void* stream)
+{
+    if (!h_points) {
+        g_err = "invalid arguments";
+        return STPC_ERR_ARG;
+    }
+    return encode_host_impl(enc, n_groups, (const char*)h_points, nullptr, point_offsets, transforms, h_out,
+                            out_cap, stream, false);
+}
+
+int stpc_encode_host_gather(stpc_encoder* enc, int32_t n_groups, const void* const* frame_points,
+                            const int64_t* frame_counts, const double* transforms, void* stream)
+{
+    if (!enc || n_groups < 1 || !frame_points || !frame_counts) {
+        g_err = "invalid arguments";
+        return STPC_ERR_ARG;
+    }
+    const long long F = (long long)n_groups * enc->n;
+    std::vector<int64_t> off(F + 1, 0);
+    for (long long f = 0; f < F; ++f) {
+        if (frame_counts[f] < 0 || (frame_counts[f] > 0 && !frame_points[f])) {
+            g_err = "invalid frame";
+            return STPC_ERR_ARG;
+        }
+        off[f + 1] = off[f] + frame_counts[f];
+    }
+    return encode_host_impl(enc, n_groups, nullptr, frame_points, off.data(), transforms, nullptr, 0, stream, true);
+}
+
+const uint8_t* stpc_result_host_blobs(const stpc_encoder* enc)
+{
+    return (enc && enc->host_result && enc->own_host_blobs) ? enc->hout.as<uint8_t>() : nullptr;
 }
 
 int stpc_encoder_wait(stpc_encoder* enc, void* stream)
@@ -752,11 +880,19 @@ const uint8_t* stpc_result_device_blobs(const stpc_encoder* enc)
 int stpc_result_copy_blobs(const stpc_encoder* enc, uint8_t* h_dst, int64_t cap, void* stream)
 {
     if (!enc || !h_dst) return STPC_ERR_ARG;
+    long long total = enc->G ? enc->h_blob_off[enc->G] : 0;
+    if (enc->host_result && enc->own_host_blobs) {
+        if (total > cap) {
+            g_err = "output buffer too small: need " + std::to_string(total);
+            return STPC_ERR_ARG;
+        }
+        memcpy(h_dst, enc->hout.p, (size_t)total);
+        return STPC_OK;
+    }
     if (enc->host_result) {
         g_err = "blobs of a pipelined host encode are already in the caller's buffer";
         return STPC_ERR_ARG;
     }
-    long long total = enc->G ? enc->h_blob_off[enc->G] : 0;
     if (total > cap) {
         g_err = "output buffer too small: need " + std::to_string(total);
         return STPC_ERR_ARG;

@@ -111,6 +111,75 @@ def poses_to_transforms(poses: Sequence, k_index: int) -> List[RigidTransform]:
     return out
 
 
+def rotations_valid(R: np.ndarray) -> np.ndarray:
+    """RigidTransform's checks (motion.py:52-62) over stacked (..., 3, 3)
+    matrices: allclose(R.T @ R, I, atol=1e-6) and isclose(det R, 1,
+    atol=1e-6).  Stacked matmul / det run the same per-matrix kernels as the
+    single-matrix calls; entries within 1e-12 of the allclose threshold (or
+    non-finite) are re-checked with the per-matrix expression."""
+    R = np.asarray(R, np.float64)
+    flat = R.reshape(-1, 3, 3)
+    eye = np.eye(3)
+    with np.errstate(all="ignore"):
+        dev = np.abs(np.matmul(np.transpose(flat, (0, 2, 1)), flat) - eye)
+        thr = ORTHONORMAL_ATOL + 1e-5 * eye
+        orth = np.all(dev <= thr, axis=(1, 2))
+        near = np.any(np.abs(dev - thr) < 1e-12, axis=(1, 2)) | ~np.all(np.isfinite(flat), axis=(1, 2))
+        detok = np.abs(np.linalg.det(flat) - 1.0) <= ORTHONORMAL_ATOL + 1e-5
+    for i in np.flatnonzero(near):
+        orth[i] = np.allclose(flat[i].T @ flat[i], eye, atol=ORTHONORMAL_ATOL)
+    return (orth & detok).reshape(R.shape[:-2]), orth.reshape(R.shape[:-2])
+
+
+def poses_to_transform_rows(poses_per_group: Sequence[Sequence], k_index: int) -> np.ndarray:
+    """poses_to_transforms + round_f32 for many groups at once, as (G*n, 12)
+    rows R | T.  Bit-identical to the per-group path: stacked np.matmul runs
+    numpy's per-matrix BLAS kernel for every item (tests/test_host.py pins
+    this), and every RigidTransform the per-group path constructs -- input
+    poses, the key inverse, the compositions, the float32-rounded results --
+    is validated the same way (ValueError on the first invalid one)."""
+    G = len(poses_per_group)
+    n = len(poses_per_group[0]) if G else 0
+    R = np.empty((G, n, 3, 3))
+    T = np.empty((G, n, 3))
+    for g, poses in enumerate(poses_per_group):
+        if len(poses) != n:
+            raise ValueError("every group needs the same number of poses")
+        for f, p in enumerate(poses):
+            if isinstance(p, RigidTransform) or (hasattr(p, "R") and hasattr(p, "T")):
+                R[g, f] = np.asarray(p.R, np.float64)
+                T[g, f] = np.asarray(p.T, np.float64).reshape(3)
+            else:
+                Rp, Tp = p
+                Rp = np.asarray(Rp, np.float64)
+                if Rp.shape != (3, 3):
+                    raise ValueError("R must be 3x3")
+                R[g, f] = Rp
+                T[g, f] = np.asarray(Tp, np.float64).reshape(3)
+
+    def check(M, what):
+        ok, orth = rotations_valid(M)
+        if not ok.all():
+            i = int(np.flatnonzero(~ok.reshape(-1))[0])
+            raise ValueError("R is not orthonormal" if not orth.reshape(-1)[i]
+                             else "R must be a proper rotation (det +1)")
+
+    check(R, "pose")
+    Rk = R[:, k_index]
+    Rki = np.transpose(Rk, (0, 2, 1))
+    Tki = -np.matmul(Rki, T[:, k_index, :, None])[:, :, 0]
+    check(Rki, "inverse")
+    CR = np.matmul(Rki[:, None], R)
+    CT = np.matmul(Rki[:, None], T[..., None])[..., 0] + Tki[:, None, :]
+    check(CR, "compose")
+    CR[:, k_index] = np.eye(3)
+    CT[:, k_index] = 0.0
+    CRf = CR.astype(np.float32).astype(np.float64)
+    CTf = CT.astype(np.float32).astype(np.float64)
+    check(CRf, "round_f32")
+    return np.concatenate([CRf.reshape(G, n, 9), CTf], axis=2).reshape(G * n, 12)
+
+
 def build_rotation(da: float, db: float, dg: float) -> np.ndarray:
     """Rz(da) @ Ry(db) @ Rx(dg) with the reference's row signs (motion.py:105-116)."""
     ca, sa = np.cos(da), np.sin(da)

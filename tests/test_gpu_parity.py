@@ -243,6 +243,37 @@ def test_batch_equals_per_group():
         assert b == compress(g.clouds, cfg, poses=g.poses)[0]
 
 
+@pytest.mark.parametrize("G,f64", [(70, False), (131, False), (66, True)])
+def test_compress_groups_gather_pipeline(G, f64):
+    """compress_groups hands per-frame arrays to stpc_encode_host_gather
+    (threaded gather into pinned staging, pipelined in 8 / 16 chunks, blobs
+    in the encoder's own arena, grown on demand); every blob equals the
+    single-group compress, and spot checks equal the oracle.  Includes empty
+    frames and a float64 batch."""
+    import math
+
+    from paper_2008_06972_b200 import AngularResolution, CodecConfig, compress, compress_groups, synth
+
+    sensor = synth.Sensor(300, 12, 2 * math.pi / 300, math.radians(2.0), math.radians(88.0))
+    cfg = CodecConfig(mode="stream", tau=0.1, tile_w=4, tile_h=3,
+                      res=AngularResolution(sensor.theta_r, sensor.phi_r), phi_offset=sensor.phi_offset,
+                      w=sensor.w, h=sensor.h, n_frames=3)
+    groups, poses = [], []
+    for gi in range(G):
+        grp = synth.make_group(8000 + gi, 3, sensor, n_boxes=4)
+        clouds = [c.astype(np.float64) for c in grp.clouds] if f64 else list(grp.clouds)
+        if gi % 17 == 5:
+            clouds[1] = np.zeros((0, 3), clouds[1].dtype)  # an empty frame
+        groups.append(clouds)
+        poses.append(grp.poses)
+    blobs, reps = compress_groups(groups, cfg, poses)
+    assert len(blobs) == G
+    for gi in (0, 5, G // 2, G - 1):
+        assert blobs[gi] == compress(groups[gi], cfg, poses=poses[gi])[0]
+        assert blobs[gi] == oracle.compress(groups[gi], cfg, poses[gi])[0]
+    assert sum(reps[5].point_counts) == sum(c.shape[0] for c in groups[5])
+
+
 def test_fit_intermediates_match_oracle():
     """Runs (s, len, f32 a/b/c), temporal offsets and tile classes per chain."""
     from paper_2008_06972_b200 import _native, get_encoder, compress, synth

@@ -285,3 +285,30 @@ def test_decoder_batched_transforms_equal_per_frame_reference_expressions():
             assert type(bad[i]) is type(exc) and str(bad[i]) == str(exc)
             continue
         assert np.array_equal(good[i], ref, equal_nan=True)
+
+
+def test_batched_pose_transforms_equal_per_group_bits():
+    """poses_to_transform_rows (compress_groups' batched path) == per-group
+    poses_to_transforms + round_f32, bit for bit, and raises ValueError for an
+    invalid pose like the per-group RigidTransform checks."""
+    from paper_2008_06972_b200.geometry import RigidTransform, poses_to_transform_rows, poses_to_transforms
+
+    rng = np.random.default_rng(11)
+    G, n, k = 40, 8, 3
+    groups = []
+    for g in range(G):
+        q = rng.normal(size=(n, 4))
+        q /= np.linalg.norm(q, axis=1, keepdims=True)
+        w, x, y, z = q.T
+        Rs = np.stack([1 - 2 * (y * y + z * z), 2 * (x * y - z * w), 2 * (x * z + y * w),
+                       2 * (x * y + z * w), 1 - 2 * (x * x + z * z), 2 * (y * z - x * w),
+                       2 * (x * z - y * w), 2 * (y * z + x * w), 1 - 2 * (x * x + y * y)], 1).reshape(n, 3, 3)
+        Ts = rng.normal(size=(n, 3)) * 40
+        groups.append([(Rs[i], Ts[i]) if i % 2 else RigidTransform(Rs[i], Ts[i]) for i in range(n)])
+    rows = poses_to_transform_rows(groups, k)
+    ref = np.concatenate([[t.round_f32().row12() for t in poses_to_transforms(p, k)] for p in groups])
+    assert np.array_equal(rows, ref)
+    bad = [list(p) for p in groups[:2]]
+    bad[1][4] = (np.eye(3) * 2.0, np.zeros(3))
+    with pytest.raises(ValueError):
+        poses_to_transform_rows(bad, k)
