@@ -250,9 +250,12 @@ __device__ __forceinline__ bool cert_holds(const float4* cert, int j, double a, 
     const double n01 = fabs((dc - da * (double)c2.x) - db * (double)c2.w);
     const double n10 = fabs((dc - da * (double)c2.y) - db * (double)c2.z);
     const double n11 = fabs((dc - da * (double)c2.y) - db * (double)c2.w);
-    double B = fmax(fmax(n00, n01), fmax(n10, n11)) / dlo;
-    B = B * (1.0 + 1e-6) + 1e-9;
-    return B < (double)c0.w && (double)c1.y - B > 0.0 && (double)c1.z + B < r_max;
+    // Division-free form of  B (1 + 1e-6) + 1e-9 < min(m, rmin, r_max - rmax)
+    // with B = max|n| / dlo (dlo > 0): the doubled relative slack absorbs the
+    // rounding of the rearranged products, so this is at least as strict.
+    const double lhs = fmax(fmax(n00, n01), fmax(n10, n11)) * (1.0 + 2e-6);
+    return lhs < ((double)c0.w - 1e-9) * dlo && lhs < ((double)c1.y - 1e-9) * dlo &&
+           lhs < ((r_max - (double)c1.z) - 1e-9) * dlo;  // a NaN field fails every comparison
 }
 
 // Union [s, e] under (a, b, c): new tile e in full, older tiles by

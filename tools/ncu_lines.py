@@ -1,6 +1,7 @@
 """Per-source-line instruction / stall-sample shares of one kernel in an ncu report.
 
     python tools/ncu_lines.py gpurun_out/rep.ncu-rep <kernel-regex> [launch-index] [top]
+    STPC_SORT=stall_long_sb python tools/ncu_lines.py ...   # rank by one stall column
 
 Maps the report's SASS page (addresses) to CUDA source lines through the
 line table of the in-tree library's cubins (nvdisasm -g), because the CSV
@@ -19,8 +20,8 @@ import sys
 import tempfile
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-LIB = os.path.join(ROOT, "paper_2008_06972_b200", "libstpc_b200.so")
-CSRC = os.path.join(ROOT, "paper_2008_06972_b200", "csrc")
+LIB = os.environ.get("STPC_B200_LIB", os.path.join(ROOT, "paper_2008_06972_b200", "libstpc_b200.so"))
+CSRC = os.environ.get("STPC_CSRC", os.path.join(ROOT, "paper_2008_06972_b200", "csrc"))
 
 
 def line_table(func_regex):
@@ -63,7 +64,9 @@ def main():
             cur["rows"].append(r)
     blk = blocks[idx]
     h, data = blk["hdr"], blk["rows"]
-    ie, smp = h.index("Instructions Executed"), h.index("# Samples")
+    ie = h.index("Instructions Executed")
+    # STPC_SORT=<column> (e.g. stall_long_sb) ranks lines by that sample column
+    smp = h.index(os.environ.get("STPC_SORT", "# Samples"))
     fname = re.sub(r"[<(].*", "", kre)
     table = line_table(fname)
     base = int(data[0][0], 16)
@@ -80,7 +83,7 @@ def main():
     for f in glob.glob(os.path.join(CSRC, "*.cu*")):
         src[os.path.basename(f)] = open(f).read().split("\n")
     print(f"{kre} #{idx}: {ti} warp instructions, {ts} samples")
-    for k, v in sorted(agg.items(), key=lambda x: -x[1][0])[:top]:
+    for k, v in sorted(agg.items(), key=lambda x: -x[1][1 if "STPC_SORT" in os.environ else 0])[:top]:
         txt = src[k[0]][k[1] - 1].strip()[:80] if k[0] in src and k[1] > 0 else ""
         print(f"{k[0]:>14}:{k[1]:<5} inst {100 * v[0] / ti:5.1f}%  smp {100 * v[1] / ts:5.1f}%  {txt}")
 
