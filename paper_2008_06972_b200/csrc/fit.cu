@@ -258,6 +258,24 @@ __device__ __forceinline__ bool cert_holds(const float4* cert, int j, double a, 
            lhs < ((r_max - (double)c1.z) - 1e-9) * dlo;  // a NaN field fails every comparison
 }
 
+// cert_holds without branches: all three loads issue at once (their latency
+// can overlap other work), stale fields of an empty tile are ignored.
+__device__ __forceinline__ bool cert_holds_bf(const float4* cert, int j, double a, double b, double c,
+                                              double r_max)
+{
+    const float4 c0 = cert[CERT_F4 * j], c1 = cert[CERT_F4 * j + 1], c2 = cert[CERT_F4 * j + 2];
+    const double da = a - (double)c0.x, db = b - (double)c0.y, dc = c - (double)c0.z;
+    const double dlo = (double)c1.x - (fabs(da) + fabs(db));
+    const double n00 = fabs((dc - da * (double)c2.x) - db * (double)c2.z);
+    const double n01 = fabs((dc - da * (double)c2.x) - db * (double)c2.w);
+    const double n10 = fabs((dc - da * (double)c2.y) - db * (double)c2.z);
+    const double n11 = fabs((dc - da * (double)c2.y) - db * (double)c2.w);
+    const double lhs = fmax(fmax(n00, n01), fmax(n10, n11)) * (1.0 + 2e-6);
+    const bool proven = dlo > 2e-12 && lhs < ((double)c0.w - 1e-9) * dlo && lhs < ((double)c1.y - 1e-9) * dlo &&
+                        lhs < ((r_max - (double)c1.z) - 1e-9) * dlo;
+    return c0.w >= CERT_EMPTY || proven;
+}
+
 // Union [s, e] under (a, b, c): new tile e in full, older tiles by
 // certificate, falling back to a full test where the certificate is too weak.
 __device__ bool union_fits(const Chain& ch, const Geometry& g, const Trig& tg, int s, int e, double a,
@@ -973,13 +991,18 @@ __global__ void __launch_bounds__(FIT_WARPS * 32, STPC_PAIR_MINB) fit_pair_kerne
         const bool testing = live && grow && cnt > 0 && ok;
         bool pass = false;
         if (__any_sync(STPC_FULL, testing)) {
+            // the first certificate batch of [s, t) does not depend on the new
+            // tile's verdict: its loads and checks are issued before the pixel
+            // test so the two latency chains overlap
+            const bool weak0 = testing && s + gl < t && !cert_holds_bf(ch.cert, s + gl, na, nb, nc, A.r_max);
             pass = test_tile_pair(testing, ch, g, A.tg, t, na, nb, nc, A.tau, A.r_max);
             FIT_STAT(5, testing && gl == 0);        // growth tests
             FIT_STAT(6, testing && pass && gl == 0);  // growth tests passed (new tile)
             int base = s;
             while (__any_sync(STPC_FULL, pass && base < t)) {
                 const int j = base + gl;
-                const bool weak = pass && j < t && !cert_holds(ch.cert, j, na, nb, nc, A.r_max);
+                const bool weak =
+                    pass && j < t && (base == s ? weak0 : !cert_holds_bf(ch.cert, j, na, nb, nc, A.r_max));
                 FIT_STAT(3, pass && j < t);  // certificate checks
                 FIT_STAT(4, weak);           // weak certificates -> full re-test
                 unsigned wm = (__ballot_sync(STPC_FULL, weak) & gmask) >> (sub * 16);
