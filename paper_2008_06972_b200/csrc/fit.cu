@@ -700,6 +700,12 @@ __device__ __forceinline__ unsigned group_max(unsigned v, int sub, unsigned neut
 
 // Pixel test of tile `tile` for every active chain of the warp; on pass the
 // group's lane 0 stores the certificate.  Returns this chain's verdict.
+// One pixel per lane, so each certificate statistic of a lane is its own
+// pixel's value (or the reduction's neutral element): no per-lane min/max and
+// no clamping (a passing pixel has 0 < r_hat <= r_max).  The margin, r_hat
+// lower bound and r_max headroom share one field, the pixel's slack
+// X = min(tau - |r - r_hat|, r_hat, r_max - r_hat): cert_holds' three tests
+// B < m, B < rmin, B < r_max - rmax become B < X with c1.y = X, c1.z = 0.
 __device__ bool test_tile_pair(bool active, const Chain& ch, const Geometry& g, const Trig& tg, int tile,
                                double a, double b, double c, double tau, double r_max)
 {
@@ -712,8 +718,8 @@ __device__ bool test_tile_pair(bool active, const Chain& ch, const Geometry& g, 
         cols = min(g.tw, g.w - u0);
         npx = ch.rows * cols;
     }
-    double m = 1e300, dmin = 1e300, rmin = 1e300, rmax = 0.0;
-    double ylo = 1e300, yhi = -1e300, zlo = 1e300, zhi = -1e300;
+    const unsigned NEUT_MIN = 0xffffffffu, NEUT_MAX = 0u;
+    unsigned kx = NEUT_MIN, kd = NEUT_MIN, ky0 = NEUT_MIN, ky1 = NEUT_MAX, kz0 = NEUT_MIN, kz1 = NEUT_MAX;
     bool bad = false;
     if (gl < npx) {
         int dv, du;
@@ -729,35 +735,38 @@ __device__ bool test_tile_pair(bool active, const Chain& ch, const Geometry& g, 
                 bad = true;
             } else {
                 const double r_hat = c / den;
-                if (r_hat <= 0.0 || r_hat > r_max || fabs(r - r_hat) > tau) {
+                const double err = fabs(r - r_hat);
+                if (r_hat <= 0.0 || r_hat > r_max || err > tau) {
                     bad = true;
                 } else {
-                    m = tau - fabs(r - r_hat);
-                    dmin = ad;
-                    rmin = r_hat;
-                    rmax = r_hat;
-                    ylo = yhi = r_hat * dy;
-                    zlo = zhi = r_hat * dz;
+                    kx = __float_as_uint(__double2float_rd(fmin(fmin(tau - err, r_hat), r_max - r_hat)));
+                    kd = __float_as_uint(__double2float_rd(ad));
+                    const double yh = r_hat * dy, zh = r_hat * dz;
+                    ky0 = f2key(__double2float_rd(yh));
+                    ky1 = f2key(__double2float_ru(yh));
+                    kz0 = f2key(__double2float_rd(zh));
+                    kz1 = f2key(__double2float_ru(zh));
                 }
             }
         }
     }
     const bool fail = (__ballot_sync(STPC_FULL, bad) & gmask) != 0;
     if (!__any_sync(STPC_FULL, active && !fail)) return false;
-    const unsigned NEUT_MIN = 0xffffffffu, NEUT_MAX = 0u;
-    const unsigned um = group_min(__float_as_uint(__double2float_rd(fmin(m, 3.0e38))), sub, NEUT_MIN);
-    const unsigned ud = group_min(__float_as_uint(__double2float_rd(fmin(dmin, 3.0e38))), sub, NEUT_MIN);
-    const unsigned ulo = group_min(__float_as_uint(__double2float_rd(fmin(rmin, 3.0e38))), sub, NEUT_MIN);
-    const unsigned uhi = group_max(__float_as_uint(__double2float_ru(rmax)), sub, NEUT_MAX);
-    const unsigned ky0 = group_min(f2key(__double2float_rd(fmax(fmin(ylo, 3.0e38), -3.0e38))), sub, NEUT_MIN);
-    const unsigned ky1 = group_max(f2key(__double2float_ru(fmin(fmax(yhi, -3.0e38), 3.0e38))), sub, NEUT_MAX);
-    const unsigned kz0 = group_min(f2key(__double2float_rd(fmax(fmin(zlo, 3.0e38), -3.0e38))), sub, NEUT_MIN);
-    const unsigned kz1 = group_max(f2key(__double2float_ru(fmin(fmax(zhi, -3.0e38), 3.0e38))), sub, NEUT_MAX);
+    // X, dmin >= 0: their float bit patterns order like their values
+    const unsigned ux = group_min(kx, sub, NEUT_MIN);
+    const unsigned ud = group_min(kd, sub, NEUT_MIN);
+    ky0 = group_min(ky0, sub, NEUT_MIN);
+    ky1 = group_max(ky1, sub, NEUT_MAX);
+    kz0 = group_min(kz0, sub, NEUT_MIN);
+    kz1 = group_max(kz1, sub, NEUT_MAX);
     const bool pass = active && !fail;
     if (pass && gl == 0) {
         float4* ce = ch.cert + CERT_F4 * tile;
-        ce[0] = make_float4((float)a, (float)b, (float)c, __uint_as_float(um));
-        ce[1] = make_float4(__uint_as_float(ud), __uint_as_float(ulo), __uint_as_float(uhi), 0.0f);
+        // a tile whose pixels are all invalid certifies as empty (no neutral
+        // keys leak into the float fields)
+        const float xf = ux == NEUT_MIN ? CERT_EMPTY : __uint_as_float(ux);
+        ce[0] = make_float4((float)a, (float)b, (float)c, xf);
+        ce[1] = make_float4(__uint_as_float(ud), xf, 0.0f, 0.0f);
         ce[2] = make_float4(key2f(ky0), key2f(ky1), key2f(kz0), key2f(kz1));
     }
     return pass;
