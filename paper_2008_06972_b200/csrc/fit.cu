@@ -706,29 +706,19 @@ __device__ __forceinline__ unsigned group_max(unsigned v, int sub, unsigned neut
 // lower bound and r_max headroom share one field, the pixel's slack
 // X = min(tau - |r - r_hat|, r_hat, r_max - r_hat): cert_holds' three tests
 // B < m, B < rmin, B < r_max - rmax become B < X with c1.y = X, c1.z = 0.
-__device__ bool test_tile_pair(bool active, const Chain& ch, const Geometry& g, const Trig& tg, int tile,
-                               double a, double b, double c, double tau, double r_max)
+// `has`: the lane holds a valid pixel (r, direction) of the tile.
+__device__ __forceinline__ bool test_px_pair(bool active, bool has, double r, double dx, double dy, double dz,
+                                             const Chain& ch, int tile, double a, double b, double c,
+                                             double tau, double r_max)
 {
     const int lane = threadIdx.x & 31;
     const int sub = lane >> 4, gl = lane & 15;
     const unsigned gmask = 0xffffu << (sub * 16);
-    int npx = 0, u0 = 0, cols = 1;
-    if (active) {
-        u0 = tile * g.tw;
-        cols = min(g.tw, g.w - u0);
-        npx = ch.rows * cols;
-    }
     const unsigned NEUT_MIN = 0xffffffffu, NEUT_MAX = 0u;
     unsigned kx = NEUT_MIN, kd = NEUT_MIN, ky0 = NEUT_MIN, ky1 = NEUT_MAX, kz0 = NEUT_MIN, kz1 = NEUT_MAX;
     bool bad = false;
-    if (gl < npx) {
-        int dv, du;
-        divmod_small(gl, cols, __frcp_rn((float)cols), dv, du);
-        const int v = ch.v0 + dv, u = u0 + du;
-        const double r = ch.img[(long long)v * g.w + u];
-        if (isfinite(r)) {
-            double dx, dy, dz;
-            ray_dir(tg, v, u, dx, dy, dz);
+    {
+        if (has) {
             const double den = (dx + a * dy) + b * dz;
             const double ad = fabs(den);
             if (ad < STPC_PARALLEL_EPS) {
@@ -770,6 +760,30 @@ __device__ bool test_tile_pair(bool active, const Chain& ch, const Geometry& g, 
         ce[2] = make_float4(key2f(ky0), key2f(ky1), key2f(kz0), key2f(kz1));
     }
     return pass;
+}
+
+// test_px_pair with the lane's pixel of `tile` loaded from global memory.
+__device__ bool test_tile_pair(bool active, const Chain& ch, const Geometry& g, const Trig& tg, int tile,
+                               double a, double b, double c, double tau, double r_max)
+{
+    const int gl = threadIdx.x & 15;
+    bool has = false;
+    double r = 0.0, dx = 0.0, dy = 0.0, dz = 0.0;
+    if (active) {
+        const int u0 = tile * g.tw;
+        const int cols = min(g.tw, g.w - u0);
+        if (gl < ch.rows * cols) {
+            int dv, du;
+            divmod_small(gl, cols, __frcp_rn((float)cols), dv, du);
+            const int v = ch.v0 + dv, u = u0 + du;
+            r = ch.img[(long long)v * g.w + u];
+            if (isfinite(r)) {
+                ray_dir(tg, v, u, dx, dy, dz);
+                has = true;
+            }
+        }
+    }
+    return test_px_pair(active, has, r, dx, dy, dz, ch, tile, a, b, c, tau, r_max);
 }
 
 #ifndef STPC_PAIR_MINB
@@ -935,6 +949,7 @@ __global__ void __launch_bounds__(FIT_WARPS * 32, STPC_PAIR_MINB) fit_pair_kerne
         const int cols = live ? min(g.tw, g.w - u0) : 1;
         const int npx = masked ? 0 : ch.rows * cols;
         double x = 0.0, y = 0.0, z = 0.0, one = 0.0;
+        double fr = 0.0, fdx = 0.0, fdy = 0.0, fdz = 0.0;  // the lane's pixel, kept for the tile test
         if (gl < npx) {
             int dv, du;
             divmod_small(gl, cols, __frcp_rn((float)cols), dv, du);
@@ -947,6 +962,10 @@ __global__ void __launch_bounds__(FIT_WARPS * 32, STPC_PAIR_MINB) fit_pair_kerne
                 y = r * dy;
                 z = r * dz;
                 one = 1.0;
+                fr = r;
+                fdx = dx;
+                fdy = dy;
+                fdz = dz;
             }
         }
         const int cnt = __popc(__ballot_sync(STPC_FULL, one != 0.0) & gmask);
@@ -966,6 +985,11 @@ __global__ void __launch_bounds__(FIT_WARPS * 32, STPC_PAIR_MINB) fit_pair_kerne
             for (int j = 0; j < PG; ++j) acc += sm[j * 9 + kk];  // zeros beyond npx: exact
         }
         __syncwarp();
+        // the lane's pixel stays in its own transpose row for this step's tile test
+        row[0] = fr;
+        row[1] = fdx;
+        row[2] = fdy;
+        row[3] = fdz;
         // prefetch the next tile's pixel gl
         if (live && t + 1 < g.tx) {
             const int nu0 = (t + 1) * g.tw;
@@ -1004,7 +1028,8 @@ __global__ void __launch_bounds__(FIT_WARPS * 32, STPC_PAIR_MINB) fit_pair_kerne
             // tile's verdict: its loads and checks are issued before the pixel
             // test so the two latency chains overlap
             const bool weak0 = testing && s + gl < t && !cert_holds_bf(ch.cert, s + gl, na, nb, nc, A.r_max);
-            pass = test_tile_pair(testing, ch, g, A.tg, t, na, nb, nc, A.tau, A.r_max);
+            pass = test_px_pair(testing, testing && one != 0.0, row[0], row[1], row[2], row[3], ch, t, na, nb, nc,
+                                A.tau, A.r_max);
             FIT_STAT(5, testing && gl == 0);        // growth tests
             FIT_STAT(6, testing && pass && gl == 0);  // growth tests passed (new tile)
             int base = s;
