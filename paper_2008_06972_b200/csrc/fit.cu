@@ -786,6 +786,52 @@ __device__ bool test_tile_pair(bool active, const Chain& ch, const Geometry& g, 
     return test_px_pair(active, has, r, dx, dy, dz, ch, tile, a, b, c, tau, r_max);
 }
 
+// plane_from_sums (common.cuh; _kernels.py:23-76) for the half-warp that holds
+// the running sums (lane k of the group owns sum k): the six divides of the
+// inverse run in parallel, cofactor k in lane k, and are exchanged by
+// shuffles.  Every operation, operand and order is that of plane_from_sums,
+// so the bits are identical; all lanes of the warp must call it.
+__device__ __forceinline__ bool plane_from_sums_pair(double acc, int sub, int gl, double cond_limit, double& a,
+                                                     double& b, double& c)
+{
+    const int b0 = sub * PG;
+    const double s0 = shfl_d(acc, b0), s1 = shfl_d(acc, b0 + 1), s2 = shfl_d(acc, b0 + 2);
+    const double s3 = shfl_d(acc, b0 + 3), s4 = shfl_d(acc, b0 + 4), s5 = shfl_d(acc, b0 + 5);
+    const double s6 = shfl_d(acc, b0 + 6), s7 = shfl_d(acc, b0 + 7), s8 = shfl_d(acc, b0 + 8);
+    const double m00 = s0, m01 = s1, m02 = -s3, m11 = s2, m12 = -s4, m22 = s8;
+    const double r0 = -s5, r1 = -s6, r2 = s7;
+    const double c00 = m11 * m22 - m12 * m12;
+    const double c01 = m02 * m12 - m01 * m22;
+    const double c02 = m01 * m12 - m02 * m11;
+    const double det = (m00 * c00 + m01 * c01) + m02 * c02;
+    double num;
+    if (gl == 0) num = c00;
+    else if (gl == 1) num = c01;
+    else if (gl == 2) num = c02;
+    else if (gl == 3) num = m00 * m22 - m02 * m02;  // c11
+    else if (gl == 4) num = m01 * m02 - m00 * m12;  // c12
+    else num = m00 * m11 - m01 * m01;               // c22
+    const double q = num / det;
+    const double i00 = shfl_d(q, b0), i01 = shfl_d(q, b0 + 1), i02 = shfl_d(q, b0 + 2);
+    const double i11 = shfl_d(q, b0 + 3), i12 = shfl_d(q, b0 + 4), i22 = shfl_d(q, b0 + 5);
+    a = b = c = 0.0;
+    if (det == 0.0 || !isfinite(det)) return false;
+    const double norm_m = pymax3((fabs(m00) + fabs(m01)) + fabs(m02), (fabs(m01) + fabs(m11)) + fabs(m12),
+                                 (fabs(m02) + fabs(m12)) + fabs(m22));
+    const double norm_i = pymax3((fabs(i00) + fabs(i01)) + fabs(i02), (fabs(i01) + fabs(i11)) + fabs(i12),
+                                 (fabs(i02) + fabs(i12)) + fabs(i22));
+    const double cond = norm_m * norm_i;
+    if (!isfinite(cond) || cond > cond_limit) return false;
+    const double pa = (i00 * r0 + i01 * r1) + i02 * r2;
+    const double pb = (i01 * r0 + i11 * r1) + i12 * r2;
+    const double pc = (i02 * r0 + i12 * r1) + i22 * r2;
+    if (!(isfinite(pa) && isfinite(pb) && isfinite(pc))) return false;
+    a = pa;
+    b = pb;
+    c = pc;
+    return true;
+}
+
 #ifndef STPC_PAIR_MINB
 #define STPC_PAIR_MINB 8  // measured (fit_p): 5 -> 28.5 ms, 6 -> 29.1, 7 -> 26.5, 8 -> 26.3, 10 -> 29.8 (more chains in flight beat the spills)
 #endif
@@ -1010,13 +1056,12 @@ __global__ void __launch_bounds__(FIT_WARPS * 32, STPC_PAIR_MINB) fit_pair_kerne
         double na = 0.0, nb = 0.0, nc = 0.0;
         bool ok = false;
         {
-            double sv[9];
-#pragma unroll
-            for (int k = 0; k < 9; ++k) sv[k] = __shfl_sync(STPC_FULL, acc, sub * PG + k);
-            if (need && plane_from_sums(sv, A.cond_limit, na, nb, nc)) {
-                na = f32_round(na);
-                nb = f32_round(nb);
-                nc = f32_round(nc);
+            double pa, pb, pc;
+            const bool solved = plane_from_sums_pair(acc, sub, gl, A.cond_limit, pa, pb, pc);
+            if (need && solved) {
+                na = f32_round(pa);
+                nb = f32_round(pb);
+                nc = f32_round(pc);
                 ok = true;
             }
         }
