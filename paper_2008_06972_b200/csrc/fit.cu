@@ -1279,12 +1279,14 @@ __global__ void __launch_bounds__(128, STPC_REFIT_MINB) refit_kernel(RefitArgs A
             cnt += __popc(__ballot_sync(STPC_FULL, valid));
             sm[lane] = prod;  // +0.0 for invalid pixels: exact (see fit_rows)
             __syncwarp();
-            const int nj = min(32, npx - base);
-            if (nj == 32) {
+            // lanes past the span hold +0.0, so a fixed-length unrolled fold
+            // is exact; a one-tile span (16 pixels of 4x4) adds 16 terms
+            if (npx - base > 16) {
 #pragma unroll
                 for (int jj = 0; jj < 32; ++jj) acc += sm[jj];
             } else {
-                for (int jj = 0; jj < nj; ++jj) acc += sm[jj];
+#pragma unroll
+                for (int jj = 0; jj < 16; ++jj) acc += sm[jj];
             }
             __syncwarp();
         }
