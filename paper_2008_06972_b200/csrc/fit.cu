@@ -870,35 +870,30 @@ __global__ void __launch_bounds__(FIT_WARPS * 32, STPC_PAIR_MINB) fit_pair_kerne
 
     // Work stealing: each half-warp pulls chains from a global counter, so a
     // half whose chain finished early never idles beside a longer partner.
-    long long cid = -1;
+    // Chain state is kept lean (64 registers at 8 blocks per SM): the
+    // per-chain arrays are addressed from `slot` on use.
     bool finished = false;  // no chains left for this half
     bool done = true;       // current chain complete
-    int frame = 0, tr = 0;
-    long long slot = 0;
+    long long slot = 0;     // frame * ty + tile-row
     Chain ch;
     ch.skip1 = A.mode != 0;
-    uint8_t* crow = A.cls;
-    const uint8_t* sok = A.start_ok;
-    uint16_t* rs = A.run_s;
-    uint16_t* rl = A.run_len;
-    float* rabc = A.run_abc;
     int t = 0, s = 0, n_runs = 0;
     bool grow = false;
     double acc = 0.0, a = 0.0, b = 0.0, c = 0.0;
     int pf_t = -1;
     double pf_r = 0.0;
-    auto next_chain = [&]() {
-        long long nc = 0;
-        if (gl == 0) nc = (long long)atomicAdd(A.chain_counter, 1u);
-        nc = __shfl_sync(STPC_FULL, nc, sub * 16);
-        cid = nc;
+#define CROW (A.cls + slot * g.tx)
+#define SOK (A.start_ok + slot * g.tx)
+#define CERT (A.cert + slot * g.tx * CERT_F4)
+    auto take_chain = [&](long long cid) {
         if (cid >= n_chains) {
             finished = true;
             done = true;
             return;
         }
         const int job = (int)(cid / g.ty);
-        tr = (int)(cid % g.ty);
+        const int tr = (int)(cid % g.ty);
+        int frame;
         if (A.mode == 0) {
             frame = job * A.n_frames_group + A.k;
         } else {
@@ -908,15 +903,8 @@ __global__ void __launch_bounds__(FIT_WARPS * 32, STPC_PAIR_MINB) fit_pair_kerne
         }
         slot = (long long)frame * g.ty + tr;
         ch.img = A.best + (long long)frame * g.P;
-        crow = A.cls + slot * g.tx;
-        ch.crow = crow;
-        ch.cert = A.cert + slot * g.tx * CERT_F4;
         ch.v0 = tr * g.th;
         ch.rows = min(g.th, g.h - ch.v0);
-        sok = A.start_ok + slot * g.tx;
-        rs = A.run_s + slot * g.tx;
-        rl = A.run_len + slot * g.tx;
-        rabc = A.run_abc + slot * g.tx * 3;
         t = 0;
         s = 0;
         n_runs = 0;
@@ -925,7 +913,11 @@ __global__ void __launch_bounds__(FIT_WARPS * 32, STPC_PAIR_MINB) fit_pair_kerne
         pf_t = -1;
         done = false;
     };
-    next_chain();
+    {
+        long long nc = 0;
+        if (gl == 0) nc = (long long)atomicAdd(A.chain_counter, 1u);
+        take_chain(__shfl_sync(STPC_FULL, nc, sub * 16));
+    }
 
     while (__any_sync(STPC_FULL, !finished)) {
         // ---- (1) chains between runs jump to their next start tile
@@ -936,7 +928,7 @@ __global__ void __launch_bounds__(FIT_WARPS * 32, STPC_PAIR_MINB) fit_pair_kerne
             int base = t;
             while (__any_sync(STPC_FULL, scan && !found && base < g.tx)) {
                 const int j = base + gl;
-                const bool f = scan && !found && j < g.tx && sok[j];
+                const bool f = scan && !found && j < g.tx && SOK[j];
                 const unsigned mm = (__ballot_sync(STPC_FULL, f) & gmask) >> (sub * 16);
                 if (mm && !found) {
                     nt = base + __ffs(mm) - 1;
@@ -952,14 +944,14 @@ __global__ void __launch_bounds__(FIT_WARPS * 32, STPC_PAIR_MINB) fit_pair_kerne
         // ---- (1b) pass 2: a growing run extends over temporally covered
         // (class-1, fully masked) tiles without changing its sums, plane or
         // verdict; skip the whole stretch at once, certifying the tiles empty
-        if (__any_sync(STPC_FULL, !done && grow && ch.skip1 && crow[t] == 1)) {
-            const bool sk = !done && grow && ch.skip1 && crow[t] == 1;
+        if (__any_sync(STPC_FULL, !done && grow && ch.skip1 && CROW[t] == 1)) {
+            const bool sk = !done && grow && ch.skip1 && CROW[t] == 1;
             int nt = g.tx;
             bool found = false;
             int base = t;
             while (__any_sync(STPC_FULL, sk && !found && base < g.tx)) {
                 const int j = base + gl;
-                const bool f = sk && !found && j < g.tx && crow[j] != 1;
+                const bool f = sk && !found && j < g.tx && CROW[j] != 1;
                 const unsigned mm = (__ballot_sync(STPC_FULL, f) & gmask) >> (sub * 16);
                 if (mm && !found) {
                     nt = base + __ffs(mm) - 1;
@@ -969,18 +961,19 @@ __global__ void __launch_bounds__(FIT_WARPS * 32, STPC_PAIR_MINB) fit_pair_kerne
             }
             if (sk) {
                 for (int tt = t + gl; tt < nt; tt += PG)
-                    ch.cert[CERT_F4 * tt] = make_float4(0.f, 0.f, 0.f, CERT_EMPTY);
+                    CERT[CERT_F4 * tt] = make_float4(0.f, 0.f, 0.f, CERT_EMPTY);
                 t = nt;
                 if (t >= g.tx) {  // the run reaches the row end
                     if (gl == 0) {
-                        rs[n_runs] = (uint16_t)s;
-                        rl[n_runs] = (uint16_t)(g.tx - s);
-                        rabc[3 * n_runs] = (float)a;
-                        rabc[3 * n_runs + 1] = (float)b;
-                        rabc[3 * n_runs + 2] = (float)c;
+                        A.run_s[slot * g.tx + n_runs] = (uint16_t)s;
+                        A.run_len[slot * g.tx + n_runs] = (uint16_t)(g.tx - s);
+                        float* rabc = A.run_abc + (slot * g.tx + n_runs) * 3;
+                        rabc[0] = (float)a;
+                        rabc[1] = (float)b;
+                        rabc[2] = (float)c;
                     }
                     for (int tt = s + gl; tt < g.tx; tt += PG)
-                        if (crow[tt] != 1) crow[tt] = run_cls;
+                        if (CROW[tt] != 1) CROW[tt] = run_cls;
                     n_runs += 1;
                     grow = false;
                     done = true;
@@ -990,7 +983,7 @@ __global__ void __launch_bounds__(FIT_WARPS * 32, STPC_PAIR_MINB) fit_pair_kerne
         // ---- (2) fold tile t (a start folds from zero)
         const bool live = !done;
         if (live && !grow) acc = 0.0;
-        const bool masked = !live || (ch.skip1 && crow[t] == 1);
+        const bool masked = !live || (ch.skip1 && CROW[t] == 1);
         const int u0 = live ? t * g.tw : 0;
         const int cols = live ? min(g.tw, g.w - u0) : 1;
         const int npx = masked ? 0 : ch.rows * cols;
@@ -1069,6 +1062,7 @@ __global__ void __launch_bounds__(FIT_WARPS * 32, STPC_PAIR_MINB) fit_pair_kerne
         const bool testing = live && grow && cnt > 0 && ok;
         bool pass = false;
         if (__any_sync(STPC_FULL, testing)) {
+            ch.cert = CERT;
             // the first certificate batch of [s, t) does not depend on the new
             // tile's verdict: its loads and checks are issued before the pixel
             // test so the two latency chains overlap
@@ -1104,7 +1098,7 @@ __global__ void __launch_bounds__(FIT_WARPS * 32, STPC_PAIR_MINB) fit_pair_kerne
                 grow = true;
                 t += 1;
             } else if (cnt == 0) {
-                if (gl == 0) ch.cert[CERT_F4 * t] = make_float4(0.f, 0.f, 0.f, CERT_EMPTY);
+                if (gl == 0) CERT[CERT_F4 * t] = make_float4(0.f, 0.f, 0.f, CERT_EMPTY);
                 t += 1;
             } else if (pass) {
                 a = na; b = nb; c = nc;
@@ -1122,14 +1116,15 @@ __global__ void __launch_bounds__(FIT_WARPS * 32, STPC_PAIR_MINB) fit_pair_kerne
             }
             if (emit_e >= 0) {
                 if (gl == 0) {
-                    rs[n_runs] = (uint16_t)s;
-                    rl[n_runs] = (uint16_t)(emit_e - s);
-                    rabc[3 * n_runs] = (float)a;
-                    rabc[3 * n_runs + 1] = (float)b;
-                    rabc[3 * n_runs + 2] = (float)c;
+                    A.run_s[slot * g.tx + n_runs] = (uint16_t)s;
+                    A.run_len[slot * g.tx + n_runs] = (uint16_t)(emit_e - s);
+                    float* rabc = A.run_abc + (slot * g.tx + n_runs) * 3;
+                    rabc[0] = (float)a;
+                    rabc[1] = (float)b;
+                    rabc[2] = (float)c;
                 }
                 for (int tt = s + gl; tt < emit_e; tt += PG)
-                    if (!(ch.skip1 && crow[tt] == 1)) crow[tt] = run_cls;
+                    if (!(ch.skip1 && CROW[tt] == 1)) CROW[tt] = run_cls;
                 n_runs += 1;
             }
         }
@@ -1141,42 +1136,12 @@ __global__ void __launch_bounds__(FIT_WARPS * 32, STPC_PAIR_MINB) fit_pair_kerne
             long long nc = 0;
             if (handover && gl == 0) nc = (long long)atomicAdd(A.chain_counter, 1u);
             nc = __shfl_sync(STPC_FULL, nc, sub * 16);
-            if (handover) {
-                cid = nc;
-                if (cid >= n_chains) {
-                    finished = true;
-                } else {
-                    const int job = (int)(cid / g.ty);
-                    tr = (int)(cid % g.ty);
-                    if (A.mode == 0) {
-                        frame = job * A.n_frames_group + A.k;
-                    } else {
-                        int np = A.n_frames_group - 1;
-                        int grp = job / np, ii = job % np;
-                        frame = grp * A.n_frames_group + (ii < A.k ? ii : ii + 1);
-                    }
-                    slot = (long long)frame * g.ty + tr;
-                    ch.img = A.best + (long long)frame * g.P;
-                    crow = A.cls + slot * g.tx;
-                    ch.crow = crow;
-                    ch.cert = A.cert + slot * g.tx * CERT_F4;
-                    ch.v0 = tr * g.th;
-                    ch.rows = min(g.th, g.h - ch.v0);
-                    sok = A.start_ok + slot * g.tx;
-                    rs = A.run_s + slot * g.tx;
-                    rl = A.run_len + slot * g.tx;
-                    rabc = A.run_abc + slot * g.tx * 3;
-                    t = 0;
-                    s = 0;
-                    n_runs = 0;
-                    grow = false;
-                    acc = 0.0;
-                    pf_t = -1;
-                    done = false;
-                }
-            }
+            if (handover) take_chain(nc);
         }
     }
+#undef CROW
+#undef SOK
+#undef CERT
 }
 
 void launch_start_tiles(const FitArgs& a, cudaStream_t s)
