@@ -832,8 +832,18 @@ __device__ __forceinline__ bool plane_from_sums_pair(double acc, int sub, int gl
     return true;
 }
 
+// Asynchronous global -> shared copy (cp.async): a prefetch that holds no
+// register across the step.
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem)
+{
+    const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
+
 #ifndef STPC_PAIR_MINB
-#define STPC_PAIR_MINB 8  // measured (fit_p): 5 -> 28.5 ms, 6 -> 29.1, 7 -> 26.5, 8 -> 26.3, 10 -> 29.8 (more chains in flight beat the spills)
+#define STPC_PAIR_MINB 8  // measured (fit_p): 5 -> 28.5 ms, 6 -> 29.1, 7 -> 26.5, 8 -> 26.3, 10 -> 29.8; re-measured after the slimmer step: 6 -> 22.7, 7 -> 22.1, 8 -> 21.9, 9 -> 22.1
 #endif
 #ifdef STPC_FIT_STATS
 // diagnostic build only (tools/fit_stats.py): chain-step counters
@@ -881,7 +891,8 @@ __global__ void __launch_bounds__(FIT_WARPS * 32, STPC_PAIR_MINB) fit_pair_kerne
     bool grow = false;
     double acc = 0.0, a = 0.0, b = 0.0, c = 0.0;
     int pf_t = -1;
-    double pf_r = 0.0;
+    __shared__ double pf_slot[FIT_WARPS * 32];  // the lane's prefetched pixel (cp.async: no register)
+    double& pf_s = pf_slot[threadIdx.x];
 #define CROW (A.cls + slot * g.tx)
 #define SOK (A.start_ok + slot * g.tx)
 #define CERT (A.cert + slot * g.tx * CERT_F4)
@@ -993,7 +1004,13 @@ __global__ void __launch_bounds__(FIT_WARPS * 32, STPC_PAIR_MINB) fit_pair_kerne
             int dv, du;
             divmod_small(gl, cols, __frcp_rn((float)cols), dv, du);
             const int v = ch.v0 + dv, u = u0 + du;
-            const double r = pf_t == t ? pf_r : ch.img[(long long)v * g.w + u];
+            double r;
+            if (pf_t == t) {
+                cp_async_wait_all();
+                r = pf_s;
+            } else {
+                r = ch.img[(long long)v * g.w + u];
+            }
             if (isfinite(r)) {
                 double dx, dy, dz;
                 ray_dir(A.tg, v, u, dx, dy, dz);
@@ -1033,12 +1050,15 @@ __global__ void __launch_bounds__(FIT_WARPS * 32, STPC_PAIR_MINB) fit_pair_kerne
         if (live && t + 1 < g.tx) {
             const int nu0 = (t + 1) * g.tw;
             const int ncols = min(g.tw, g.w - nu0);
-            pf_r = __longlong_as_double(0x7ff0000000000000ll);
+            cp_async_wait_all();  // an unconsumed earlier copy into the slot has landed
             if (gl < ch.rows * ncols) {
                 int dv, du;
                 divmod_small(gl, ncols, __frcp_rn((float)ncols), dv, du);
-                pf_r = ch.img[(long long)(ch.v0 + dv) * g.w + nu0 + du];
+                cp_async8(&pf_s, ch.img + (long long)(ch.v0 + dv) * g.w + nu0 + du);
+            } else {
+                pf_s = __longlong_as_double(0x7ff0000000000000ll);
             }
+            cp_async_commit();
             pf_t = t + 1;
         }
         // ---- (3) solve: starts (verdict known ok) and growing chains with new pixels
