@@ -1202,113 +1202,184 @@ void launch_fit_rows(const FitArgs& a, cudaStream_t s)
     launch_fit_chains(a, s);
 }
 
-// K3a: one warp per (key-frame chain, P channel); for each run of the chain,
-// c' = f32(mean over the channel's valid span pixels of r * (d . n)), folded
-// v-major over the whole span in the reference's order, then the span re-test
-// with (a, b, c').  Spans that pass mark their tiles class 1 in the channel
-// and poison the channel's pixels there (+inf) for pass 2.  A second tiny
-// kernel sizes each chain's temporal records (18 B + presence bits + 4 B per
-// present P channel, bitstream.py:222-245).
+// K3a: the temporal offset refit (refit_kernel below) and a second tiny
+// kernel that sizes each key chain's temporal records (18 B + presence bits +
+// 4 B per present P channel, bitstream.py:222-245).
 #ifndef STPC_REFIT_MINB
 #define STPC_REFIT_MINB 10  // measured: unbounded 5.74 ms, 10 -> 5.66, 16 -> 5.65 (latency-bound; more warps beat a few spills)
 #endif
+// One run's span [U0, U0 + U) x rows of one P channel, full warp: c' = f32
+// of the v-major ordered mean of r (d . n) over the valid pixels, then the
+// span re-test (refit_spans, _kernels.py:231-279).  Returns ok, sets c.
+__device__ __forceinline__ bool refit_span(const RefitArgs& A, const double* img, double* sm, int v0, int rows,
+                                           int U0, int U, double a, double b, double& c)
+{
+    const Geometry& g = A.g;
+    const int lane = threadIdx.x & 31;
+    const int npx = rows * U;
+    const float ru = __frcp_rn((float)U);
+    double acc = 0.0;
+    int cnt = 0;
+    for (int base = 0; base < npx; base += 32) {
+        int p = base + lane;
+        double prod = 0.0;
+        bool valid = false;
+        if (p < npx) {
+            int dv, du;
+            divmod_small(p, U, ru, dv, du);
+            int v = v0 + dv, u = U0 + du;
+            double r = img[(long long)v * g.w + u];
+            if (isfinite(r)) {
+                double dx, dy, dz;
+                ray_dir(A.tg, v, u, dx, dy, dz);
+                double den = (dx + a * dy) + b * dz;
+                prod = r * den;
+                valid = true;
+            }
+        }
+        cnt += __popc(__ballot_sync(STPC_FULL, valid));
+        sm[lane] = prod;  // +0.0 for invalid pixels: exact (see fit_rows)
+        __syncwarp();
+        // lanes past the span hold +0.0, so a fixed-length unrolled fold
+        // is exact; a one-tile span (16 pixels of 4x4) adds 16 terms
+        if (npx - base > 16) {
+#pragma unroll
+            for (int jj = 0; jj < 32; ++jj) acc += sm[jj];
+        } else {
+#pragma unroll
+            for (int jj = 0; jj < 16; ++jj) acc += sm[jj];
+        }
+        __syncwarp();
+    }
+    c = 0.0;
+    if (cnt == 0) return false;
+    c = f32_round(acc / (double)cnt);
+    bool ok = true;
+    for (int base = 0; base < npx && ok; base += 32) {
+        int p = base + lane;
+        bool bad = false;
+        if (p < npx) {
+            int dv, du;
+            divmod_small(p, U, ru, dv, du);
+            int v = v0 + dv, u = U0 + du;
+            double r = img[(long long)v * g.w + u];
+            if (isfinite(r)) {
+                double dx, dy, dz;
+                ray_dir(A.tg, v, u, dx, dy, dz);
+                bad = !pixel_fits(r, dx, dy, dz, a, b, c, A.tau, A.r_max);
+            }
+        }
+        ok = !__any_sync(STPC_FULL, bad);
+    }
+    return ok;
+}
+
+// Spans of at most 16 pixels (one 4x4 tile), two channels at once: half h of
+// the warp refits channel h of the pair with the same arithmetic and order.
+__device__ __forceinline__ bool refit_span_pair(const RefitArgs& A, const double* img, double* sm, int v0, int U0,
+                                                int U, int npx, double a, double b, double& c)
+{
+    const Geometry& g = A.g;
+    const int lane = threadIdx.x & 31, half = lane >> 4, hl = lane & 15;
+    const unsigned hmask = 0xffffu << (half * 16);
+    double r = 0.0, dx = 0.0, dy = 0.0, dz = 0.0, prod = 0.0;
+    bool valid = false;
+    if (hl < npx) {
+        int dv, du;
+        divmod_small(hl, U, __frcp_rn((float)U), dv, du);
+        const int v = v0 + dv, u = U0 + du;
+        r = img[(long long)v * g.w + u];
+        if (isfinite(r)) {
+            ray_dir(A.tg, v, u, dx, dy, dz);
+            prod = r * ((dx + a * dy) + b * dz);
+            valid = true;
+        }
+    }
+    const int cnt = __popc(__ballot_sync(STPC_FULL, valid) & hmask);
+    sm[lane] = prod;
+    __syncwarp();
+    double acc = 0.0;
+#pragma unroll
+    for (int jj = 0; jj < 16; ++jj) acc += sm[half * 16 + jj];  // +0.0 past the span: exact
+    __syncwarp();
+    c = cnt > 0 ? f32_round(acc / (double)cnt) : 0.0;
+    const bool bad = valid && !pixel_fits(r, dx, dy, dz, a, b, c, A.tau, A.r_max);
+    const unsigned bm = __ballot_sync(STPC_FULL, bad);  // every lane votes (no short-circuit)
+    return cnt > 0 && (bm & hmask) == 0;
+}
+
+// K3a: one warp per (key-frame chain, pair of P channels); for each run of the
+// chain, c' = f32(mean over the channel's valid span pixels of r * (d . n)),
+// folded v-major over the whole span in the reference's order, then the span
+// re-test with (a, b, c').  One-tile spans refit both channels of the pair at
+// once (half a warp each); longer spans take the full warp per channel.
+// Spans that pass mark their tiles class 1 in the channel and poison the
+// channel's pixels there (+inf) for pass 2.
 __global__ void __launch_bounds__(128, STPC_REFIT_MINB) refit_kernel(RefitArgs A)
 {
     __shared__ double smem[4][32];
     const Geometry& g = A.g;
-    const int lane = threadIdx.x & 31;
+    const int lane = threadIdx.x & 31, half = lane >> 4;
     double* sm = smem[threadIdx.x >> 5];
     const int np = A.n - 1;
+    const int npairs = (np + 1) / 2;
     const long long wid = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-    if (np < 1 || wid >= (long long)A.n_groups * g.ty * np) return;
-    const long long kc = wid / np;  // key chain
-    const int pi = (int)(wid % np);
-    const int chn = pi < A.k ? pi : pi + 1;
+    if (np < 1 || wid >= (long long)A.n_groups * g.ty * npairs) return;
+    const long long kc = wid / npairs;  // key chain
+    const int q = (int)(wid % npairs);
+    const int np_here = min(2, np - 2 * q);  // channels in this pair
     const int grp = (int)(kc / g.ty);
     const int tr = (int)(kc % g.ty);
     const long long kslot = ((long long)grp * A.n + A.k) * g.ty + tr;
     const int nr = A.n_runs[kslot];
     const int v0 = tr * g.th;
     const int rows = min(g.th, g.h - v0);
-    const int frame = grp * A.n + chn;
-    double* img = A.best + (long long)frame * g.P;
-    uint8_t* crow = A.cls + ((long long)frame * g.ty + tr) * g.tx;
+    int chn[2];
+    for (int h = 0; h < 2; ++h) {
+        const int pi = min(2 * q + h, np - 1);
+        chn[h] = pi < A.k ? pi : pi + 1;
+    }
     for (int j = 0; j < nr; ++j) {
         const long long ri = kslot * g.tx + j;
         const int s = A.run_s[ri], len = A.run_len[ri];
         const double a = (double)A.run_abc[3 * ri], b = (double)A.run_abc[3 * ri + 1];
         const int U0 = s * g.tw;
-        const int U1 = min((s + len) * g.tw, g.w);
-        const int U = U1 - U0;
+        const int U = min((s + len) * g.tw, g.w) - U0;
         const int npx = rows * U;
-        const float ru = __frcp_rn((float)U);
-        double acc = 0.0;
-        int cnt = 0;
-        for (int base = 0; base < npx; base += 32) {
-            int p = base + lane;
-            double prod = 0.0;
-            bool valid = false;
-            if (p < npx) {
-                int dv, du;
-                divmod_small(p, U, ru, dv, du);
-                int v = v0 + dv, u = U0 + du;
-                double r = img[(long long)v * g.w + u];
-                if (isfinite(r)) {
-                    double dx, dy, dz;
-                    ray_dir(A.tg, v, u, dx, dy, dz);
-                    double den = (dx + a * dy) + b * dz;
-                    prod = r * den;
-                    valid = true;
-                }
+        const long long rj = (kc * g.tx + j) * A.n;
+        if (lane == 0 && q == 0) A.ref_ok[rj + A.k] = 1;
+        bool ok[2] = {false, false};
+        double cc[2] = {0.0, 0.0};
+        if (npx <= 16 && np_here == 2) {
+            const int frame = grp * A.n + chn[half];
+            double c;
+            const bool okh = refit_span_pair(A, A.best + (long long)frame * g.P, sm, v0, U0, U, npx, a, b, c);
+            ok[0] = __shfl_sync(STPC_FULL, okh, 0);
+            ok[1] = __shfl_sync(STPC_FULL, okh, 16);
+            cc[0] = __shfl_sync(STPC_FULL, c, 0);
+            cc[1] = __shfl_sync(STPC_FULL, c, 16);
+        } else {
+            for (int h = 0; h < np_here; ++h) {
+                const int frame = grp * A.n + chn[h];
+                ok[h] = refit_span(A, A.best + (long long)frame * g.P, sm, v0, rows, U0, U, a, b, cc[h]);
             }
-            cnt += __popc(__ballot_sync(STPC_FULL, valid));
-            sm[lane] = prod;  // +0.0 for invalid pixels: exact (see fit_rows)
-            __syncwarp();
-            // lanes past the span hold +0.0, so a fixed-length unrolled fold
-            // is exact; a one-tile span (16 pixels of 4x4) adds 16 terms
-            if (npx - base > 16) {
-#pragma unroll
-                for (int jj = 0; jj < 32; ++jj) acc += sm[jj];
-            } else {
-#pragma unroll
-                for (int jj = 0; jj < 16; ++jj) acc += sm[jj];
-            }
-            __syncwarp();
         }
-        bool ok = false;
-        double c = 0.0;
-        if (cnt > 0) {
-            c = f32_round(acc / (double)cnt);
-            ok = true;
-            for (int base = 0; base < npx && ok; base += 32) {
-                int p = base + lane;
-                bool bad = false;
-                if (p < npx) {
+        for (int h = 0; h < np_here; ++h) {
+            const int frame = grp * A.n + chn[h];
+            if (lane == 0) {
+                A.ref_ok[rj + chn[h]] = ok[h];
+                A.ref_c[rj + chn[h]] = (float)cc[h];
+            }
+            if (ok[h]) {
+                uint8_t* crow = A.cls + ((long long)frame * g.ty + tr) * g.tx;
+                double* img = A.best + (long long)frame * g.P;
+                for (int tt = s + lane; tt < s + len; tt += 32) crow[tt] = 1;
+                const float ru = __frcp_rn((float)U);
+                for (int p = lane; p < npx; p += 32) {
                     int dv, du;
                     divmod_small(p, U, ru, dv, du);
-                    int v = v0 + dv, u = U0 + du;
-                    double r = img[(long long)v * g.w + u];
-                    if (isfinite(r)) {
-                        double dx, dy, dz;
-                        ray_dir(A.tg, v, u, dx, dy, dz);
-                        bad = !pixel_fits(r, dx, dy, dz, a, b, c, A.tau, A.r_max);
-                    }
+                    img[(long long)(v0 + dv) * g.w + U0 + du] = __longlong_as_double(0x7ff0000000000000ll);
                 }
-                ok = !__any_sync(STPC_FULL, bad);
-            }
-        }
-        const long long rj = (kc * g.tx + j) * A.n;
-        if (lane == 0) {
-            A.ref_ok[rj + chn] = ok;
-            A.ref_c[rj + chn] = (float)c;
-            if (pi == 0) A.ref_ok[rj + A.k] = 1;
-        }
-        if (ok) {
-            for (int tt = s + lane; tt < s + len; tt += 32) crow[tt] = 1;
-            for (int p = lane; p < npx; p += 32) {
-                int dv, du;
-                divmod_small(p, U, ru, dv, du);
-                img[(long long)(v0 + dv) * g.w + U0 + du] = __longlong_as_double(0x7ff0000000000000ll);
             }
         }
     }
@@ -1341,7 +1412,7 @@ void launch_refit(const RefitArgs& a, cudaStream_t s)
 {
     long long kchains = (long long)a.n_groups * a.g.ty;
     if (kchains <= 0) return;
-    long long warps = kchains * (a.n - 1);
+    long long warps = kchains * (a.n / 2);  // pairs of P channels: ceil((n - 1) / 2)
     if (warps > 0) {
         STPC_LAUNCH();
         refit_kernel<<<(unsigned)((warps + 3) / 4), 128, 0, s>>>(a);
