@@ -52,7 +52,10 @@ def main():
     rep, kre = sys.argv[1], sys.argv[2]
     idx = int(sys.argv[3]) if len(sys.argv) > 3 else 0
     top = int(sys.argv[4]) if len(sys.argv) > 4 else 25
-    out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--kernel-name", f"regex:{kre}"],
+    # one launch at a time: the source page of a multi-launch report repeats
+    # the first launch's counters otherwise
+    out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--kernel-name", f"regex:{kre}",
+                          "--launch-skip", str(idx), "--launch-count", "1"],
                          capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
     blocks, cur = [], None
@@ -62,7 +65,7 @@ def main():
             blocks.append(cur)
         elif cur is not None and r and r[0].startswith("0x"):
             cur["rows"].append(r)
-    blk = blocks[idx]
+    blk = blocks[0]
     h, data = blk["hdr"], blk["rows"]
     ie = h.index("Instructions Executed")
     # STPC_SORT=<column> (e.g. stall_long_sb) ranks lines by that sample column
