@@ -396,12 +396,20 @@ def main():
     import torch
 
     dist = None
+    # one GPU per rank; STPC_DIST_BACKEND=gloo (host collectives) lets a
+    # multi-rank run share fewer GPUs for a plumbing check -- ranks never wait
+    # on each other's kernels, only on the final gathers
+    backend = os.environ.get("STPC_DIST_BACKEND", "nccl")
+    local = local % max(torch.cuda.device_count(), 1) if backend != "nccl" else local
     if world > 1:
         import torch.distributed as dist_mod
 
         dist = dist_mod
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     else:
         torch.cuda.set_device(local)
     device = torch.device("cuda", local)
