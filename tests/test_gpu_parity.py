@@ -547,3 +547,29 @@ def test_decompress_many_mixed_batch_reports_first_error():
     for b, cl in zip(good, clouds):
         for a, r in zip(cl, decompress(b)):
             assert np.array_equal(a, r)
+
+
+def test_repeated_calls_deterministic_and_coverage_partition():
+    """Reference acceptance 5 and 9 (pkg/tests/test_acceptance.py:224-251,
+    343-368): the same input gives the same bytes on every call (the encoder
+    reuses its workspace and alternates its double-buffered range grids), and
+    every frame's valid pixels split exactly into temporal + spatial fallback +
+    residual (temporal.py:258-290)."""
+    from paper_2008_06972_b200 import compress_groups, synth
+
+    cfg = _cfg(synth.SENSOR_64, 10, 0.1, 4)  # configs[1] shape
+    groups = [synth.make_group(6100 + i, 10) for i in range(2)]
+    clouds, poses = [g.clouds for g in groups], [g.poses for g in groups]
+    first, reps = compress_groups(clouds, cfg, poses)
+    for _ in range(3):
+        again, _ = compress_groups(clouds, cfg, poses)
+        assert again == first
+    for rep in reps:
+        assert len(rep.coverage) == cfg.n_frames
+        for c in rep.coverage:
+            assert c["temporal"] + c["fallback"] + c["residual"] == c["valid"]
+        # the key frame's runs carry its own offset, so they count as temporal
+        # (coverage_counts, temporal.py:269-290); it has no fallback rows
+        assert rep.coverage[cfg.k_index]["fallback"] == 0
+        assert rep.coverage[cfg.k_index]["temporal"] > 0
+        assert sum(c["temporal"] for i, c in enumerate(rep.coverage) if i != cfg.k_index) > 0
