@@ -209,6 +209,12 @@ int stpc_malloc(void** dev_ptr, int64_t bytes);
 int stpc_free(void* dev_ptr);
 int stpc_memcpy_d2h(void* dst, const void* src, int64_t bytes);
 int stpc_memcpy_h2d(void* dst, const void* src, int64_t bytes);
+/* Host copy of n blobs (src + offsets[i], lengths[i] bytes) to dst[i] with
+ * host threads: how compress_groups fills its bytes objects.  Replaces the
+ * per-blob bytes(...) of the reference's result assembly
+ * (/root/reference/pkg/src/stpc/bitstream.py:289-290, one blob per compress). */
+int stpc_host_scatter(const uint8_t* src, const int64_t* offsets, const int64_t* lengths, uint8_t* const* dst,
+                      int32_t n);
 int stpc_device_count(void);
 const char* stpc_last_error(void);
 const char* stpc_version(void);

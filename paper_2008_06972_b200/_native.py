@@ -29,7 +29,7 @@ EXPORTS = [
     "stpc_result_groups", "stpc_result_blobs", "stpc_result_device_blobs",
     "stpc_result_copy_blobs", "stpc_result_frame_stats", "stpc_result_payload_lengths",
     "stpc_encoder_buffer", "stpc_project", "stpc_malloc", "stpc_free", "stpc_memcpy_d2h",
-    "stpc_memcpy_h2d", "stpc_device_count", "stpc_last_error", "stpc_version",
+    "stpc_memcpy_h2d", "stpc_host_scatter", "stpc_device_count", "stpc_last_error", "stpc_version",
     "stpc_encoder_profile", "stpc_encoder_stage_ms", "stpc_stage_name", "stpc_launch_count",
     "stpc_decoder_create", "stpc_decoder_destroy", "stpc_decoder_load", "stpc_decoder_load_gather",
     "stpc_decoder_heads",
@@ -102,6 +102,7 @@ def load(require_device: bool = False):
                 "stpc_free": ([P], ctypes.c_int),
                 "stpc_memcpy_d2h": ([P, P, I64], ctypes.c_int),
                 "stpc_memcpy_h2d": ([P, P, I64], ctypes.c_int),
+                "stpc_host_scatter": ([P, P, P, P, I32], ctypes.c_int),
                 "stpc_device_count": ([], ctypes.c_int),
                 "stpc_last_error": ([], ctypes.c_char_p),
                 "stpc_version": ([], ctypes.c_char_p),

@@ -113,6 +113,29 @@ class EncodeReport:
     eps_band_points: int = 0  # binnings within 1e-9 of a bin edge
 
 
+_new_bytes = ctypes.pythonapi.PyBytes_FromStringAndSize
+_new_bytes.restype = ctypes.py_object
+_new_bytes.argtypes = [ctypes.c_void_p, ctypes.c_ssize_t]
+_bytes_buf = ctypes.pythonapi.PyBytes_AsString
+_bytes_buf.restype = ctypes.c_void_p
+_bytes_buf.argtypes = [ctypes.py_object]
+
+
+def _bytes_from_arena(L, base: int, off: np.ndarray, ln: np.ndarray) -> List[bytes]:
+    """One bytes object per blob of a host arena.  The objects are allocated
+    uninitialised (PyBytes_FromStringAndSize(NULL, n), as CPython's own
+    builders do) and filled by one threaded native copy before they are
+    returned, so no other code ever sees them unfilled."""
+    G = len(ln)
+    out = [_new_bytes(None, int(n)) for n in ln]
+    if G:
+        dst = (ctypes.c_void_p * G)(*[_bytes_buf(b) for b in out])
+        src_off = np.ascontiguousarray(off[:G], np.int64)
+        lens = np.ascontiguousarray(ln, np.int64)
+        _native.check(L.stpc_host_scatter(base, src_off.ctypes.data, lens.ctypes.data, dst, G))
+    return out
+
+
 class Encoder:
     """One native encoder (device workspace + trig tables) per config and
     input dtype; reuse it across calls to amortise allocation."""
@@ -190,12 +213,12 @@ class Encoder:
     def blobs(self, arena: Optional[np.ndarray] = None) -> List[bytes]:
         off, ln = self.blob_layout()
         host = self._L.stpc_result_host_blobs(self._h) if arena is None else None
-        if host:  # blobs already in the encoder's pinned arena: one copy per blob
-            return [ctypes.string_at(host + int(o), int(n)) for o, n in zip(off[:-1], ln)]
+        if host:  # blobs already in the encoder's pinned arena: one parallel copy
+            return _bytes_from_arena(self._L, host, off, ln)
         if arena is None:
             arena = np.empty(int(off[-1]), np.uint8)
             _native.check(self._L.stpc_result_copy_blobs(self._h, arena.ctypes.data, arena.nbytes, None))
-        return [arena[o:o + n].tobytes() for o, n in zip(off[:-1], ln)]
+        return _bytes_from_arena(self._L, arena.ctypes.data, off, ln)
 
     def frame_stats(self) -> np.ndarray:
         G = self._L.stpc_result_groups(self._h)

@@ -20,10 +20,13 @@ def main():
     args = bench.parse()
     sensor, n, tile, tau, scene, G = bench.workload(args)
     cfg = bench.codec_config(sensor, n, tile, tau)
+    import torch
+
+    dev = "cuda" if torch.cuda.is_available() else "cpu"
     t = time.perf_counter()
     groups, poses = [], []
     for g in range(G):
-        grp = synth.make_group(bench.group_seed(0, g, 4), n, sensor, **scene)
+        grp = synth.make_group(bench.group_seed(0, g, 4), n, sensor, device=dev, **scene)
         groups.append(grp.clouds)
         poses.append(grp.poses)
     print(f"generated {G} groups in {time.perf_counter() - t:.1f} s")

@@ -38,7 +38,7 @@ def main():
     if dbg is not None:
         st = (ctypes.c_ulonglong * 8)()
         dbg(st)
-        names = ["steps", "starts", "empty", "cert_checks", "weak_certs", "growth_tests", "growth_pass", "merged_weak"]
+        names = ["steps", "starts", "empty", "cert_checks", "weak_certs", "growth_tests", "growth_pass", "retest_fail"]
         print("fit counters (key + P):", {k: int(v) for k, v in zip(names, st)})
     F = G * n
     tx = -(-cfg.w // cfg.tile_w)
