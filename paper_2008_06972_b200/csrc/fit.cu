@@ -1322,12 +1322,15 @@ __global__ void __launch_bounds__(128, STPC_REFIT_MINB) refit_kernel(RefitArgs A
     const int lane = threadIdx.x & 31, half = lane >> 4;
     double* sm = smem[threadIdx.x >> 5];
     const int np = A.n - 1;
-    const int npairs = (np + 1) / 2;
+    // pairs of channels only where one-tile spans fit half a warp; larger
+    // tiles keep one warp per channel (twice the warps in flight)
+    const int per = g.tw * g.th <= 16 ? 2 : 1;
+    const int npairs = (np + per - 1) / per;
     const long long wid = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
     if (np < 1 || wid >= (long long)A.n_groups * g.ty * npairs) return;
     const long long kc = wid / npairs;  // key chain
     const int q = (int)(wid % npairs);
-    const int np_here = min(2, np - 2 * q);  // channels in this pair
+    const int np_here = min(per, np - per * q);  // channels of this warp
     const int grp = (int)(kc / g.ty);
     const int tr = (int)(kc % g.ty);
     const long long kslot = ((long long)grp * A.n + A.k) * g.ty + tr;
@@ -1336,7 +1339,7 @@ __global__ void __launch_bounds__(128, STPC_REFIT_MINB) refit_kernel(RefitArgs A
     const int rows = min(g.th, g.h - v0);
     int chn[2];
     for (int h = 0; h < 2; ++h) {
-        const int pi = min(2 * q + h, np - 1);
+        const int pi = min(per * q + h, np - 1);
         chn[h] = pi < A.k ? pi : pi + 1;
     }
     for (int j = 0; j < nr; ++j) {
@@ -1412,7 +1415,8 @@ void launch_refit(const RefitArgs& a, cudaStream_t s)
 {
     long long kchains = (long long)a.n_groups * a.g.ty;
     if (kchains <= 0) return;
-    long long warps = kchains * (a.n / 2);  // pairs of P channels: ceil((n - 1) / 2)
+    const int per = a.g.tw * a.g.th <= 16 ? 2 : 1;  // P channels per warp (refit_kernel)
+    long long warps = kchains * ((a.n - 1 + per - 1) / per);
     if (warps > 0) {
         STPC_LAUNCH();
         refit_kernel<<<(unsigned)((warps + 3) / 4), 128, 0, s>>>(a);
