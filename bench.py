@@ -301,6 +301,36 @@ def host_cores():
         return os.cpu_count() or 1
 
 
+def cpu_model():
+    """The host CPU's model name (BASELINE.md §3 asks for it beside the core count)."""
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
+def cpu_single_rate(sample, cfg, n, seconds):
+    """Frames/s of the oracle port in this one process (single core)."""
+    from oracle import oracle
+
+    global _CPU_SAMPLE
+    oracle.build()
+    cfgt = tuple(oracle.OracleConfig.of(cfg).__dict__.values())
+    _CPU_SAMPLE = [(c, x, cfgt) for c, x in sample]
+    _cpu_job(0)  # warm
+    t0 = time.perf_counter()
+    done = 0
+    while True:
+        _cpu_job(done % len(sample))
+        done += 1
+        if time.perf_counter() - t0 >= seconds:
+            break
+    return done * n / (time.perf_counter() - t0)
+
+
 # ------------------------------------------------------------------- roofline
 
 def algorithmic_bytes(stage, cfg, n, G, npts, raw_bytes=0, blob_bytes=0):
@@ -572,7 +602,9 @@ def main():
             rate, done, dt = cpu_pool_rate(sample, cfg, n, args.cpu_seconds, cores)
             cpu = {"value": rate, "unit": "frames/s", "cores": cores, "kind": "port",
                    "sample": f"{done} groups ({done * n} frames) of this workload through the C/numpy "
-                             f"oracle in {dt:.1f} s, ProcessPool x{cores}"}
+                             f"oracle in {dt:.1f} s, ProcessPool x{cores}",
+                   "cpu_model": cpu_model(),
+                   "single_core_value": cpu_single_rate(sample, cfg, n, min(3.0, args.cpu_seconds / 5))}
         except Exception as exc:  # never let the baseline kill the GPU line
             cpu = {"value": None, "error": repr(exc)[:200]}
 
@@ -636,7 +668,7 @@ def run_reference(args, cfg, config, n, rank, world):
         "impl": "reference",
         "cpu_baseline": {"value": value, "unit": "frames/s", "cores": cores, "kind": "port",
                          "sample": f"each step: rounds of {cores} groups (1 per core) through the C/numpy "
-                                   f"oracle for ~{per_step:.0f} s"},
+                                   f"oracle for ~{per_step:.0f} s", "cpu_model": cpu_model()},
         "e2e": {"value": value, "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line))
