@@ -615,13 +615,13 @@ __global__ void __launch_bounds__(FIT_WARPS * 32, 5) fit_rows_kernel(FitArgs A)
     Prefetch pf;
     const uint8_t* sok = A.start_ok + slot * g.tx;
     while (t < g.tx) {
-        if (!sok[t]) {
+        if (!sok[t] || (ch.skip1 && crow[t] == 1)) {
             // residual start tiles (class 0 stays; covered tiles keep class 1):
             // jump to the next start tile with a 32-wide ballot
             int nt = g.tx;
             for (int base = t + 1; base < g.tx; base += 32) {
                 const int j = base + lane;
-                const uint32_t m = __ballot_sync(STPC_FULL, j < g.tx && sok[j]);
+                const uint32_t m = __ballot_sync(STPC_FULL, j < g.tx && sok[j] && !(ch.skip1 && crow[j] == 1));
                 if (m) {
                     nt = base + __ffs(m) - 1;
                     break;
@@ -939,7 +939,9 @@ __global__ void __launch_bounds__(FIT_WARPS * 32, STPC_PAIR_MINB) fit_pair_kerne
             int base = t;
             while (__any_sync(STPC_FULL, scan && !found && base < g.tx)) {
                 const int j = base + gl;
-                const bool f = scan && !found && j < g.tx && SOK[j];
+                // pass 2: a temporally covered tile is never a start (its start
+                // verdict may predate the refit that covered it)
+                const bool f = scan && !found && j < g.tx && SOK[j] && !(ch.skip1 && CROW[j] == 1);
                 const unsigned mm = (__ballot_sync(STPC_FULL, f) & gmask) >> (sub * 16);
                 if (mm && !found) {
                     nt = base + __ffs(mm) - 1;
