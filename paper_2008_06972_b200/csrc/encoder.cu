@@ -697,8 +697,9 @@ static int encode_host_impl(stpc_encoder* enc, int32_t n_groups, const char* hp,
     // Small batches: one H2D + encode + D2H.
     // measured on the bench workload (1024 groups): 8 chunks 232.5 ms,
     // 16: 227.7, 24: 226.8, 32: 239.4 -- the tail (last chunk's encode + blob
-    // D2H) shrinks with chunk size until per-chunk syncs and launches dominate
-    int n_chunks = n_groups >= 128 ? 16 : (n_groups >= 64 ? 8 : 1);
+    // D2H) shrinks with chunk size until per-chunk syncs and launches dominate;
+    // re-measured after the fit trims: 16: 227.5, 24: 225.7, 32: 227.6
+    int n_chunks = n_groups >= 384 ? 24 : n_groups >= 128 ? 16 : (n_groups >= 64 ? 8 : 1);
     if (n_chunks > 1 && getenv("STPC_PIPE_CHUNKS")) {  // tuning knob
         n_chunks = std::max(2, std::min(atoi(getenv("STPC_PIPE_CHUNKS")), n_groups / 8));
     }
