@@ -179,7 +179,7 @@ __device__ bool test_tile(const Chain& ch, const Geometry& g, const Trig& tg, in
     const int cols = min(g.tw, g.w - u0);
     const int npx = ch.rows * cols;  // callers never test masked (class-1) tiles
     const float rc = __frcp_rn((float)cols);
-    double m = 1e300, dmin = 1e300, rmin = 1e300, rmax = 0.0;
+    double X = 1e300, dmin = 1e300;  // slack min(tau - |r - r_hat|, r_hat, r_max - r_hat), as test_tile_pair
     double ylo = 1e300, yhi = -1e300, zlo = 1e300, zhi = -1e300;
     for (int base = 0; base < npx; base += 32) {
         int p = base + lane;
@@ -201,10 +201,8 @@ __device__ bool test_tile(const Chain& ch, const Geometry& g, const Trig& tg, in
                     if (r_hat <= 0.0 || r_hat > r_max || fabs(r - r_hat) > tau) {
                         bad = true;
                     } else {
-                        m = fmin(m, tau - fabs(r - r_hat));
+                        X = fmin(X, fmin(fmin(tau - fabs(r - r_hat), r_hat), r_max - r_hat));
                         dmin = fmin(dmin, ad);
-                        rmin = fmin(rmin, r_hat);
-                        rmax = fmax(rmax, r_hat);
                         const double yh = r_hat * dy, zh = r_hat * dz;
                         ylo = fmin(ylo, yh);
                         yhi = fmax(yhi, yh);
@@ -216,21 +214,19 @@ __device__ bool test_tile(const Chain& ch, const Geometry& g, const Trig& tg, in
         }
         if (__any_sync(STPC_FULL, bad)) return false;
     }
-    // m, dmin, rmin, rmax are >= 0: their float bit patterns order like their
-    // values; the signed box uses an order-preserving key.  One REDUX each,
-    // every value rounded outward first.
-    const unsigned um = __reduce_min_sync(STPC_FULL, __float_as_uint(__double2float_rd(fmin(m, 3.0e38))));
+    // X, dmin are >= 0: their float bit patterns order like their values; the
+    // signed box uses an order-preserving key.  One REDUX each, every value
+    // rounded outward first.
+    const unsigned ux = __reduce_min_sync(STPC_FULL, __float_as_uint(__double2float_rd(fmin(X, 3.0e38))));
     const unsigned ud = __reduce_min_sync(STPC_FULL, __float_as_uint(__double2float_rd(fmin(dmin, 3.0e38))));
-    const unsigned ulo = __reduce_min_sync(STPC_FULL, __float_as_uint(__double2float_rd(fmin(rmin, 3.0e38))));
-    const unsigned uhi = __reduce_max_sync(STPC_FULL, __float_as_uint(__double2float_ru(rmax)));
     const unsigned ky0 = __reduce_min_sync(STPC_FULL, f2key(__double2float_rd(fmax(fmin(ylo, 3.0e38), -3.0e38))));
     const unsigned ky1 = __reduce_max_sync(STPC_FULL, f2key(__double2float_ru(fmin(fmax(yhi, -3.0e38), 3.0e38))));
     const unsigned kz0 = __reduce_min_sync(STPC_FULL, f2key(__double2float_rd(fmax(fmin(zlo, 3.0e38), -3.0e38))));
     const unsigned kz1 = __reduce_max_sync(STPC_FULL, f2key(__double2float_ru(fmin(fmax(zhi, -3.0e38), 3.0e38))));
     if (lane == 0) {
         float4* ce = ch.cert + CERT_F4 * t;
-        ce[0] = make_float4((float)a, (float)b, (float)c, __uint_as_float(um));  // a/b/c are f32-exact
-        ce[1] = make_float4(__uint_as_float(ud), __uint_as_float(ulo), __uint_as_float(uhi), 0.0f);
+        ce[0] = make_float4((float)a, (float)b, (float)c, __uint_as_float(ux));  // a/b/c are f32-exact
+        ce[1] = make_float4(__uint_as_float(ud), __uint_as_float(ux), 0.0f, 0.0f);
         ce[2] = make_float4(key2f(ky0), key2f(ky1), key2f(kz0), key2f(kz1));
     }
     return true;
@@ -565,12 +561,55 @@ __global__ void __launch_bounds__(256, STPC_START_MINB) start_tiles_kernel(FitAr
                         __double2float_ru(zhi));
 }
 
+// plane_from_sums (common.cuh; _kernels.py:23-76) for the lanes b0.. that hold
+// the running sums (lane b0 + k owns sum k; gl = lane - b0): the six divides
+// of the inverse run in parallel, cofactor k in lane b0 + k, and are
+// exchanged by shuffles.  Every operation, operand and order is that of
+// plane_from_sums, so the bits are identical; all lanes of the warp must call
+// it.
+__device__ __forceinline__ bool plane_from_sums_lanes(double acc, int b0, int gl, double cond_limit, double& a,
+                                                      double& b, double& c)
+{
+    const double s0 = shfl_d(acc, b0), s1 = shfl_d(acc, b0 + 1), s2 = shfl_d(acc, b0 + 2);
+    const double s3 = shfl_d(acc, b0 + 3), s4 = shfl_d(acc, b0 + 4), s5 = shfl_d(acc, b0 + 5);
+    const double s6 = shfl_d(acc, b0 + 6), s7 = shfl_d(acc, b0 + 7), s8 = shfl_d(acc, b0 + 8);
+    const double m00 = s0, m01 = s1, m02 = -s3, m11 = s2, m12 = -s4, m22 = s8;
+    const double r0 = -s5, r1 = -s6, r2 = s7;
+    const double c00 = m11 * m22 - m12 * m12;
+    const double c01 = m02 * m12 - m01 * m22;
+    const double c02 = m01 * m12 - m02 * m11;
+    const double det = (m00 * c00 + m01 * c01) + m02 * c02;
+    double num;
+    if (gl == 0) num = c00;
+    else if (gl == 1) num = c01;
+    else if (gl == 2) num = c02;
+    else if (gl == 3) num = m00 * m22 - m02 * m02;  // c11
+    else if (gl == 4) num = m01 * m02 - m00 * m12;  // c12
+    else num = m00 * m11 - m01 * m01;               // c22
+    const double q = num / det;
+    const double i00 = shfl_d(q, b0), i01 = shfl_d(q, b0 + 1), i02 = shfl_d(q, b0 + 2);
+    const double i11 = shfl_d(q, b0 + 3), i12 = shfl_d(q, b0 + 4), i22 = shfl_d(q, b0 + 5);
+    a = b = c = 0.0;
+    if (det == 0.0 || !isfinite(det)) return false;
+    const double norm_m = pymax3((fabs(m00) + fabs(m01)) + fabs(m02), (fabs(m01) + fabs(m11)) + fabs(m12),
+                                 (fabs(m02) + fabs(m12)) + fabs(m22));
+    const double norm_i = pymax3((fabs(i00) + fabs(i01)) + fabs(i02), (fabs(i01) + fabs(i11)) + fabs(i12),
+                                 (fabs(i02) + fabs(i12)) + fabs(i22));
+    const double cond = norm_m * norm_i;
+    if (!isfinite(cond) || cond > cond_limit) return false;
+    const double pa = (i00 * r0 + i01 * r1) + i02 * r2;
+    const double pb = (i01 * r0 + i11 * r1) + i12 * r2;
+    const double pc = (i02 * r0 + i12 * r1) + i22 * r2;
+    if (!(isfinite(pa) && isfinite(pb) && isfinite(pc))) return false;
+    a = pa;
+    b = pb;
+    c = pc;
+    return true;
+}
+
 __device__ __forceinline__ bool solve_round(double acc, double cond_limit, double& a, double& b, double& c)
 {
-    double s[9];
-#pragma unroll
-    for (int k = 0; k < 9; ++k) s[k] = shfl_d(acc, k);
-    if (!plane_from_sums(s, cond_limit, a, b, c)) return false;
+    if (!plane_from_sums_lanes(acc, 0, threadIdx.x & 31, cond_limit, a, b, c)) return false;
     a = f32_round(a);
     b = f32_round(b);
     c = f32_round(c);
@@ -786,50 +825,11 @@ __device__ bool test_tile_pair(bool active, const Chain& ch, const Geometry& g, 
     return test_px_pair(active, has, r, dx, dy, dz, ch, tile, a, b, c, tau, r_max);
 }
 
-// plane_from_sums (common.cuh; _kernels.py:23-76) for the half-warp that holds
-// the running sums (lane k of the group owns sum k): the six divides of the
-// inverse run in parallel, cofactor k in lane k, and are exchanged by
-// shuffles.  Every operation, operand and order is that of plane_from_sums,
-// so the bits are identical; all lanes of the warp must call it.
+// plane_from_sums for a half-warp (see plane_from_sums_lanes).
 __device__ __forceinline__ bool plane_from_sums_pair(double acc, int sub, int gl, double cond_limit, double& a,
                                                      double& b, double& c)
 {
-    const int b0 = sub * PG;
-    const double s0 = shfl_d(acc, b0), s1 = shfl_d(acc, b0 + 1), s2 = shfl_d(acc, b0 + 2);
-    const double s3 = shfl_d(acc, b0 + 3), s4 = shfl_d(acc, b0 + 4), s5 = shfl_d(acc, b0 + 5);
-    const double s6 = shfl_d(acc, b0 + 6), s7 = shfl_d(acc, b0 + 7), s8 = shfl_d(acc, b0 + 8);
-    const double m00 = s0, m01 = s1, m02 = -s3, m11 = s2, m12 = -s4, m22 = s8;
-    const double r0 = -s5, r1 = -s6, r2 = s7;
-    const double c00 = m11 * m22 - m12 * m12;
-    const double c01 = m02 * m12 - m01 * m22;
-    const double c02 = m01 * m12 - m02 * m11;
-    const double det = (m00 * c00 + m01 * c01) + m02 * c02;
-    double num;
-    if (gl == 0) num = c00;
-    else if (gl == 1) num = c01;
-    else if (gl == 2) num = c02;
-    else if (gl == 3) num = m00 * m22 - m02 * m02;  // c11
-    else if (gl == 4) num = m01 * m02 - m00 * m12;  // c12
-    else num = m00 * m11 - m01 * m01;               // c22
-    const double q = num / det;
-    const double i00 = shfl_d(q, b0), i01 = shfl_d(q, b0 + 1), i02 = shfl_d(q, b0 + 2);
-    const double i11 = shfl_d(q, b0 + 3), i12 = shfl_d(q, b0 + 4), i22 = shfl_d(q, b0 + 5);
-    a = b = c = 0.0;
-    if (det == 0.0 || !isfinite(det)) return false;
-    const double norm_m = pymax3((fabs(m00) + fabs(m01)) + fabs(m02), (fabs(m01) + fabs(m11)) + fabs(m12),
-                                 (fabs(m02) + fabs(m12)) + fabs(m22));
-    const double norm_i = pymax3((fabs(i00) + fabs(i01)) + fabs(i02), (fabs(i01) + fabs(i11)) + fabs(i12),
-                                 (fabs(i02) + fabs(i12)) + fabs(i22));
-    const double cond = norm_m * norm_i;
-    if (!isfinite(cond) || cond > cond_limit) return false;
-    const double pa = (i00 * r0 + i01 * r1) + i02 * r2;
-    const double pb = (i01 * r0 + i11 * r1) + i12 * r2;
-    const double pc = (i02 * r0 + i12 * r1) + i22 * r2;
-    if (!(isfinite(pa) && isfinite(pb) && isfinite(pc))) return false;
-    a = pa;
-    b = pb;
-    c = pc;
-    return true;
+    return plane_from_sums_lanes(acc, sub * PG, gl, cond_limit, a, b, c);
 }
 
 // Asynchronous global -> shared copy (cp.async): a prefetch that holds no
