@@ -63,7 +63,7 @@ def workload(args):
     sensor, n, tile, tau, scene = synth.config_params(args.config)
     tile = args.tile or tile
     tau = args.tau or tau
-    default_groups = {1: 64, 2: 128, 3: 128, 4: 1024, 5: 8}[args.config]
+    default_groups = {1: 64, 2: 128, 3: 128, 4: 1024, 5: 64}[args.config]
     groups = args.groups or default_groups
     return sensor, n, tile, tau, scene, groups
 
