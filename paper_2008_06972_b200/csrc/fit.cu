@@ -154,6 +154,14 @@ __device__ __forceinline__ int fold_tile(const Chain& ch, const Geometry& g, con
 // reference's per-pixel test decides, and the tile is not re-tested;
 // otherwise it is tested pixel by pixel (and re-certified).  Verdicts are
 // identical; only the work changes.
+//
+// Layout (CERT_F4 float4): c0 = (a, b, c, m), c1 = (dmin, rmin, rmax, 0),
+// c2 = (ymin, ymax, zmin, zmax).  The chain kernels' own tests store the
+// per-pixel slack X = min(tau - |r - r_hat|, r_hat, r_max - r_hat) instead:
+// c0.w = c1.y = min X, c1.z = 0, which the same three comparisons read as
+// B < min X (the start kernels keep the three fields).  The check itself is
+// division-free: B (1 + 1e-6) + 1e-9 < F becomes
+// max|n| (1 + 2e-6) < (F - 1e-9) (dmin - |da| - |db|), at least as strict.
 // ---------------------------------------------------------------------------
 
 // Order-preserving map of a float to unsigned (for REDUX min/max of signed values).
