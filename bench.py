@@ -554,10 +554,14 @@ def main():
             ems = pdist.max_over_ranks(ems, device)
         ems /= max(args.steps, 1)
         off2, len2 = enc.blob_layout()
+        h2d = int(hp.nbytes + off.nbytes + xf.nbytes)
+        d2h = int(off2[-1] + 8 * (3 * G + 2))
+        if dist:  # whole job, like the value
+            h2d = pdist.sum_over_ranks(h2d, device)
+            d2h = pdist.sum_over_ranks(d2h, device)
         e2e = {"value": frames_all / (ems / 1e3), "unit": "frames/s",
                "mpoints_per_s": total_pts / (ems / 1e3) / 1e6, "ms_per_step": ems,
-               "h2d_bytes_per_step": int(hp.nbytes + off.nbytes + xf.nbytes),
-               "d2h_bytes_per_step": int(off2[-1] + 8 * (3 * G + 2))}
+               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h}
 
     # ---------------- roofline of the dominant stage
     peaks = {}
