@@ -409,7 +409,7 @@ static int encode_impl(stpc_encoder* e, int G, const void* d_points, const int64
     // first writer of P-frame pixels and classes.  (Running the refit on the
     // high-priority stream too starved the verdicts: 143.6k vs 145.3k
     // frames/s; without priorities the two kernels only time-share.)
-    const bool ovl = n > 1;
+    const bool ovl = n > 1 && fit_overlap_pays(g, (long long)G * g.ty);
 #else
     const bool ovl = false;
 #endif

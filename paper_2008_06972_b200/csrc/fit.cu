@@ -1206,6 +1206,19 @@ void launch_fit_chains(const FitArgs& a, cudaStream_t s)
     }
 }
 
+// Does running the P-frame start verdicts beside the key-frame fit pay?
+// Measured (frames/s, overlapped vs serial): configs[3] 1024 groups 145.2k vs
+// 143.4k (16 k key chains: the fit's last wave leaves slots idle) and
+// configs[2] with 16x16 tiles 36.5k vs 33.2k (fit_rows: one warp per chain
+// leaves SMs idle) win; with fewer key chains than the pair kernel's resident
+// slots the verdicts' blocks slow the latency-bound chains, which stay the
+// critical path: configs[1] 102.6k vs 106.1k, configs[2] 4x4 26.3k vs 27.3k.
+bool fit_overlap_pays(const Geometry& g, long long key_chains)
+{
+    if (g.tw * g.th > PG) return true;
+    return key_chains > 148LL * STPC_PAIR_MINB * FIT_WARPS * 2;
+}
+
 void launch_fit_rows(const FitArgs& a, cudaStream_t s)
 {
     launch_start_tiles(a, s);

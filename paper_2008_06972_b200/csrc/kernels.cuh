@@ -88,6 +88,7 @@ struct FitArgs {
 void launch_fit_rows(const FitArgs& a, cudaStream_t s);  // = start_tiles + fit_chains
 void launch_start_tiles(const FitArgs& a, cudaStream_t s);
 void launch_fit_chains(const FitArgs& a, cudaStream_t s);
+bool fit_overlap_pays(const Geometry& g, long long key_chains);  // key fit beside the P start verdicts?
 
 struct RefitArgs {
     double* best;  // covered P-frame pixels are overwritten with +inf
