@@ -49,6 +49,28 @@ def test_library_loads_and_reports_devices():
     assert L.stpc_device_count() >= 0
 
 
+def test_host_scatter_fills_bytes_objects():
+    """stpc_host_scatter (host threads, no GPU) behind compress_groups' result
+    bytes: every blob lands in its own freshly allocated bytes object,
+    including empty blobs and a batch large enough to use several threads."""
+    import numpy as np
+
+    from paper_2008_06972_b200 import _native
+    from paper_2008_06972_b200.codec import _bytes_from_arena
+
+    L = _native.load()
+    rng = np.random.default_rng(5)
+    for lens in ([3, 0, 5, 1], [0], list(rng.integers(0, 400_000, 24))):
+        lens = np.asarray(lens, np.int64)
+        off = np.zeros(len(lens) + 1, np.int64)
+        off[1:] = np.cumsum(lens)
+        arena = rng.integers(0, 256, int(off[-1]) + 7, dtype=np.uint8)
+        got = _bytes_from_arena(L, arena.ctypes.data, off, lens)
+        assert [len(b) for b in got] == list(lens)
+        for i, b in enumerate(got):
+            assert isinstance(b, bytes) and b == arena[off[i]:off[i] + lens[i]].tobytes()
+
+
 @pytest.mark.skipif(gpu_available(), reason="only meaningful without a GPU")
 def test_no_cpu_fallback_without_gpu():
     from paper_2008_06972_b200 import compress, _native
