@@ -1114,6 +1114,7 @@ __global__ void __launch_bounds__(FIT_WARPS * 32, STPC_PAIR_MINB) fit_pair_kerne
                     const int jj = act ? base + __ffs(wm) - 1 : 0;
                     if (act) wm &= wm - 1;
                     const bool r = test_tile_pair(act, ch, g, A.tg, jj, na, nb, nc, A.tau, A.r_max);
+                    FIT_STAT(7, act && !r && gl == 0);  // re-tests that fail the union
                     if (act && !r) pass = false;
                 }
                 base += PG;
