@@ -510,7 +510,10 @@ __global__ void __launch_bounds__(256, STPC_EMIT_MINB) emit_residual_kernel(Emit
             const long long idx = w0px + lane;
             uint32_t d = (uint32_t)(idx - prev);
             const int len = has ? varint_len(d) : 0;
-            const int vinc = warp_incl_scan(len);
+            // one-byte deltas everywhere (dense residual words): the varint
+            // offsets are a popcount, not a scan
+            const int vinc = __all_sync(STPC_FULL, len <= 1) ? __popc(m & (lt | (1u << lane)))
+                                                             : warp_incl_scan(len);
             if (has) {
                 uint8_t* vo = vptr + (vinc - len);
                 while (d >= 0x80u) {
