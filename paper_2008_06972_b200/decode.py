@@ -154,8 +154,15 @@ def _transforms_batch(heads: np.ndarray, raw_len: np.ndarray, idxs: List[int], n
         thr = ORTHONORMAL_ATOL + 1e-5 * eye  # allclose: atol + rtol * |b|
         orth = np.all(dev <= thr, axis=(1, 2))
         near = np.any(np.abs(dev - thr) < 1e-12, axis=(1, 2)) | ~np.all(np.isfinite(R), axis=(1, 2))
-        det = np.linalg.det(R)
-        detok = np.abs(det - 1.0) <= ORTHONORMAL_ATOL + 1e-5
+        # det by cofactors (vectorised); LAPACK's np.linalg.det only where the
+        # two could disagree about the tolerance
+        det = (R[:, 0, 0] * (R[:, 1, 1] * R[:, 2, 2] - R[:, 1, 2] * R[:, 2, 1])
+               - R[:, 0, 1] * (R[:, 1, 0] * R[:, 2, 2] - R[:, 1, 2] * R[:, 2, 0])
+               + R[:, 0, 2] * (R[:, 1, 0] * R[:, 2, 1] - R[:, 1, 1] * R[:, 2, 0]))
+        dtol = ORTHONORMAL_ATOL + 1e-5
+        detok = np.abs(det - 1.0) <= dtol
+        for f in np.flatnonzero(~(np.abs(np.abs(det - 1.0) - dtol) > 1e-9) | ~np.isfinite(det)):
+            detok[f] = bool(np.abs(np.linalg.det(R[f]) - 1.0) <= dtol)
         Tinv = -np.matmul(Rt, T[:, :, None])[:, :, 0]
     for f in np.flatnonzero(near):
         orth[f] = np.allclose(R[f].T @ R[f], eye, atol=ORTHONORMAL_ATOL)
@@ -217,13 +224,28 @@ class Decoder:
         heads = np.zeros((n, cap), np.uint8)
         _native.check(L.stpc_decoder_heads(self.h, cap, heads.ctypes.data, raw_len.ctypes.data, stream))
         cfgs: Dict[int, dict] = {}
+        parsed: Dict[bytes, object] = {}  # a batch's blobs mostly share one config block
         for i in range(n):
             if i in errors:
                 continue
-            try:
-                cfgs[i] = _config(heads[i].tobytes(), int(raw_len[i]))
-            except Exception as exc:  # noqa: BLE001 -- reported per blob
-                errors[i] = exc
+            if raw_len[i] < _CFG.size:
+                try:
+                    _config(heads[i].tobytes(), int(raw_len[i]))
+                except Exception as exc:  # noqa: BLE001 -- reported per blob
+                    errors[i] = exc
+                continue
+            key = heads[i, :_CFG.size].tobytes()
+            hit = parsed.get(key)
+            if hit is None:
+                try:
+                    hit = _config(key, int(raw_len[i]))
+                except Exception as exc:  # noqa: BLE001 -- reported per blob
+                    hit = exc
+                parsed[key] = hit
+            if isinstance(hit, Exception):
+                errors[i] = type(hit)(*hit.args)
+            else:
+                cfgs[i] = hit
         need = max([c["n_frames"] for c in cfgs.values()], default=0)
         if need > _HEAD_FRAMES:
             cap = _CFG.size + 48 * need
