@@ -149,7 +149,12 @@ def _transforms_batch(heads: np.ndarray, raw_len: np.ndarray, idxs: List[int], n
     Rt = np.transpose(R, (0, 2, 1))
     eye = np.eye(3)
     with np.errstate(all="ignore"):
-        M = np.matmul(Rt, R)
+        # R^T R and R^T T as explicit left-to-right K=3 sums (elementwise over
+        # the batch; the products are exact, float32 x float32)
+        M = np.empty_like(R)
+        for i in range(3):
+            for j in range(3):
+                M[:, i, j] = (R[:, 0, i] * R[:, 0, j] + R[:, 1, i] * R[:, 1, j]) + R[:, 2, i] * R[:, 2, j]
         dev = np.abs(M - eye)
         thr = ORTHONORMAL_ATOL + 1e-5 * eye  # allclose: atol + rtol * |b|
         orth = np.all(dev <= thr, axis=(1, 2))
@@ -163,7 +168,9 @@ def _transforms_batch(heads: np.ndarray, raw_len: np.ndarray, idxs: List[int], n
         detok = np.abs(det - 1.0) <= dtol
         for f in np.flatnonzero(~(np.abs(np.abs(det - 1.0) - dtol) > 1e-9) | ~np.isfinite(det)):
             detok[f] = bool(np.abs(np.linalg.det(R[f]) - 1.0) <= dtol)
-        Tinv = -np.matmul(Rt, T[:, :, None])[:, :, 0]
+        Tinv = np.empty_like(T)
+        for i in range(3):
+            Tinv[:, i] = -((R[:, 0, i] * T[:, 0] + R[:, 1, i] * T[:, 1]) + R[:, 2, i] * T[:, 2])
     for f in np.flatnonzero(near):
         orth[f] = np.allclose(R[f].T @ R[f], eye, atol=ORTHONORMAL_ATOL)
     rows = np.concatenate([Rt.reshape(-1, 9), Tinv], axis=1).reshape(len(ok), n, 12)
