@@ -542,8 +542,14 @@ __global__ void heads_kernel(const uint8_t* raw, const long long* raw_off, const
 // ---------------------------------------------------------------- records
 
 constexpr int PK_THREADS = 256;
-constexpr int PK_BATCH = 1024;
-constexpr int PK_WIN = 16384;  // staged bytes of the run section
+#ifndef STPC_PK_BATCH
+#define STPC_PK_BATCH 512  // records per batch; 512 (with 8 blocks per SM) fits 1024 blobs in one wave: frames 31.9 -> 28.3 ms
+#endif
+#ifndef STPC_PK_WIN
+#define STPC_PK_WIN 16384
+#endif
+constexpr int PK_BATCH = STPC_PK_BATCH;
+constexpr int PK_WIN = STPC_PK_WIN;  // staged bytes of the run section
 
 // Block per blob: validates the record sections in the reference's reading
 // order and turns them into per-(frame, tile) plane maps (a, b, c, kind:
@@ -553,7 +559,7 @@ constexpr int PK_WIN = 16384;  // staged bytes of the run section
 // batches that the block then expands in parallel; residual varints are
 // scanned block-parallel (terminator bytes < 0x80).
 #ifndef STPC_PARSE_MINB
-#define STPC_PARSE_MINB 6  // measured (frames phase): 1 -> 35.5 ms, 6 -> 31.7, 8 -> 32.7
+#define STPC_PARSE_MINB 8  // measured (frames phase): 1 -> 35.5 ms, 6 -> 31.7, 8 -> 32.7 (smem-limited to 6 at 1024-record batches); 8 with 512-record batches -> 28.3
 #endif
 __global__ void __launch_bounds__(PK_THREADS, STPC_PARSE_MINB) parse_kernel(DecGeom G, const uint8_t* raw, const long long* raw_off,
                                                            const long long* raw_len, const int* sel, float4* tmap,
