@@ -1053,23 +1053,30 @@ __global__ void __launch_bounds__(1024) unproject_kernel(DecGeom G, Trig tg, con
     const bool have = pix < G.P && __double_as_longlong(out_r[i]) != DEC_NOPT;
     const unsigned m = __ballot_sync(STPC_FULL, have);
     __shared__ int ws[32];
+    __shared__ double stage[32][96];  // a warp's points, xyz interleaved, for coalesced stores
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     if (lane == 0) ws[wid] = __popc(m);
     __syncthreads();
     int before = 0;
     for (int w = 0; w < wid; ++w) before += ws[w];
-    if (!have) return;
-    const long long o = frame_off[f] + blk_off[f * gridDim.x + blockIdx.x] + before +
-                        __popc(m & ((1u << lane) - 1u));
-    const int v = (int)(pix / G.w), u = (int)(pix - (long long)v * G.w);
-    double dx, dy, dz;
-    ray_dir(tg, v, u, dx, dy, dz);
-    const double r = out_r[i];
-    const double x = r * dx, y = r * dy, z = r * dz;
-    const double* R = xf_inv + 12 * f;
-    pts[3 * o] = xform_coord(x, y, z, R[0], R[1], R[2], R[9]);
-    pts[3 * o + 1] = xform_coord(x, y, z, R[3], R[4], R[5], R[10]);
-    pts[3 * o + 2] = xform_coord(x, y, z, R[6], R[7], R[8], R[11]);
+    const int rank = __popc(m & ((1u << lane) - 1u));
+    if (have) {
+        const int v = (int)(pix / G.w), u = (int)(pix - (long long)v * G.w);
+        double dx, dy, dz;
+        ray_dir(tg, v, u, dx, dy, dz);
+        const double r = out_r[i];
+        const double x = r * dx, y = r * dy, z = r * dz;
+        const double* R = xf_inv + 12 * f;
+        stage[wid][3 * rank] = xform_coord(x, y, z, R[0], R[1], R[2], R[9]);
+        stage[wid][3 * rank + 1] = xform_coord(x, y, z, R[3], R[4], R[5], R[10]);
+        stage[wid][3 * rank + 2] = xform_coord(x, y, z, R[6], R[7], R[8], R[11]);
+    }
+    __syncwarp();
+    // the warp's points are contiguous in the output: write them as 3 x 32
+    // consecutive doubles
+    const int nw = 3 * __popc(m);
+    double* dst = pts + 3 * (frame_off[f] + blk_off[f * gridDim.x + blockIdx.x] + before);
+    for (int k = lane; k < nw; k += 32) dst[k] = stage[wid][k];
 }
 
 }  // namespace stpc
