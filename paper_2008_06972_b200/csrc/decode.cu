@@ -821,7 +821,11 @@ __global__ void __launch_bounds__(PK_THREADS, STPC_PARSE_MINB) parse_kernel(DecG
                 }
                 ++vi;
             }
-            if (dsum) atomicAdd(&s_flat, dsum);
+            // one shared atomic per warp (a per-thread 64-bit atomic on the one
+            // address serialised the block: ~45% of the kernel's instructions)
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) dsum += __shfl_xor_sync(STPC_FULL, dsum, o);
+            if ((tid & 31) == 0 && dsum) atomicAdd(&s_flat, dsum);
             __syncthreads();
             const long long end = s_end;
             const long long lim = end >= 0 ? end : len;
