@@ -47,7 +47,25 @@ struct DecGeom {
     long long bits_off;  // 57 + 48 n: first validity bitmap
     long long runs_off;  // bits_off + n nb: temporal run count
     double quant, r_max;
+    double rw, rtw, rth, rn;  // fl(1 / w), 1 / tw, 1 / th, 1 / n for dmod
 };
+
+// q, r = p / d, p % d for 0 <= p < 2^50 through the double reciprocal rd =
+// fl(1 / d): the estimate is off by at most one, fixed exactly (per-pixel
+// 64-bit integer divides dominated the pixel kernels' instruction counts).
+__device__ __forceinline__ long long dmod(long long p, long long d, double rd, long long& r)
+{
+    long long q = (long long)((double)p * rd);
+    r = p - q * d;
+    if (r < 0) {
+        q -= 1;
+        r += d;
+    } else if (r >= d) {
+        q += 1;
+        r -= d;
+    }
+    return q;
+}
 
 struct ResSec {
     long long pos_var;   // first varint byte
@@ -892,7 +910,8 @@ __global__ void __launch_bounds__(1024) reconstruct_kernel(DecGeom G, Trig tg, c
                                                            double* out_r, unsigned long long* failed)
 {
     const long long f = blockIdx.y;
-    const int j = (int)(f / G.n), ch = (int)(f - (long long)j * G.n);
+    long long chl;
+    const int j = (int)dmod(f, G.n, G.rn, chl), ch = (int)chl;
     if (pstat[j] != DEC_NONE) return;
     const long long pix = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     int nfail = 0;
@@ -901,8 +920,10 @@ __global__ void __launch_bounds__(1024) reconstruct_kernel(DecGeom G, Trig tg, c
         const bool valid = (dec_u8(vb + (pix >> 3)) >> (7 - (pix & 7))) & 1u;
         long long r = DEC_NOPT;
         if (valid) {
-            const int v = (int)(pix / G.w), u = (int)(pix - (long long)v * G.w);
-            const float4 pl = tmap[(f * G.ty + v / G.th) * G.tx + u / G.tw];
+            long long ul, rv, ru;
+            const int v = (int)dmod(pix, G.w, G.rw, ul), u = (int)ul;
+            const long long tv = dmod(v, G.th, G.rth, rv), tu = dmod(u, G.tw, G.rtw, ru);
+            const float4 pl = tmap[(f * G.ty + tv) * G.tx + tu];
             if (pl.w != 0.0f) {
                 double dx, dy, dz;
                 ray_dir(tg, v, u, dx, dy, dz);
@@ -990,7 +1011,8 @@ __global__ void __launch_bounds__(1024) count_points_kernel(DecGeom G, const dou
                                                             const unsigned long long* pstat, int* blk_count)
 {
     const long long f = blockIdx.y;
-    const int j = (int)(f / G.n);
+    long long fch;
+    const int j = (int)dmod(f, G.n, G.rn, fch);
     const long long pix = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     const bool have = pstat[j] == DEC_NONE && pix < G.P &&
                       __double_as_longlong(out_r[f * G.P + pix]) != DEC_NOPT;
@@ -1050,7 +1072,8 @@ __global__ void __launch_bounds__(1024) unproject_kernel(DecGeom G, Trig tg, con
                                                          double* pts)
 {
     const long long f = blockIdx.y;
-    const int j = (int)(f / G.n);
+    long long fch;
+    const int j = (int)dmod(f, G.n, G.rn, fch);
     if (pstat[j] != DEC_NONE) return;
     const long long pix = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     const long long i = f * G.P + pix;
@@ -1065,7 +1088,8 @@ __global__ void __launch_bounds__(1024) unproject_kernel(DecGeom G, Trig tg, con
     for (int w = 0; w < wid; ++w) before += ws[w];
     const int rank = __popc(m & ((1u << lane) - 1u));
     if (have) {
-        const int v = (int)(pix / G.w), u = (int)(pix - (long long)v * G.w);
+        long long ul;
+        const int v = (int)dmod(pix, G.w, G.rw, ul), u = (int)ul;
         double dx, dy, dz;
         ray_dir(tg, v, u, dx, dy, dz);
         const double r = out_r[i];
@@ -1386,6 +1410,10 @@ int stpc_decoder_frames(stpc_decoder* d, const stpc_decode_geom* g, const int32_
     G.runs_off = G.bits_off + (long long)G.n * G.nb;
     G.quant = g->range_quant;
     G.r_max = g->r_max;
+    G.rw = 1.0 / G.w;
+    G.rtw = 1.0 / G.tw;
+    G.rth = 1.0 / G.th;
+    G.rn = 1.0 / G.n;
     d->m = m;
     d->F = (long long)m * G.n;
     d->bpf = (G.P + 1023) / 1024;
