@@ -1084,8 +1084,18 @@ __global__ void __launch_bounds__(1024) unproject_kernel(DecGeom G, Trig tg, con
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     if (lane == 0) ws[wid] = __popc(m);
     __syncthreads();
-    int before = 0;
-    for (int w = 0; w < wid; ++w) before += ws[w];
+    if (wid == 0) {  // exclusive scan of the warp counts by warp 0
+        const int c = lane < (int)(blockDim.x >> 5) ? ws[lane] : 0;
+        int x = c;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int t = __shfl_up_sync(STPC_FULL, x, o);
+            if (lane >= o) x += t;
+        }
+        if (lane < (int)(blockDim.x >> 5)) ws[lane] = x - c;
+    }
+    __syncthreads();
+    const int before = ws[wid];
     const int rank = __popc(m & ((1u << lane) - 1u));
     if (have) {
         long long ul;
