@@ -52,6 +52,7 @@ def parse():
     ap.add_argument("--stages", action="store_true", help="print per-stage ms to stderr")
     ap.add_argument("--no-decode", action="store_true", help="skip the decompress measurement")
     ap.add_argument("--decode-e2e-groups", type=int, default=128)
+    ap.add_argument("--no-parity", action="store_true", help="skip the post-timing oracle comparison")
     return ap.parse_args()
 
 
@@ -331,6 +332,90 @@ def cpu_single_rate(sample, cfg, n, seconds):
     return done * n / (time.perf_counter() - t0)
 
 
+# ------------------------------------------------------------------- parity
+
+def pipeline_chunks(G):
+    """Chunking of stpc_encode_host's pipeline (encoder.cu encode_host_impl):
+    (n_chunks, groups per chunk)."""
+    nc = 24 if G >= 384 else 16 if G >= 128 else (8 if G >= 64 else 1)
+    return nc, -(-G // nc)
+
+
+def parity_groups(G, want=96):
+    """Groups whose blobs are compared with the oracle: the first and last
+    group, both sides of every pipeline-chunk boundary of the host path, and
+    evenly spaced others up to `want`."""
+    nc, gc = pipeline_chunks(G)
+    sel = {0, G - 1}
+    for c in range(1, nc):
+        if c * gc < G:
+            sel.update((c * gc - 1, c * gc))
+    step = max(1, G // max(1, want - len(sel)))
+    sel.update(range(0, G, step))
+    return sorted(sel) if G > want else list(range(G))
+
+
+_PAR_SAMPLE = None
+
+
+def _oracle_blob_job(i):
+    """Oracle blob of one group (test infrastructure: the checker)."""
+    from oracle import oracle
+
+    clouds, xf, cfgt = _PAR_SAMPLE[i]
+    ocfg = oracle.OracleConfig(*cfgt)
+    ts = [(row[:9].reshape(3, 3), row[9:]) for row in xf]
+    enc = oracle.encode_stream(clouds, ts, ocfg)
+    return oracle.entropy_blob(oracle.payload_bytes(enc, ocfg))
+
+
+def _oracle_decode_job(blob):
+    from oracle import decode as odec
+
+    return [np.ascontiguousarray(c) for c in odec.decompress(blob)]
+
+
+def headline_parity(cfg, n, pts_host, off, xf, sel, blob_sets, decode_blobs=True, cores=None):
+    """Byte-compare GPU blobs of the groups `sel` with the oracle's.
+
+    pts_host: host float32 points of the whole batch; off/xf: the batch's
+    frame offsets / transforms; blob_sets: {path name: list of blobs (bytes)
+    indexed like sel}.  The oracle runs on all host cores (it is the checker,
+    run after timing).  Returns the bench line's "parity" block."""
+    import concurrent.futures as cf
+    import multiprocessing as mp
+
+    from oracle import oracle
+    from paper_2008_06972_b200 import decompress_many
+
+    global _PAR_SAMPLE
+    oracle.build()
+    cfgt = tuple(oracle.OracleConfig.of(cfg).__dict__.values())
+    sample = []
+    for g in sel:
+        clouds = [np.asarray(pts_host[off[g * n + i]: off[g * n + i + 1]]) for i in range(n)]
+        sample.append((clouds, xf[g * n:(g + 1) * n], cfgt))
+    _PAR_SAMPLE = sample
+    cores = cores or host_cores()
+    t0 = time.perf_counter()
+    with cf.ProcessPoolExecutor(max_workers=cores, mp_context=mp.get_context("fork")) as ex:
+        ref = list(ex.map(_oracle_blob_job, range(len(sel)), chunksize=1))
+        out = {"groups_checked": len(sel), "groups": sorted(int(g) for g in sel)[:4] + ["..."] + [int(sel[-1])]}
+        for name, blobs in blob_sets.items():
+            same = [a == b for a, b in zip(blobs, ref)]
+            out[name] = {"identical": int(sum(same)),
+                         "first_mismatch": next((int(g) for g, s in zip(sel, same) if not s), None)}
+        out["identical"] = min(v["identical"] for k, v in out.items() if isinstance(v, dict))
+        if decode_blobs:
+            first = next(iter(blob_sets.values()))
+            mine, _ = decompress_many(first)
+            refd = list(ex.map(_oracle_decode_job, first, chunksize=1))
+            out["decode_identical"] = int(sum(
+                len(a) == len(b) and all(np.array_equal(x, y) for x, y in zip(a, b)) for a, b in zip(mine, refd)))
+    out["oracle_s"] = round(time.perf_counter() - t0, 2)
+    return out
+
+
 # ------------------------------------------------------------------- roofline
 
 def algorithmic_bytes(stage, cfg, n, G, npts, raw_bytes=0, blob_bytes=0):
@@ -512,6 +597,13 @@ def main():
     raw = enc.payload_lengths()
     blob_bytes = int(len_b.sum())
     stats = enc.frame_stats()
+    psel = parity_groups(G) if not args.no_parity else []
+    dev_blobs = None
+    if psel:  # this step's device-path blobs of the checked groups (compared after timing)
+        arena = np.empty(int(off_b[-1]), np.uint8)
+        L.stpc_memcpy_d2h(arena.ctypes.data, L.stpc_result_device_blobs(enc.handle), arena.nbytes)
+        dev_blobs = [arena[off_b[g]:off_b[g] + len_b[g]].tobytes() for g in psel]
+        del arena
     if dist:
         from paper_2008_06972_b200 import dist as pdist
 
@@ -561,7 +653,10 @@ def main():
             d2h = pdist.sum_over_ranks(d2h, device)
         e2e = {"value": frames_all / (ems / 1e3), "unit": "frames/s",
                "mpoints_per_s": total_pts / (ems / 1e3) / 1e6, "ms_per_step": ems,
-               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h}
+               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+               "path": f"stpc_encode_host: pinned host points -> {pipeline_chunks(G)[0]}-chunk pipelined "
+                       f"H2D + encode + blob D2H"}
+        host_blobs = [h_out[off2[g]:off2[g] + len2[g]].tobytes() for g in psel]
 
     # ---------------- roofline of the dominant stage
     peaks = {}
@@ -597,6 +692,20 @@ def main():
                                       kernel="emit_residual_kernel (traffic); stage time covers all emit kernels")
     roofline["fit_utilisation"] = fit_utilisation(args, G)
 
+    # ---------------- parity of the timed workload (after timing; oracle = checker)
+    parity = None
+    if psel:
+        try:
+            sets = {"encode_device": dev_blobs}
+            if e2e:
+                sets["encode_host"] = host_blobs
+            pts_h = hp if e2e else d_pts.cpu().numpy()
+            parity = headline_parity(cfg, n, pts_h, off, xf, psel, sets)
+            parity["eps_band_points"] = int(stats[:, 8].sum())
+            parity["eps_band_scope"] = f"all {G} groups of the rank's batch (STPC_STAT_EPS_BAND)"
+        except Exception as exc:  # never let the checker kill the line
+            parity = {"error": repr(exc)[:300]}
+
     # ---------------- CPU baseline (rank 0, N=1)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
@@ -629,6 +738,7 @@ def main():
             "gpu_launches": launches,
             "stage_ms": {nm: round(float(v), 4) for nm, v in zip(names, stage_ms)},
             "decode": decode,
+            "parity": parity,
             "impl": "b200",
         }
         print(json.dumps(line))

@@ -21,6 +21,7 @@ from .codec import (
     compress,
     compress_groups,
     get_encoder,
+    release_cached,
 )
 from .decode import DecodeReport, decompress, decompress_full, decompress_many
 from .errors import (

@@ -248,18 +248,94 @@ class Encoder:
         return out
 
 
-_enc_cache: Dict[tuple, Encoder] = {}
-_enc_lock = threading.Lock()
+class _Pool:
+    """Bounded pool of native contexts (encoders / decoders) keyed by config.
+
+    A call checks a context out (so concurrent calls never share one), and
+    returns it afterwards; at most ``max_idle`` idle contexts are kept, least
+    recently used evicted first.  Each context holds grow-only device
+    workspaces (two F*P fp64 grids for an encoder: ~17 GB at 1024 groups), so
+    an unbounded per-thread / per-config cache would exhaust HBM under thread
+    pools or config sweeps.  Evicted contexts are dropped, not closed: one
+    still referenced elsewhere is freed when its last reference goes."""
+
+    def __init__(self, env: str, default: int):
+        import os
+        from collections import OrderedDict
+
+        self.max_idle = max(0, int(os.environ.get(env, default)))
+        self.idle: "OrderedDict[tuple, List]" = OrderedDict()
+        self.lock = threading.Lock()
+
+    def acquire(self, key, factory):
+        with self.lock:
+            lst = self.idle.get(key)
+            if lst:
+                obj = lst.pop()
+                if not lst:
+                    del self.idle[key]
+                return obj
+        return factory()
+
+    def peek(self, key, factory):
+        """The most recently returned idle context of ``key`` (left in the
+        pool), created if there is none: how tests read the intermediates of
+        the last call."""
+        with self.lock:
+            lst = self.idle.get(key)
+            if lst:
+                self.idle.move_to_end(key)
+                return lst[-1]
+        obj = factory()
+        self.release(key, obj)
+        return obj
+
+    def release(self, key, obj):
+        with self.lock:
+            self.idle.setdefault(key, []).append(obj)
+            self.idle.move_to_end(key)
+            total = sum(len(v) for v in self.idle.values())
+            while total > self.max_idle and self.idle:
+                k0, lst = next(iter(self.idle.items()))
+                lst.pop(0)
+                total -= 1
+                if not lst:
+                    del self.idle[k0]
+
+    def clear(self):
+        with self.lock:
+            self.idle.clear()
+
+
+_encoders = _Pool("STPC_ENCODER_POOL", 2)
 
 
 def get_encoder(cfg: CodecConfig, points_f64: bool = False) -> Encoder:
-    key = (cfg, bool(points_f64), threading.get_ident())
-    with _enc_lock:
-        enc = _enc_cache.get(key)
-        if enc is None:
-            enc = Encoder(cfg, points_f64)
-            _enc_cache[key] = enc
-        return enc
+    """The pooled encoder of ``cfg`` that served the most recent call (or a
+    new one)."""
+    return _encoders.peek((cfg, bool(points_f64)), lambda: Encoder(cfg, points_f64))
+
+
+class _checkout:
+    def __init__(self, pool: _Pool, key, factory):
+        self.pool, self.key, self.factory = pool, key, factory
+
+    def __enter__(self):
+        self.obj = self.pool.acquire(self.key, self.factory)
+        return self.obj
+
+    def __exit__(self, *exc):
+        self.pool.release(self.key, self.obj)
+        return False
+
+
+def release_cached() -> None:
+    """Free every idle pooled encoder and decoder (their device workspaces go
+    when the last reference does)."""
+    from . import decode
+
+    _encoders.clear()
+    decode._decoders.clear()
 
 
 def _transforms_for(cfg: CodecConfig, poses, imu_samples, frame_times, v0) -> List[RigidTransform]:
@@ -367,8 +443,7 @@ def compress_groups(groups: Sequence[Sequence[np.ndarray]], cfg: CodecConfig,
         xf = np.asarray(xf, np.float64).reshape(-1, 12)
     t1 = time.perf_counter()
     frames, f64, counts = _frame_arrays([c for grp in groups for c in grp])
-    enc = get_encoder(cfg, f64)
-    with enc.lock:
+    with _checkout(_encoders, (cfg, f64), lambda: Encoder(cfg, f64)) as enc:
         enc.encode_host_gather(len(groups), frames, xf)
         blobs = enc.blobs()
         stats = enc.frame_stats()
@@ -389,8 +464,7 @@ def compress(clouds: Sequence[np.ndarray], cfg: CodecConfig, poses=None, imu_sam
     xf = np.asarray([t.row12() for t in ts], np.float64)
     t1 = time.perf_counter()
     pts, off, f64, counts = _stack_points(clouds)
-    enc = get_encoder(cfg, f64)
-    with enc.lock:
+    with _checkout(_encoders, (cfg, f64), lambda: Encoder(cfg, f64)) as enc:
         enc.encode_host(1, pts, off, xf)
         blobs = enc.blobs()
         stats = enc.frame_stats()

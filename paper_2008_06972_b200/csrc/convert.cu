@@ -179,8 +179,10 @@ __device__ __forceinline__ bool fast_bin(double x, double y, double z, const Geo
     const float xf = (float)x, yf = (float)y, zf = (float)z;
     const float mxy = fmaxf(fabsf(xf), fabsf(yf));
     const float mall = fmaxf(mxy, fabsf(zf));
-    // keep squares and ratios in float range; degenerate directions go exact
-    if (!(mall < 1e15f && mxy > 1e-30f)) return false;
+    // keep squares and ratios in float range (coordinates outside [1e-15,
+    // 1e15] go exact: below 1e-15 x^2 + y^2 could underflow); degenerate
+    // directions go exact
+    if (!(mall < 1e15f && mxy > 1e-15f)) return false;
     float th = fast_atan2f(xf, yf);
     th = th < 0.0f ? th + 6.28318548f : th;
     const float qu = th * inv_tr;
@@ -189,8 +191,13 @@ __device__ __forceinline__ bool fast_bin(double x, double y, double z, const Geo
     const float flu = floorf(qu), flv = floorf(qv);
     const float fu = qu - flu, fv = qv - flv;
     if (fu < mu || fu > 1.0f - mu || fv < mv || fv > 1.0f - mv) return false;
-    const int uq = (int)flu;  // 0 <= qu <= w (th <= 2 pi)
-    u = uq >= g.w ? uq - g.w : uq;
+    // 0 <= qu <= 2 pi / theta_r, which CodecConfig does not tie to w: the
+    // reference's floor(theta / theta_r) % w needs a true modulo whenever the
+    // sensor's w bins cover less than the full circle.  (A point is only
+    // accepted with mu < 0.5, i.e. 1/theta_r < 5e4, so qu < 3.2e5 fits an int;
+    // see launch_convert.)
+    const int uq = (int)flu;
+    u = uq >= g.w ? uq % g.w : uq;
     v = (int)flv;
     return true;
 }
@@ -398,6 +405,11 @@ void launch_convert(const ConvertArgs& a0, int max_pts, cudaStream_t s)
     a.phi_off = (float)a.g.phi_offset;
     a.mu = (float)FAST_MARGIN * a.inv_tr;
     a.mv = (float)FAST_MARGIN * a.inv_pr;
+    // The fp32 decision is only sound where the margin is below half a bin
+    // and phi_offset survives the float rounding within the error budget
+    // (2^-24 |phi_offset| << FAST_MARGIN): otherwise every point takes the
+    // exact path (mu = 1 rejects every fraction).
+    if (!(a.mu < 0.5f && a.mv < 0.5f && fabs(a.g.phi_offset) < 16.0)) a.mu = a.mv = 1.0f;
     launch_zero(a.q_count, sizeof(unsigned long long), s);
     STPC_LAUNCH();
     if (a.pts_f64)

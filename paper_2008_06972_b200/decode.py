@@ -321,25 +321,23 @@ class Decoder:
         return clouds, reports, errors
 
 
-_decoders: Dict[int, Decoder] = {}
+from .codec import _checkout, _Pool  # noqa: E402
+
+_decoders = _Pool("STPC_DECODER_POOL", 1)
 
 
 def get_decoder() -> Decoder:
-    import threading
-
-    key = threading.get_ident()
-    if key not in _decoders:
-        _decoders[key] = Decoder()
-    return _decoders[key]
+    """The pooled decoder that served the most recent call (or a new one)."""
+    return _decoders.peek((), Decoder)
 
 
 def decompress_many(blobs: Sequence[bytes]) -> Tuple[List[List[np.ndarray]], List[DecodeReport]]:
     """Decode a batch of blobs (one device pass per distinct configuration).
     Raises the reference's exception for the first blob that fails."""
-    dec = get_decoder()
     if not len(blobs):
         return [], []
-    clouds, reports, errors = dec.decode(0, None, False, host_blobs=blobs)
+    with _checkout(_decoders, (), Decoder) as dec:
+        clouds, reports, errors = dec.decode(0, None, False, host_blobs=blobs)
     if errors:
         raise errors[min(errors)]
     return clouds, reports  # type: ignore[return-value]

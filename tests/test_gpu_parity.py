@@ -159,6 +159,82 @@ def test_project_fine_bins_exact_path_overflow(lib, rng):
     assert np.array_equal(counts[0], oc)
 
 
+@pytest.mark.parametrize("w,h,tr,pr,off", [
+    # the reference's own conftest sensor: w=64, h=8 at the default
+    # AngularResolution (theta_r = 2 pi / 1800, phi_r = 0.00698, phi_offset
+    # 1.48; /root/reference/pkg/tests/conftest.py:14-18) -- the w bins cover
+    # 1/28 of the circle, so floor(theta / theta_r) % w wraps ~28 times
+    (64, 8, 2 * np.pi / 1800, 0.00698, 1.48),
+    # a 90-degree sector sensor (sector_res, conftest.py:27-29)
+    (200, 20, np.pi / 2 / 200, 0.5 / 20, 1.2),
+    # |phi_offset| too large for the fp32 fast path's float rounding
+    (300, 3000, 2 * np.pi / 300, 0.01, -20.0),
+])
+def test_project_wrapping_sensors(lib, rng, w, h, tr, pr, off):
+    """Sensors whose w bins do not span the full circle: the azimuth bin is a
+    true modulo (a single subtraction corrupted these pixels)."""
+    n = 200_000
+    th = rng.uniform(0, 2 * np.pi, n)
+    lo, hi = max(0.01, off - 0.05), min(np.pi - 0.01, off + h * pr + 0.05)
+    if lo >= hi:
+        lo, hi = 0.01, np.pi - 0.01
+    ph = rng.uniform(lo, hi, n)
+    r = rng.uniform(0.5, 120, n)
+    pts = np.stack([r * np.sin(ph) * np.sin(th), r * np.sin(ph) * np.cos(th), r * np.cos(ph)], 1).astype(np.float32)
+    ocfg = oracle.OracleConfig("single", 0.1, 4, 4, tr, pr, off, w, h, 1, 0)
+    ob, ow, oc = oracle.convert(pts, np.eye(3), np.zeros(3), ocfg)
+    best, win, counts = gpu_project(lib, [pts], [(np.eye(3), np.zeros(3))], w, h, tr, pr, off)
+    eps = _eps_band(pts.astype(np.float64), tr, pr, off)
+    diff = np.nonzero(best[0].view(np.uint64) != ob.view(np.uint64))[0]
+    for pix in diff:
+        g_idx, o_idx = win[0][pix], ow[pix]
+        assert (g_idx >= 0 and eps[g_idx]) or (o_idx >= 0 and eps[o_idx]), f"pixel {pix} differs outside the eps band"
+    assert counts[0][0] == oc[0] and counts[0][1] == oc[1]
+    assert oc[2] > 0
+
+
+def test_project_tiny_and_huge_coordinates(lib):
+    """Coordinates below 1e-15 or above 1e15 must take the exact fp64 path
+    (x = y = 1e-25 underflowed the fp32 elevation)."""
+    w, h, tr, pr, off = 360, 180, 2 * np.pi / 360, np.pi / 180, 0.0
+    vals = []
+    for s in (1e-30, 1e-25, 1e-20, 1e-16, 1e-15, 1e-14, 1e14, 1e15, 1e16):
+        for d in ((1, 1, -1), (1, -2, 3), (-3, 1, 0.5), (0.2, 0.1, -7), (1, 0, 0), (0, 1, 1)):
+            vals.append(np.array(d) * s)
+    pts = np.asarray(vals, np.float64)
+    ocfg = oracle.OracleConfig("single", 0.1, 4, 4, tr, pr, off, w, h, 1, 0)
+    ob, ow, oc = oracle.convert(pts, np.eye(3), np.zeros(3), ocfg)
+    for f64 in (True, False):
+        p = pts if f64 else pts.astype(np.float32)
+        ob, ow, oc = oracle.convert(p, np.eye(3), np.zeros(3), ocfg)
+        best, win, counts = gpu_project(lib, [p], [(np.eye(3), np.zeros(3))], w, h, tr, pr, off, f64=f64)
+        assert np.array_equal(best[0].view(np.uint64), ob.view(np.uint64))
+        assert np.array_equal(win[0], ow)
+        assert np.array_equal(counts[0], oc)
+
+
+def test_reference_conftest_sensor_blob(rng):
+    """The reference test suite's own session config, CodecConfig(mode=
+    "stream", n_frames=2, w=64, h=8, default res) -- whole pipeline, blob
+    byte-identical to the oracle."""
+    from paper_2008_06972_b200 import CodecConfig, compress, synth
+
+    sensor = synth.Sensor(64, 8, 2 * np.pi / 1800, 0.00698, 1.48)
+    grp = synth.make_group(31337, 2, sensor, n_boxes=6)
+    # plus points in every azimuth: they wrap onto the 64 columns
+    clouds = []
+    for c in grp.clouds:
+        th = rng.uniform(0, 2 * np.pi, 20000)
+        ph = 1.48 + rng.uniform(0, 8 * 0.00698, 20000)
+        r = rng.uniform(2, 60, 20000)
+        extra = np.stack([r * np.sin(ph) * np.sin(th), r * np.sin(ph) * np.cos(th), r * np.cos(ph)], 1)
+        clouds.append(np.concatenate([c, extra.astype(np.float32)]))
+    cfg = CodecConfig(mode="stream", n_frames=2, w=64, h=8)
+    mine, _ = compress(clouds, cfg, poses=grp.poses)
+    ref, _ = oracle.compress(clouds, cfg, grp.poses)
+    assert mine == ref, _first_divergence(mine, ref)
+
+
 # ------------------------------------------------------------- whole pipeline
 
 

@@ -334,3 +334,35 @@ def test_batched_pose_transforms_equal_per_group_bits():
     bad[1][4] = (np.eye(3) * 2.0, np.zeros(3))
     with pytest.raises(ValueError):
         poses_to_transform_rows(bad, k)
+
+
+def test_context_pool_bounded_lru_and_exclusive():
+    """Encoder/decoder pooling: a checked-out context is never
+    handed to a second caller, at most max_idle contexts stay cached, and the
+    least recently used config is evicted first."""
+    from paper_2008_06972_b200.codec import _checkout, _Pool
+
+    pool = _Pool("STPC_TEST_POOL_UNSET", 2)
+    made = []
+
+    def factory(tag):
+        def f():
+            made.append(tag)
+            return object()
+        return f
+
+    with _checkout(pool, "a", factory("a")) as a1:
+        with _checkout(pool, "a", factory("a")) as a2:
+            assert a1 is not a2  # concurrent calls never share a context
+    assert made == ["a", "a"]
+    with _checkout(pool, "a", factory("a")) as a3:
+        assert a3 in (a1, a2)  # reused
+    with _checkout(pool, "b", factory("b")):
+        pass
+    with _checkout(pool, "c", factory("c")):
+        pass
+    assert sum(len(v) for v in pool.idle.values()) == 2
+    assert "a" not in pool.idle  # least recently used config went first
+    assert pool.peek("c", factory("c")) is pool.idle["c"][-1]
+    pool.clear()
+    assert not pool.idle
