@@ -584,7 +584,7 @@ constexpr int PK_WIN = STPC_PK_WIN;  // staged bytes of the run section
 #endif
 __global__ void __launch_bounds__(PK_THREADS, STPC_PARSE_MINB) parse_kernel(DecGeom G, const uint8_t* raw, const long long* raw_off,
                                                            const long long* raw_len, const int* sel, float4* tmap,
-                                                           ResSec* res, unsigned long long* pstat)
+                                                           ResSec* res, unsigned long long* pstat, long long* ovl)
 {
     const int j = blockIdx.x;
     const int b = sel[j];
@@ -600,7 +600,20 @@ __global__ void __launch_bounds__(PK_THREADS, STPC_PARSE_MINB) parse_kernel(DecG
     __shared__ int s_ch;
     __shared__ unsigned long long s_flat;
     __shared__ int s_dbad, s_vbad;
-    if (tid == 0) st = DEC_NONE;
+    // Run order check.  The encoder emits temporal runs sorted by (row, s)
+    // and disjoint, and per frame fallback rows in increasing row order with
+    // sorted, disjoint runs; then one plane per (frame, tile) is exact.  Any
+    // other order (a hand-made blob the reference's deserialize accepts) may
+    // overlap, and the reference's stream-order last-writer semantics
+    // (temporal.py:307-331) are replayed by ordered_reconstruct_kernel.
+    __shared__ int s_ovl, s_frow;
+    __shared__ long long s_tend, s_fbpos;
+    if (tid == 0) {
+        st = DEC_NONE;
+        s_ovl = 0;
+        s_tend = -1;
+        s_fbpos = 0;
+    }
     float4* tm = tmap + (long long)j * G.n * G.ty * G.tx;
     const long long ntile = (long long)G.n * G.ty * G.tx;
     for (long long i = tid; i < ntile; i += PK_THREADS) tm[i] = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -646,6 +659,11 @@ __global__ void __launch_bounds__(PK_THREADS, STPC_PARSE_MINB) parse_kernel(DecG
                         break;
                     }
                     recs[c++] = q;
+                    {
+                        const long long key = (long long)(wb(q) | (wb(q + 1) << 8)) * G.tx + (wb(q + 2) | (wb(q + 3) << 8));
+                        if (key < s_tend) s_ovl = 1;
+                        s_tend = key + (wb(q + 4) | (wb(q + 5) << 8));
+                    }
                     if (q + 18 + G.pm > len) {
                         fail(q + 18, 1, STPC_DEC_TRUNCATED);
                         break;
@@ -711,6 +729,7 @@ __global__ void __launch_bounds__(PK_THREADS, STPC_PARSE_MINB) parse_kernel(DecG
         s_ch = 0;
         s_left = 0;
         s_done = 0;
+        s_fbpos = s_pos;
     }
     __syncthreads();
     for (;;) {
@@ -734,6 +753,7 @@ __global__ void __launch_bounds__(PK_THREADS, STPC_PARSE_MINB) parse_kernel(DecG
                         break;
                     }
                     s_left = nrows;
+                    s_frow = -1;
                     ++s_ch;
                     continue;
                 }
@@ -743,6 +763,8 @@ __global__ void __launch_bounds__(PK_THREADS, STPC_PARSE_MINB) parse_kernel(DecG
                 }
                 const int row = (int)dec_u16(p + q), nr = (int)dec_u16(p + q + 2);
                 q += 4;
+                if (row <= s_frow) s_ovl = 1;
+                s_frow = row;
                 if (row >= G.ty || nr > G.tx) {
                     fail(q, 0, STPC_DEC_MALFORMED);
                     break;
@@ -778,6 +800,7 @@ __global__ void __launch_bounds__(PK_THREADS, STPC_PARSE_MINB) parse_kernel(DecG
                     fail(rp + 16, 0, STPC_DEC_MALFORMED);
                     continue;
                 }
+                if (i > 0 && s < (int)dec_u16(p + rp - 16) + (int)dec_u16(p + rp - 14)) s_ovl = 1;
                 const float4 v = make_float4(dec_f32(p + rp + 4), dec_f32(p + rp + 8), dec_f32(p + rp + 12), 2.f);
                 for (int t = s; t < s + ln; ++t)
                     if (dst[t].w != 1.f) dst[t] = v;  // temporal coverage wins (remaining mask)
@@ -898,7 +921,10 @@ __global__ void __launch_bounds__(PK_THREADS, STPC_PARSE_MINB) parse_kernel(DecG
 
 finish:
     __syncthreads();
-    if (tid == 0) pstat[j] = st;
+    if (tid == 0) {
+        pstat[j] = st;
+        ovl[j] = st == DEC_NONE && s_ovl ? s_fbpos : 0;
+    }
 }
 
 // Per pixel of every frame: plane reconstruction from the tile map, exactly
@@ -907,12 +933,13 @@ finish:
 __global__ void __launch_bounds__(1024) reconstruct_kernel(DecGeom G, Trig tg, const uint8_t* raw,
                                                            const long long* raw_off, const int* sel,
                                                            const float4* tmap, const unsigned long long* pstat,
-                                                           double* out_r, unsigned long long* failed)
+                                                           const long long* ovl, double* out_r,
+                                                           unsigned long long* failed)
 {
     const long long f = blockIdx.y;
     long long chl;
     const int j = (int)dmod(f, G.n, G.rn, chl), ch = (int)chl;
-    if (pstat[j] != DEC_NONE) return;
+    if (pstat[j] != DEC_NONE || ovl[j]) return;
     const long long pix = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     int nfail = 0;
     if (pix < G.P) {
@@ -941,6 +968,96 @@ __global__ void __launch_bounds__(1024) reconstruct_kernel(DecGeom G, Trig tg, c
     }
     for (int o = 16; o > 0; o >>= 1) nfail += __shfl_xor_sync(STPC_FULL, nfail, o);
     if ((threadIdx.x & 31) == 0 && nfail) atomicAdd(failed + j, (unsigned long long)nfail);
+}
+
+// Blobs whose runs are not sorted and disjoint (parse_kernel's order check):
+// decode_stream_images' loops replayed in stream order (temporal.py:307-331).
+// Block per (frame, blob): every thread walks the records (uniform loads);
+// each run's pixels are reconstructed block-parallel, a barrier after each
+// run, so a later run overwrites an earlier one and a failed reconstruction
+// keeps the earlier value; failures count per (run, pixel) like the
+// reference's.  Fallback runs see remaining = valid & ~temporal cover (the
+// tile map's w == 1 marks, written only by temporal runs).
+__global__ void __launch_bounds__(256) ordered_reconstruct_kernel(DecGeom G, Trig tg, const uint8_t* raw,
+                                                                  const long long* raw_off, const int* sel,
+                                                                  const float4* tmap,
+                                                                  const unsigned long long* pstat,
+                                                                  const long long* ovl, double* out_r,
+                                                                  unsigned long long* failed)
+{
+    const int ch = blockIdx.x, j = blockIdx.y;
+    if (pstat[j] != DEC_NONE || ovl[j] == 0) return;
+    const long long f = (long long)j * G.n + ch;
+    const uint8_t* p = raw + raw_off[sel[j]];
+    const uint8_t* vb = p + G.bits_off + (long long)ch * G.nb;
+    double* dst = out_r + f * G.P;
+    for (long long pix = threadIdx.x; pix < G.P; pix += blockDim.x) dst[pix] = __longlong_as_double(DEC_NOPT);
+    __syncthreads();
+    unsigned long long nfail = 0;
+    auto apply = [&](int row, int s, int ln, double a, double b, double c, bool fallback) {
+        const int v0 = row * G.th, v1 = min(v0 + G.th, G.h);
+        const int u0 = s * G.tw, u1 = min((s + ln) * G.tw, G.w);
+        const int cols = u1 - u0;
+        const long long cnt = (long long)(v1 - v0) * cols;
+        for (long long i = threadIdx.x; i < cnt; i += blockDim.x) {
+            const int v = v0 + (int)(i / cols), u = u0 + (int)(i % cols);
+            const long long pix = (long long)v * G.w + u;
+            if (!((dec_u8(vb + (pix >> 3)) >> (7 - (pix & 7))) & 1u)) continue;
+            if (fallback && tmap[(f * G.ty + row) * G.tx + u / G.tw].w == 1.f) continue;
+            double dx, dy, dz;
+            ray_dir(tg, v, u, dx, dy, dz);
+            const double den = (dx + a * dy) + b * dz;
+            if (fabs(den) < STPC_PARALLEL_EPS) {
+                ++nfail;
+                continue;
+            }
+            const double r_hat = c / den;
+            if (r_hat <= 0.0 || r_hat > G.r_max) {
+                ++nfail;
+                continue;
+            }
+            dst[pix] = r_hat;
+        }
+        __syncthreads();
+    };
+    // temporal runs <HHH fff> + presence mask + f32 per present non-key frame
+    long long q = G.runs_off;
+    const long long n_runs = dec_u32(p + q);
+    q += 4;
+    for (long long r = 0; r < n_runs; ++r) {
+        const int row = (int)dec_u16(p + q), s = (int)dec_u16(p + q + 2), ln = (int)dec_u16(p + q + 4);
+        const double a = dec_f32(p + q + 6), b = dec_f32(p + q + 10), c = dec_f32(p + q + 14);
+        int extra = 0, before = 0;
+        bool pres = false;
+        for (int c2 = 0; c2 < G.n; ++c2) {
+            if (!((dec_u8(p + q + 18 + (c2 >> 3)) >> (c2 & 7)) & 1u)) continue;
+            if (c2 == ch) pres = true;
+            if (c2 == G.k) continue;
+            if (c2 < ch) ++before;
+            ++extra;
+        }
+        if (pres) apply(row, s, ln, a, b, ch == G.k ? c : (double)dec_f32(p + q + 18 + G.pm + 4 * before), false);
+        q += 18 + G.pm + 4ll * extra;
+    }
+    // fallback rows: per frame <I> rows, each <HH> + nr x <HH fff>
+    q = ovl[j];
+    for (int c2 = 0; c2 < G.n; ++c2) {
+        const long long nrows = dec_u32(p + q);
+        q += 4;
+        for (long long rr = 0; rr < nrows; ++rr) {
+            const int row = (int)dec_u16(p + q), nr = (int)dec_u16(p + q + 2);
+            q += 4;
+            if (c2 == ch)
+                for (int i = 0; i < nr; ++i) {
+                    const uint8_t* rp = p + q + 16ll * i;
+                    apply(row, (int)dec_u16(rp), (int)dec_u16(rp + 2), dec_f32(rp + 4), dec_f32(rp + 8),
+                          dec_f32(rp + 12), true);
+                }
+            q += 16ll * nr;
+        }
+    }
+    for (int o = 16; o > 0; o >>= 1) nfail += __shfl_xor_sync(STPC_FULL, nfail, o);
+    if ((threadIdx.x & 31) == 0 && nfail) atomicAdd(failed + j, nfail);
 }
 
 // Residual pixels override (rng_out[vs, us] = ranges, temporal.py:336-338):
@@ -1146,7 +1263,7 @@ struct stpc_decoder {
     int m = 0;
     DecGeom G{};
     long long F = 0, bpf = 0, total = 0;
-    DevBuf sel, tmap, res, pstat, outr, trig, xfi, blkcnt, fcnt, foff, failed, pts;
+    DevBuf sel, tmap, res, pstat, ovl, outr, trig, xfi, blkcnt, fcnt, foff, failed, pts;
     std::vector<unsigned long long> h_pstat;
     const double* last_points = nullptr;
     // host output path: pinned double buffer + copy threads
@@ -1432,6 +1549,7 @@ int stpc_decoder_frames(stpc_decoder* d, const stpc_decode_geom* g, const int32_
     DRET(d->tmap.ensure(sizeof(float4) * F * G.ty * G.tx));
     DRET(d->res.ensure(sizeof(ResSec) * F));
     DRET(d->pstat.ensure(sizeof(unsigned long long) * m));
+    DRET(d->ovl.ensure(sizeof(long long) * m));
     DRET(d->outr.ensure(sizeof(double) * F * G.P));
     DRET(d->trig.ensure(sizeof(double) * 2 * (G.w + G.h)));
     DRET(d->xfi.ensure(sizeof(double) * 12 * F));
@@ -1454,11 +1572,16 @@ int stpc_decoder_frames(stpc_decoder* d, const stpc_decode_geom* g, const int32_
     STPC_LAUNCH();
     parse_kernel<<<m, PK_THREADS, 0, s>>>(G, raw, roff, d->rlen.as<long long>(), d->sel.as<int>(),
                                           d->tmap.as<float4>(), d->res.as<ResSec>(),
-                                          d->pstat.as<unsigned long long>());
+                                          d->pstat.as<unsigned long long>(), d->ovl.as<long long>());
     const dim3 fg((unsigned)bpf, (unsigned)F);
     STPC_LAUNCH();
     reconstruct_kernel<<<fg, 1024, 0, s>>>(G, tg, raw, roff, d->sel.as<int>(), d->tmap.as<float4>(), pst,
-                                           d->outr.as<double>(), d->failed.as<unsigned long long>());
+                                           d->ovl.as<long long>(), d->outr.as<double>(),
+                                           d->failed.as<unsigned long long>());
+    STPC_LAUNCH();
+    ordered_reconstruct_kernel<<<dim3((unsigned)G.n, (unsigned)m), 256, 0, s>>>(
+        G, tg, raw, roff, d->sel.as<int>(), d->tmap.as<float4>(), pst, d->ovl.as<long long>(),
+        d->outr.as<double>(), d->failed.as<unsigned long long>());
     STPC_LAUNCH();
     residual_kernel<<<dim3((unsigned)G.n, (unsigned)m), PK_THREADS, 0, s>>>(G, raw, roff, d->sel.as<int>(),
                                                                             d->res.as<ResSec>(), pst,

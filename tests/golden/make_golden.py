@@ -401,6 +401,87 @@ def decode_error_cases():
                         blobs=np.concatenate(data), offsets=off)
 
 
+def overlap_cases():
+    """Blobs whose runs overlap or come out of order -- the encoder never
+    writes them, but the reference's deserialize accepts them and its decoder
+    applies temporal runs, then fallback runs, in stream order: per pixel the
+    last successful reconstruction wins and each failed (run, pixel) counts
+    (temporal.py:307-331, _kernels.py:282-308).  Built by editing a real
+    StreamEncoded and re-serializing it with the reference's own serialize;
+    the expected decode is the reference's decompress_full."""
+    import dataclasses
+
+    from stpc.bitstream import decompress_full, deserialize, serialize
+    from stpc.plane import Plane
+    from stpc.spatial import EncodedRow, PlaneRun
+
+    g = synth.make_group(311, 4, SMALL, n_boxes=25)
+    cfg = ref_cfg(SMALL, 4, 0.1, 4, 4)
+    poses = [RigidTransform(R=R, T=T) for R, T in g.poses]
+    blob, _ = stpc.compress(g.clouds, cfg, poses=poses)
+    enc, cfg2 = deserialize(blob)
+    k = enc.k_index
+    tr = enc.temporal_runs
+    long_i = max(range(len(tr)), key=lambda i: tr[i].length)
+    lr = tr[long_i]
+    out = {}
+
+    def shifted(run, ds, dlen, da=0.0, dc=0.0, offsets=None):
+        pl = Plane(float(np.float32(run.plane.a + da)), float(np.float32(run.plane.b)),
+                   float(np.float32(run.plane.c + dc)))
+        offs = offsets if offsets is not None else [
+            None if o is None else float(np.float32(o + dc)) for o in run.offsets]
+        return dataclasses.replace(run, s=run.s + ds, length=run.length + dlen, plane=pl, offsets=offs)
+
+    # (1) a temporal run overlapping the longest one, later in the stream,
+    #     with a tilted plane; every channel present
+    extra = shifted(lr, max(0, lr.length // 3), -(lr.length // 3) if lr.length > 2 else 0, da=0.02, dc=0.3,
+                    offsets=[float(np.float32(o + 0.3)) if o is not None else float(np.float32(lr.plane.c + 0.1))
+                             for o in lr.offsets])
+    out["t_overlap"] = dataclasses.replace(enc, temporal_runs=tr + [extra])
+    # (2) the same overlap with a negative offset on one channel: r_hat <= 0
+    #     fails there, so the earlier run's value must survive
+    bad = dataclasses.replace(extra, offsets=[(-5.0 if ch == (k + 1) % enc.n else o)
+                                              for ch, o in enumerate(extra.offsets)])
+    out["t_overlap_fail"] = dataclasses.replace(enc, temporal_runs=tr + [bad])
+    # (3) temporal runs in reverse stream order (disjoint): decodes as (0)
+    out["t_reversed"] = dataclasses.replace(enc, temporal_runs=list(reversed(tr)))
+    # (4) fallback: a duplicated row with another plane, plus an overlapping
+    #     run inside a row
+    ch = max((c for c in range(enc.n) if c != k), key=lambda c: len(enc.fallback_rows[c]))
+    rows = list(enc.fallback_rows[ch])
+    assert len(rows) >= 3
+    r0 = rows[0]
+    run0 = r0.runs[0]
+    ov = PlaneRun(s=run0.s, length=run0.length, plane=Plane(float(np.float32(run0.plane.a)),
+                  float(np.float32(run0.plane.b + 0.01)), float(np.float32(run0.plane.c + 0.2))))
+    dup = EncodedRow(row_id=r0.row_id, runs=[ov])
+    inner = EncodedRow(row_id=rows[-2].row_id, runs=list(rows[-2].runs) + [
+        PlaneRun(s=rows[-2].runs[0].s, length=1, plane=Plane(0.0, 0.0, -1.0))])  # r_hat < 0: failures
+    fb = [list(x) for x in enc.fallback_rows]
+    fb[ch] = rows[:-2] + [inner, dup]  # same row count (the format caps it at tiles_y)
+    out["fb_overlap"] = dataclasses.replace(enc, fallback_rows=fb)
+
+    names, data, shas, counts, failed = [], [], [], [], []
+    for name, e in out.items():
+        b = serialize(e, cfg2)
+        clouds, rep = decompress_full(b)
+        names.append(name)
+        data.append(np.frombuffer(b, np.uint8))
+        shas.append([hashlib.sha256(np.ascontiguousarray(p).tobytes()).hexdigest() for p in clouds])
+        counts.append([p.shape[0] for p in clouds])
+        failed.append(rep.failed_reconstructions)
+        print(f"  {name:16s} {len(b)} B, failed {rep.failed_reconstructions}, points {counts[-1]}")
+    off = np.zeros(len(data) + 1, np.int64)
+    off[1:] = np.cumsum([d.size for d in data])
+    theta = (np.arange(SMALL.w, dtype=np.float64) + 0.5) * SMALL.theta_r
+    phi = SMALL.phi_offset + (np.arange(SMALL.h, dtype=np.float64) + 0.5) * SMALL.phi_r
+    np.savez_compressed(os.path.join(HERE, "decode_overlap.npz"), names=np.array(names), blobs=np.concatenate(data),
+                        offsets=off, dec_sha256=np.array(shas), dec_counts=np.array(counts),
+                        failed=np.array(failed, np.int64),
+                        trig=np.concatenate([np.sin(theta), np.cos(theta), np.sin(phi), np.cos(phi)]))
+
+
 CASES = {
     "single_4x4": lambda: compress_case("single_4x4", 101, 1, 0.1, 4, 4),
     "stream3_4x4": lambda: compress_case("stream3_4x4", 102, 3, 0.1, 4, 4),
@@ -421,6 +502,8 @@ if __name__ == "__main__":
         huffman_cases()
     if not only or "decode_errors" in only:
         decode_error_cases()
+    if not only or "decode_overlap" in only:
+        overlap_cases()
     for name, fn in CASES.items():
         if not only or name in only:
             fn()
