@@ -146,6 +146,17 @@ int stpc_project(const void* d_points, int32_t points_f64, const int64_t* point_
                  const double* transforms, int32_t w, int32_t h, double theta_r, double phi_r,
                  double phi_offset, double* d_best, int64_t* d_win, int64_t* h_counts, void* stream);
 
+/* The entropy stage alone (huffman.encode_bytes huffman.py:107-118 with the
+ * 32-bit cap repair :51-58, canonical codes :63-77, huffman_encode_kernel
+ * _kernels.py:363-382, header + zlib.crc32 bitstream.py:279-289) on n raw
+ * payloads in host memory (payload i = h_payloads[offsets[i], offsets[i+1])):
+ * blob i lands at h_out[out_offsets[i], out_offsets[i+1]).  The kernels are
+ * the ones stpc_encode_* run; this entry exists so a payload of any byte
+ * statistics (e.g. a Fibonacci histogram that forces the cap repair) can be
+ * coded on the device. */
+int stpc_entropy_encode(const uint8_t* h_payloads, const int64_t* offsets, int32_t n, uint8_t* h_out,
+                        int64_t out_cap, int64_t* out_offsets);
+
 /* Decoder (decompress / decompress_full, bitstream.py:605-631; SURVEY.md
  * §8(f) rank 3), batched over blobs, all on the GPU:
  *

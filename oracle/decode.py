@@ -179,7 +179,16 @@ def reconstruct(rng_out, msk_out, allowed, dirs, v0, u0, u1, a, b, c, r_max=200.
 
 
 def decompress(blob: bytes) -> List[np.ndarray]:
+    return decompress_full(blob)[0]
+
+
+def decompress_full(blob: bytes):
+    """(clouds, failed reconstructions) as stpc.decompress_full
+    (bitstream.py:605-625): runs are applied in stream order, the last
+    successful reconstruction of a pixel wins, and every failed (run, pixel)
+    counts (temporal.py:307-331)."""
     dec = deserialize(blob)
+    failed = 0
     c = dec.cfg
     n, w, h, tw, th = c["n_frames"], c["w"], c["h"], c["tile_w"], c["tile_h"]
     tx, ty = -(-w // tw), -(-h // th)
@@ -202,7 +211,7 @@ def decompress(blob: bytes) -> List[np.ndarray]:
             u0 = dec.t_s[j] * tw
             u1 = min((dec.t_s[j] + dec.t_len[j]) * tw, w)
             a, b, _ = dec.t_abc[j]
-            reconstruct(rng_out, msk_out, valid[v0:v1, u0:u1].copy(), dirs, v0, u0, u1, a, b, offs[ch])
+            failed += reconstruct(rng_out, msk_out, valid[v0:v1, u0:u1].copy(), dirs, v0, u0, u1, a, b, offs[ch])
         remaining = valid & ~t_cov
         for row, runs in dec.fallback[ch]:
             v0 = row * th
@@ -210,8 +219,8 @@ def decompress(blob: bytes) -> List[np.ndarray]:
             for s, ln, a, b, cc in runs:
                 u0 = s * tw
                 u1 = min((s + ln) * tw, w)
-                reconstruct(rng_out, msk_out, remaining[v0:v1, u0:u1].copy(), dirs, v0, u0, u1,
-                            float(a), float(b), float(cc))
+                failed += reconstruct(rng_out, msk_out, remaining[v0:v1, u0:u1].copy(), dirs, v0, u0, u1,
+                                      float(a), float(b), float(cc))
         flat, ranges = dec.residuals[ch]
         if flat.size:
             rng_out.reshape(-1)[flat] = ranges
@@ -221,4 +230,4 @@ def decompress(blob: bytes) -> List[np.ndarray]:
         Rinv = R.T
         Tinv = -(R.T @ T)
         out.append(orc.transform(pts, Rinv, Tinv))  # pts @ Rinv.T + Tinv (motion.py:70-72)
-    return out
+    return out, failed

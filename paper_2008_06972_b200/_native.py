@@ -34,7 +34,7 @@ EXPORTS = [
     "stpc_decoder_create", "stpc_decoder_destroy", "stpc_decoder_load", "stpc_decoder_load_gather",
     "stpc_decoder_heads",
     "stpc_decoder_frames", "stpc_decoder_total_points", "stpc_decoder_points",
-    "stpc_decoder_device_points",
+    "stpc_decoder_device_points", "stpc_entropy_encode",
 ]
 
 # stpc_decoder_* status kinds
@@ -123,6 +123,7 @@ def load(require_device: bool = False):
                 "stpc_decoder_total_points": ([P], I64),
                 "stpc_decoder_points": ([P, P, I32, I64, P], ctypes.c_int),
                 "stpc_decoder_device_points": ([P], P),
+                "stpc_entropy_encode": ([P, P, I32, P, I64, P], ctypes.c_int),
             }
             for name, (args, res) in sig.items():
                 fn = getattr(L, name)

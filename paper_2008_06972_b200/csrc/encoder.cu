@@ -1030,6 +1030,88 @@ int stpc_encoder_buffer(const stpc_encoder* enc, int32_t which, void** dev_ptr, 
     return STPC_OK;
 }
 
+// The entropy stage alone on caller-supplied raw payloads (the same kernels
+// and launch sequence as encode_impl's entropy stage).
+int stpc_entropy_encode(const uint8_t* h_payloads, const int64_t* offsets, int32_t n, uint8_t* h_out,
+                        int64_t out_cap, int64_t* out_offsets)
+{
+    if (n < 1 || !h_payloads || !offsets || !h_out || !out_offsets) {
+        g_err = "invalid arguments";
+        return STPC_ERR_ARG;
+    }
+    cudaStream_t s = nullptr;
+    std::vector<long long> len(n), poff(n + 1, 0);
+    long long max_payload = 0;
+    for (int i = 0; i < n; ++i) {
+        len[i] = offsets[i + 1] - offsets[i];
+        if (len[i] < 0) {
+            g_err = "invalid offsets";
+            return STPC_ERR_ARG;
+        }
+        poff[i + 1] = poff[i] + (len[i] + 15) / 16 * 16;  // 16-byte aligned like the encoder's arena
+        max_payload = std::max(max_payload, len[i]);
+    }
+    DevBuf payload, plen, pofs, hist, lens, codes, enc_len, blob_off, chunk_bits, seg_crc, blobs;
+    ENS(payload, (size_t)poff[n] + 16);
+    ENS(plen, sizeof(long long) * n);
+    ENS(pofs, sizeof(long long) * (n + 1));
+    ENS(hist, sizeof(unsigned) * 256 * n);
+    ENS(lens, 256 * (size_t)n);
+    ENS(codes, sizeof(unsigned) * 256 * n);
+    ENS(enc_len, sizeof(long long) * n);
+    ENS(blob_off, sizeof(long long) * (n + 1));
+    for (int i = 0; i < n; ++i)
+        if (len[i]) CK(cudaMemcpy(payload.as<uint8_t>() + poff[i], h_payloads + offsets[i], (size_t)len[i],
+                                  cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(plen.p, len.data(), sizeof(long long) * n, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(pofs.p, poff.data(), sizeof(long long) * (n + 1), cudaMemcpyHostToDevice));
+    EntropyArgs en;
+    en.G = n;
+    en.payload = payload.as<uint8_t>();
+    en.payload_off = pofs.as<long long>();
+    en.payload_len = plen.as<long long>();
+    en.hist = hist.as<unsigned>();
+    en.lens = lens.as<uint8_t>();
+    en.codes = codes.as<unsigned>();
+    en.enc_len = enc_len.as<long long>();
+    en.blob_off = blob_off.as<long long>();
+    en.max_chunks = (int)((max_payload + PACK_CHUNK - 1) / PACK_CHUNK);
+    launch_zero(en.hist, sizeof(unsigned) * 256 * n, s);
+    launch_histogram(en, (int)max_payload, s);
+    launch_code_lengths(en, s);
+    launch_group_scan(en.enc_len, en.blob_off, n, 16, HDR, s);
+    std::vector<long long> el(n), bo(n + 1);
+    CK(cudaMemcpy(el.data(), en.enc_len, sizeof(long long) * n, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(bo.data(), en.blob_off, sizeof(long long) * (n + 1), cudaMemcpyDeviceToHost));
+    long long max_enc = 0;
+    for (int i = 0; i < n; ++i) max_enc = std::max(max_enc, el[i]);
+    en.max_segs = (int)((max_enc + CRC_SEG - 1) / CRC_SEG);
+    ENS(chunk_bits, sizeof(long long) * (size_t)n * std::max(en.max_chunks, 1));
+    ENS(seg_crc, sizeof(unsigned) * (size_t)n * std::max(en.max_segs, 1));
+    ENS(blobs, (size_t)bo[n] + 16);
+    en.chunk_bits = chunk_bits.as<long long>();
+    en.seg_crc = seg_crc.as<unsigned>();
+    en.blobs = blobs.as<uint8_t>();
+    launch_zero(en.blobs, bo[n], s);
+    launch_pack(en, s);
+    launch_crc(en, s);
+    CK(cudaGetLastError());
+    long long total = 0;
+    for (int i = 0; i < n; ++i) total += HDR + el[i];
+    if (total > out_cap) {
+        g_err = "output buffer too small: need " + std::to_string(total);
+        return STPC_ERR_ARG;
+    }
+    CK(cudaStreamSynchronize(s));
+    out_offsets[0] = 0;
+    for (int i = 0; i < n; ++i) {
+        CK(cudaMemcpy(h_out + out_offsets[i], blobs.as<uint8_t>() + bo[i], (size_t)(HDR + el[i]),
+                      cudaMemcpyDeviceToHost));
+        out_offsets[i + 1] = out_offsets[i] + HDR + el[i];
+    }
+    return STPC_OK;
+}
+
 int stpc_project(const void* d_points, int32_t points_f64, const int64_t* point_offsets, int32_t n_frames,
                  const double* transforms, int32_t w, int32_t h, double theta_r, double phi_r,
                  double phi_offset, double* d_best, int64_t* d_win, int64_t* h_counts, void* stream)

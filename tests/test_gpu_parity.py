@@ -649,3 +649,78 @@ def test_repeated_calls_deterministic_and_coverage_partition():
         assert rep.coverage[cfg.k_index]["fallback"] == 0
         assert rep.coverage[cfg.k_index]["temporal"] > 0
         assert sum(c["temporal"] for i, c in enumerate(rep.coverage) if i != cfg.k_index) > 0
+
+
+def test_decompress_overlapping_runs_match_reference():
+    """Blobs with overlapping temporal runs, a failing overlap, reversed run
+    order, and duplicated / overlapping fallback runs (decode_overlap.npz,
+    made by the reference's own serialize): the GPU decoder replays the
+    reference's stream-order semantics -- last successful reconstruction
+    wins, failures count per (run, pixel) (temporal.py:307-331) -- and its
+    clouds and failure count equal the reference's decompress_full."""
+    import hashlib
+
+    from oracle import decode as odec
+    from paper_2008_06972_b200 import decompress_full, decompress_many
+
+    z = np.load(os.path.join(GOLDEN, "decode_overlap.npz"))
+    from paper_2008_06972_b200 import synth
+
+    sm = synth.Sensor(360, 12, 2 * np.pi / 360, np.radians(2.2), np.radians(88.0))
+    th = (np.arange(sm.w, dtype=np.float64) + 0.5) * sm.theta_r
+    ph = sm.phi_offset + (np.arange(sm.h, dtype=np.float64) + 0.5) * sm.phi_r
+    same_trig = np.array_equal(np.concatenate([np.sin(th), np.cos(th), np.sin(ph), np.cos(ph)]), z["trig"])
+    blobs = []
+    for i, name in enumerate(z["names"]):
+        blob = z["blobs"][z["offsets"][i]:z["offsets"][i + 1]].tobytes()
+        blobs.append(blob)
+        clouds, rep = decompress_full(blob)
+        ref, ref_failed = odec.decompress_full(blob)
+        for a, b in zip(clouds, ref):
+            assert np.array_equal(a, b), name
+        assert rep.failed_reconstructions == ref_failed == z["failed"][i], name
+        if same_trig:
+            assert [hashlib.sha256(np.ascontiguousarray(c).tobytes()).hexdigest() for c in clouds] == \
+                list(z["dec_sha256"][i]), name
+    # mixed in one batch with ordinary blobs (only the flagged ones take the ordered path)
+    good = load_case("stream3_4x4")[3]
+    clouds, reps = decompress_many([good] + blobs + [good])
+    assert [r.failed_reconstructions for r in reps[1:-1]] == list(z["failed"])
+    for a, b in zip(clouds[0], odec.decompress(good)):
+        assert np.array_equal(a, b)
+
+
+def test_entropy_stage_cap_repair_on_device(lib):
+    """The device entropy stage (stpc_entropy_encode: histogram, code lengths,
+    canonical codes, packing, CRC) on payloads with Fibonacci byte counts:
+    34 symbols give a 33-deep Huffman tree, so the 32-bit cap repair
+    (huffman.py:51-58; entropy.cu code_lengths_kernel) must run.  Blobs equal
+    the oracle's byte for byte (the oracle's code lengths are pinned against
+    the reference's on huffman.npz's 40-symbol Fibonacci case)."""
+    rng = np.random.default_rng(11)
+    fib = [1, 1]
+    while len(fib) < 40:
+        fib.append(fib[-1] + fib[-2])
+    payloads = []
+    for nsym, perm in ((34, False), (35, True), (33, False)):
+        h = np.zeros(256, np.int64)
+        syms = rng.permutation(256)[:nsym] if perm else np.arange(nsym)
+        h[syms] = fib[:nsym]
+        p = np.repeat(np.arange(256, dtype=np.uint8), h)
+        rng.shuffle(p)
+        payloads.append(p.tobytes())
+        assert oracle.code_lengths(h).max() == 32 and (nsym < 34 or nsym - 1 > 32)
+    payloads += [bytes([9]) * 1000, b"", bytes(rng.integers(0, 256, 5000, dtype=np.uint8))]
+    buf = np.frombuffer(b"".join(payloads), np.uint8)
+    off = np.zeros(len(payloads) + 1, np.int64)
+    off[1:] = np.cumsum([len(p) for p in payloads])
+    cap = sum(len(p) for p in payloads) + 300 * len(payloads) + 4096
+    out = np.zeros(cap, np.uint8)
+    oo = np.zeros(len(payloads) + 1, np.int64)
+    rc = lib.stpc_entropy_encode(buf.ctypes.data, off.ctypes.data, len(payloads), out.ctypes.data, cap, oo.ctypes.data)
+    assert rc == 0, lib.stpc_last_error()
+    for i, p in enumerate(payloads):
+        mine = out[oo[i]:oo[i + 1]].tobytes()
+        ref = oracle.entropy_blob(p)
+        assert mine == ref, (i, _first_divergence(mine, ref))
+    assert out[oo[0] + 28:oo[0] + 284].max() == 32  # the repaired table reached the cap

@@ -83,3 +83,29 @@ def test_oracle_decoder_matches_reference_decompress(name):
     dec = odec.decompress(blob)
     assert [p.shape[0] for p in dec] == list(z["dec_counts"])
     assert [hashlib.sha256(np.ascontiguousarray(p).tobytes()).hexdigest() for p in dec] == list(z["dec_sha256"])
+
+
+def test_oracle_decoder_overlapping_runs_match_reference():
+    """decode_overlap.npz: overlapping / duplicated / out-of-order runs that
+    the reference's deserialize accepts; the oracle decoder reproduces the
+    reference's decompress_full (stream-order last writer, per-(run, pixel)
+    failure count)."""
+    import hashlib
+
+    from oracle import decode as odec
+
+    z = np.load(os.path.join(GOLDEN, "decode_overlap.npz"))
+    from paper_2008_06972_b200 import synth
+
+    sm = synth.Sensor(360, 12, 2 * np.pi / 360, np.radians(2.2), np.radians(88.0))  # make_golden.SMALL
+    th = (np.arange(sm.w, dtype=np.float64) + 0.5) * sm.theta_r
+    ph = sm.phi_offset + (np.arange(sm.h, dtype=np.float64) + 0.5) * sm.phi_r
+    same_trig = np.array_equal(np.concatenate([np.sin(th), np.cos(th), np.sin(ph), np.cos(ph)]), z["trig"])
+    for i, name in enumerate(z["names"]):
+        blob = z["blobs"][z["offsets"][i]:z["offsets"][i + 1]].tobytes()
+        clouds, failed = odec.decompress_full(blob)
+        assert [c.shape[0] for c in clouds] == list(z["dec_counts"][i]), name
+        assert failed == z["failed"][i], name
+        shas = [hashlib.sha256(np.ascontiguousarray(c).tobytes()).hexdigest() for c in clouds]
+        if same_trig:
+            assert shas == list(z["dec_sha256"][i]), name
