@@ -22,6 +22,75 @@
 using namespace stpc;
 
 unsigned long long stpc::g_launch_count = 0;
+
+#ifdef STPC_GUARD
+#include <mutex>
+#include <set>
+namespace {
+std::mutex g_guard_mu;
+std::set<DevBuf*> g_guard_bufs;
+constexpr unsigned char GUARD_BYTE = 0xA5;
+
+__global__ void guard_count_kernel(const unsigned char* p, long long n, unsigned long long* bad)
+{
+    unsigned long long c = 0;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+        c += p[i] != GUARD_BYTE;
+    if (c) atomicAdd(bad, c);
+}
+}  // namespace
+
+void stpc::guard_arm(DevBuf* b, size_t from)
+{
+    cudaDeviceSynchronize();
+    if (b->cap > from) cudaMemset((char*)b->p + from, GUARD_BYTE, b->cap - from);
+    cudaDeviceSynchronize();
+    std::lock_guard<std::mutex> lk(g_guard_mu);
+    g_guard_bufs.insert(b);
+}
+
+void stpc::guard_forget(DevBuf* b)
+{
+    std::lock_guard<std::mutex> lk(g_guard_mu);
+    g_guard_bufs.erase(b);
+}
+
+// Canary bytes changed past each live workspace's requested size; a report
+// line per damaged buffer goes to `report`.
+extern "C" int64_t stpc_debug_guard_check(char* report, int32_t cap)
+{
+    cudaDeviceSynchronize();
+    std::lock_guard<std::mutex> lk(g_guard_mu);
+    unsigned long long* d_bad = nullptr;
+    cudaMalloc(&d_bad, sizeof(unsigned long long));
+    std::string rep;
+    long long total = 0;
+    for (DevBuf* b : g_guard_bufs) {
+        if (!b->p || b->cap <= b->used) continue;
+        cudaMemset(d_bad, 0, sizeof(unsigned long long));
+        guard_count_kernel<<<148, 256>>>((const unsigned char*)b->p + b->used, (long long)(b->cap - b->used), d_bad);
+        unsigned long long bad = 0;
+        cudaMemcpy(&bad, d_bad, sizeof(bad), cudaMemcpyDeviceToHost);
+        if (bad) {
+            total += (long long)bad;
+            rep += "buffer " + std::to_string((unsigned long long)(uintptr_t)b->p) + " used " + std::to_string(b->used) +
+                   " cap " + std::to_string(b->cap) + ": " + std::to_string(bad) + " bytes past the end changed\n";
+        }
+    }
+    cudaFree(d_bad);
+    if (report && cap > 0) {
+        strncpy(report, rep.c_str(), (size_t)cap - 1);
+        report[cap - 1] = 0;
+    }
+    return cudaGetLastError() == cudaSuccess ? total : -1;
+}
+
+extern "C" int32_t stpc_debug_guard_buffers(void)
+{
+    std::lock_guard<std::mutex> lk(g_guard_mu);
+    return (int32_t)g_guard_bufs.size();
+}
+#endif
 static thread_local std::string g_err;
 void stpc::set_last_error(const std::string& msg) { g_err = msg; }
 
@@ -288,9 +357,12 @@ static int encode_impl(stpc_encoder* e, int G, const void* d_points, const int64
     // --- workspace
     const int bi = e->best_cur;
     DevBuf& best = e->best2[bi];
+    // both grids sized to an even element count: the pack kernels' prefill
+    // of the other grid stores 16 bytes at a time
+    const long long PE = (F * g.P + 1) / 2 * 2;
     {
         void* before = best.p;
-        ENS(best, sizeof(double) * F * g.P);
+        ENS(best, sizeof(double) * PE);
         if (best.p != before) e->best_filled[bi] = 0;
     }
     ENS(e->vbits, (size_t)F * g.pbs);
@@ -521,11 +593,11 @@ static int encode_impl(stpc_encoder* e, int G, const void* d_points, const int64
     DevBuf& nxt_best = e->best2[nb];
     {
         void* before = nxt_best.p;
-        ENS(nxt_best, sizeof(double) * F * g.P);
+        ENS(nxt_best, sizeof(double) * PE);
         if (nxt_best.p != before) e->best_filled[nb] = 0;
     }
     en.prefill = nxt_best.as<unsigned long long>();
-    en.prefill_n = (F * g.P + 1) / 2 * 2;
+    en.prefill_n = PE;
     en.payload_off = pa.payload_off;
     en.payload_len = pa.payload_len;
     en.hist = e->hist.as<unsigned>();
