@@ -445,46 +445,32 @@ def algorithmic_bytes(stage, cfg, n, G, npts, raw_bytes=0, blob_bytes=0):
     return None
 
 
-# stage -> (kernel name in the ncu capture, which of its launches)
-_NCU_KERNEL = {"fit_p": ("fit_pair_kernel", -1), "fit_key": ("fit_pair_kernel", 0),
-               "convert": ("void convert_kernel<float>", 0), "emit": ("emit_residual_kernel", 0)}
+# the limiter of each stage: HBM for the
+# streaming kernels, issue slots / dependent latency for the fits and the
+# byte-serial entropy kernels
+STAGE_BOUND = {"convert": "hbm", "bitmaps": "hbm", "emit": "hbm", "plan": "latency", "init": "latency",
+               "start_key": "issue", "start_p": "issue", "fit_key": "issue", "fit_p": "issue", "refit": "issue",
+               "huffman": "issue", "pack": "issue", "crc": "issue"}
 
 
-def ncu_traffic(stage, args, G):
-    """dram__bytes_read + dram__bytes_write per launch of the stage's kernel,
-    from the committed `ncu --set full` capture of this exact workload
-    (profiles/r1_ncu_full_1024groups.json), else null."""
-    path = os.path.join(ROOT, "profiles", "r1_ncu_full_1024groups.json")
-    if stage not in _NCU_KERNEL or args.config != 4 or G != 1024 or args.tile or args.tau:
-        return {"traffic": None}
-    try:
-        rows = json.load(open(path))
-        name, idx = _NCU_KERNEL[stage]
-        rows = [r for r in rows if r["kernel"] == name]
-        r = rows[idx]
-        scale = {"Gbyte": 1e9, "Mbyte": 1e6, "Kbyte": 1e3, "byte": 1.0}
-        t = r["dram_read"] * scale[r["dram_read_unit"]] + r["dram_write"] * scale[r["dram_write_unit"]]
-        return {"traffic": t, "traffic_unit": "bytes/launch",
-                "traffic_source": "profiles/r1_ncu_full_1024groups.json (ncu --set full, same workload)"}
-    except Exception:
-        return {"traffic": None}
+def ncu_stages():
+    """Per-stage ncu metrics (DRAM traffic, IPC) of the newest committed
+    capture whose source hash equals this build's sources
+    (tools/ncu_stages.py), else None -- numbers from other code are refused."""
+    import glob
 
+    from paper_2008_06972_b200 import build
 
-def fit_utilisation(args, G):
-    """SM / FP64-pipe utilisation of the fitting kernel (BASELINE asks for it
-    instead of an HBM fraction) from the committed ncu capture."""
-    if args.config != 4 or G != 1024 or args.tile or args.tau:
-        return None
-    try:
-        rows = [r for r in json.load(open(os.path.join(ROOT, "profiles", "r1_ncu_full_1024groups.json")))
-                if r["kernel"] == "fit_pair_kernel"]
-        r = rows[-1]
-        return {"kernel": "fit_pair_kernel (P frames)", "sm_throughput_pct": r["sm_throughput_pct"],
-                "fp64_pipe_pct": r["fp64_pipe_pct"], "ipc": r["ipc"],
-                "achieved_occupancy_pct": r["achieved_occupancy_pct"],
-                "source": "profiles/r1_ncu_full_1024groups.json (ncu --set full)"}
-    except Exception:
-        return None
+    h = build.source_hash()
+    for path in sorted(glob.glob(os.path.join(ROOT, "profiles", "*_ncu_stages.json")), reverse=True):
+        try:
+            d = json.load(open(path))
+        except Exception:
+            continue
+        if d.get("source_hash") == h:
+            d["path"] = os.path.relpath(path, ROOT)
+            return d
+    return None
 
 
 def main():
@@ -665,6 +651,8 @@ def main():
         peak, peak_src = float(peaks["hbm_gbs"]), "measured"
     except Exception:
         peak, peak_src = 6650.0, "fallback"
+    prof = ncu_stages()
+    pst = (prof or {}).get("stages", {})
     order = np.argsort(-stage_ms)
     dom = names[int(order[0])]
     dom_ms = float(stage_ms[int(order[0])])
@@ -672,25 +660,40 @@ def main():
     roofline = {"bound": "hbm", "kernel": dom, "ms": dom_ms,
                 "share_of_step": dom_ms / ms_step if ms_step else None,
                 "achieved": (ab / (dom_ms / 1e3) / 1e9) if ab else None, "peak": peak,
-                "peak_source": peak_src, "unit": "GB/s", "traffic": None}
+                "peak_source": peak_src, "unit": "GB/s", "traffic": None,
+                "limiter": STAGE_BOUND.get(dom, "hbm")}
     roofline["frac"] = roofline["achieved"] / peak if roofline["achieved"] else None
-    roofline.update(ncu_traffic(dom, args, G))
+    if dom in pst:
+        roofline["traffic"] = pst[dom]["dram_bytes"]
+        roofline["traffic_unit"] = "bytes/launch (ncu dram__bytes_read+write)"
+        if roofline["limiter"] == "issue":
+            roofline["issue"] = {"ipc": pst[dom].get("ipc"), "peak_ipc": 4.0, "frac": pst[dom].get("issue_frac"),
+                                 "fp64_pipe_pct": pst[dom].get("fp64_pipe_pct"),
+                                 "warp_instructions": pst[dom].get("warp_instructions")}
+    if prof:
+        roofline["profile"] = {"path": prof["path"], "source_hash": prof["source_hash"]}
+    else:
+        roofline["profile"] = "no ncu capture of these sources committed: traffic/issue fields null"
     # per-stage achieved fraction of the HBM roofline (BASELINE: "per-kernel
-    # achieved fraction"; conversion and compaction called out)
+    # achieved fraction"; conversion and compaction called out), with the
+    # stage's limiter, its measured DRAM bytes and issue rate where captured
     stages = {}
     for nm, v in zip(names, stage_ms):
         b = algorithmic_bytes(nm, cfg, n, G, npts, int(raw.sum()), blob_bytes)
         if b and v > 0:
             gbs = b / (float(v) / 1e3) / 1e9
-            stages[nm] = {"ms": round(float(v), 4), "algorithmic_GB": round(b / 1e9, 3), "achieved": round(gbs, 1),
-                          "frac": round(gbs / peak, 4)}
+            st = {"ms": round(float(v), 4), "bound": STAGE_BOUND.get(nm, "hbm"), "algorithmic_GB": round(b / 1e9, 3),
+                  "achieved": round(gbs, 1), "frac": round(gbs / peak, 4)}
+            if nm in pst:
+                tb = pst[nm]["dram_bytes"]
+                st["traffic_GB"] = round(tb / 1e9, 3)
+                st["traffic_frac"] = round(tb / (float(v) / 1e3) / 1e9 / peak, 4)  # measured bytes / live time
+                st["ipc"] = pst[nm].get("ipc")
+                st["issue_frac"] = pst[nm].get("issue_frac")
+            stages[nm] = st
     roofline["stages"] = stages
     roofline["convert"] = stages.get("convert")
     roofline["compaction"] = stages.get("emit")
-    if roofline["compaction"]:
-        roofline["compaction"] = dict(roofline["compaction"], **ncu_traffic("emit", args, G),
-                                      kernel="emit_residual_kernel (traffic); stage time covers all emit kernels")
-    roofline["fit_utilisation"] = fit_utilisation(args, G)
 
     # ---------------- parity of the timed workload (after timing; oracle = checker)
     parity = None

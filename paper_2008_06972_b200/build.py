@@ -41,6 +41,19 @@ def deps():
     return sources() + glob.glob(os.path.join(CSRC, "*.cuh")) + [os.path.join(ROOT, "include", "stpc_b200.h")]
 
 
+def source_hash() -> str:
+    """sha256 of every compiled input and the flags: stamps profiles taken
+    from a build, so bench.py can refuse numbers from different code."""
+    import hashlib
+
+    h = hashlib.sha256(" ".join(NVCC_FLAGS).encode())
+    for p in sorted(deps()):
+        h.update(os.path.basename(p).encode())
+        with open(p, "rb") as f:
+            h.update(f.read())
+    return h.hexdigest()[:16]
+
+
 def needs_build(out: str = LIB) -> bool:
     if not os.path.exists(out):
         return True
