@@ -53,6 +53,9 @@ def parse():
     ap.add_argument("--no-decode", action="store_true", help="skip the decompress measurement")
     ap.add_argument("--decode-e2e-groups", type=int, default=128)
     ap.add_argument("--no-parity", action="store_true", help="skip the post-timing oracle comparison")
+    ap.add_argument("--shard", action="store_true",
+                    help="headline = strong scaling: the one configs[3] batch split across the ranks "
+                         "(default: weak, each rank its own batch; N>1 always adds the strong block)")
     return ap.parse_args()
 
 
@@ -136,9 +139,10 @@ class ClockSampler:
 
 # ------------------------------------------------------------------ inputs
 
-def make_inputs(args, rank, device):
-    """Seeded groups generated on the GPU; returns device points, host offsets
-    and transforms, plus a few host copies for the CPU baseline."""
+def make_inputs(args, rank, device, groups=None):
+    """Seeded groups generated on the GPU (seeds of `rank`; `groups`: the
+    group indices, default all of the config's); returns device points, host
+    offsets and transforms."""
     import torch
 
     from paper_2008_06972_b200 import synth
@@ -147,7 +151,7 @@ def make_inputs(args, rank, device):
     sensor, n, tile, tau, scene, G = workload(args)
     k = n // 2
     frames, xf, counts = [], [], []
-    for g in range(G):
+    for g in (range(G) if groups is None else groups):
         grp = synth.make_group(group_seed(rank, g, args.config), n, sensor, device=device,
                                as_numpy=False, **scene)
         frames.extend(grp.clouds)
@@ -502,15 +506,26 @@ def main():
     # on each other's kernels, only on the final gathers
     backend = os.environ.get("STPC_DIST_BACKEND", "nccl")
     local = local % max(torch.cuda.device_count(), 1) if backend != "nccl" else local
+    numa = None
     if world > 1:
         import torch.distributed as dist_mod
 
+        from paper_2008_06972_b200 import dist as pdist
+
         dist = dist_mod
         torch.cuda.set_device(local)
+        numa = pdist.bind_to_gpu_numa(local)
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+        t_init = time.perf_counter()
         if backend == "nccl":
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         else:
             dist.init_process_group(backend)
+        dist.barrier()
+        print(f"[rank {rank}/{world}] {dist.get_backend()} communicator up in {time.perf_counter() - t_init:.2f} s "
+              f"on cuda:{local}, NUMA node {numa['numa_node']} ({numa['cpus']} cpus bound)", file=sys.stderr,
+              flush=True)
     else:
         torch.cuda.set_device(local)
     device = torch.device("cuda", local)
@@ -605,6 +620,48 @@ def main():
     frames_all = G * n * world
     fps = frames_all / (ms_step / 1e3)
     mpts = total_pts / (ms_step / 1e3) / 1e6
+
+    # ---------------- strong scaling: ONE fixed batch (configs[3]: 1024
+    # groups, rank-0 seeds) split across the ranks by contiguous group
+    # shards (dist.shard_range; replaces parallel.py:12-17's fan-out), no
+    # data-path collective, ragged per-group sizes gathered at the end
+    strong = None
+    if world > 1 or args.shard:
+        from paper_2008_06972_b200 import dist as pdist
+
+        lo, hi = pdist.shard_range(G, rank, world) if world > 1 else (0, G)
+        d_sh, off_sh, xf_sh = make_inputs(args, 0, device, groups=range(lo, hi))
+        Gs = hi - lo
+        for _ in range(max(args.warmup, 0)):
+            enc.encode_device(Gs, d_sh.data_ptr(), off_sh, xf_sh, sptr)
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+        s0 = torch.cuda.Event(enable_timing=True)
+        s1 = torch.cuda.Event(enable_timing=True)
+        s0.record(stream)
+        for _ in range(args.steps):
+            enc.encode_device(Gs, d_sh.data_ptr(), off_sh, xf_sh, sptr)
+        L.stpc_encoder_wait(enc.handle, sptr)
+        s1.record(stream)
+        torch.cuda.synchronize()
+        sms = s0.elapsed_time(s1) / max(args.steps, 1)
+        _, len_sh = enc.blob_layout()
+        if dist:
+            sms = pdist.max_over_ranks(sms, device)
+            sizes = pdist.gather_ragged(torch.as_tensor(len_sh, device=device), G, world).cpu().numpy()
+            spts = pdist.sum_over_ranks(int(off_sh[-1]), device)
+        else:
+            sizes, spts = len_sh, int(off_sh[-1])
+        strong = {"value": G * n / (sms / 1e3), "unit": "frames/s", "ms_per_step": sms, "groups_total": G,
+                  "groups_per_rank": [list(pdist.shard_range(G, r, world)) for r in range(world)],
+                  "mpoints_per_s": spts / (sms / 1e3) / 1e6, "scaling": "strong",
+                  "blob_bytes_total": int(np.sum(sizes)),
+                  # rank 0's own batch above is the same 1024 groups: every
+                  # gathered per-group size must equal its single-rank size
+                  "sizes_match_single_rank": bool(rank == 0 and np.array_equal(sizes, len_b)) if rank == 0 else None}
+        del d_sh
+        torch.cuda.empty_cache()
 
     # ---------------- end to end through the public host API
     e2e = None
@@ -744,6 +801,17 @@ def main():
             "parity": parity,
             "impl": "b200",
         }
+        if numa:
+            line["numa"] = numa
+        if strong:
+            line["strong"] = strong
+            if args.shard:  # the fixed batch split across ranks is the headline
+                line["weak"] = {"value": fps, "ms_per_step": ms_step, "scaling": "weak",
+                                "workload": config["workload"]}
+                line["value"], line["ms_per_step"], line["scaling"] = strong["value"], strong["ms_per_step"], "strong"
+                line["mpoints_per_s"] = strong["mpoints_per_s"]
+                line["config"] = dict(config, workload=f"{wl}: {G} groups x (1K+{n - 1}P) in total, split across "
+                                                       f"{world} GPU(s) by contiguous group shards")
         print(json.dumps(line))
     if dist:
         dist.destroy_process_group()

@@ -2,7 +2,7 @@
 
 On the GPU box (after the same bench command has exited 0 without ncu):
 
-    ncu --clock-control none --kernel-name-base mangled -k regex:_ZN4stpc \\
+    ncu --clock-control none --kernel-name-base demangled -k regex:stpc:: \\
         --metrics <METRICS below, comma-joined> --csv --log-file gpurun_out/stages.csv \\
         python bench.py --steps 1 --warmup 0 --no-e2e --no-cpu --no-decode --no-parity
 
@@ -95,6 +95,8 @@ def main():
     seen, stages = {}, {}
     for L in launches:
         base = re.sub(r"^_ZN4stpc\d+", "", L["kernel"])
+        base = re.sub(r"^void\s+", "", base)
+        base = re.sub(r"^stpc::", "", base)
         base = re.match(r"[A-Za-z_0-9]+", base).group(0)
         st = kernel_stage(base, seen)
         S = stages.setdefault(st, {"kernels": {}, "dram_bytes": 0.0, "warp_instructions": 0.0, "ms": 0.0})
