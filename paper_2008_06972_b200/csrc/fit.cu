@@ -809,7 +809,26 @@ __device__ __forceinline__ bool test_px_pair(bool active, bool has, double r, do
     return pass;
 }
 
+// Tile shape of the pair kernel: F44 = every tile is a full 4x4 (tile 4x4,
+// w and h multiples of 4, e.g. every BASELINE 4x4 config): lane gl's pixel is
+// (gl >> 2, gl & 3) with no runtime divide; otherwise the general shape.
+template <bool F44>
+__device__ __forceinline__ bool tile_px(const Chain& ch, const Geometry& g, int u0, int gl, int& dv, int& du)
+{
+    if constexpr (F44) {
+        dv = gl >> 2;
+        du = gl & 3;
+        return true;
+    } else {
+        const int cols = min(g.tw, g.w - u0);
+        if (gl >= ch.rows * cols) return false;
+        divmod_small(gl, cols, __frcp_rn((float)cols), dv, du);
+        return true;
+    }
+}
+
 // test_px_pair with the lane's pixel of `tile` loaded from global memory.
+template <bool F44>
 __device__ bool test_tile_pair(bool active, const Chain& ch, const Geometry& g, const Trig& tg, int tile,
                                double a, double b, double c, double tau, double r_max)
 {
@@ -818,10 +837,8 @@ __device__ bool test_tile_pair(bool active, const Chain& ch, const Geometry& g, 
     double r = 0.0, dx = 0.0, dy = 0.0, dz = 0.0;
     if (active) {
         const int u0 = tile * g.tw;
-        const int cols = min(g.tw, g.w - u0);
-        if (gl < ch.rows * cols) {
-            int dv, du;
-            divmod_small(gl, cols, __frcp_rn((float)cols), dv, du);
+        int dv, du;
+        if (tile_px<F44>(ch, g, u0, gl, dv, du)) {
             const int v = ch.v0 + dv, u = u0 + du;
             r = ch.img[(long long)v * g.w + u];
             if (isfinite(r)) {
@@ -853,6 +870,10 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 #ifndef STPC_PAIR_MINB
 #define STPC_PAIR_MINB 8  // measured (fit_p): 5 -> 28.5 ms, 6 -> 29.1, 7 -> 26.5, 8 -> 26.3, 10 -> 29.8; re-measured after the slimmer step: 6 -> 22.7, 7 -> 22.1, 8 -> 21.9, 9 -> 22.1
 #endif
+#ifndef STPC_PAIR44_MINB
+#define STPC_PAIR44_MINB 7  // the full-4x4 instantiation (fit_p): 8 -> 19.6-19.9 ms (110 B spilled), 7 -> 19.4 (34 B)
+#endif
+template <bool F44> constexpr int pair_minb() { return F44 ? STPC_PAIR44_MINB : STPC_PAIR_MINB; }
 #ifdef STPC_FIT_STATS
 // diagnostic build only (tools/fit_stats.py): chain-step counters
 __device__ unsigned long long g_fit_stats[8];
@@ -873,7 +894,8 @@ extern "C" int stpc_debug_fit_stats_reset()
 #else
 #define FIT_STAT(i, pred) ((void)0)
 #endif
-__global__ void __launch_bounds__(FIT_WARPS * 32, STPC_PAIR_MINB) fit_pair_kernel(FitArgs A)
+template <bool F44>
+__global__ void __launch_bounds__(FIT_WARPS * 32, pair_minb<F44>()) fit_pair_kernel(FitArgs A)
 {
     __shared__ double smem[FIT_WARPS][2][PG * 9];
     const Geometry& g = A.g;
@@ -901,9 +923,18 @@ __global__ void __launch_bounds__(FIT_WARPS * 32, STPC_PAIR_MINB) fit_pair_kerne
     int pf_t = -1;
     __shared__ double pf_slot[FIT_WARPS * 32];  // the lane's prefetched pixel (cp.async: no register)
     double& pf_s = pf_slot[threadIdx.x];
+#ifdef STPC_PAIR_PTRS
+    uint8_t* crowp = nullptr;
+    const uint8_t* sokp = nullptr;
+    float4* certp = nullptr;
+#define CROW crowp
+#define SOK sokp
+#define CERT certp
+#else
 #define CROW (A.cls + slot * g.tx)
 #define SOK (A.start_ok + slot * g.tx)
 #define CERT (A.cert + slot * g.tx * CERT_F4)
+#endif
     auto take_chain = [&](long long cid) {
         if (cid >= n_chains) {
             finished = true;
@@ -921,6 +952,11 @@ __global__ void __launch_bounds__(FIT_WARPS * 32, STPC_PAIR_MINB) fit_pair_kerne
             frame = grp * A.n_frames_group + (i < A.k ? i : i + 1);
         }
         slot = (long long)frame * g.ty + tr;
+#ifdef STPC_PAIR_PTRS
+        crowp = A.cls + slot * g.tx;
+        sokp = A.start_ok + slot * g.tx;
+        certp = A.cert + slot * g.tx * CERT_F4;
+#endif
         ch.img = A.best + (long long)frame * g.P;
         ch.v0 = tr * g.th;
         ch.rows = min(g.th, g.h - ch.v0);
@@ -1006,13 +1042,10 @@ __global__ void __launch_bounds__(FIT_WARPS * 32, STPC_PAIR_MINB) fit_pair_kerne
         if (live && !grow) acc = 0.0;
         const bool masked = !live || (ch.skip1 && CROW[t] == 1);
         const int u0 = live ? t * g.tw : 0;
-        const int cols = live ? min(g.tw, g.w - u0) : 1;
-        const int npx = masked ? 0 : ch.rows * cols;
         double x = 0.0, y = 0.0, z = 0.0, one = 0.0;
         double fr = 0.0, fdx = 0.0, fdy = 0.0, fdz = 0.0;  // the lane's pixel, kept for the tile test
-        if (gl < npx) {
-            int dv, du;
-            divmod_small(gl, cols, __frcp_rn((float)cols), dv, du);
+        int dv, du;
+        if (!masked && tile_px<F44>(ch, g, u0, gl, dv, du)) {
             const int v = ch.v0 + dv, u = u0 + du;
             double r;
             if (pf_t == t) {
@@ -1059,11 +1092,8 @@ __global__ void __launch_bounds__(FIT_WARPS * 32, STPC_PAIR_MINB) fit_pair_kerne
         // prefetch the next tile's pixel gl
         if (live && t + 1 < g.tx) {
             const int nu0 = (t + 1) * g.tw;
-            const int ncols = min(g.tw, g.w - nu0);
             cp_async_wait_all();  // an unconsumed earlier copy into the slot has landed
-            if (gl < ch.rows * ncols) {
-                int dv, du;
-                divmod_small(gl, ncols, __frcp_rn((float)ncols), dv, du);
+            if (tile_px<F44>(ch, g, nu0, gl, dv, du)) {
                 cp_async8(&pf_s, ch.img + (long long)(ch.v0 + dv) * g.w + nu0 + du);
             } else {
                 pf_s = __longlong_as_double(0x7ff0000000000000ll);
@@ -1113,7 +1143,7 @@ __global__ void __launch_bounds__(FIT_WARPS * 32, STPC_PAIR_MINB) fit_pair_kerne
                     const bool act = pass && wm != 0;
                     const int jj = act ? base + __ffs(wm) - 1 : 0;
                     if (act) wm &= wm - 1;
-                    const bool r = test_tile_pair(act, ch, g, A.tg, jj, na, nb, nc, A.tau, A.r_max);
+                    const bool r = test_tile_pair<F44>(act, ch, g, A.tg, jj, na, nb, nc, A.tau, A.r_max);
                     FIT_STAT(7, act && !r && gl == 0);  // re-tests that fail the union
                     if (act && !r) pass = false;
                 }
@@ -1191,6 +1221,8 @@ void launch_start_tiles(const FitArgs& a, cudaStream_t s)
     }
 }
 
+static bool pair_full44(const Geometry& g) { return g.tw == 4 && g.th == 4 && g.w % 4 == 0 && g.h % 4 == 0; }
+
 void launch_fit_chains(const FitArgs& a, cudaStream_t s)
 {
     long long warps = (long long)a.n_jobs * a.g.ty;
@@ -1199,9 +1231,14 @@ void launch_fit_chains(const FitArgs& a, cudaStream_t s)
     if (a.g.tw * a.g.th <= PG) {
         // work-stealing grid: STPC_PAIR_MINB resident blocks per SM, capped by the chain count
         long long pairs = (warps + 1) / 2;
-        long long blocks = std::min<long long>((pairs + FIT_WARPS - 1) / FIT_WARPS, 148LL * STPC_PAIR_MINB);
+        const bool f44 = pair_full44(a.g);
+        long long blocks = std::min<long long>((pairs + FIT_WARPS - 1) / FIT_WARPS,
+                                               148LL * (f44 ? STPC_PAIR44_MINB : STPC_PAIR_MINB));
         launch_zero(a.chain_counter, sizeof(unsigned), s);
-        fit_pair_kernel<<<(unsigned)blocks, FIT_WARPS * 32, 0, s>>>(a);
+        if (f44)
+            fit_pair_kernel<true><<<(unsigned)blocks, FIT_WARPS * 32, 0, s>>>(a);
+        else
+            fit_pair_kernel<false><<<(unsigned)blocks, FIT_WARPS * 32, 0, s>>>(a);
     } else {
         fit_rows_kernel<<<(unsigned)((warps + FIT_WARPS - 1) / FIT_WARPS), FIT_WARPS * 32, 0, s>>>(a);
     }
@@ -1217,7 +1254,7 @@ void launch_fit_chains(const FitArgs& a, cudaStream_t s)
 bool fit_overlap_pays(const Geometry& g, long long key_chains)
 {
     if (g.tw * g.th > PG) return true;
-    return key_chains > 148LL * STPC_PAIR_MINB * FIT_WARPS * 2;
+    return key_chains > 148LL * (pair_full44(g) ? STPC_PAIR44_MINB : STPC_PAIR_MINB) * FIT_WARPS * 2;
 }
 
 void launch_fit_rows(const FitArgs& a, cudaStream_t s)
