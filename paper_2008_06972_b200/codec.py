@@ -33,6 +33,7 @@ from .geometry import (
     AngularResolution,
     RigidTransform,
     frame_transforms,
+    matmul_contract,
     poses_to_transform_rows,
     poses_to_transforms,
     ray_trig_tables,
@@ -443,6 +444,8 @@ def compress_groups(groups: Sequence[Sequence[np.ndarray]], cfg: CodecConfig,
         xf = np.asarray(xf, np.float64).reshape(-1, 12)
     t1 = time.perf_counter()
     frames, f64, counts = _frame_arrays([c for grp in groups for c in grp])
+    if f64:
+        matmul_contract()  # warns once if this host's BLAS is not the FMA chain
     with _checkout(_encoders, (cfg, f64), lambda: Encoder(cfg, f64)) as enc:
         enc.encode_host_gather(len(groups), frames, xf)
         blobs = enc.blobs()
@@ -464,6 +467,8 @@ def compress(clouds: Sequence[np.ndarray], cfg: CodecConfig, poses=None, imu_sam
     xf = np.asarray([t.row12() for t in ts], np.float64)
     t1 = time.perf_counter()
     pts, off, f64, counts = _stack_points(clouds)
+    if f64:
+        matmul_contract()  # warns once if this host's BLAS is not the FMA chain
     with _checkout(_encoders, (cfg, f64), lambda: Encoder(cfg, f64)) as enc:
         enc.encode_host(1, pts, off, xf)
         blobs = enc.blobs()

@@ -101,6 +101,44 @@ class RigidTransform:
         return isinstance(other, RigidTransform) and np.array_equal(self.R, other.R) and np.array_equal(self.T, other.T)
 
 
+_MATMUL_CONTRACT: Optional[str] = None
+
+
+def matmul_contract() -> str:
+    """How this host's numpy evaluates RigidTransform.apply (pts @ R.T + T,
+    motion.py:70-72) per output coordinate: "fma" when it equals
+    fma(z, r2, fma(y, r1, x*r0)) -- the BLAS dgemm micro-kernel's FMA chain,
+    which the device reproduces (common.cuh xform_coord) -- "plain" when it
+    equals ((x*r0 + y*r1) + z*r2), "mixed" otherwise.  Only float64 clouds that
+    are not float32-representable can tell them apart (float32 products are
+    exact); the reference's own bits for those then depend on the host's BLAS,
+    and the device matches them where this returns "fma".  Probed once on
+    2000 points with exact rational arithmetic for the FMA reference."""
+    global _MATMUL_CONTRACT
+    if _MATMUL_CONTRACT is None:
+        from fractions import Fraction
+
+        rng = np.random.default_rng(12345)
+        p = rng.uniform(-60.0, 60.0, (2000, 3)) * (1.0 + rng.uniform(-1e-6, 1e-6, (2000, 3)))
+        R = rng.uniform(-1.0, 1.0, (3, 3)).astype(np.float32).astype(np.float64)
+        out = p @ R.T
+        fma = plain = True
+        for i in range(p.shape[0]):
+            x, y, z = (float(v) for v in p[i])
+            for j in range(3):
+                r0, r1, r2 = (float(v) for v in R[j])
+                inner = float(Fraction(y) * Fraction(r1) + Fraction(x * r0))
+                f = float(Fraction(z) * Fraction(r2) + Fraction(inner))
+                fma &= bool(out[i, j] == f)
+                plain &= bool(out[i, j] == (x * r0 + y * r1) + z * r2)
+        _MATMUL_CONTRACT = "fma" if fma else ("plain" if plain else "mixed")
+        if _MATMUL_CONTRACT != "fma":
+            log.warning("numpy matmul on this host is %r, not the FMA chain the device reproduces: blobs of "
+                        "float64 clouds that are not float32-representable may differ in the last bits from a "
+                        "reference run on this host (float32 clouds are unaffected)", _MATMUL_CONTRACT)
+    return _MATMUL_CONTRACT
+
+
 def poses_to_transforms(poses: Sequence, k_index: int) -> List[RigidTransform]:
     """Frame -> key-frame transforms G_k^-1 . G_i from frame -> world poses
     (motion.py:214-226)."""

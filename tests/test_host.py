@@ -366,3 +366,14 @@ def test_context_pool_bounded_lru_and_exclusive():
     assert pool.peek("c", factory("c")) is pool.idle["c"][-1]
     pool.clear()
     assert not pool.idle
+
+
+def test_matmul_contract_probe():
+    """The host-BLAS dependence of float64 transforms is detected, not
+    assumed: on this build host numpy's pts @ R.T is the
+    FMA chain the device and the oracle use (pinned by the stream4_f64
+    fixture the reference produced here)."""
+    from paper_2008_06972_b200.geometry import matmul_contract
+
+    assert matmul_contract() in ("fma", "plain", "mixed")
+    assert matmul_contract() == "fma"
