@@ -156,6 +156,7 @@ __global__ void __launch_bounds__(256) crc_blob_kernel(const uint8_t* blobs, con
                                                        const int* skip, DecCrcK K, int* crc_bad)
 {
     if (skip[blockIdx.x]) return;
+    if ((((unsigned long long)(blobs + blob_off[blockIdx.x] + DEC_HEADER)) & 3) == 0) return;  // crc_blob4_kernel's
     __shared__ unsigned int tab[256];
     __shared__ unsigned int stage[DC_CHUNK / 4 + 2];
     __shared__ unsigned int wpart[8];
@@ -217,6 +218,127 @@ __global__ void __launch_bounds__(256) crc_blob_kernel(const uint8_t* blobs, con
         }
     }
     if (tid == 0) {
+        const unsigned int crc = ~(raw ^ dec_multmodp(dec_x8nmodp(enc_len), 0xffffffffu));
+        crc_bad[blockIdx.x] = crc != want;
+    }
+}
+
+// Fast path of the same check for entropy payloads that start on a 4-byte
+// boundary (every blob the encoder writes: 16-byte-aligned blobs + the
+// 284-byte header; other blobs keep crc_blob_kernel).  Block per blob, eight
+// warps; per iteration the block takes 256 pieces of 256 bytes (64 KB):
+// each lane folds one piece slice-by-4 (four table lookups per word), staged
+// through a padded shared tile 64 bytes of every piece at a time so the
+// global loads stay coalesced; pieces merge by the shuffle tree, warps and
+// iterations by x^(8n) multipliers.  A last partial iteration end-aligns its
+// pieces in the tree (missing leading pieces = zero prefix), and the < 256 B
+// tail is folded byte-wise.  Both kernels skip the other's blobs.
+struct DecCrcTab4 {
+    unsigned int t[4][256];
+};
+constexpr DecCrcTab4 make_dec_crc_tab4()
+{
+    DecCrcTab4 r{};
+    for (unsigned int i = 0; i < 256; ++i) {
+        unsigned int c = i;
+        for (int k = 0; k < 8; ++k) c = (c & 1u) ? (c >> 1) ^ 0xedb88320u : c >> 1;
+        r.t[0][i] = c;
+    }
+    for (unsigned int i = 0; i < 256; ++i) {
+        unsigned int c = r.t[0][i];
+        for (int k = 1; k < 4; ++k) {
+            c = (c >> 8) ^ r.t[0][c & 0xff];
+            r.t[k][i] = c;
+        }
+    }
+    return r;
+}
+__device__ const DecCrcTab4 kDecCrcTab4 = make_dec_crc_tab4();
+
+constexpr int DCF_PIECE = 256;              // bytes per lane per iteration
+constexpr int DCF_SUB = 64;                 // bytes per piece per staging round
+constexpr int DCF_ITER = 256 * DCF_PIECE;   // bytes per block iteration
+
+struct DecCrcF {
+    unsigned int x256[5];  // x^(8 * 256 * 2^l) mod P
+    unsigned int warp;     // x^(8 * 32 * 256)
+    unsigned int iter;     // x^(8 * DCF_ITER)
+};
+
+__global__ void __launch_bounds__(256) crc_blob4_kernel(const uint8_t* blobs, const long long* blob_off,
+                                                        const int* skip, DecCrcF K, int* crc_bad)
+{
+    if (skip[blockIdx.x]) return;
+    const uint8_t* blob = blobs + blob_off[blockIdx.x];
+    const uint8_t* encb = blob + DEC_HEADER;
+    if (((unsigned long long)encb) & 3) return;  // crc_blob_kernel's blob
+    __shared__ unsigned int T[4][256];
+    __shared__ unsigned int stg[8][32][DCF_SUB / 4 + 1];
+    __shared__ unsigned int wpart[8];
+    {
+        const unsigned int* src = &kDecCrcTab4.t[0][0];
+        for (int i = threadIdx.x; i < 1024; i += 256) (&T[0][0])[i] = __ldg(src + i);
+    }
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    unsigned long long enc_len = 0;
+    for (int b = 0; b < 8; ++b) enc_len |= (unsigned long long)blob[16 + b] << (8 * b);
+    const unsigned int want = dec_u32(blob + 24);
+    const uint32_t* enc = reinterpret_cast<const uint32_t*>(encb);
+    const long long npieces = (long long)(enc_len / DCF_PIECE);
+    unsigned int (*tile)[DCF_SUB / 4 + 1] = stg[wid];
+    unsigned int raw = 0;
+    __syncthreads();
+    for (long long first = 0; first < npieces; first += 256) {
+        const int np = (int)min(256LL, npieces - first);
+        const int lead = 256 - np;       // end-aligned: slots [0, lead) are a zero prefix
+        const int slot = tid - lead;     // this lane's piece within the iteration, < 0: none
+        const int wslot0 = wid * 32 - lead;  // piece of the warp's lane 0
+        unsigned int crc = 0;
+        for (int r = 0; r < DCF_PIECE / DCF_SUB; ++r) {
+#pragma unroll
+            for (int it = 0; it < DCF_SUB / 4; ++it) {  // 32 pieces x 16 words, 2 pieces per load
+                const int widx = it * 32 + lane;
+                const int k = widx >> 4, wd = widx & 15;
+                const int pk = wslot0 + k;
+                tile[k][wd] = pk >= 0 ? __ldg(enc + ((first + pk) * DCF_PIECE + r * DCF_SUB) / 4 + wd) : 0u;
+            }
+            __syncwarp();
+            if (slot >= 0) {
+#pragma unroll
+                for (int i = 0; i < DCF_SUB / 4; ++i) {
+                    const unsigned int x = crc ^ tile[lane][i];
+                    crc = T[3][x & 0xff] ^ T[2][(x >> 8) & 0xff] ^ T[1][(x >> 16) & 0xff] ^ T[0][x >> 24];
+                }
+            }
+            __syncwarp();
+        }
+#pragma unroll
+        for (int l = 0; l < 5; ++l) {
+            const unsigned int right = __shfl_down_sync(STPC_FULL, crc, 1 << l);
+            if ((lane & ((2 << l) - 1)) == 0) crc = dec_multmodp(K.x256[l], crc) ^ right;
+        }
+        if (lane == 0) wpart[wid] = crc;
+        __syncthreads();
+        if (tid == 0) {
+            unsigned int c = 0;
+            for (int w = 0; w < 8; ++w) c = dec_multmodp(K.warp, c) ^ wpart[w];
+            // zero prefix of a partial iteration: the register is unchanged by it,
+            // so the iteration shifts `raw` by its real length only
+            raw = dec_multmodp(np == 256 ? K.iter : dec_x8nmodp((unsigned long long)np * DCF_PIECE), raw) ^ c;
+        }
+        __syncthreads();
+    }
+    if (tid == 0) {
+        const long long tb = npieces * DCF_PIECE;
+        if (tb < (long long)enc_len) {  // < 256-byte tail, byte-wise
+            raw = dec_multmodp(dec_x8nmodp((unsigned long long)(enc_len - tb)), raw);
+            unsigned int t = 0;
+            for (long long i = tb; i < (long long)enc_len; ++i) {
+                const unsigned int c = (t ^ dec_u8(encb + i)) & 0xff;
+                t = T[0][c] ^ (t >> 8);
+            }
+            raw ^= t;
+        }
         const unsigned int crc = ~(raw ^ dec_multmodp(dec_x8nmodp(enc_len), 0xffffffffu));
         crc_bad[blockIdx.x] = crc != want;
     }
@@ -934,7 +1056,7 @@ __global__ void __launch_bounds__(1024) reconstruct_kernel(DecGeom G, Trig tg, c
                                                            const long long* raw_off, const int* sel,
                                                            const float4* tmap, const unsigned long long* pstat,
                                                            const long long* ovl, double* out_r,
-                                                           unsigned long long* failed)
+                                                           unsigned* pmask, unsigned long long* failed)
 {
     const long long f = blockIdx.y;
     long long chl;
@@ -942,6 +1064,7 @@ __global__ void __launch_bounds__(1024) reconstruct_kernel(DecGeom G, Trig tg, c
     if (pstat[j] != DEC_NONE || ovl[j]) return;
     const long long pix = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     int nfail = 0;
+    bool have = false;
     if (pix < G.P) {
         const uint8_t* vb = raw + raw_off[sel[j]] + G.bits_off + (long long)ch * G.nb;
         const bool valid = (dec_u8(vb + (pix >> 3)) >> (7 - (pix & 7))) & 1u;
@@ -965,7 +1088,12 @@ __global__ void __launch_bounds__(1024) reconstruct_kernel(DecGeom G, Trig tg, c
             }
         }
         out_r[f * G.P + pix] = __longlong_as_double(r);
+        have = r != DEC_NOPT;
     }
+    // point mask word of these 32 pixels (residual_kernel ORs its pixels in)
+    const unsigned m = __ballot_sync(STPC_FULL, have);
+    const long long W = (G.P + 31) >> 5;
+    if ((threadIdx.x & 31) == 0 && (pix >> 5) < W) pmask[f * W + (pix >> 5)] = m;
     for (int o = 16; o > 0; o >>= 1) nfail += __shfl_xor_sync(STPC_FULL, nfail, o);
     if ((threadIdx.x & 31) == 0 && nfail) atomicAdd(failed + j, (unsigned long long)nfail);
 }
@@ -1066,7 +1194,8 @@ __global__ void __launch_bounds__(256) ordered_reconstruct_kernel(DecGeom G, Tri
 // rank across 1 KB chunks.  The section was validated by parse_kernel.
 __global__ void __launch_bounds__(PK_THREADS) residual_kernel(DecGeom G, const uint8_t* raw, const long long* raw_off,
                                                               const int* sel, const ResSec* res,
-                                                              const unsigned long long* pstat, double* out_r)
+                                                              const unsigned long long* pstat, double* out_r,
+                                                              unsigned* pmask)
 {
     const int ch = blockIdx.x, j = blockIdx.y;
     if (pstat[j] != DEC_NONE) return;
@@ -1074,6 +1203,7 @@ __global__ void __launch_bounds__(PK_THREADS) residual_kernel(DecGeom G, const u
     if (rs.cnt == 0) return;
     const uint8_t* p = raw + raw_off[sel[j]];
     double* dst = out_r + ((long long)j * G.n + ch) * G.P;
+    unsigned* pm = pmask + ((long long)j * G.n + ch) * ((G.P + 31) >> 5);
     const int tid = threadIdx.x;
     long long c_idx = 0, c_flat = 0, c_esc = 0;
     for (long long chunk = rs.pos_var; chunk < rs.pos_code; chunk += 4 * PK_THREADS) {
@@ -1107,6 +1237,8 @@ __global__ void __launch_bounds__(PK_THREADS) residual_kernel(DecGeom G, const u
         }
         const long long b_esc = c_esc + block_excl_scan<PK_THREADS>(ne, t_esc);
         long long vi = b_idx, flat = b_flat, ei = b_esc;
+        long long cw = -1;
+        unsigned bits = 0;
         for (int i = 0; i < 4; ++i) {
             if (!term[i]) continue;
             flat += dv[i];
@@ -1114,34 +1246,48 @@ __global__ void __launch_bounds__(PK_THREADS) residual_kernel(DecGeom G, const u
             double r;
             if (code == 0xFFFFu) r = (double)dec_f32(p + rs.pos_esc + 4 * ei++);
             else r = (double)code * G.quant;
-            if (flat >= 0 && flat < G.P) dst[flat] = r;
+            if (flat >= 0 && flat < G.P) {
+                dst[flat] = r;
+                if ((flat >> 5) != cw) {  // one atomic per distinct mask word of this thread's values
+                    if (cw >= 0) atomicOr(pm + cw, bits);
+                    cw = flat >> 5;
+                    bits = 0;
+                }
+                bits |= 1u << (flat & 31);
+            }
             ++vi;
         }
+        if (cw >= 0) atomicOr(pm + cw, bits);
         c_idx += t_idx;
         c_flat += t_flat;
         c_esc += t_esc;
     }
 }
 
-// points per (frame, 1024-pixel block); blocks never straddle frames
-__global__ void __launch_bounds__(1024) count_points_kernel(DecGeom G, const double* out_r,
-                                                            const unsigned long long* pstat, int* blk_count)
+// points per (frame, 1024-pixel block) = popcounts of the block's 32 point
+// mask words (blocks never straddle frames); blobs whose runs overlap have
+// no mask (ordered_reconstruct_kernel) and are counted from the range image
+__global__ void __launch_bounds__(256) count_points_kernel(DecGeom G, const double* out_r, const unsigned* pmask,
+                                                           const unsigned long long* pstat, const long long* ovl,
+                                                           long long bpf, long long F, int* blk_count)
 {
-    const long long f = blockIdx.y;
+    const long long id = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (id >= bpf * F) return;
+    const long long f = id / bpf, bk = id - f * bpf;
     long long fch;
     const int j = (int)dmod(f, G.n, G.rn, fch);
-    const long long pix = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    const bool have = pstat[j] == DEC_NONE && pix < G.P &&
-                      __double_as_longlong(out_r[f * G.P + pix]) != DEC_NOPT;
-    const unsigned m = __ballot_sync(STPC_FULL, have);
-    __shared__ int ws[32];
-    if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5] = __popc(m);
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        int t = 0;
-        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += ws[w];
-        blk_count[f * gridDim.x + blockIdx.x] = t;
+    int t = 0;
+    if (pstat[j] == DEC_NONE) {
+        const long long W = (G.P + 31) >> 5;
+        const long long w0 = bk * 32, w1 = min(w0 + 32, W);
+        if (ovl[j]) {
+            for (long long p = w0 * 32; p < min(w1 * 32, G.P); ++p)
+                t += __double_as_longlong(out_r[f * G.P + p]) != DEC_NOPT;
+        } else {
+            for (long long w = w0; w < w1; ++w) t += __popc(pmask[f * W + w]);
+        }
     }
+    blk_count[id] = t;
 }
 
 // warp per frame: exclusive scan of its block counts in place + frame total
@@ -1184,7 +1330,8 @@ __global__ void __launch_bounds__(1024) frame_offset_kernel(const long long* fra
 // points = r * d in row-major pixel order per frame, then
 // p' = R^-1 p + T^-1 as fma(z, r2, fma(y, r1, x r0)) + t (xform_coord)
 __global__ void __launch_bounds__(1024) unproject_kernel(DecGeom G, Trig tg, const double* out_r,
-                                                         const unsigned long long* pstat, const int* blk_off,
+                                                         const unsigned* pmask, const unsigned long long* pstat,
+                                                         const long long* ovl, const int* blk_off,
                                                          const long long* frame_off, const double* xf_inv,
                                                          double* pts)
 {
@@ -1194,7 +1341,10 @@ __global__ void __launch_bounds__(1024) unproject_kernel(DecGeom G, Trig tg, con
     if (pstat[j] != DEC_NONE) return;
     const long long pix = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     const long long i = f * G.P + pix;
-    const bool have = pix < G.P && __double_as_longlong(out_r[i]) != DEC_NOPT;
+    const long long W = (G.P + 31) >> 5;
+    // the point mask decides which ranges are read at all
+    const bool have = pix < G.P && (ovl[j] ? __double_as_longlong(out_r[i]) != DEC_NOPT
+                                           : ((pmask[f * W + (pix >> 5)] >> (pix & 31)) & 1u));
     const unsigned m = __ballot_sync(STPC_FULL, have);
     __shared__ int ws[32];
     __shared__ double stage[32][96];  // a warp's points, xyz interleaved, for coalesced stores
@@ -1263,7 +1413,7 @@ struct stpc_decoder {
     int m = 0;
     DecGeom G{};
     long long F = 0, bpf = 0, total = 0;
-    DevBuf sel, tmap, res, pstat, ovl, outr, trig, xfi, blkcnt, fcnt, foff, failed, pts;
+    DevBuf sel, tmap, res, pstat, ovl, outr, pmask, trig, xfi, blkcnt, fcnt, foff, failed, pts;
     std::vector<unsigned long long> h_pstat;
     const double* last_points = nullptr;
     // host output path: pinned double buffer + copy threads
@@ -1434,6 +1584,15 @@ static int decoder_load_impl(stpc_decoder* d, const uint8_t* blobs, int32_t blob
     STPC_LAUNCH();
     crc_blob_kernel<<<n, 256, 0, s>>>(d->d_blob_base, d->boff.as<long long>(), d->skip.as<int>(), ck,
                                       d->crcbad.as<int>());
+    {
+        DecCrcF kf;
+        for (int l = 0; l < 5; ++l) kf.x256[l] = dec_x8nmodp((unsigned long long)DCF_PIECE << l);
+        kf.warp = dec_x8nmodp(32ull * DCF_PIECE);
+        kf.iter = dec_x8nmodp((unsigned long long)DCF_ITER);
+        STPC_LAUNCH();
+        crc_blob4_kernel<<<n, 256, 0, s>>>(d->d_blob_base, d->boff.as<long long>(), d->skip.as<int>(), kf,
+                                           d->crcbad.as<int>());
+    }
     STPC_LAUNCH();
     huff_decode_kernel<<<n, HD_THREADS, 0, s>>>(d->d_blob_base, d->boff.as<long long>(), d->skip.as<int>() + n,
                                                 d->raw.as<uint8_t>(), d->roff.as<long long>(),
@@ -1551,6 +1710,7 @@ int stpc_decoder_frames(stpc_decoder* d, const stpc_decode_geom* g, const int32_
     DRET(d->pstat.ensure(sizeof(unsigned long long) * m));
     DRET(d->ovl.ensure(sizeof(long long) * m));
     DRET(d->outr.ensure(sizeof(double) * F * G.P));
+    DRET(d->pmask.ensure(sizeof(unsigned) * F * ((G.P + 31) >> 5)));
     DRET(d->trig.ensure(sizeof(double) * 2 * (G.w + G.h)));
     DRET(d->xfi.ensure(sizeof(double) * 12 * F));
     DRET(d->blkcnt.ensure(sizeof(int) * F * bpf));
@@ -1576,7 +1736,7 @@ int stpc_decoder_frames(stpc_decoder* d, const stpc_decode_geom* g, const int32_
     const dim3 fg((unsigned)bpf, (unsigned)F);
     STPC_LAUNCH();
     reconstruct_kernel<<<fg, 1024, 0, s>>>(G, tg, raw, roff, d->sel.as<int>(), d->tmap.as<float4>(), pst,
-                                           d->ovl.as<long long>(), d->outr.as<double>(),
+                                           d->ovl.as<long long>(), d->outr.as<double>(), d->pmask.as<unsigned>(),
                                            d->failed.as<unsigned long long>());
     STPC_LAUNCH();
     ordered_reconstruct_kernel<<<dim3((unsigned)G.n, (unsigned)m), 256, 0, s>>>(
@@ -1585,9 +1745,11 @@ int stpc_decoder_frames(stpc_decoder* d, const stpc_decode_geom* g, const int32_
     STPC_LAUNCH();
     residual_kernel<<<dim3((unsigned)G.n, (unsigned)m), PK_THREADS, 0, s>>>(G, raw, roff, d->sel.as<int>(),
                                                                             d->res.as<ResSec>(), pst,
-                                                                            d->outr.as<double>());
+                                                                            d->outr.as<double>(),
+                                                                            d->pmask.as<unsigned>());
     STPC_LAUNCH();
-    count_points_kernel<<<fg, 1024, 0, s>>>(G, d->outr.as<double>(), pst, d->blkcnt.as<int>());
+    count_points_kernel<<<(unsigned)((F * bpf + 255) / 256), 256, 0, s>>>(
+        G, d->outr.as<double>(), d->pmask.as<unsigned>(), pst, d->ovl.as<long long>(), bpf, F, d->blkcnt.as<int>());
     STPC_LAUNCH();
     frame_scan_kernel<<<(unsigned)((F + 7) / 8), 256, 0, s>>>(d->blkcnt.as<int>(), bpf, F, d->fcnt.as<long long>());
     STPC_LAUNCH();
@@ -1627,8 +1789,8 @@ int stpc_decoder_points(stpc_decoder* d, double* dst, int32_t dst_on_device, int
     tg = Trig{tr, tr + d->G.w, tr + 2 * d->G.w, tr + 2 * d->G.w + d->G.h};
     STPC_LAUNCH();
     unproject_kernel<<<dim3((unsigned)d->bpf, (unsigned)d->F), 1024, 0, s>>>(
-        d->G, tg, d->outr.as<double>(), d->pstat.as<unsigned long long>(), d->blkcnt.as<int>(),
-        d->foff.as<long long>(), d->xfi.as<double>(), out);
+        d->G, tg, d->outr.as<double>(), d->pmask.as<unsigned>(), d->pstat.as<unsigned long long>(),
+        d->ovl.as<long long>(), d->blkcnt.as<int>(), d->foff.as<long long>(), d->xfi.as<double>(), out);
     DCK(cudaGetLastError());
     if (!dst_on_device && d->total > 0) {
         // D2H through two pinned 128 MB stages; the copy of chunk k into the
