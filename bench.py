@@ -598,7 +598,8 @@ def main():
     raw = enc.payload_lengths()
     blob_bytes = int(len_b.sum())
     stats = enc.frame_stats()
-    psel = parity_groups(G) if not args.no_parity else []
+    # the oracle comparison runs on rank 0 (its ProcessPool takes every host core)
+    psel = parity_groups(G) if not args.no_parity and rank == 0 else []
     dev_blobs = None
     if psel:  # this step's device-path blobs of the checked groups (compared after timing)
         arena = np.empty(int(off_b[-1]), np.uint8)
