@@ -156,7 +156,7 @@ __global__ void __launch_bounds__(256) crc_blob_kernel(const uint8_t* blobs, con
                                                        const int* skip, DecCrcK K, int* crc_bad)
 {
     if (skip[blockIdx.x]) return;
-    if ((((unsigned long long)(blobs + blob_off[blockIdx.x] + DEC_HEADER)) & 3) == 0) return;  // crc_blob4_kernel's
+    if ((((unsigned long long)(blobs + blob_off[blockIdx.x] + DEC_HEADER)) & 3) == 0) return;  // crc_dseg_kernel's
     __shared__ unsigned int tab[256];
     __shared__ unsigned int stage[DC_CHUNK / 4 + 2];
     __shared__ unsigned int wpart[8];
@@ -225,14 +225,13 @@ __global__ void __launch_bounds__(256) crc_blob_kernel(const uint8_t* blobs, con
 
 // Fast path of the same check for entropy payloads that start on a 4-byte
 // boundary (every blob the encoder writes: 16-byte-aligned blobs + the
-// 284-byte header; other blobs keep crc_blob_kernel).  Block per blob, eight
-// warps; per iteration the block takes 256 pieces of 256 bytes (64 KB):
-// each lane folds one piece slice-by-4 (four table lookups per word), staged
-// through a padded shared tile 64 bytes of every piece at a time so the
-// global loads stay coalesced; pieces merge by the shuffle tree, warps and
-// iterations by x^(8n) multipliers.  A last partial iteration end-aligns its
-// pieces in the tree (missing leading pieces = zero prefix), and the < 256 B
-// tail is folded byte-wise.  Both kernels skip the other's blobs.
+// 284-byte header; other blobs keep crc_blob_kernel), spread over many warps
+// per blob (the encoder's CRC scheme, entropy.cu): each lane folds one
+// 256-byte piece slice-by-4 (four table lookups per word), staged through a
+// padded shared tile 64 bytes of every piece at a time so the global loads
+// stay coalesced; a warp's 32 pieces merge by a shuffle tree into a segment
+// CRC, and crc_dfinish combines the segments with x^(8n) multipliers.  Both
+// paths skip the other's blobs.
 struct DecCrcTab4 {
     unsigned int t[4][256];
 };
@@ -255,55 +254,62 @@ constexpr DecCrcTab4 make_dec_crc_tab4()
 }
 __device__ const DecCrcTab4 kDecCrcTab4 = make_dec_crc_tab4();
 
-constexpr int DCF_PIECE = 256;              // bytes per lane per iteration
-constexpr int DCF_SUB = 64;                 // bytes per piece per staging round
-constexpr int DCF_ITER = 256 * DCF_PIECE;   // bytes per block iteration
+constexpr int DCF_PIECE = 256;  // bytes per lane
+constexpr int DCF_SUB = 64;     // bytes per piece per staging round
 
 struct DecCrcF {
     unsigned int x256[5];  // x^(8 * 256 * 2^l) mod P
-    unsigned int warp;     // x^(8 * 32 * 256)
-    unsigned int iter;     // x^(8 * DCF_ITER)
+    unsigned int warp;     // x^(8 * 32 * 256): one segment
 };
 
-__global__ void __launch_bounds__(256) crc_blob4_kernel(const uint8_t* blobs, const long long* blob_off,
-                                                        const int* skip, DecCrcF K, int* crc_bad)
+constexpr int DCF_WARPS = 8;
+constexpr int DCF_SEGS_PER_WARP = 4;  // segments per warp (amortises the table copy)
+constexpr int DCF_SEG = 32 * DCF_PIECE;  // bytes per segment (a warp's 32 pieces)
+
+// grid (segments / (DCF_WARPS * DCF_SEGS_PER_WARP), blobs): warp-segments of
+// 32 pieces of 256 B from the payload's start; only full pieces here (the
+// < 256 B tail is crc_dfinish's).  The last segment's pieces are end-aligned
+// in the 32-slot tree (missing leading slots = zero prefix).
+__global__ void __launch_bounds__(DCF_WARPS * 32) crc_dseg_kernel(const uint8_t* blobs, const long long* blob_off,
+                                                                  const int* skip, DecCrcF K, int max_segs,
+                                                                  unsigned* seg_crc)
 {
-    if (skip[blockIdx.x]) return;
-    const uint8_t* blob = blobs + blob_off[blockIdx.x];
+    const int b = blockIdx.y;
+    if (skip[b]) return;
+    const uint8_t* blob = blobs + blob_off[b];
     const uint8_t* encb = blob + DEC_HEADER;
     if (((unsigned long long)encb) & 3) return;  // crc_blob_kernel's blob
     __shared__ unsigned int T[4][256];
-    __shared__ unsigned int stg[8][32][DCF_SUB / 4 + 1];
-    __shared__ unsigned int wpart[8];
+    __shared__ unsigned int stg[DCF_WARPS][32][DCF_SUB / 4 + 1];
     {
         const unsigned int* src = &kDecCrcTab4.t[0][0];
-        for (int i = threadIdx.x; i < 1024; i += 256) (&T[0][0])[i] = __ldg(src + i);
+        for (int i = threadIdx.x; i < 1024; i += blockDim.x) (&T[0][0])[i] = __ldg(src + i);
     }
-    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-    unsigned long long enc_len = 0;
-    for (int b = 0; b < 8; ++b) enc_len |= (unsigned long long)blob[16 + b] << (8 * b);
-    const unsigned int want = dec_u32(blob + 24);
-    const uint32_t* enc = reinterpret_cast<const uint32_t*>(encb);
-    const long long npieces = (long long)(enc_len / DCF_PIECE);
-    unsigned int (*tile)[DCF_SUB / 4 + 1] = stg[wid];
-    unsigned int raw = 0;
     __syncthreads();
-    for (long long first = 0; first < npieces; first += 256) {
-        const int np = (int)min(256LL, npieces - first);
-        const int lead = 256 - np;       // end-aligned: slots [0, lead) are a zero prefix
-        const int slot = tid - lead;     // this lane's piece within the iteration, < 0: none
-        const int wslot0 = wid * 32 - lead;  // piece of the warp's lane 0
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    unsigned long long enc_len = 0;
+    for (int i = 0; i < 8; ++i) enc_len |= (unsigned long long)blob[16 + i] << (8 * i);
+    const long long npieces = (long long)(enc_len / DCF_PIECE);
+    const long long nseg = (npieces + 31) / 32;
+    const uint32_t* enc = reinterpret_cast<const uint32_t*>(encb);
+    unsigned int (*tile)[DCF_SUB / 4 + 1] = stg[wib];
+    for (int rep = 0; rep < DCF_SEGS_PER_WARP; ++rep) {
+        const long long sgi = ((long long)blockIdx.x * DCF_SEGS_PER_WARP + rep) * DCF_WARPS + wib;
+        if (sgi >= nseg) return;
+        const long long first = sgi * 32;
+        const int np = (int)min(32LL, npieces - first);
+        const int slot_piece = lane - (32 - np);  // end-aligned
         unsigned int crc = 0;
         for (int r = 0; r < DCF_PIECE / DCF_SUB; ++r) {
 #pragma unroll
             for (int it = 0; it < DCF_SUB / 4; ++it) {  // 32 pieces x 16 words, 2 pieces per load
                 const int widx = it * 32 + lane;
                 const int k = widx >> 4, wd = widx & 15;
-                const int pk = wslot0 + k;
+                const int pk = k - (32 - np);
                 tile[k][wd] = pk >= 0 ? __ldg(enc + ((first + pk) * DCF_PIECE + r * DCF_SUB) / 4 + wd) : 0u;
             }
             __syncwarp();
-            if (slot >= 0) {
+            if (slot_piece >= 0) {
 #pragma unroll
                 for (int i = 0; i < DCF_SUB / 4; ++i) {
                     const unsigned int x = crc ^ tile[lane][i];
@@ -317,31 +323,44 @@ __global__ void __launch_bounds__(256) crc_blob4_kernel(const uint8_t* blobs, co
             const unsigned int right = __shfl_down_sync(STPC_FULL, crc, 1 << l);
             if ((lane & ((2 << l) - 1)) == 0) crc = dec_multmodp(K.x256[l], crc) ^ right;
         }
-        if (lane == 0) wpart[wid] = crc;
-        __syncthreads();
-        if (tid == 0) {
-            unsigned int c = 0;
-            for (int w = 0; w < 8; ++w) c = dec_multmodp(K.warp, c) ^ wpart[w];
-            // zero prefix of a partial iteration: the register is unchanged by it,
-            // so the iteration shifts `raw` by its real length only
-            raw = dec_multmodp(np == 256 ? K.iter : dec_x8nmodp((unsigned long long)np * DCF_PIECE), raw) ^ c;
-        }
-        __syncthreads();
+        if (lane == 0) seg_crc[(long long)b * max_segs + sgi] = crc;
     }
-    if (tid == 0) {
-        const long long tb = npieces * DCF_PIECE;
-        if (tb < (long long)enc_len) {  // < 256-byte tail, byte-wise
-            raw = dec_multmodp(dec_x8nmodp((unsigned long long)(enc_len - tb)), raw);
-            unsigned int t = 0;
-            for (long long i = tb; i < (long long)enc_len; ++i) {
-                const unsigned int c = (t ^ dec_u8(encb + i)) & 0xff;
-                t = T[0][c] ^ (t >> 8);
-            }
-            raw ^= t;
-        }
-        const unsigned int crc = ~(raw ^ dec_multmodp(dec_x8nmodp(enc_len), 0xffffffffu));
-        crc_bad[blockIdx.x] = crc != want;
+}
+
+// block per blob (one thread): the segment CRCs in order, then the < 256 B
+// tail byte-wise, then the comparison with the header's CRC
+__global__ void crc_dfinish_kernel(const uint8_t* blobs, const long long* blob_off, const int* skip, DecCrcF K,
+                                   int max_segs, const unsigned* seg_crc, int* crc_bad)
+{
+    const int b = blockIdx.x;
+    if (skip[b] || threadIdx.x != 0) return;
+    const uint8_t* blob = blobs + blob_off[b];
+    const uint8_t* encb = blob + DEC_HEADER;
+    if (((unsigned long long)encb) & 3) return;
+    unsigned long long enc_len = 0;
+    for (int i = 0; i < 8; ++i) enc_len |= (unsigned long long)blob[16 + i] << (8 * i);
+    const unsigned int want = dec_u32(blob + 24);
+    const long long npieces = (long long)(enc_len / DCF_PIECE);
+    const long long nseg = (npieces + 31) / 32;
+    unsigned int raw = 0;
+    for (long long sgi = 0; sgi < nseg; ++sgi) {
+        const long long np = min(32LL, npieces - sgi * 32);
+        const unsigned int X = np == 32 ? K.warp : dec_x8nmodp((unsigned long long)np * DCF_PIECE);
+        raw = dec_multmodp(X, raw) ^ seg_crc[(long long)b * max_segs + sgi];
     }
+    const long long tb = npieces * DCF_PIECE;
+    if (tb < (long long)enc_len) {
+        raw = dec_multmodp(dec_x8nmodp((unsigned long long)(enc_len - tb)), raw);
+        unsigned int t = 0;
+        for (long long i = tb; i < (long long)enc_len; ++i) {
+            unsigned int c = (t ^ dec_u8(encb + i)) & 0xff;
+            for (int k = 0; k < 8; ++k) c = c & 1 ? (c >> 1) ^ 0xedb88320u : c >> 1;
+            t = c ^ (t >> 8);
+        }
+        raw ^= t;
+    }
+    const unsigned int crc = ~(raw ^ dec_multmodp(dec_x8nmodp(enc_len), 0xffffffffu));
+    crc_bad[b] = crc != want;
 }
 
 // ---------------------------------------------------------------- Huffman
@@ -1408,7 +1427,7 @@ struct stpc_decoder {
     std::vector<long long> raw_len, raw_off;
     std::vector<int> ok;
     const uint8_t* d_blob_base = nullptr;
-    DevBuf blobs, boff, skip, raw, roff, rlen, crcbad, hstat, okdev, heads;
+    DevBuf blobs, boff, skip, raw, roff, rlen, crcbad, hstat, okdev, heads, segcrc;
     // phase 2
     int m = 0;
     DecGeom G{};
@@ -1541,11 +1560,13 @@ static int decoder_load_impl(stpc_decoder* d, const uint8_t* blobs, int32_t blob
     d->raw_off.assign(n + 1, 0);
     d->ok.assign(n, 0);
     std::vector<int> pre(n, 0), skip(n, 1), table(n, 0);
+    std::vector<long long> hdr_enc(n, 0);
     long long ro = 0;
     for (int i = 0; i < n; ++i) {
         long long rl = 0, el = 0;
         const uint8_t* h = hdr.data() + (size_t)i * DEC_HEADER;
         pre[i] = check_header(h, blen_of(i), rl, el);
+        hdr_enc[i] = el;
         d->raw_off[i] = ro;
         if (!pre[i]) {
             d->raw_len[i] = rl;
@@ -1588,10 +1609,19 @@ static int decoder_load_impl(stpc_decoder* d, const uint8_t* blobs, int32_t blob
         DecCrcF kf;
         for (int l = 0; l < 5; ++l) kf.x256[l] = dec_x8nmodp((unsigned long long)DCF_PIECE << l);
         kf.warp = dec_x8nmodp(32ull * DCF_PIECE);
-        kf.iter = dec_x8nmodp((unsigned long long)DCF_ITER);
+        long long max_enc = 0;
+        for (int i = 0; i < n; ++i)
+            if (!skip[i]) max_enc = std::max<long long>(max_enc, hdr_enc[i]);
+        const int max_segs = (int)std::max<long long>(1, (max_enc / DCF_PIECE + 31) / 32);
+        DRET(d->segcrc.ensure(sizeof(unsigned) * (size_t)n * max_segs));
+        const int per_block = DCF_WARPS * DCF_SEGS_PER_WARP;
         STPC_LAUNCH();
-        crc_blob4_kernel<<<n, 256, 0, s>>>(d->d_blob_base, d->boff.as<long long>(), d->skip.as<int>(), kf,
-                                           d->crcbad.as<int>());
+        crc_dseg_kernel<<<dim3((unsigned)((max_segs + per_block - 1) / per_block), (unsigned)n), DCF_WARPS * 32, 0,
+                          s>>>(d->d_blob_base, d->boff.as<long long>(), d->skip.as<int>(), kf, max_segs,
+                               d->segcrc.as<unsigned>());
+        STPC_LAUNCH();
+        crc_dfinish_kernel<<<n, 32, 0, s>>>(d->d_blob_base, d->boff.as<long long>(), d->skip.as<int>(), kf, max_segs,
+                                            d->segcrc.as<unsigned>(), d->crcbad.as<int>());
     }
     STPC_LAUNCH();
     huff_decode_kernel<<<n, HD_THREADS, 0, s>>>(d->d_blob_base, d->boff.as<long long>(), d->skip.as<int>() + n,

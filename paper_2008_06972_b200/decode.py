@@ -175,10 +175,10 @@ def _transforms_batch(heads: np.ndarray, raw_len: np.ndarray, idxs: List[int], n
         orth[f] = np.allclose(R[f].T @ R[f], eye, atol=ORTHONORMAL_ATOL)
     rows = np.concatenate([Rt.reshape(-1, 9), Tinv], axis=1).reshape(len(ok), n, 12)
     valid = (orth & detok).reshape(len(ok), n)
-    for j, i in enumerate(ok):
-        if valid[j].all():
-            good[i] = rows[j]
-            continue
+    allv = valid.all(axis=1)
+    good.update(zip((ok[j] for j in np.flatnonzero(allv)), rows[allv]))
+    for j in np.flatnonzero(~allv):
+        i = ok[j]
         f = int(np.flatnonzero(~valid[j])[0])
         why = "R is not orthonormal" if not orth.reshape(len(ok), n)[j, f] else "R must be a proper rotation (det +1)"
         errors[i] = MalformedBlobError(f"transform {f}: {why}")
@@ -231,28 +231,32 @@ class Decoder:
         heads = np.zeros((n, cap), np.uint8)
         _native.check(L.stpc_decoder_heads(self.h, cap, heads.ctypes.data, raw_len.ctypes.data, stream))
         cfgs: Dict[int, dict] = {}
-        parsed: Dict[bytes, object] = {}  # a batch's blobs mostly share one config block
-        for i in range(n):
-            if i in errors:
-                continue
-            if raw_len[i] < _CFG.size:
-                try:
-                    _config(heads[i].tobytes(), int(raw_len[i]))
-                except Exception as exc:  # noqa: BLE001 -- reported per blob
-                    errors[i] = exc
-                continue
-            key = heads[i, :_CFG.size].tobytes()
-            hit = parsed.get(key)
-            if hit is None:
-                try:
-                    hit = _config(key, int(raw_len[i]))
-                except Exception as exc:  # noqa: BLE001 -- reported per blob
-                    hit = exc
-                parsed[key] = hit
+        cfg_id = np.full(n, -1, np.int64)  # index of the blob's distinct config block
+        live = np.ones(n, bool)
+        if errors:
+            live[list(errors)] = False
+        for i in np.flatnonzero(live & (raw_len < _CFG.size)):
+            try:
+                _config(heads[i].tobytes(), int(raw_len[i]))
+            except Exception as exc:  # noqa: BLE001 -- reported per blob
+                errors[int(i)] = exc
+        full = np.flatnonzero(live & (raw_len >= _CFG.size))
+        # a batch's blobs mostly share one config block: parse each distinct one once
+        keys = np.ascontiguousarray(heads[full, :_CFG.size]).view(np.dtype((np.void, _CFG.size))).ravel()
+        uniq, inv = np.unique(keys, return_inverse=True)
+        parsed = []
+        for u in uniq:
+            try:
+                parsed.append(_config(u.tobytes(), _CFG.size))
+            except Exception as exc:  # noqa: BLE001 -- reported per blob
+                parsed.append(exc)
+        for i, q in zip(full.tolist(), inv.tolist()):
+            hit = parsed[q]
             if isinstance(hit, Exception):
                 errors[i] = type(hit)(*hit.args)
             else:
                 cfgs[i] = hit
+                cfg_id[i] = q
         need = max([c["n_frames"] for c in cfgs.values()], default=0)
         if need > _HEAD_FRAMES:
             cap = _CFG.size + 48 * need
@@ -269,9 +273,9 @@ class Decoder:
                 errors[i] = exc
                 del cfgs[i]
         t1 = time.perf_counter()
-        groups: Dict[bytes, List[int]] = {}
+        groups: Dict[int, List[int]] = {}
         for i in cfgs:
-            groups.setdefault(heads[i, :_CFG.size].tobytes(), []).append(i)
+            groups.setdefault(int(cfg_id[i]), []).append(i)
         clouds: List[Optional[List[np.ndarray]]] = [None] * n
         reports: List[Optional[DecodeReport]] = [None] * n
         t_frames = t_points = 0.0
