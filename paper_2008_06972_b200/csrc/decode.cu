@@ -1069,30 +1069,54 @@ finish:
 }
 
 // Per pixel of every frame: plane reconstruction from the tile map, exactly
-// reconstruct_span's arithmetic; failures counted per blob.  Grid (blocks per
-// frame, frames).  out_r: DEC_NOPT = no point.
-__global__ void __launch_bounds__(1024) reconstruct_kernel(DecGeom G, Trig tg, const uint8_t* raw,
-                                                           const long long* raw_off, const int* sel,
-                                                           const float4* tmap, const unsigned long long* pstat,
-                                                           const long long* ovl, double* out_r,
-                                                           unsigned* pmask, unsigned long long* failed)
+// reconstruct_span's arithmetic; failures counted per blob.  Block per
+// (frame, 1024-pixel block), 8 warps; warp w handles mask words w, w + 8,
+// w + 16, w + 24.  Only pixels that get a plane range are stored (the point
+// mask word of every 32 pixels says which; unproject reads nothing else), and
+// the mask word is the warp's ballot, later OR-ed with the residual pixels.
+constexpr int RC_WARPS = 8;
+__global__ void __launch_bounds__(RC_WARPS * 32) reconstruct_kernel(DecGeom G, Trig tg, const uint8_t* raw,
+                                                                    const long long* raw_off, const int* sel,
+                                                                    const float4* tmap,
+                                                                    const unsigned long long* pstat,
+                                                                    const long long* ovl, double* out_r,
+                                                                    unsigned* pmask, unsigned long long* failed)
 {
     const long long f = blockIdx.y;
     long long chl;
     const int j = (int)dmod(f, G.n, G.rn, chl), ch = (int)chl;
     if (pstat[j] != DEC_NONE || ovl[j]) return;
-    const long long pix = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const long long W = (G.P + 31) >> 5;
+    const long long pb = (long long)blockIdx.x * 1024;
+    const uint8_t* vb = raw + raw_off[sel[j]] + G.bits_off + (long long)ch * G.nb;
+    const float4* tm = tmap + f * G.ty * G.tx;
+    double* dst = out_r + f * G.P;
+    long long ul;
+    const int v0 = (int)dmod(pb, G.w, G.rw, ul), u0 = (int)ul;
     int nfail = 0;
-    bool have = false;
-    if (pix < G.P) {
-        const uint8_t* vb = raw + raw_off[sel[j]] + G.bits_off + (long long)ch * G.nb;
-        const bool valid = (dec_u8(vb + (pix >> 3)) >> (7 - (pix & 7))) & 1u;
-        long long r = DEC_NOPT;
-        if (valid) {
-            long long ul, rv, ru;
-            const int v = (int)dmod(pix, G.w, G.rw, ul), u = (int)ul;
+    for (int k = wid; k < 32; k += RC_WARPS) {
+        const long long wd = (pb >> 5) + k;
+        if (wd >= W) break;
+        const long long p = pb + 32 * k + lane;
+        bool have = false;
+        if (p < G.P && ((dec_u8(vb + (p >> 3)) >> (7 - (p & 7))) & 1u)) {
+            int v, u;
+            if (G.w >= 1024) {  // the block spans at most two rows
+                u = u0 + 32 * k + lane;
+                v = v0;
+                if (u >= G.w) {
+                    u -= G.w;
+                    ++v;
+                }
+            } else {
+                long long uu;
+                v = (int)dmod(p, G.w, G.rw, uu);
+                u = (int)uu;
+            }
+            long long rv, ru;
             const long long tv = dmod(v, G.th, G.rth, rv), tu = dmod(u, G.tw, G.rtw, ru);
-            const float4 pl = tmap[(f * G.ty + tv) * G.tx + tu];
+            const float4 pl = tm[tv * G.tx + tu];
             if (pl.w != 0.0f) {
                 double dx, dy, dz;
                 ray_dir(tg, v, u, dx, dy, dz);
@@ -1101,20 +1125,20 @@ __global__ void __launch_bounds__(1024) reconstruct_kernel(DecGeom G, Trig tg, c
                     ++nfail;
                 } else {
                     const double r_hat = (double)pl.z / den;
-                    if (r_hat <= 0.0 || r_hat > G.r_max) ++nfail;
-                    else r = __double_as_longlong(r_hat);
+                    if (r_hat <= 0.0 || r_hat > G.r_max) {
+                        ++nfail;
+                    } else {
+                        dst[p] = r_hat;
+                        have = true;
+                    }
                 }
             }
         }
-        out_r[f * G.P + pix] = __longlong_as_double(r);
-        have = r != DEC_NOPT;
+        const unsigned m = __ballot_sync(STPC_FULL, have);
+        if (lane == 0) pmask[f * W + wd] = m;
     }
-    // point mask word of these 32 pixels (residual_kernel ORs its pixels in)
-    const unsigned m = __ballot_sync(STPC_FULL, have);
-    const long long W = (G.P + 31) >> 5;
-    if ((threadIdx.x & 31) == 0 && (pix >> 5) < W) pmask[f * W + (pix >> 5)] = m;
     for (int o = 16; o > 0; o >>= 1) nfail += __shfl_xor_sync(STPC_FULL, nfail, o);
-    if ((threadIdx.x & 31) == 0 && nfail) atomicAdd(failed + j, (unsigned long long)nfail);
+    if (lane == 0 && nfail) atomicAdd(failed + j, (unsigned long long)nfail);
 }
 
 // Blobs whose runs are not sorted and disjoint (parse_kernel's order check):
@@ -1347,60 +1371,96 @@ __global__ void __launch_bounds__(1024) frame_offset_kernel(const long long* fra
 }
 
 // points = r * d in row-major pixel order per frame, then
-// p' = R^-1 p + T^-1 as fma(z, r2, fma(y, r1, x r0)) + t (xform_coord)
-__global__ void __launch_bounds__(1024) unproject_kernel(DecGeom G, Trig tg, const double* out_r,
-                                                         const unsigned* pmask, const unsigned long long* pstat,
-                                                         const long long* ovl, const int* blk_off,
-                                                         const long long* frame_off, const double* xf_inv,
-                                                         double* pts)
+// p' = R^-1 p + T^-1 as fma(z, r2, fma(y, r1, x r0)) + t (xform_coord).
+// Block per (frame, 1024-pixel block), 8 warps; warp w handles mask words
+// w, w + 8, w + 16, w + 24 of the block.  The block's 32 point-mask words
+// (for blobs with overlapping runs: ballots over the range image) and their
+// exclusive popcount scan give every word's output offset up front, so the
+// per-word work is the points alone; the inverse transform, the output base
+// and the block's first pixel coordinates are loaded once per block.
+constexpr int UP_WARPS = 8;
+__global__ void __launch_bounds__(UP_WARPS * 32) unproject_kernel(DecGeom G, Trig tg, const double* out_r,
+                                                                  const unsigned* pmask,
+                                                                  const unsigned long long* pstat,
+                                                                  const long long* ovl, const int* blk_off,
+                                                                  const long long* frame_off, const double* xf_inv,
+                                                                  double* pts)
 {
     const long long f = blockIdx.y;
     long long fch;
     const int j = (int)dmod(f, G.n, G.rn, fch);
     if (pstat[j] != DEC_NONE) return;
-    const long long pix = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    const long long i = f * G.P + pix;
-    const long long W = (G.P + 31) >> 5;
-    // the point mask decides which ranges are read at all
-    const bool have = pix < G.P && (ovl[j] ? __double_as_longlong(out_r[i]) != DEC_NOPT
-                                           : ((pmask[f * W + (pix >> 5)] >> (pix & 31)) & 1u));
-    const unsigned m = __ballot_sync(STPC_FULL, have);
-    __shared__ int ws[32];
-    __shared__ double stage[32][96];  // a warp's points, xyz interleaved, for coalesced stores
+    __shared__ unsigned s_m[32];
+    __shared__ int s_off[32];
+    __shared__ double s_R[12];
+    __shared__ long long s_base;
+    __shared__ double stage[UP_WARPS][96];  // a warp's points, xyz interleaved, for coalesced stores
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    if (lane == 0) ws[wid] = __popc(m);
+    const long long W = (G.P + 31) >> 5;
+    const long long pb = (long long)blockIdx.x * 1024;  // the block's first pixel
+    const bool ord = ovl[j] != 0;
+    for (int k = wid; k < 32; k += UP_WARPS) {
+        const long long wd = (pb >> 5) + k;
+        unsigned m = 0;
+        if (ord) {
+            const long long p = pb + 32 * k + lane;
+            m = __ballot_sync(STPC_FULL, p < G.P && __double_as_longlong(out_r[f * G.P + p]) != DEC_NOPT);
+        } else if (wd < W) {
+            m = pmask[f * W + wd];
+        }
+        if (lane == 0) s_m[k] = m;
+    }
+    if (threadIdx.x < 12) s_R[threadIdx.x] = xf_inv[12 * f + threadIdx.x];
+    if (threadIdx.x == 12) s_base = frame_off[f] + blk_off[f * gridDim.x + blockIdx.x];
     __syncthreads();
-    if (wid == 0) {  // exclusive scan of the warp counts by warp 0
-        const int c = lane < (int)(blockDim.x >> 5) ? ws[lane] : 0;
+    if (wid == 0) {
+        const int c = __popc(s_m[lane]);
         int x = c;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
             const int t = __shfl_up_sync(STPC_FULL, x, o);
             if (lane >= o) x += t;
         }
-        if (lane < (int)(blockDim.x >> 5)) ws[lane] = x - c;
+        s_off[lane] = x - c;
     }
     __syncthreads();
-    const int before = ws[wid];
-    const int rank = __popc(m & ((1u << lane) - 1u));
-    if (have) {
-        long long ul;
-        const int v = (int)dmod(pix, G.w, G.rw, ul), u = (int)ul;
-        double dx, dy, dz;
-        ray_dir(tg, v, u, dx, dy, dz);
-        const double r = out_r[i];
-        const double x = r * dx, y = r * dy, z = r * dz;
-        const double* R = xf_inv + 12 * f;
-        stage[wid][3 * rank] = xform_coord(x, y, z, R[0], R[1], R[2], R[9]);
-        stage[wid][3 * rank + 1] = xform_coord(x, y, z, R[3], R[4], R[5], R[10]);
-        stage[wid][3 * rank + 2] = xform_coord(x, y, z, R[6], R[7], R[8], R[11]);
+    long long ul;
+    const int v0 = (int)dmod(pb, G.w, G.rw, ul), u0 = (int)ul;
+    const unsigned lt = (1u << lane) - 1u;
+    for (int k = wid; k < 32; k += UP_WARPS) {
+        const unsigned m = s_m[k];
+        if (!m) continue;
+        if ((m >> lane) & 1u) {
+            const long long p = pb + 32 * k + lane;
+            int v, u;
+            if (G.w >= 1024) {  // the block spans at most two rows
+                u = u0 + 32 * k + lane;
+                v = v0;
+                if (u >= G.w) {
+                    u -= G.w;
+                    ++v;
+                }
+            } else {
+                long long uu;
+                v = (int)dmod(p, G.w, G.rw, uu);
+                u = (int)uu;
+            }
+            double dx, dy, dz;
+            ray_dir(tg, v, u, dx, dy, dz);
+            const double r = out_r[f * G.P + p];
+            const double x = r * dx, y = r * dy, z = r * dz;
+            const int rank = __popc(m & lt);
+            stage[wid][3 * rank] = xform_coord(x, y, z, s_R[0], s_R[1], s_R[2], s_R[9]);
+            stage[wid][3 * rank + 1] = xform_coord(x, y, z, s_R[3], s_R[4], s_R[5], s_R[10]);
+            stage[wid][3 * rank + 2] = xform_coord(x, y, z, s_R[6], s_R[7], s_R[8], s_R[11]);
+        }
+        __syncwarp();
+        // the word's points are contiguous in the output: up to 3 x 32 doubles
+        const int nw = 3 * __popc(m);
+        double* dst = pts + 3 * (s_base + s_off[k]);
+        for (int q = lane; q < nw; q += 32) dst[q] = stage[wid][q];
+        __syncwarp();
     }
-    __syncwarp();
-    // the warp's points are contiguous in the output: write them as 3 x 32
-    // consecutive doubles
-    const int nw = 3 * __popc(m);
-    double* dst = pts + 3 * (frame_off[f] + blk_off[f * gridDim.x + blockIdx.x] + before);
-    for (int k = lane; k < nw; k += 32) dst[k] = stage[wid][k];
 }
 
 }  // namespace stpc
@@ -1765,7 +1825,7 @@ int stpc_decoder_frames(stpc_decoder* d, const stpc_decode_geom* g, const int32_
                                           d->pstat.as<unsigned long long>(), d->ovl.as<long long>());
     const dim3 fg((unsigned)bpf, (unsigned)F);
     STPC_LAUNCH();
-    reconstruct_kernel<<<fg, 1024, 0, s>>>(G, tg, raw, roff, d->sel.as<int>(), d->tmap.as<float4>(), pst,
+    reconstruct_kernel<<<fg, RC_WARPS * 32, 0, s>>>(G, tg, raw, roff, d->sel.as<int>(), d->tmap.as<float4>(), pst,
                                            d->ovl.as<long long>(), d->outr.as<double>(), d->pmask.as<unsigned>(),
                                            d->failed.as<unsigned long long>());
     STPC_LAUNCH();
@@ -1818,7 +1878,7 @@ int stpc_decoder_points(stpc_decoder* d, double* dst, int32_t dst_on_device, int
     const double* tr = d->trig.as<double>();
     tg = Trig{tr, tr + d->G.w, tr + 2 * d->G.w, tr + 2 * d->G.w + d->G.h};
     STPC_LAUNCH();
-    unproject_kernel<<<dim3((unsigned)d->bpf, (unsigned)d->F), 1024, 0, s>>>(
+    unproject_kernel<<<dim3((unsigned)d->bpf, (unsigned)d->F), UP_WARPS * 32, 0, s>>>(
         d->G, tg, d->outr.as<double>(), d->pmask.as<unsigned>(), d->pstat.as<unsigned long long>(),
         d->ovl.as<long long>(), d->blkcnt.as<int>(), d->foff.as<long long>(), d->xfi.as<double>(), out);
     DCK(cudaGetLastError());
