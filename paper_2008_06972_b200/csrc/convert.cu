@@ -14,6 +14,7 @@
 // computes the same minimum independent of thread order; the optional second
 // pass resolves the winning index with an atomicMin over indices whose range
 // equals the minimum (identical to "first index wins").
+#include <cstdlib>
 #include <cstring>
 
 #include "kernels.cuh"
@@ -22,6 +23,12 @@
 namespace stpc {
 
 static constexpr unsigned long long INF_BITS = 0x7ff0000000000000ull;
+
+static bool getenv_flag(const char* name)
+{
+    const char* v = std::getenv(name);
+    return v && *v && *v != '0';
+}
 
 __global__ void fill_u64_kernel(unsigned long long* p, unsigned long long v, long long n)
 {
@@ -136,23 +143,42 @@ __device__ __forceinline__ void warp_add_stats(long long* fs, int rej, int drop,
 }
 
 // Fast bin decision in fp32 (SURVEY.md §7 "K1 convert").  The fp32 angles are
-// within ~1.3e-6 rad of the true ones (input rounding 2^-24 relative plus the
+// within ~1.5e-6 rad of the true ones (input rounding 2^-24 relative plus the
 // polynomial atan below); whenever both angles lie more than
 // FAST_MARGIN = 1e-5 rad from a bin edge the floor is therefore the same as
 // the reference's fp64 (glibc) floor and the point is binned here.  The ~1%
 // of points inside the margin (and any point with coordinates outside
-// [1e-15, 1e15]) go to the exact fp64 path.  Returns false when undecided.
+// [1e-15, 1e15]) go to the exact fp64 path.
 constexpr double FAST_MARGIN = 1e-5;
+
+// 1/x and sqrt(x) on the MUFU with no IEEE fix-up sequence: both are within
+// 2 ulp (2^-22 relative) of the rounded result for the normal, finite
+// arguments the fast path feeds them (max >= 1e-15, x^2 + y^2 in [1e-30, 2e30]).
+__device__ __forceinline__ float rcp_approx(float x)
+{
+    float r;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
+__device__ __forceinline__ float sqrt_approx(float x)
+{
+    float r;
+    asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
 
 // atan2 for the fast path, entirely in fp32: odd minimax-style polynomial of
 // degree 13 in t = min/max (max error 3.2e-7 rad in float32 FMA evaluation,
-// measured on 2M points) and float reflections (pi/2, pi rounded to float:
-// <= 9e-8 rad each, plus half-ulp roundings <= 1.2e-7 rad per step).
+// measured on 2M points; t carries <= 2^-21 relative error from the approximate
+// reciprocal and product, i.e. <= 4.8e-7 rad) and float reflections (pi/2, pi
+// rounded to float: <= 9e-8 rad each, plus half-ulp roundings <= 1.2e-7 rad per
+// step).  The denominator is >= 1e-15 (normal); a subnormal numerator flushes
+// to t = 0, an angle error below 1e-23 rad.
 __device__ __forceinline__ float fast_atan2f(float y, float x)
 {
     const float ax = fabsf(x), ay = fabsf(y);
     const float mx = fmaxf(ax, ay), mn = fminf(ax, ay);
-    const float t = __fdividef(mn, mx);
+    const float t = mn * rcp_approx(mx);
     const float s2 = t * t;
     float p = 0.006811790633946657f;
     p = __fmaf_rn(p, s2, -0.0336042121052742f);
@@ -167,45 +193,92 @@ __device__ __forceinline__ float fast_atan2f(float y, float x)
     return y < 0.0f ? -r : r;
 }
 
+// floor(q) for |q| < 2^22 on the FMA pipe: the round-down sum with 1.5 * 2^23
+// holds floor(q) in its low mantissa bits (no FRND / F2I on the XU).
+__device__ __forceinline__ float floor_bias(float q) { return __fadd_rd(q, 12582912.0f); }
+__device__ __forceinline__ int bias_int(float biased) { return __float_as_int(biased) - 0x4B400000; }
+
 // Error budget of the fp32 decision (in bins of the azimuth; elevation is
-// analogous and smaller): angle error <= 3.2e-7 (polynomial) + 1.2e-7 (input
-// rounding of x, y, z to float) + 5e-7 (reflections, + 2 pi wrap) rad, and
-// qu = th * inv_tr in float adds a relative 1.2e-7, i.e. <= 2 pi * 1.2e-7 *
-// inv_tr bins.  Total < 2.75e-6 * inv_tr bins against a margin of
-// FAST_MARGIN * inv_tr = 1e-5 * inv_tr bins: 3.6x headroom at any resolution.
-__device__ __forceinline__ bool fast_bin(double x, double y, double z, const Geometry& g, float inv_tr,
-                                         float inv_pr, float phi_off, float mu, float mv, int& u, int& v)
+// analogous): angle error <= 3.2e-7 (polynomial) + 4.8e-7 (approximate t) +
+// 1.2e-7 (input rounding of x, y, z to float) + 5e-7 (reflections, + 2 pi
+// wrap) rad, plus for the elevation 2.4e-7 rad from the approximate sqrt of
+// x^2 + y^2, and qu = th * inv_tr in float adds a relative 1.2e-7, i.e. <=
+// 2 pi * 1.2e-7 * inv_tr bins.  Total < 2.4e-6 * inv_tr bins against a margin
+// of FAST_MARGIN * inv_tr = 1e-5 * inv_tr bins: 4x headroom at any
+// resolution.  The margin test |frac - 1/2| < 1/2 - mu rounds frac - 1/2 by
+// at most 3e-8 bins (exact for frac >= 1/4), far inside that headroom.
+__device__ __forceinline__ bool fast_bin(float xf, float yf, float zf, bool guard, const ConvertArgs& a, int& u,
+                                         int& v)
 {
-    const float xf = (float)x, yf = (float)y, zf = (float)z;
-    const float mxy = fmaxf(fabsf(xf), fabsf(yf));
-    const float mall = fmaxf(mxy, fabsf(zf));
-    // keep squares and ratios in float range (coordinates outside [1e-15,
-    // 1e15] go exact: below 1e-15 x^2 + y^2 could underflow); degenerate
-    // directions go exact
-    if (!(mall < 1e15f && mxy > 1e-15f)) return false;
-    float th = fast_atan2f(xf, yf);
-    th = th < 0.0f ? th + 6.28318548f : th;
-    const float qu = th * inv_tr;
-    const float ph = fast_atan2f(sqrtf(xf * xf + yf * yf), zf);
-    const float qv = (ph - phi_off) * inv_pr;
-    const float flu = floorf(qu), flv = floorf(qv);
-    const float fu = qu - flu, fv = qv - flv;
-    if (fu < mu || fu > 1.0f - mu || fv < mv || fv > 1.0f - mv) return false;
+    // azimuth atan2(x, y) and elevation atan2(sqrt(x^2 + y^2), z) side by side
+    // in packed fp32 (FFMA2 / FMUL2 / FADD2: the same IEEE roundings as
+    // fast_atan2f, two lanes per instruction)
+    const float rxy = sqrt_approx(__fmaf_rn(xf, xf, yf * yf));
+    const float ax = fabsf(yf), ay = fabsf(xf), bx = fabsf(zf);
+    const float2 mx = make_float2(fmaxf(ax, ay), fmaxf(bx, rxy));
+    const float2 mn = make_float2(fminf(ax, ay), fminf(bx, rxy));
+    const float2 t = __fmul2_rn(mn, make_float2(rcp_approx(mx.x), rcp_approx(mx.y)));
+    const float2 s2 = __fmul2_rn(t, t);
+    float2 p = make_float2(0.006811790633946657f, 0.006811790633946657f);
+    p = __ffma2_rn(p, s2, make_float2(-0.0336042121052742f, -0.0336042121052742f));
+    p = __ffma2_rn(p, s2, make_float2(0.07962366193532944f, 0.07962366193532944f));
+    p = __ffma2_rn(p, s2, make_float2(-0.1323334127664566f, -0.1323334127664566f));
+    p = __ffma2_rn(p, s2, make_float2(0.19807815551757812f, 0.19807815551757812f));
+    p = __ffma2_rn(p, s2, make_float2(-0.3331736922264099f, -0.3331736922264099f));
+    p = __ffma2_rn(p, s2, make_float2(0.9999961256980896f, 0.9999961256980896f));
+    float2 r = __fmul2_rn(p, t);
+    r.x = ay > ax ? 1.57079637f - r.x : r.x;
+    r.x = yf < 0.0f ? 3.14159274f - r.x : r.x;
+    r.x = xf < 0.0f ? -r.x : r.x;
+    r.x = r.x < 0.0f ? r.x + 6.28318548f : r.x;
+    r.y = rxy > bx ? 1.57079637f - r.y : r.y;
+    r.y = zf < 0.0f ? 3.14159274f - r.y : r.y;
+    // (qu, qv) = (theta / theta_r, (phi - phi_offset) / phi_r)
+    const float2 q = __fmul2_rn(__fadd2_rn(r, make_float2(0.0f, -a.phi_off)), make_float2(a.inv_tr, a.inv_pr));
+    const float bu = floor_bias(q.x), bv = floor_bias(q.y);
+    const float2 fl = __fadd2_rn(make_float2(bu, bv), make_float2(-12582912.0f, -12582912.0f));  // exact
+    const float2 d = __fadd2_rn(__fadd2_rn(q, make_float2(-fl.x, -fl.y)), make_float2(-0.5f, -0.5f));
+    if (!(guard && fabsf(d.x) < a.hu && fabsf(d.y) < a.hv)) return false;
     // 0 <= qu <= 2 pi / theta_r, which CodecConfig does not tie to w: the
     // reference's floor(theta / theta_r) % w needs a true modulo whenever the
     // sensor's w bins cover less than the full circle.  (A point is only
-    // accepted with mu < 0.5, i.e. 1/theta_r < 5e4, so qu < 3.2e5 fits an int;
-    // see launch_convert.)
-    const int uq = (int)flu;
-    u = uq >= g.w ? uq % g.w : uq;
-    v = (int)flv;
+    // accepted with mu < 0.5, i.e. 1/theta_r < 5e4, so |qu|, |qv| < 1e6 fit
+    // the biased floor; see launch_convert.)
+    const int uq = bias_int(bu);
+    u = uq >= a.g.w ? uq % a.g.w : uq;
+    v = bias_int(bv);
     return true;
+}
+
+// The classification every convert pass agrees on (the main kernels, the
+// queue's overflow re-pass): PT_DROP / PT_KEEP (pix, r) decided here,
+// PT_QUEUE for the exact fp64 path (bin_point), which also rejects the
+// non-finite and zero-range points.  The fast decision needs 1e-15 <
+// max(|x|, |y|), max |coord| < 1e15 and s < 1e30 (false for NaN and
+// infinities), so coordinates are finite and r = sqrt(s) finite and
+// positive wherever it is taken.
+enum { PT_DROP = 1, PT_KEEP = 2, PT_QUEUE = 3 };
+__device__ __forceinline__ int fast_point(double x, double y, double z, const ConvertArgs& a, int& pix, double& r)
+{
+    const double s = (x * x + y * y) + z * z;
+    const float xf = (float)x, yf = (float)y, zf = (float)z;
+    const float mxy = fmaxf(fabsf(xf), fabsf(yf));
+    const float mall = fmaxf(mxy, fabsf(zf));
+    const bool guard = s < 1e30 && mxy > 1e-15f && mall < 1e15f;
+    int u, v;
+    if (!fast_bin(xf, yf, zf, guard, a, u, v)) return PT_QUEUE;
+    if (v < 0 || v >= a.g.h) return PT_DROP;
+    r = sqrt(s);
+    pix = v * a.g.w + u;
+    return PT_KEEP;
 }
 
 // Points per thread: loads for all of them are issued before any binning.
 template <class T> struct PPT { static constexpr int value = 8; };
 template <> struct PPT<double> { static constexpr int value = 4; };
 
+// Register-staged variant for inputs that are not 16-byte aligned (the TMA
+// path below needs 16-byte source addresses).
 // grid: (x = chunks of 256*PPT points of a frame, y = frame)
 template <class T>
 #ifndef STPC_CONVERT_MINB
@@ -250,24 +323,17 @@ __global__ void __launch_bounds__(256, STPC_CONVERT_MINB) convert_kernel(Convert
         double x = xform_coord(qx, qy, qz, xf[0], xf[1], xf[2], xf[9]);
         double y = xform_coord(qx, qy, qz, xf[3], xf[4], xf[5], xf[10]);
         double z = xform_coord(qx, qy, qz, xf[6], xf[7], xf[8], xf[11]);
-        if (!(isfinite(x) && isfinite(y) && isfinite(z))) {
-            rej += 1;
-            continue;
-        }
-        double r = sqrt((x * x + y * y) + z * z);
-        int u, v;
-        if (r <= 0.0) {
-            rej += 1;
-        } else if (isfinite(r) && fast_bin(x, y, z, a.g, a.inv_tr, a.inv_pr, a.phi_off, a.mu, a.mv, u, v)) {
-            if (v < 0 || v >= a.g.h) {
-                drop += 1;
-            } else {
-                kept += 1;
-                atomicMin(best + (v * a.g.w + u), (unsigned long long)__double_as_longlong(r));
-            }
-        } else {  // undecided: block-local queue
+        int pix;
+        double r;
+        const int st = fast_point(x, y, z, a, pix, r);
+        if (st == PT_KEEP) {
+            kept += 1;
+            atomicMin(best + pix, (unsigned long long)__double_as_longlong(r));
+        } else if (st == PT_QUEUE) {  // undecided: block-local queue
             int slot = atomicAdd(&q_n, 1);
             q_local[slot] = (int)(i - cb);
+        } else {
+            drop += 1;
         }
     }
     // block-level stats and one global reservation for the queued points
@@ -301,6 +367,239 @@ __global__ void __launch_bounds__(256, STPC_CONVERT_MINB) convert_kernel(Convert
     }
 }
 
+// ---------------------------------------------------------------------------
+// TMA-staged persistent convert (the product path for 16-byte aligned inputs).
+//
+// Work unit = CH = 256 consecutive points of one frame (unit u: frame u / mc,
+// chunk u % mc, mc = chunks of the largest frame).  Every warp runs its own
+// S-stage pipeline in shared memory over units gw, gw + GW, ... (gw = global
+// warp index, GW = warps in the grid): lane 0 streams a unit's points and
+// its frame's 12 transform coefficients in with cp.async.bulk, completing on
+// the stage's mbarrier, and refills the stage with the unit S steps ahead as
+// soon as the warp has read it.  No warp ever waits on another warp, and the
+// loads of the next S - 1 units are in flight while a unit is binned (one
+// unit is ~8 points x ~150 instructions per lane, several microseconds at
+// the SM's shared issue rate: two stages hide the copy latency).
+//
+// Undecided points go into this CTA's private segment of the exact-path queue
+// (a shared-memory slot counter, no global atomics); the per-CTA counts land
+// in q_bcount and their total in q_count (a segment overflow forces the
+// re-pass by pushing q_count past q_cap).  Frame statistics are warp-reduced
+// per unit and added with one global atomic per nonzero counter.
+__device__ __forceinline__ unsigned smem_u32(const void* p)
+{
+    return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count)
+{
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_tx(unsigned long long* bar, unsigned bytes)
+{
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity)
+{
+    unsigned done;
+    do {
+        asm volatile(
+            "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
+            : "=r"(done)
+            : "r"(smem_u32(bar)), "r"(parity)
+            : "memory");
+    } while (!done);
+}
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, unsigned bytes, unsigned long long* bar)
+{
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+
+#ifndef STPC_CONVERT_STAGES
+#define STPC_CONVERT_STAGES 2
+#endif
+template <class T> struct Staged {
+    static constexpr int CH = 256;  // points per warp unit
+    static constexpr int S = STPC_CONVERT_STAGES;
+    static constexpr int WARPS = 8;
+    static constexpr int HDR_BYTES = 32;  // UnitHdr, written by lane 0 before the copy
+    static constexpr int XF_BYTES = 96;
+    static constexpr int PT_BYTES = 3 * CH * (int)sizeof(T) + 32;
+    static constexpr int STAGE = HDR_BYTES + XF_BYTES + PT_BYTES;  // 16-byte multiple
+    static constexpr int SMEM = WARPS * S * STAGE + WARPS * S * 8;
+    static constexpr int PPL = CH / 32;  // points per lane and unit
+};
+
+// A staged unit as its consumers see it (stage header).
+struct UnitHdr {
+    long long cb;  // first point of the unit
+    int f;         // frame
+    int n;         // points in the unit (0: past its frame's end)
+    int n_staged;  // the first n_staged points are wholly in the stage
+    int lead;      // byte offset of point cb within the staged bytes
+};
+
+// Lane 0 of a warp: describe unit (f, c) in the stage header and stream its
+// points and its frame's transform in (an empty unit completes the phase with
+// a transaction-free arrive).  The header's generic stores are ordered before
+// the consumers' reads by the mbarrier's release (arrive) / acquire (wait).
+template <class T>
+__device__ __forceinline__ void issue_unit(const ConvertArgs& a, const T* pts, uint8_t* stage,
+                                           unsigned long long* full, int f, int c, long long pt_end_bytes)
+{
+    constexpr long long PB = 3 * (long long)sizeof(T);
+    const long long b = __ldg(a.pt_off + f), e = __ldg(a.pt_off + f + 1);
+    const long long cb = b + (long long)c * Staged<T>::CH;
+    const int n = (int)max(0ll, min((long long)Staged<T>::CH, e - cb));
+    UnitHdr* h = reinterpret_cast<UnitHdr*>(stage);
+    if (n == 0) {
+        h->n = 0;
+        mbar_arrive_tx(full, 0u);
+        return;
+    }
+    const long long lo = cb * PB, hi = (cb + n) * PB;
+    const long long a0 = lo & ~15ll;
+    long long a1 = (hi + 15) & ~15ll;
+    if (a1 > pt_end_bytes) a1 = hi & ~15ll;  // never read past the last point: the tail loads directly
+    const unsigned bytes = (unsigned)max(0ll, a1 - a0);
+    h->cb = cb;
+    h->f = f;
+    h->n = n;
+    h->lead = (int)(lo - a0);
+    h->n_staged = min(n, (int)max(0ll, (a1 - lo) / PB));
+    mbar_arrive_tx(full, 96u + bytes);
+    bulk_load(stage + Staged<T>::HDR_BYTES, a.xf + 12ll * f, 96u, full);
+    if (bytes) bulk_load(stage + Staged<T>::HDR_BYTES + Staged<T>::XF_BYTES, (const uint8_t*)pts + a0, bytes, full);
+}
+
+#ifndef STPC_CONVERT_STAGED_MINB
+#define STPC_CONVERT_STAGED_MINB 4
+#endif
+template <class T>
+__global__ void __launch_bounds__(256, STPC_CONVERT_STAGED_MINB)
+    convert_staged_kernel(ConvertArgs a, const T* pts, int n_units, int mc, int seg)
+{
+    using SC = Staged<T>;
+    constexpr int PB = 3 * (int)sizeof(T);
+    extern __shared__ __align__(128) uint8_t smem[];
+    __shared__ int q_n;
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    uint8_t* ring = smem + w * SC::S * SC::STAGE;
+    unsigned long long* full = reinterpret_cast<unsigned long long*>(smem + SC::WARPS * SC::S * SC::STAGE) + w * SC::S;
+    const long long pt_end_bytes = __ldg(a.pt_off + a.n_frames) * (long long)PB;
+    const int GW = gridDim.x * SC::WARPS;
+    const int gw = blockIdx.x * SC::WARPS + w;
+    // lane 0's issue cursor (frame fi, chunk ci), advanced by GW units per step
+    const int step_f = GW / mc, step_c = GW - (GW / mc) * mc;
+    int fi = gw / mc, ci = gw - (gw / mc) * mc;
+    if (tid == 0) q_n = 0;
+    if (lane == 0) {
+        for (int s = 0; s < SC::S; ++s) mbar_init(full + s, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        for (int s = 0; s < SC::S && fi < a.n_frames; ++s) {
+            issue_unit<T>(a, pts, ring + s * SC::STAGE, full + s, fi, ci, pt_end_bytes);
+            fi += step_f;
+            ci += step_c;
+            if (ci >= mc) ci -= mc, fi += 1;
+        }
+    }
+    __syncthreads();  // q_n
+    long long* qi_seg = a.q_idx + (long long)blockIdx.x * seg;
+    int* qf_seg = a.q_frame + (long long)blockIdx.x * seg;
+    int k = 0;
+    for (int u = gw; u < n_units; u += GW, ++k) {
+        const int st = k % SC::S;
+        const unsigned par = (unsigned)(k / SC::S) & 1u;
+        uint8_t* stage = ring + st * SC::STAGE;
+        mbar_wait(full + st, par);
+        const UnitHdr h = *reinterpret_cast<const UnitHdr*>(stage);
+        int drop = 0, nq = 0;  // kept = n - drop - nq (the exact path counts the queued points)
+        if (h.n > 0) {
+            const double* xfs = reinterpret_cast<const double*>(stage + SC::HDR_BYTES);
+            double c[12];
+#pragma unroll
+            for (int t = 0; t < 12; ++t) c[t] = xfs[t];
+            const uint8_t* sp = stage + SC::HDR_BYTES + SC::XF_BYTES + h.lead;
+            unsigned long long* best = a.best + (long long)h.f * a.g.P;
+#pragma unroll 2
+            for (int jj = 0; jj < SC::PPL; ++jj) {
+                const int j = jj * 32 + lane;
+                if (j < h.n) {
+                    T px, py, pz;
+                    if (j < h.n_staged) {
+                        const T* q = reinterpret_cast<const T*>(sp + PB * j);
+                        px = q[0];
+                        py = q[1];
+                        pz = q[2];
+                    } else {  // the array's last point(s) past the 16-byte-aligned stage
+                        const T* q = pts + 3 * (h.cb + j);
+                        px = __ldg(q);
+                        py = __ldg(q + 1);
+                        pz = __ldg(q + 2);
+                    }
+                    const double qx = (double)px, qy = (double)py, qz = (double)pz;
+                    const double x = xform_coord(qx, qy, qz, c[0], c[1], c[2], c[9]);
+                    const double y = xform_coord(qx, qy, qz, c[3], c[4], c[5], c[10]);
+                    const double z = xform_coord(qx, qy, qz, c[6], c[7], c[8], c[11]);
+                    int pix;
+                    double rr;
+                    const int cls = fast_point(x, y, z, a, pix, rr);
+                    if (cls == PT_KEEP) {
+#if defined(STPC_CONVERT_EXP) && STPC_CONVERT_EXP == 1
+                        if (rr == 1.2345) atomicMin(best + pix, (unsigned long long)__double_as_longlong(rr));
+#elif defined(STPC_CONVERT_EXP) && STPC_CONVERT_EXP == 2
+                        atomicMin(best + (pix & 0x3fff), (unsigned long long)__double_as_longlong(rr));
+#else
+                        atomicMin(best + pix, (unsigned long long)__double_as_longlong(rr));
+#endif
+                    } else if (cls == PT_QUEUE) {
+                        nq += 1;
+                        const int slot = atomicAdd(&q_n, 1);
+                        if (slot < seg) {
+                            qi_seg[slot] = h.cb + j;
+                            qf_seg[slot] = h.f;
+                        }
+                    } else {
+                        drop += 1;
+                    }
+                }
+            }
+        }
+        __syncwarp();  // every lane is done with the stage
+        if (lane == 0 && fi < a.n_frames) {
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            issue_unit<T>(a, pts, stage, full + st, fi, ci, pt_end_bytes);
+            fi += step_f;
+            ci += step_c;
+            if (ci >= mc) ci -= mc, fi += 1;
+        }
+        if (h.n > 0) {
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                drop += __shfl_xor_sync(STPC_FULL, drop, o);
+                nq += __shfl_xor_sync(STPC_FULL, nq, o);
+            }
+            if (lane == 0) {
+                long long* fs = a.fstats + (long long)h.f * FS_COUNT;
+                const int kept = h.n - drop - nq;
+                if (drop) atomicAdd((unsigned long long*)&fs[FS_DROPPED], (unsigned long long)drop);
+                if (kept) atomicAdd((unsigned long long*)&fs[FS_KEPT], (unsigned long long)kept);
+            }
+        }
+    }
+    __syncthreads();
+    if (tid == 0) {
+        const int nq = q_n;
+        a.q_bcount[blockIdx.x] = min(nq, seg);
+        unsigned long long add = (unsigned long long)nq;
+        if (nq > seg) add += (unsigned long long)a.q_cap + 1;  // segment overflow: force the re-pass
+        if (add) atomicAdd(a.q_count, add);
+    }
+}
+
 __device__ __forceinline__ void exact_point(const ConvertArgs& a, double px, double py, double pz, int f)
 {
     const double* xf = a.xf + 12 * f;
@@ -313,7 +612,8 @@ __device__ __forceinline__ void exact_point(const ConvertArgs& a, double px, dou
 }
 
 // Queue overflow (more than q_cap undecided points): the queue is discarded and
-// every undecided point is re-derived here.  grid (1, frames): the usual
+// every undecided point (fast_point's PT_QUEUE, the same classification every
+// main kernel applies) is re-derived here.  grid (1, frames): the usual
 // no-overflow case costs one early exit per block.
 template <class T>
 __global__ void __launch_bounds__(256) convert_overflow_kernel(ConvertArgs a, const T* pts)
@@ -328,12 +628,9 @@ __global__ void __launch_bounds__(256) convert_overflow_kernel(ConvertArgs a, co
         double x = xform_coord(px, py, pz, xf[0], xf[1], xf[2], xf[9]);
         double y = xform_coord(px, py, pz, xf[3], xf[4], xf[5], xf[10]);
         double z = xform_coord(px, py, pz, xf[6], xf[7], xf[8], xf[11]);
-        if (!(isfinite(x) && isfinite(y) && isfinite(z))) continue;
-        double r = sqrt((x * x + y * y) + z * z);
-        int u, v;
-        if (r <= 0.0 || (isfinite(r) && fast_bin(x, y, z, a.g, a.inv_tr, a.inv_pr, a.phi_off, a.mu, a.mv, u, v)))
-            continue;
-        exact_point(a, px, py, pz, f);
+        int pix;
+        double r;
+        if (fast_point(x, y, z, a, pix, r) == PT_QUEUE) exact_point(a, px, py, pz, f);
     }
 }
 
@@ -349,6 +646,20 @@ __global__ void __launch_bounds__(256) convert_exact_kernel(ConvertArgs a, const
         const long long i = a.q_idx[q];
         const T* p = pts + 3 * i;
         exact_point(a, (double)p[0], (double)p[1], (double)p[2], a.q_frame[q]);
+    }
+}
+
+// The staged kernel's queue: CTA b's undecided points are q_idx[b * seg, + q_bcount[b]).
+template <class T>
+__global__ void __launch_bounds__(256) convert_exact_seg_kernel(ConvertArgs a, const T* pts, int seg)
+{
+    if (*a.q_count > (unsigned long long)a.q_cap) return;  // overflow re-pass handles them
+    const int n = a.q_bcount[blockIdx.x];
+    const long long base = (long long)blockIdx.x * seg;
+    for (int q = threadIdx.x; q < n; q += blockDim.x) {
+        const long long i = a.q_idx[base + q];
+        const T* p = pts + 3 * i;
+        exact_point(a, (double)p[0], (double)p[1], (double)p[2], a.q_frame[base + q]);
     }
 }
 
@@ -396,6 +707,43 @@ static dim3 chunk_grid(int max_pts, int n_frames)
     return dim3(bx < 1 ? 1 : bx, n_frames);
 }
 
+template <class T>
+static void launch_regs(const ConvertArgs& a, int max_pts, cudaStream_t s)
+{
+    STPC_LAUNCH();
+    convert_kernel<T><<<chunk_grid<T>(max_pts, a.n_frames), 256, 0, s>>>(a, (const T*)a.pts);
+    STPC_LAUNCH();
+    convert_exact_kernel<T><<<148 * 4, 256, 0, s>>>(a, (const T*)a.pts);
+    STPC_LAUNCH();
+    convert_overflow_kernel<T><<<dim3(1, a.n_frames), 256, 0, s>>>(a, (const T*)a.pts);
+}
+
+template <class T>
+static void launch_staged(const ConvertArgs& a, int max_pts, cudaStream_t s)
+{
+    using SC = Staged<T>;
+    static int grid_max = 0;  // CTAs resident on the device (persistent grid)
+    if (!grid_max) {
+        cudaFuncSetAttribute(convert_staged_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, SC::SMEM);
+        int per_sm = 0, dev = 0, sms = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, convert_staged_kernel<T>, 32 * SC::WARPS, SC::SMEM);
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        grid_max = std::max(1, std::min(per_sm * sms, CONVERT_MAX_GRID));
+    }
+    const int mc = std::max(1, (max_pts + SC::CH - 1) / SC::CH);
+    const long long n_units = (long long)mc * a.n_frames;
+    if (n_units >= (1ll << 31)) return launch_regs<T>(a, max_pts, s);
+    const int grid = (int)std::min<long long>(grid_max, (n_units + SC::WARPS - 1) / SC::WARPS);
+    const int seg = (int)std::max<long long>(1, a.q_cap / grid);
+    STPC_LAUNCH();
+    convert_staged_kernel<T><<<grid, 32 * SC::WARPS, SC::SMEM, s>>>(a, (const T*)a.pts, (int)n_units, mc, seg);
+    STPC_LAUNCH();
+    convert_exact_seg_kernel<T><<<grid, 256, 0, s>>>(a, (const T*)a.pts, seg);
+    STPC_LAUNCH();
+    convert_overflow_kernel<T><<<dim3(1, a.n_frames), 256, 0, s>>>(a, (const T*)a.pts);
+}
+
 void launch_convert(const ConvertArgs& a0, int max_pts, cudaStream_t s)
 {
     if (a0.n_frames <= 0) return;
@@ -403,29 +751,26 @@ void launch_convert(const ConvertArgs& a0, int max_pts, cudaStream_t s)
     a.inv_tr = (float)(1.0 / a.g.theta_r);
     a.inv_pr = (float)(1.0 / a.g.phi_r);
     a.phi_off = (float)a.g.phi_offset;
-    a.mu = (float)FAST_MARGIN * a.inv_tr;
-    a.mv = (float)FAST_MARGIN * a.inv_pr;
+    float mu = (float)FAST_MARGIN * a.inv_tr;
+    float mv = (float)FAST_MARGIN * a.inv_pr;
     // The fp32 decision is only sound where the margin is below half a bin
     // and phi_offset survives the float rounding within the error budget
     // (2^-24 |phi_offset| << FAST_MARGIN): otherwise every point takes the
-    // exact path (mu = 1 rejects every fraction).
-    if (!(a.mu < 0.5f && a.mv < 0.5f && fabs(a.g.phi_offset) < 16.0)) a.mu = a.mv = 1.0f;
+    // exact path (a negative half-width rejects every fraction).
+    if (!(mu < 0.5f && mv < 0.5f && fabs(a.g.phi_offset) < 16.0)) mu = mv = 1.0f;
+    a.hu = 0.5f - mu;
+    a.hv = 0.5f - mv;
+    a.q_bcount = reinterpret_cast<int*>(a.q_count + 1);
     launch_zero(a.q_count, sizeof(unsigned long long), s);
-    STPC_LAUNCH();
-    if (a.pts_f64)
-        convert_kernel<double><<<chunk_grid<double>(max_pts, a.n_frames), 256, 0, s>>>(a, (const double*)a.pts);
-    else
-        convert_kernel<float><<<chunk_grid<float>(max_pts, a.n_frames), 256, 0, s>>>(a, (const float*)a.pts);
-    STPC_LAUNCH();
-    if (a.pts_f64)
-        convert_exact_kernel<double><<<148 * 4, 256, 0, s>>>(a, (const double*)a.pts);
-    else
-        convert_exact_kernel<float><<<148 * 4, 256, 0, s>>>(a, (const float*)a.pts);
-    STPC_LAUNCH();
-    if (a.pts_f64)
-        convert_overflow_kernel<double><<<dim3(1, a.n_frames), 256, 0, s>>>(a, (const double*)a.pts);
-    else
-        convert_overflow_kernel<float><<<dim3(1, a.n_frames), 256, 0, s>>>(a, (const float*)a.pts);
+    const bool aligned = (reinterpret_cast<uintptr_t>(a.pts) & 15) == 0 &&
+                         (reinterpret_cast<uintptr_t>(a.xf) & 15) == 0 && !getenv_flag("STPC_CONVERT_REGS");
+    if (aligned) {
+        if (a.pts_f64) launch_staged<double>(a, max_pts, s);
+        else launch_staged<float>(a, max_pts, s);
+        return;
+    }
+    if (a.pts_f64) launch_regs<double>(a, max_pts, s);
+    else launch_regs<float>(a, max_pts, s);
 }
 
 void launch_convert_win(const ConvertArgs& a, int max_pts, cudaStream_t s)

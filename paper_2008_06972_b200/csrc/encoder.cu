@@ -420,7 +420,7 @@ static int encode_impl(stpc_encoder* e, int G, const void* d_points, const int64
     {
         long long npts = h_off[F] - h_off[0];
         long long cap = npts / 8 + 4096;
-        ENS(e->q_count, sizeof(unsigned long long));
+        ENS(e->q_count, CONVERT_QCOUNT_BYTES);
         ENS(e->q_idx, sizeof(long long) * cap);
         ENS(e->q_frame, sizeof(int) * cap);
         ca.q_count = e->q_count.as<unsigned long long>();
@@ -1205,7 +1205,7 @@ int stpc_project(const void* d_points, int32_t points_f64, const int64_t* point_
     DevBuf off, xf, fs, qc, qi, qf;
     long long npts = point_offsets[n_frames] - point_offsets[0];
     long long cap = npts / 8 + 4096;
-    ENS(qc, sizeof(unsigned long long));
+    ENS(qc, CONVERT_QCOUNT_BYTES);
     ENS(qi, sizeof(long long) * cap);
     ENS(qf, sizeof(int) * cap);
     ENS(off, sizeof(long long) * (n_frames + 1));

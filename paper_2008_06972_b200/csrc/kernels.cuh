@@ -57,9 +57,16 @@ struct ConvertArgs {
     long long* q_idx;
     int* q_frame;
     long long q_cap;
-    // fp32 fast-path constants, set by launch_convert
-    float inv_tr = 0.f, inv_pr = 0.f, phi_off = 0.f, mu = 0.f, mv = 0.f;
+    int* q_bcount = nullptr;  // staged kernel: per-CTA queue counts (set by launch_convert)
+    // fp32 fast-path constants, set by launch_convert: a point is decided in
+    // fp32 when |frac(q) - 1/2| < hu (azimuth) and < hv (elevation)
+    float inv_tr = 0.f, inv_pr = 0.f, phi_off = 0.f, hu = 0.f, hv = 0.f;
 };
+
+// The staged convert's persistent grid cap: the exact-path queue counter
+// buffer holds 8 + 4 * CONVERT_MAX_GRID bytes (q_count, then q_bcount).
+constexpr int CONVERT_MAX_GRID = 148 * 8;
+constexpr size_t CONVERT_QCOUNT_BYTES = 8 + 4 * CONVERT_MAX_GRID;
 
 void launch_fill_u64(unsigned long long* p, unsigned long long v, long long n, cudaStream_t s);
 void launch_zero(void* p, long long bytes, cudaStream_t s);
