@@ -421,18 +421,6 @@ __device__ __forceinline__ void bulk_load(void* dst, const void* src, unsigned b
 #ifndef STPC_CONVERT_STAGES
 #define STPC_CONVERT_STAGES 2
 #endif
-template <class T> struct Staged {
-    static constexpr int CH = 256;  // points per warp unit
-    static constexpr int S = STPC_CONVERT_STAGES;
-    static constexpr int WARPS = 8;
-    static constexpr int HDR_BYTES = 32;  // UnitHdr, written by lane 0 before the copy
-    static constexpr int XF_BYTES = 96;
-    static constexpr int PT_BYTES = 3 * CH * (int)sizeof(T) + 32;
-    static constexpr int STAGE = HDR_BYTES + XF_BYTES + PT_BYTES;  // 16-byte multiple
-    static constexpr int SMEM = WARPS * S * STAGE + WARPS * S * 8;
-    static constexpr int PPL = CH / 32;  // points per lane and unit
-};
-
 // A staged unit as its consumers see it (stage header).
 struct UnitHdr {
     long long cb;  // first point of the unit
@@ -440,6 +428,19 @@ struct UnitHdr {
     int n;         // points in the unit (0: past its frame's end)
     int n_staged;  // the first n_staged points are wholly in the stage
     int lead;      // byte offset of point cb within the staged bytes
+};
+
+template <class T> struct Staged {
+    static constexpr int CH = 256;  // points per warp unit
+    static constexpr int S = STPC_CONVERT_STAGES;
+    static constexpr int WARPS = 8;
+    static constexpr int HDR_BYTES = 32;  // UnitHdr, written by lane 0 before the copy
+    static_assert(sizeof(UnitHdr) <= HDR_BYTES, "stage header");
+    static constexpr int XF_BYTES = 96;
+    static constexpr int PT_BYTES = 3 * CH * (int)sizeof(T) + 32;
+    static constexpr int STAGE = HDR_BYTES + XF_BYTES + PT_BYTES;  // 16-byte multiple
+    static constexpr int SMEM = WARPS * S * STAGE + WARPS * S * 8;
+    static constexpr int PPL = CH / 32;  // points per lane and unit
 };
 
 // Lane 0 of a warp: describe unit (f, c) in the stage header and stream its
@@ -469,7 +470,7 @@ __device__ __forceinline__ void issue_unit(const ConvertArgs& a, const T* pts, u
     h->f = f;
     h->n = n;
     h->lead = (int)(lo - a0);
-    h->n_staged = min(n, (int)max(0ll, (a1 - lo) / PB));
+    h->n_staged = a1 > lo ? min(n, (int)(a1 - lo) / (int)PB) : 0;
     mbar_arrive_tx(full, 96u + bytes);
     bulk_load(stage + Staged<T>::HDR_BYTES, a.xf + 12ll * f, 96u, full);
     if (bytes) bulk_load(stage + Staged<T>::HDR_BYTES + Staged<T>::XF_BYTES, (const uint8_t*)pts + a0, bytes, full);
@@ -524,47 +525,48 @@ __global__ void __launch_bounds__(256, STPC_CONVERT_STAGED_MINB)
             for (int t = 0; t < 12; ++t) c[t] = xfs[t];
             const uint8_t* sp = stage + SC::HDR_BYTES + SC::XF_BYTES + h.lead;
             unsigned long long* best = a.best + (long long)h.f * a.g.P;
+            auto bin = [&](int j, T px, T py, T pz) {
+                const double qx = (double)px, qy = (double)py, qz = (double)pz;
+                const double x = xform_coord(qx, qy, qz, c[0], c[1], c[2], c[9]);
+                const double y = xform_coord(qx, qy, qz, c[3], c[4], c[5], c[10]);
+                const double z = xform_coord(qx, qy, qz, c[6], c[7], c[8], c[11]);
+                int pix;
+                double rr;
+                const int cls = fast_point(x, y, z, a, pix, rr);
+                if (cls == PT_KEEP) {
+#if defined(STPC_CONVERT_EXP) && STPC_CONVERT_EXP == 1
+                    if (rr == 1.2345) atomicMin(best + pix, (unsigned long long)__double_as_longlong(rr));
+#elif defined(STPC_CONVERT_EXP) && STPC_CONVERT_EXP == 2
+                    atomicMin(best + (pix & 0x3fff), (unsigned long long)__double_as_longlong(rr));
+#else
+                    atomicMin(best + pix, (unsigned long long)__double_as_longlong(rr));
+#endif
+                } else if (cls == PT_QUEUE) {
+                    nq += 1;
+                    const int slot = atomicAdd(&q_n, 1);
+                    if (slot < seg) {
+                        qi_seg[slot] = h.cb + j;
+                        qf_seg[slot] = h.f;
+                    }
+                } else {
+                    drop += 1;
+                }
+            };
+            // the staged points from shared memory ...
 #pragma unroll 2
             for (int jj = 0; jj < SC::PPL; ++jj) {
                 const int j = jj * 32 + lane;
+                if (j < h.n_staged) {
+                    const T* q = reinterpret_cast<const T*>(sp + PB * j);
+                    bin(j, q[0], q[1], q[2]);
+                }
+            }
+            // ... and the array's last point(s) past the 16-byte-aligned stage
+            if (h.n_staged < h.n) {
+                const int j = h.n_staged + lane;
                 if (j < h.n) {
-                    T px, py, pz;
-                    if (j < h.n_staged) {
-                        const T* q = reinterpret_cast<const T*>(sp + PB * j);
-                        px = q[0];
-                        py = q[1];
-                        pz = q[2];
-                    } else {  // the array's last point(s) past the 16-byte-aligned stage
-                        const T* q = pts + 3 * (h.cb + j);
-                        px = __ldg(q);
-                        py = __ldg(q + 1);
-                        pz = __ldg(q + 2);
-                    }
-                    const double qx = (double)px, qy = (double)py, qz = (double)pz;
-                    const double x = xform_coord(qx, qy, qz, c[0], c[1], c[2], c[9]);
-                    const double y = xform_coord(qx, qy, qz, c[3], c[4], c[5], c[10]);
-                    const double z = xform_coord(qx, qy, qz, c[6], c[7], c[8], c[11]);
-                    int pix;
-                    double rr;
-                    const int cls = fast_point(x, y, z, a, pix, rr);
-                    if (cls == PT_KEEP) {
-#if defined(STPC_CONVERT_EXP) && STPC_CONVERT_EXP == 1
-                        if (rr == 1.2345) atomicMin(best + pix, (unsigned long long)__double_as_longlong(rr));
-#elif defined(STPC_CONVERT_EXP) && STPC_CONVERT_EXP == 2
-                        atomicMin(best + (pix & 0x3fff), (unsigned long long)__double_as_longlong(rr));
-#else
-                        atomicMin(best + pix, (unsigned long long)__double_as_longlong(rr));
-#endif
-                    } else if (cls == PT_QUEUE) {
-                        nq += 1;
-                        const int slot = atomicAdd(&q_n, 1);
-                        if (slot < seg) {
-                            qi_seg[slot] = h.cb + j;
-                            qf_seg[slot] = h.f;
-                        }
-                    } else {
-                        drop += 1;
-                    }
+                    const T* q = pts + 3 * (h.cb + j);
+                    bin(j, __ldg(q), __ldg(q + 1), __ldg(q + 2));
                 }
             }
         }
@@ -577,11 +579,8 @@ __global__ void __launch_bounds__(256, STPC_CONVERT_STAGED_MINB)
             if (ci >= mc) ci -= mc, fi += 1;
         }
         if (h.n > 0) {
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) {
-                drop += __shfl_xor_sync(STPC_FULL, drop, o);
-                nq += __shfl_xor_sync(STPC_FULL, nq, o);
-            }
+            drop = __reduce_add_sync(STPC_FULL, drop);
+            nq = __reduce_add_sync(STPC_FULL, nq);
             if (lane == 0) {
                 long long* fs = a.fstats + (long long)h.f * FS_COUNT;
                 const int kept = h.n - drop - nq;
