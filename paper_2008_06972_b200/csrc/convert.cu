@@ -476,6 +476,11 @@ __device__ __forceinline__ void issue_unit(const ConvertArgs& a, const T* pts, u
     if (bytes) bulk_load(stage + Staged<T>::HDR_BYTES + Staged<T>::XF_BYTES, (const uint8_t*)pts + a0, bytes, full);
 }
 
+#ifndef STPC_CONVERT_UNROLL
+#define STPC_CONVERT_UNROLL 1
+#endif
+constexpr int CONVERT_UNROLL = STPC_CONVERT_UNROLL;
+
 #ifndef STPC_CONVERT_STAGED_MINB
 #define STPC_CONVERT_STAGED_MINB 4
 #endif
@@ -553,7 +558,7 @@ __global__ void __launch_bounds__(256, STPC_CONVERT_STAGED_MINB)
                 }
             };
             // the staged points from shared memory ...
-#pragma unroll 2
+#pragma unroll CONVERT_UNROLL
             for (int jj = 0; jj < SC::PPL; ++jj) {
                 const int j = jj * 32 + lane;
                 if (j < h.n_staged) {
