@@ -684,6 +684,10 @@ int stpc_encode_device(stpc_encoder* enc, int32_t n_groups, const void* d_points
         g_err = "invalid arguments";
         return STPC_ERR_ARG;
     }
+    if ((uintptr_t)d_points % (enc->cfg.points_f64 ? 8 : 4)) {
+        g_err = "device points are not aligned to their element size";
+        return STPC_ERR_ARG;
+    }
     return encode_impl(enc, n_groups, d_points, (const int64_t*)point_offsets, transforms, (cudaStream_t)stream);
 }
 
@@ -1190,6 +1194,10 @@ int stpc_project(const void* d_points, int32_t points_f64, const int64_t* point_
 {
     if (n_frames < 1 || w < 1 || h < 1 || !point_offsets || !transforms || !d_best || !h_counts) {
         g_err = "invalid arguments";
+        return STPC_ERR_ARG;
+    }
+    if ((uintptr_t)d_points % (points_f64 ? 8 : 4)) {
+        g_err = "device points are not aligned to their element size";
         return STPC_ERR_ARG;
     }
     cudaStream_t s = (cudaStream_t)stream;

@@ -159,6 +159,67 @@ def test_project_fine_bins_exact_path_overflow(lib, rng):
     assert np.array_equal(counts[0], oc)
 
 
+def _project_at(lib, pts, off, xf, w, h, tr, pr, phi_off, f64, shift):
+    """stpc_project with the points `shift` bytes past a 256-aligned
+    allocation (shift % 16 != 0 takes the register-staged kernel instead of
+    the TMA-staged one)."""
+    F = len(off) - 1
+    raw = np.ascontiguousarray(pts)
+    d = Dev(lib, raw.nbytes + 64)
+    dst = ctypes.c_void_p(d.ptr.value + shift)
+    if raw.nbytes:
+        assert lib.stpc_memcpy_h2d(dst, raw.ctypes.data, raw.nbytes) == 0
+    d_best = Dev(lib, 8 * F * w * h)
+    d_win = Dev(lib, 8 * F * w * h)
+    counts = np.zeros((F, 3), np.int64)
+    rc = lib.stpc_project(dst, int(f64), off.ctypes.data, F, xf.ctypes.data, w, h, tr, pr, phi_off,
+                          d_best.ptr, d_win.ptr, counts.ctypes.data, None)
+    assert rc == 0, lib.stpc_last_error()
+    return d_best.get(np.float64, F * w * h).reshape(F, -1), d_win.get(np.int64, F * w * h).reshape(F, -1), counts
+
+
+@pytest.mark.parametrize("f64", [False, True])
+def test_project_staged_and_register_paths(lib, rng, f64):
+    """The TMA-staged convert (16-byte aligned points, per-warp cp.async.bulk
+    pipelines, the array's unaligned tail loaded directly) and the
+    register-staged one (misaligned points) against the oracle: ragged frames
+    (including empty ones and frames that end mid-16-byte word), NaN /
+    infinite / zero points (rejected by the exact path), out-of-band
+    elevations (dropped) and a rotated, translated frame."""
+    w, h, tr, pr, phi_off = 500, 16, 2 * np.pi / 500, np.radians(1.68), np.radians(88.0)
+    sizes = [0, 1, 2, 3, 255, 256, 257, 4099, 0, 30001, 7]
+    clouds = []
+    for n in sizes:
+        th = rng.uniform(0, 2 * np.pi, n)
+        ph = rng.uniform(phi_off - 0.05, phi_off + h * pr + 0.05, n)
+        r = rng.uniform(0.5, 80, n)
+        c = np.stack([r * np.sin(ph) * np.sin(th), r * np.sin(ph) * np.cos(th), r * np.cos(ph)], 1)
+        if n > 10:
+            c[rng.integers(0, n, 3)] = np.nan
+            c[rng.integers(0, n, 2), 1] = np.inf
+            c[rng.integers(0, n, 2)] = 0.0
+        clouds.append(c.astype(np.float64 if f64 else np.float32))
+    ang = 0.3
+    Rz = np.array([[np.cos(ang), -np.sin(ang), 0], [np.sin(ang), np.cos(ang), 0], [0, 0, 1]], np.float32)
+    xforms = [(np.eye(3), np.zeros(3)) if i % 2 == 0 else (Rz.astype(np.float64), np.array([1.5, -0.25, 0.125]))
+              for i in range(len(clouds))]
+    off = np.zeros(len(clouds) + 1, np.int64)
+    off[1:] = np.cumsum([c.shape[0] for c in clouds])
+    pts = np.concatenate(clouds)
+    xf = np.stack([np.concatenate([np.asarray(R, np.float64).reshape(9), np.asarray(T, np.float64)]) for R, T in xforms])
+    ocfg = oracle.OracleConfig("single", 0.1, 4, 4, tr, pr, phi_off, w, h, 1, 0)
+    ref = [oracle.convert(c, R, T, ocfg) for c, (R, T) in zip(clouds, xforms)]
+    for shift in ((0, 16, 8) if f64 else (0, 16, 4, 8)):
+        best, win, counts = _project_at(lib, pts, off, xf, w, h, tr, pr, phi_off, f64, shift)
+        for f, (ob, ow, oc) in enumerate(ref):
+            assert np.array_equal(best[f].view(np.uint64), ob.view(np.uint64)), (shift, f)
+            assert np.array_equal(win[f], ow), (shift, f)
+            assert np.array_equal(counts[f], oc), (shift, f)
+    if f64:  # a double array off its 8-byte alignment is refused, not faulted on
+        with pytest.raises(AssertionError, match="aligned"):
+            _project_at(lib, pts, off, xf, w, h, tr, pr, phi_off, f64, 4)
+
+
 @pytest.mark.parametrize("w,h,tr,pr,off", [
     # the reference's own conftest sensor: w=64, h=8 at the default
     # AngularResolution (theta_r = 2 pi / 1800, phi_r = 0.00698, phi_offset
