@@ -143,13 +143,12 @@ __device__ __forceinline__ void warp_add_stats(long long* fs, int rej, int drop,
 }
 
 // Fast bin decision in fp32 (SURVEY.md §7 "K1 convert").  The fp32 angles are
-// within ~1.5e-6 rad of the true ones (input rounding 2^-24 relative plus the
-// polynomial atan below); whenever both angles lie more than
-// FAST_MARGIN = 1e-5 rad from a bin edge the floor is therefore the same as
-// the reference's fp64 (glibc) floor and the point is binned here.  The ~1%
-// of points inside the margin (and any point with coordinates outside
+// within 2.6e-6 rad of the true ones (the budget below); whenever both angles
+// lie more than FAST_MARGIN = 5e-6 rad from a bin edge the floor is therefore
+// the same as the reference's fp64 (glibc) floor and the point is binned
+// here.  The ~0.5% of points inside the margin (and any point with coordinates outside
 // [1e-15, 1e15]) go to the exact fp64 path.
-constexpr double FAST_MARGIN = 1e-5;
+constexpr double FAST_MARGIN = 5e-6;
 
 // 1/x and sqrt(x) on the MUFU with no IEEE fix-up sequence: both are within
 // 2 ulp (2^-22 relative) of the rounded result for the normal, finite
@@ -198,15 +197,22 @@ __device__ __forceinline__ float fast_atan2f(float y, float x)
 __device__ __forceinline__ float floor_bias(float q) { return __fadd_rd(q, 12582912.0f); }
 __device__ __forceinline__ int bias_int(float biased) { return __float_as_int(biased) - 0x4B400000; }
 
-// Error budget of the fp32 decision (in bins of the azimuth; elevation is
-// analogous): angle error <= 3.2e-7 (polynomial) + 4.8e-7 (approximate t) +
-// 1.2e-7 (input rounding of x, y, z to float) + 5e-7 (reflections, + 2 pi
-// wrap) rad, plus for the elevation 2.4e-7 rad from the approximate sqrt of
-// x^2 + y^2, and qu = th * inv_tr in float adds a relative 1.2e-7, i.e. <=
-// 2 pi * 1.2e-7 * inv_tr bins.  Total < 2.4e-6 * inv_tr bins against a margin
-// of FAST_MARGIN * inv_tr = 1e-5 * inv_tr bins: 4x headroom at any
-// resolution.  The margin test |frac - 1/2| < 1/2 - mu rounds frac - 1/2 by
-// at most 3e-8 bins (exact for frac >= 1/4), far inside that headroom.
+// Error budget of the fp32 decision, in radians (a bin is theta_r or phi_r;
+// fractions of a bin scale by 1/theta_r, 1/phi_r):
+//   input rounding of x, y, z to float (|d atan2| <= relative perturbation)   0.6e-7
+//   t = min/max by rcp.approx + product (<= 2^-22 + 2^-24 relative)            3.0e-7
+//   polynomial + FFMA2 evaluation, every float t in [0, 1]
+//     (tools/fast_atan_bound.py: 3.2e-7, + 0.6e-7 for its fp64 emulation)     3.8e-7
+//   reflections: pi/2 and pi constants and roundings, the + 2 pi wrap          7.3e-7
+//   q = angle * (1/bin): float 1/bin and the product, |angle| <= 2 pi          7.5e-7
+// azimuth total 2.2e-6; the elevation replaces the wrap with
+//   sqrt.approx of the fma'd x^2 + y^2 (<= 2^-22 + 2^-23 relative)            3.6e-7
+//   phi_offset rounded to float and the subtraction, |phi_offset| <= 3.2       4.3e-7
+// elevation total 2.6e-6 rad, against a margin of FAST_MARGIN = 5e-6 rad on
+// both sides of every bin edge: 1.9x headroom at any resolution (the launch
+// takes the exact path for every point when the margin exceeds half a bin or
+// |phi_offset| > 3.2).  The margin test |frac - 1/2| < 1/2 - mu rounds frac -
+// 1/2 by at most 3e-8 bins (exact for frac >= 1/4).
 __device__ __forceinline__ bool fast_bin(float xf, float yf, float zf, bool guard, const ConvertArgs& a, int& u,
                                          int& v)
 {
@@ -638,6 +644,30 @@ __global__ void __launch_bounds__(256) convert_overflow_kernel(ConvertArgs a, co
     }
 }
 
+// exact_point for one queued point per lane, the whole warp calling (`active`
+// lanes hold a point): the frame statistics are added once per distinct
+// (frame, counter) of the warp -- consecutive queue entries mostly share a
+// frame, and per-point atomics on its few counters serialised.
+__device__ __forceinline__ void exact_point_warp(const ConvertArgs& a, bool active, double px, double py, double pz,
+                                                 int f)
+{
+    Binned o{0, 0, 0.0, false};
+    if (active) {
+        const double* xf = a.xf + 12 * f;
+        o = bin_point(px, py, pz, xf, xf + 9, a.g);
+        if (o.status == 2)
+            atomicMin(a.best + (long long)f * a.g.P + o.pix, (unsigned long long)__double_as_longlong(o.r));
+    }
+    const int lane = threadIdx.x & 31;
+    const int slot = o.status == 0 ? FS_REJECTED : o.status == 1 ? FS_DROPPED : FS_KEPT;
+    const unsigned peers = __match_any_sync(STPC_FULL, active ? f * 8 + slot : -1);
+    if (active && __ffs(peers) - 1 == lane)
+        atomicAdd((unsigned long long*)&a.fstats[(long long)f * FS_COUNT + slot], (unsigned long long)__popc(peers));
+    const unsigned ep = __match_any_sync(STPC_FULL, active && o.eps ? f : -1);
+    if (active && o.eps && __ffs(ep) - 1 == lane)
+        atomicAdd((unsigned long long*)&a.fstats[(long long)f * FS_COUNT + FS_EPS_BAND], (unsigned long long)__popc(ep));
+}
+
 // Exact fp64 path (CUDA atan2/acos + correctly rounded refinement in the eps
 // band) for the queued points.
 template <class T>
@@ -646,24 +676,40 @@ __global__ void __launch_bounds__(256) convert_exact_kernel(ConvertArgs a, const
     const unsigned long long qn = *a.q_count;
     if (qn > (unsigned long long)a.q_cap) return;  // overflow re-pass handles them
     const long long n = (long long)qn;
-    for (long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x; q < n; q += (long long)gridDim.x * blockDim.x) {
-        const long long i = a.q_idx[q];
-        const T* p = pts + 3 * i;
-        exact_point(a, (double)p[0], (double)p[1], (double)p[2], a.q_frame[q]);
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    for (long long base = (long long)blockIdx.x * blockDim.x; base < n; base += stride) {
+        const long long q = base + threadIdx.x;
+        const bool act = q < n;
+        double px = 0.0, py = 0.0, pz = 0.0;
+        int f = 0;
+        if (act) {
+            const T* p = pts + 3 * a.q_idx[q];
+            px = (double)p[0], py = (double)p[1], pz = (double)p[2];
+            f = a.q_frame[q];
+        }
+        exact_point_warp(a, act, px, py, pz, f);
     }
 }
 
-// The staged kernel's queue: CTA b's undecided points are q_idx[b * seg, + q_bcount[b]).
+// The staged kernel's queue: CTA b's undecided points are q_idx[b * seg, +
+// q_bcount[b]), spread over gridDim.y blocks per segment.
 template <class T>
 __global__ void __launch_bounds__(256) convert_exact_seg_kernel(ConvertArgs a, const T* pts, int seg)
 {
     if (*a.q_count > (unsigned long long)a.q_cap) return;  // overflow re-pass handles them
     const int n = a.q_bcount[blockIdx.x];
-    const long long base = (long long)blockIdx.x * seg;
-    for (int q = threadIdx.x; q < n; q += blockDim.x) {
-        const long long i = a.q_idx[base + q];
-        const T* p = pts + 3 * i;
-        exact_point(a, (double)p[0], (double)p[1], (double)p[2], a.q_frame[base + q]);
+    const long long off = (long long)blockIdx.x * seg;
+    for (int base = blockIdx.y * blockDim.x; base < n; base += gridDim.y * blockDim.x) {
+        const int q = base + threadIdx.x;
+        const bool act = q < n;
+        double px = 0.0, py = 0.0, pz = 0.0;
+        int f = 0;
+        if (act) {
+            const T* p = pts + 3 * a.q_idx[off + q];
+            px = (double)p[0], py = (double)p[1], pz = (double)p[2];
+            f = a.q_frame[off + q];
+        }
+        exact_point_warp(a, act, px, py, pz, f);
     }
 }
 
@@ -722,6 +768,11 @@ static void launch_regs(const ConvertArgs& a, int max_pts, cudaStream_t s)
     convert_overflow_kernel<T><<<dim3(1, a.n_frames), 256, 0, s>>>(a, (const T*)a.pts);
 }
 
+#ifndef STPC_EXACT_SPLIT
+#define STPC_EXACT_SPLIT 4
+#endif
+constexpr int EXACT_SPLIT = STPC_EXACT_SPLIT;  // blocks per queue segment
+
 template <class T>
 static void launch_staged(const ConvertArgs& a, int max_pts, cudaStream_t s)
 {
@@ -743,7 +794,7 @@ static void launch_staged(const ConvertArgs& a, int max_pts, cudaStream_t s)
     STPC_LAUNCH();
     convert_staged_kernel<T><<<grid, 32 * SC::WARPS, SC::SMEM, s>>>(a, (const T*)a.pts, (int)n_units, mc, seg);
     STPC_LAUNCH();
-    convert_exact_seg_kernel<T><<<grid, 256, 0, s>>>(a, (const T*)a.pts, seg);
+    convert_exact_seg_kernel<T><<<dim3(grid, EXACT_SPLIT), 256, 0, s>>>(a, (const T*)a.pts, seg);
     STPC_LAUNCH();
     convert_overflow_kernel<T><<<dim3(1, a.n_frames), 256, 0, s>>>(a, (const T*)a.pts);
 }
@@ -759,9 +810,9 @@ void launch_convert(const ConvertArgs& a0, int max_pts, cudaStream_t s)
     float mv = (float)FAST_MARGIN * a.inv_pr;
     // The fp32 decision is only sound where the margin is below half a bin
     // and phi_offset survives the float rounding within the error budget
-    // (2^-24 |phi_offset| << FAST_MARGIN): otherwise every point takes the
-    // exact path (a negative half-width rejects every fraction).
-    if (!(mu < 0.5f && mv < 0.5f && fabs(a.g.phi_offset) < 16.0)) mu = mv = 1.0f;
+    // (|phi_offset| <= 3.2, the error budget above): otherwise every point
+    // takes the exact path (a negative half-width rejects every fraction).
+    if (!(mu < 0.5f && mv < 0.5f && fabs(a.g.phi_offset) <= 3.2)) mu = mv = 1.0f;
     a.hu = 0.5f - mu;
     a.hv = 0.5f - mv;
     a.q_bcount = reinterpret_cast<int*>(a.q_count + 1);
