@@ -428,7 +428,10 @@ struct BitRd {
 };
 
 // One symbol; returns whether it fit (the caller derives the reference's
-// 1 / 2 status from the last `len` once, after its loop).
+// 1 / 2 status from the last `len` once, after its loop).  Branch-free apart
+// from the rare long-code search: the refill (every ~5 symbols, at different
+// steps in different lanes) is predicated, with the next word's load issued
+// under a predicate instead of a divergent branch.
 __device__ __forceinline__ bool huff_step(const HuffDev& T, BitRd& r, int& sym, int& len)
 {
     const unsigned w = (unsigned)(r.cur >> 32);
@@ -437,17 +440,29 @@ __device__ __forceinline__ bool huff_step(const HuffDev& T, BitRd& r, int& sym, 
     len = (int)(e >> 8);
     sym = (int)(e & 0xff);
     const bool fits = len != 0 && len <= r.avail - r.used;
-    if (fits) {
-        r.cur <<= len;
-        r.nb -= len;
-        r.used += len;
-        if (r.nb < 32) {
-            r.cur |= (unsigned long long)r.nxt << (32 - r.nb);
-            r.nb += 32;
-            r.nxt = r.ldw(r.wi);
-            ++r.wi;
-        }
+    const int l = fits ? len : 0;
+    r.cur <<= l;
+    r.nb -= l;
+    r.used += l;
+    const bool refill = r.nb < 32;
+    r.cur |= refill ? (unsigned long long)r.nxt << (32 - r.nb) : 0ull;
+    r.nb += refill ? 32 : 0;
+#ifndef STPC_HUFF_BRANCHY
+    unsigned nw = r.nxt;
+    const int ld = refill && r.wi <= r.wlast;
+    asm volatile(
+        "{\n .reg .pred p;\n setp.ne.s32 p, %2, 0;\n @p ld.global.nc.u32 %0, [%1];\n}"
+        : "+r"(nw)
+        : "l"(r.words + r.wi), "r"(ld));
+    nw = ld ? __byte_perm(nw, 0, 0x0123) : 0u;
+    r.nxt = refill ? nw : r.nxt;
+    r.wi += refill ? 1 : 0;
+#else
+    if (refill) {
+        r.nxt = r.ldw(r.wi);
+        ++r.wi;
     }
+#endif
     return fits;
 }
 
