@@ -2,6 +2,7 @@
 
     python tools/ncu_lines.py gpurun_out/rep.ncu-rep <kernel-regex> [launch-index] [top]
     STPC_SORT=stall_long_sb python tools/ncu_lines.py ...   # rank by one stall column
+    STPC_FUNC=fit_pair_kernelILb1 python tools/ncu_lines.py ...  # pick a template instantiation
 
 Maps the report's SASS page (addresses) to CUDA source lines through the
 line table of the in-tree library's cubins (nvdisasm -g), because the CSV
@@ -70,7 +71,11 @@ def main():
     ie = h.index("Instructions Executed")
     # STPC_SORT=<column> (e.g. stall_long_sb) ranks lines by that sample column
     smp = h.index(os.environ.get("STPC_SORT", "# Samples"))
-    fname = re.sub(r"[<(].*", "", kre)
+    # the cubin function whose line table maps the addresses: STPC_FUNC (a
+    # regex over mangled names, e.g. fit_pair_kernelILb1 for the <true>
+    # instantiation) -- a template kernel's instantiations share a base name,
+    # and the first match is not necessarily the profiled one
+    fname = os.environ.get("STPC_FUNC") or re.sub(r"[<(].*", "", kre)
     table = line_table(fname)
     base = int(data[0][0], 16)
     agg = collections.defaultdict(lambda: [0, 0])
