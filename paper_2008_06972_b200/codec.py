@@ -463,8 +463,13 @@ def compress(clouds: Sequence[np.ndarray], cfg: CodecConfig, poses=None, imu_sam
     if len(clouds) != cfg.n_frames:
         raise DataError(f"config expects {cfg.n_frames} frames, got {len(clouds)}")
     t0 = time.perf_counter()
-    ts = _transforms_for(cfg, poses, imu_samples, frame_times, v0)
-    xf = np.asarray([t.row12() for t in ts], np.float64)
+    if cfg.n_frames > 1 and poses is not None:
+        if len(poses) != cfg.n_frames:
+            raise DataError("need one pose per frame")
+        xf = poses_to_transform_rows([poses], cfg.k_index)  # batched: same bits, no per-frame objects
+    else:
+        ts = _transforms_for(cfg, poses, imu_samples, frame_times, v0)
+        xf = np.asarray([t.row12() for t in ts], np.float64)
     t1 = time.perf_counter()
     pts, off, f64, counts = _stack_points(clouds)
     if f64:
