@@ -44,6 +44,8 @@ def kernel_stage(name: str, seen: dict) -> str:
     seen[name] = n + 1
     if "convert" in name or "fill_u64" in name:
         return "convert"
+    if "emit" in name:  # before "bitmap": emit_bitmaps_kernel is part of emit
+        return "emit"
     if "bitmap" in name:
         return "bitmaps"
     if "start_tiles" in name:
