@@ -207,6 +207,18 @@ int stpc_decoder_load(stpc_decoder* dec, const uint8_t* blobs, int32_t blobs_on_
 int stpc_decoder_load_gather(stpc_decoder* dec, const uint8_t* const* blobs, const int64_t* lengths, int32_t n,
                              int32_t* status, void* stream);
 int stpc_decoder_heads(stpc_decoder* dec, int32_t head_cap, uint8_t* h_heads, int64_t* h_raw_len, void* stream);
+/* stpc_decode_transforms  host-side RigidTransform checks (motion.py:52-62:
+ *                        allclose(R.T @ R, I, atol), isclose(det R, 1)) and
+ *                        inverses (motion.py:78-79) of the float32 transforms
+ *                        of blobs rows[0..m) of a stpc_decoder_heads array
+ *                        (head_stride bytes per blob, transforms at `offset`):
+ *                        xf_inv double[m*n][12] (R^T | -R^T T), orth_state /
+ *                        det_state int8[m*n]: 0 passes, 1 fails, 2 too close to
+ *                        the tolerance or non-finite (the caller re-checks with
+ *                        the reference's numpy expressions). */
+int stpc_decode_transforms(const uint8_t* heads, int64_t head_stride, const int64_t* rows, int32_t m,
+                           int32_t n_frames, int32_t offset, double atol, double* xf_inv, int8_t* orth_state,
+                           int8_t* det_state);
 int stpc_decoder_frames(stpc_decoder* dec, const stpc_decode_geom* geom, const int32_t* sel, int32_t m,
                         const double* sin_theta, const double* cos_theta, const double* sin_phi,
                         const double* cos_phi, const double* xf_inv, int64_t* frame_counts, int64_t* status,

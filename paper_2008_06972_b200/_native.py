@@ -32,7 +32,7 @@ EXPORTS = [
     "stpc_memcpy_h2d", "stpc_host_scatter", "stpc_device_count", "stpc_last_error", "stpc_version",
     "stpc_encoder_profile", "stpc_encoder_stage_ms", "stpc_stage_name", "stpc_launch_count",
     "stpc_decoder_create", "stpc_decoder_destroy", "stpc_decoder_load", "stpc_decoder_load_gather",
-    "stpc_decoder_heads",
+    "stpc_decoder_heads", "stpc_decode_transforms",
     "stpc_decoder_frames", "stpc_decoder_total_points", "stpc_decoder_points",
     "stpc_decoder_device_points", "stpc_entropy_encode",
 ]
@@ -118,6 +118,7 @@ def load(require_device: bool = False):
                 "stpc_decoder_load": ([P, P, I32, P, I32, P, P], ctypes.c_int),
                 "stpc_decoder_load_gather": ([P, P, P, I32, P, P], ctypes.c_int),
                 "stpc_decoder_heads": ([P, I32, P, P, P], ctypes.c_int),
+                "stpc_decode_transforms": ([P, I64, P, I32, I32, I32, D, P, P, P], ctypes.c_int),
                 "stpc_decoder_frames": ([P, ctypes.POINTER(StpcDecodeGeom), P, I32, P, P, P, P, P, P, P, P, P],
                                         ctypes.c_int),
                 "stpc_decoder_total_points": ([P], I64),

@@ -123,15 +123,15 @@ def _transforms(head: bytes, raw_len: int, n: int) -> np.ndarray:
 
 def _transforms_batch(heads: np.ndarray, raw_len: np.ndarray, idxs: List[int], n: int
                       ) -> Tuple[Dict[int, np.ndarray], Dict[int, Exception]]:
-    """_transforms for many blobs with one frame count, vectorised: the
-    RigidTransform checks (motion.py:52-62: allclose(R.T @ R, I, atol=1e-6),
-    isclose(det R, 1, atol=1e-6)) on the stacked matrices, and the inverse
-    R.T | -(R.T @ T) by one batched matmul -- bit-identical to the per-frame
-    numpy expressions (R and T are float32-exact, so every product is exact
-    and numpy's K=3 sums run left to right either way; checked in
-    tests/test_host.py).  Frames whose orthonormality residual lies within
-    1e-12 of the tolerance, or hold non-finite values, are re-checked with
-    the per-frame reference expression."""
+    """_transforms for many blobs with one frame count: the RigidTransform
+    checks (motion.py:52-62: allclose(R.T @ R, I, atol=1e-6), isclose(det R,
+    1, atol=1e-6)) and the inverse R.T | -(R.T @ T), in native code
+    (stpc_decode_transforms) -- bit-identical to the per-frame numpy
+    expressions (R and T are float32-exact, so every product is exact and the
+    K=3 sums run left to right either way; checked in tests/test_host.py).
+    Frames whose orthonormality residual or determinant lies within 1e-12 /
+    1e-9 of the tolerance, or hold non-finite values, are re-checked with the
+    per-frame reference expression."""
     from .geometry import ORTHONORMAL_ATOL
 
     good: Dict[int, np.ndarray] = {}
@@ -143,37 +143,26 @@ def _transforms_batch(heads: np.ndarray, raw_len: np.ndarray, idxs: List[int], n
             errors[i] = TruncatedBlobError(f"payload ends at byte {int(raw_len[i])}, needed {end}")
     if not ok:
         return good, errors
-    blk = np.ascontiguousarray(heads[ok, _CFG.size:end]).view("<f4").astype(np.float64).reshape(len(ok), n, 12)
-    R = blk[:, :, :9].reshape(-1, 3, 3)
-    T = blk[:, :, 9:].reshape(-1, 3)
-    Rt = np.transpose(R, (0, 2, 1))
+    heads = np.ascontiguousarray(heads)
+    sel = np.asarray(ok, np.int64)
+    m = len(ok)
+    rows = np.empty((m * n, 12), np.float64)
+    ost = np.empty(m * n, np.int8)
+    dst = np.empty(m * n, np.int8)
+    _native.check(_native.load().stpc_decode_transforms(
+        heads.ctypes.data, heads.strides[0], sel.ctypes.data, m, n, _CFG.size, ORTHONORMAL_ATOL,
+        rows.ctypes.data, ost.ctypes.data, dst.ctypes.data))
+    orth = ost == 0
+    detok = dst == 0
     eye = np.eye(3)
-    with np.errstate(all="ignore"):
-        # R^T R and R^T T as explicit left-to-right K=3 sums (elementwise over
-        # the batch; the products are exact, float32 x float32)
-        M = np.empty_like(R)
-        for i in range(3):
-            for j in range(3):
-                M[:, i, j] = (R[:, 0, i] * R[:, 0, j] + R[:, 1, i] * R[:, 1, j]) + R[:, 2, i] * R[:, 2, j]
-        dev = np.abs(M - eye)
-        thr = ORTHONORMAL_ATOL + 1e-5 * eye  # allclose: atol + rtol * |b|
-        orth = np.all(dev <= thr, axis=(1, 2))
-        near = np.any(np.abs(dev - thr) < 1e-12, axis=(1, 2)) | ~np.all(np.isfinite(R), axis=(1, 2))
-        # det by cofactors (vectorised); LAPACK's np.linalg.det only where the
-        # two could disagree about the tolerance
-        det = (R[:, 0, 0] * (R[:, 1, 1] * R[:, 2, 2] - R[:, 1, 2] * R[:, 2, 1])
-               - R[:, 0, 1] * (R[:, 1, 0] * R[:, 2, 2] - R[:, 1, 2] * R[:, 2, 0])
-               + R[:, 0, 2] * (R[:, 1, 0] * R[:, 2, 1] - R[:, 1, 1] * R[:, 2, 0]))
-        dtol = ORTHONORMAL_ATOL + 1e-5
-        detok = np.abs(det - 1.0) <= dtol
-        for f in np.flatnonzero(~(np.abs(np.abs(det - 1.0) - dtol) > 1e-9) | ~np.isfinite(det)):
-            detok[f] = bool(np.abs(np.linalg.det(R[f]) - 1.0) <= dtol)
-        Tinv = np.empty_like(T)
-        for i in range(3):
-            Tinv[:, i] = -((R[:, 0, i] * T[:, 0] + R[:, 1, i] * T[:, 1]) + R[:, 2, i] * T[:, 2])
-    for f in np.flatnonzero(near):
-        orth[f] = np.allclose(R[f].T @ R[f], eye, atol=ORTHONORMAL_ATOL)
-    rows = np.concatenate([Rt.reshape(-1, 9), Tinv], axis=1).reshape(len(ok), n, 12)
+    for f in np.flatnonzero((ost == 2) | (dst == 2)):
+        R = rows[f, :9].reshape(3, 3).T  # rows hold R^T
+        with np.errstate(all="ignore"):
+            if ost[f] == 2:
+                orth[f] = np.allclose(R.T @ R, eye, atol=ORTHONORMAL_ATOL)
+            if dst[f] == 2:
+                detok[f] = bool(np.abs(np.linalg.det(R) - 1.0) <= ORTHONORMAL_ATOL + 1e-5)
+    rows = rows.reshape(m, n, 12)
     valid = (orth & detok).reshape(len(ok), n)
     allv = valid.all(axis=1)
     good.update(zip((ok[j] for j in np.flatnonzero(allv)), rows[allv]))

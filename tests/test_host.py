@@ -296,10 +296,15 @@ def test_decoder_batched_transforms_equal_per_frame_reference_expressions():
     heads[9, 57 + 48 + 36:57 + 48 + 40] = f32(np.nan)
     heads[11, 57 + 144:57 + 148] = f32(np.inf)
     heads[13, 57:57 + 36] = np.diag([1.0, 1.0, -1.0]).reshape(9).astype("<f4").view(np.uint8)
+    # scalings whose R^T R diagonal / determinant sit at the tolerances
+    # (1e-6 + 1e-5): the native check hands these to the numpy expressions
+    for row, target in ((15, 1.1e-5), (17, -1.1e-5), (19, 1.1e-5 / 3), (21, 1.2e-5)):
+        s_ = np.float32(np.sqrt(1.0 + target))
+        heads[row, 57 + 48:57 + 84] = np.diag([s_, s_, s_]).reshape(9).astype("<f4").view(np.uint8)
     raw_len = np.full(B, 10 ** 6, np.int64)
     raw_len[7] = 100
     good, bad = D._transforms_batch(heads, raw_len, list(range(B)), n)
-    assert sorted(bad) == [5, 7, 11, 13]
+    assert {5, 7, 11, 13} <= set(bad) and 21 in bad
     for i in range(B):
         try:
             ref = D._transforms(heads[i].tobytes(), int(raw_len[i]), n)
