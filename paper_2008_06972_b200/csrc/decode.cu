@@ -1395,7 +1395,16 @@ __global__ void __launch_bounds__(1024) frame_offset_kernel(const long long* fra
 // per-word work is the points alone; the inverse transform, the output base
 // and the block's first pixel coordinates are loaded once per block.
 constexpr int UP_WARPS = 8;
-__global__ void __launch_bounds__(UP_WARPS * 32) unproject_kernel(DecGeom G, Trig tg, const double* out_r,
+#ifndef STPC_UP_MINB
+#define STPC_UP_MINB 5
+#endif
+// Block per 1024 pixels of one frame; warp w owns the block's words 4w..4w+3
+// (128 consecutive pixels).  Every point of the block lands in a shared
+// staging area at its rank within the block (the block's points are
+// contiguous in the output), then the block writes its 3 x count doubles
+// with 16-byte stores.  Each lane issues the range loads of all four of its
+// words before any arithmetic.
+__global__ void __launch_bounds__(UP_WARPS * 32, STPC_UP_MINB) unproject_kernel(DecGeom G, Trig tg, const double* out_r,
                                                                   const unsigned* pmask,
                                                                   const unsigned long long* pstat,
                                                                   const long long* ovl, const int* blk_off,
@@ -1407,10 +1416,10 @@ __global__ void __launch_bounds__(UP_WARPS * 32) unproject_kernel(DecGeom G, Tri
     const int j = (int)dmod(f, G.n, G.rn, fch);
     if (pstat[j] != DEC_NONE) return;
     __shared__ unsigned s_m[32];
-    __shared__ int s_off[32];
+    __shared__ int s_off[33];
     __shared__ double s_R[12];
     __shared__ long long s_base;
-    __shared__ double stage[UP_WARPS][96];  // a warp's points, xyz interleaved, for coalesced stores
+    __shared__ __align__(16) double stage[3 * 1024 + 2];  // the block's points, xyz interleaved
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const long long W = (G.P + 31) >> 5;
     const long long pb = (long long)blockIdx.x * 1024;  // the block's first pixel
@@ -1438,16 +1447,25 @@ __global__ void __launch_bounds__(UP_WARPS * 32) unproject_kernel(DecGeom G, Tri
             if (lane >= o) x += t;
         }
         s_off[lane] = x - c;
+        if (lane == 31) s_off[32] = x;
     }
     __syncthreads();
+    const unsigned lt = (1u << lane) - 1u;
+    const double* img = out_r + f * G.P;
+    double r[4];
+    unsigned mk[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const int k = 4 * wid + i;
+        mk[i] = s_m[k];
+        r[i] = (mk[i] >> lane) & 1u ? img[pb + 32 * k + lane] : 0.0;
+    }
     long long ul;
     const int v0 = (int)dmod(pb, G.w, G.rw, ul), u0 = (int)ul;
-    const unsigned lt = (1u << lane) - 1u;
-    for (int k = wid; k < 32; k += UP_WARPS) {
-        const unsigned m = s_m[k];
-        if (!m) continue;
-        if ((m >> lane) & 1u) {
-            const long long p = pb + 32 * k + lane;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const int k = 4 * wid + i;
+        if ((mk[i] >> lane) & 1u) {
             int v, u;
             if (G.w >= 1024) {  // the block spans at most two rows
                 u = u0 + 32 * k + lane;
@@ -1458,25 +1476,30 @@ __global__ void __launch_bounds__(UP_WARPS * 32) unproject_kernel(DecGeom G, Tri
                 }
             } else {
                 long long uu;
-                v = (int)dmod(p, G.w, G.rw, uu);
+                v = (int)dmod(pb + 32 * k + lane, G.w, G.rw, uu);
                 u = (int)uu;
             }
             double dx, dy, dz;
             ray_dir(tg, v, u, dx, dy, dz);
-            const double r = out_r[f * G.P + p];
-            const double x = r * dx, y = r * dy, z = r * dz;
-            const int rank = __popc(m & lt);
-            stage[wid][3 * rank] = xform_coord(x, y, z, s_R[0], s_R[1], s_R[2], s_R[9]);
-            stage[wid][3 * rank + 1] = xform_coord(x, y, z, s_R[3], s_R[4], s_R[5], s_R[10]);
-            stage[wid][3 * rank + 2] = xform_coord(x, y, z, s_R[6], s_R[7], s_R[8], s_R[11]);
+            const double x = r[i] * dx, y = r[i] * dy, z = r[i] * dz;
+            double* o = stage + 3 * (s_off[k] + __popc(mk[i] & lt));
+            o[0] = xform_coord(x, y, z, s_R[0], s_R[1], s_R[2], s_R[9]);
+            o[1] = xform_coord(x, y, z, s_R[3], s_R[4], s_R[5], s_R[10]);
+            o[2] = xform_coord(x, y, z, s_R[6], s_R[7], s_R[8], s_R[11]);
         }
-        __syncwarp();
-        // the word's points are contiguous in the output: up to 3 x 32 doubles
-        const int nw = 3 * __popc(m);
-        double* dst = pts + 3 * (s_base + s_off[k]);
-        for (int q = lane; q < nw; q += 32) dst[q] = stage[wid][q];
-        __syncwarp();
     }
+    __syncthreads();
+    // 3 x count doubles to pts + 3 s_base: a leading double when that start is
+    // odd, then 16-byte stores
+    const int nd = 3 * s_off[32];
+    if (nd == 0) return;
+    double* dst = pts + 3 * s_base;
+    const int head = (int)((reinterpret_cast<uintptr_t>(dst) >> 3) & 1);
+    if (head && threadIdx.x == 0) dst[0] = stage[0];
+    const int n2 = (nd - head) >> 1;
+    double2* d2 = reinterpret_cast<double2*>(dst + head);
+    for (int q = threadIdx.x; q < n2; q += blockDim.x) d2[q] = make_double2(stage[head + 2 * q], stage[head + 2 * q + 1]);
+    if (((nd - head) & 1) && threadIdx.x == 0) dst[nd - 1] = stage[nd - 1];
 }
 
 }  // namespace stpc
