@@ -510,7 +510,10 @@ def main():
     backend = os.environ.get("STPC_DIST_BACKEND", "nccl")
     local = local % max(torch.cuda.device_count(), 1) if backend != "nccl" else local
     numa = None
-    if world > 1:
+    # STPC_DIST_FORCE=1: the process group (NCCL init, barriers, the size
+    # gathers, max-over-ranks) even for a single rank -- exercises the
+    # multi-rank code path on a one-GPU box
+    if world > 1 or os.environ.get("STPC_DIST_FORCE", "0") not in ("", "0"):
         import torch.distributed as dist_mod
 
         from paper_2008_06972_b200 import dist as pdist
