@@ -482,6 +482,10 @@ def ncu_stages():
 
 def main():
     args = parse()
+    if int(os.environ.get("WORLD_SIZE", "1")) > 1 or os.environ.get("STPC_DIST_FORCE", "0") not in ("", "0"):
+        # NCCL reads these when torch first touches it: before any torch import
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
