@@ -42,7 +42,9 @@ def kernel_stage(name: str, seen: dict) -> str:
     """Stage of a launch (encoder.cu encode_impl order); `seen` counts launches."""
     n = seen.get(name, 0)
     seen[name] = n + 1
-    if "convert" in name or "fill_u64" in name:
+    if "fill_u64" in name:  # the first call's +inf grid fill (steady-state calls get it from the previous pack)
+        return "other"
+    if "convert" in name:
         return "convert"
     if "emit" in name:  # before "bitmap": emit_bitmaps_kernel is part of emit
         return "emit"
