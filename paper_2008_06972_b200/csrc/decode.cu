@@ -49,6 +49,10 @@ struct DecGeom {
     long long runs_off;  // bits_off + n nb: temporal run count
     double quant, r_max;
     double rw, rtw, rth, rn;  // fl(1 / w), 1 / tw, 1 / th, 1 / n for dmod
+    // x / tw and x / th as __umulhi(x, m) (exact for x, divisor < 2^16:
+    // m = ceil(2^32 / d) overshoots by less than d per unit, so x (m d - 2^32)
+    // < 2^32); 0 when the geometry is too large (dmod then)
+    unsigned mtw, mth;
 };
 
 // q, r = p / d, p % d for 0 <= p < 2^50 through the double reciprocal rd =
@@ -1130,8 +1134,15 @@ __global__ void __launch_bounds__(RC_WARPS * 32) reconstruct_kernel(DecGeom G, T
                 v = (int)dmod(p, G.w, G.rw, uu);
                 u = (int)uu;
             }
-            long long rv, ru;
-            const long long tv = dmod(v, G.th, G.rth, rv), tu = dmod(u, G.tw, G.rtw, ru);
+            long long tv, tu;
+            if (G.mtw) {
+                tv = __umulhi((unsigned)v, G.mth);
+                tu = __umulhi((unsigned)u, G.mtw);
+            } else {
+                long long rv, ru;
+                tv = dmod(v, G.th, G.rth, rv);
+                tu = dmod(u, G.tw, G.rtw, ru);
+            }
             const float4 pl = tm[tv * G.tx + tu];
             if (pl.w != 0.0f) {
                 double dx, dy, dz;
@@ -1884,6 +1895,9 @@ int stpc_decoder_frames(stpc_decoder* d, const stpc_decode_geom* g, const int32_
     G.rtw = 1.0 / G.tw;
     G.rth = 1.0 / G.th;
     G.rn = 1.0 / G.n;
+    const bool small = G.w < 65536 && G.h < 65536 && G.tw < 65536 && G.th < 65536;
+    G.mtw = small ? (unsigned)((0x100000000ull + G.tw - 1) / G.tw) : 0u;
+    G.mth = small ? (unsigned)((0x100000000ull + G.th - 1) / G.th) : 0u;
     d->m = m;
     d->F = (long long)m * G.n;
     d->bpf = (G.P + 1023) / 1024;
