@@ -1296,9 +1296,14 @@ __global__ void __launch_bounds__(PK_THREADS) residual_kernel(DecGeom G, const u
             ++nv;
             dsum += (long long)v;
         }
-        long long t_idx, t_flat, t_esc;
-        const long long b_idx = c_idx + block_excl_scan<PK_THREADS>(nv, t_idx);
-        const long long b_flat = c_flat + block_excl_scan<PK_THREADS>(dsum, t_flat);
+        // value count and delta sum in one scan: nv sums to at most 4 *
+        // PK_THREADS < 2^11 per chunk, so it never carries into the sum
+        long long t_idx, t_flat, t_esc, t_pk;
+        const long long b_pk = block_excl_scan<PK_THREADS>((dsum << 11) | nv, t_pk);
+        const long long b_idx = c_idx + (b_pk & 2047);
+        const long long b_flat = c_flat + (b_pk >> 11);
+        t_idx = t_pk & 2047;
+        t_flat = t_pk >> 11;
         // escape flags need the value index, so count them after the index scan
         {
             long long vi = b_idx;
