@@ -51,7 +51,7 @@ struct DecGeom {
     double rw, rtw, rth, rn;  // fl(1 / w), 1 / tw, 1 / th, 1 / n for dmod
     // x / tw and x / th as __umulhi(x, m) (exact for x, divisor < 2^16:
     // m = ceil(2^32 / d) overshoots by less than d per unit, so x (m d - 2^32)
-    // < 2^32); 0 when the geometry is too large (dmod then)
+    // < 2^32); both 0 when the geometry is too large or a divisor is 1 (dmod)
     unsigned mtw, mth;
 };
 
@@ -1900,7 +1900,8 @@ int stpc_decoder_frames(stpc_decoder* d, const stpc_decode_geom* g, const int32_
     G.rtw = 1.0 / G.tw;
     G.rth = 1.0 / G.th;
     G.rn = 1.0 / G.n;
-    const bool small = G.w < 65536 && G.h < 65536 && G.tw < 65536 && G.th < 65536;
+    // (a divisor of 1 would need m = 2^32: those geometries keep dmod)
+    const bool small = G.w < 65536 && G.h < 65536 && G.tw < 65536 && G.th < 65536 && G.tw > 1 && G.th > 1;
     G.mtw = small ? (unsigned)((0x100000000ull + G.tw - 1) / G.tw) : 0u;
     G.mth = small ? (unsigned)((0x100000000ull + G.th - 1) / G.th) : 0u;
     d->m = m;

@@ -144,15 +144,9 @@ __global__ void __launch_bounds__(256, STPC_ROWSTATS_MINB) rowstats_kernel(PlanA
         prev = max(prev, last);
         int len = 0;
         if (res) len = (__popc(res) - 1) + (prev >= 0 ? varint_len((uint32_t)(wfirst - prev)) : 0);
-        int c = __popc(res), e = __popc(esc), t1 = __popc(tmp), f2 = __popc(fb);
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-            len += __shfl_xor_sync(STPC_FULL, len, o);
-            c += __shfl_xor_sync(STPC_FULL, c, o);
-            e += __shfl_xor_sync(STPC_FULL, e, o);
-            t1 += __shfl_xor_sync(STPC_FULL, t1, o);
-            f2 += __shfl_xor_sync(STPC_FULL, f2, o);
-        }
+        len = __reduce_add_sync(STPC_FULL, len);
+        const int c = __reduce_add_sync(STPC_FULL, __popc(res)), e = __reduce_add_sync(STPC_FULL, __popc(esc));
+        const int t1 = __reduce_add_sync(STPC_FULL, __popc(tmp)), f2 = __reduce_add_sync(STPC_FULL, __popc(fb));
         // batch first/last
         const unsigned nz = __ballot_sync(STPC_FULL, res != 0);
         if (nz) {
