@@ -777,12 +777,17 @@ template <class T>
 static void launch_staged(const ConvertArgs& a, int max_pts, cudaStream_t s)
 {
     using SC = Staged<T>;
-    static int grid_max = 0;  // CTAs resident on the device (persistent grid)
+    // CTAs resident per device (persistent grid); the dynamic shared-memory
+    // opt-in is a per-device function attribute
+    constexpr int MAX_DEV = 64;
+    static int grid_max_dev[MAX_DEV] = {};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    int& grid_max = grid_max_dev[dev < MAX_DEV ? dev : MAX_DEV - 1];
     if (!grid_max) {
         cudaFuncSetAttribute(convert_staged_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, SC::SMEM);
-        int per_sm = 0, dev = 0, sms = 0;
+        int per_sm = 0, sms = 0;
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, convert_staged_kernel<T>, 32 * SC::WARPS, SC::SMEM);
-        cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
         grid_max = std::max(1, std::min(per_sm * sms, CONVERT_MAX_GRID));
     }
