@@ -5,7 +5,8 @@ For BASELINE configs[0], [1], [2] (one sweep point) and [4]: one seeded group,
 ``compress(clouds, cfg, poses=...)`` -- host numpy clouds in, ``bytes`` out,
 exactly the reference's call (pkg/tests/test_acceptance.py:171-194 times the
 same call) -- and the single-core oracle port's per-call time on the same
-input.  Also ``compress_groups`` on the configs[3] 1024-group batch (pageable
+input; likewise ``decompress(blob)`` (bytes in, float64 numpy clouds out)
+beside the oracle decoder.  Also ``compress_groups`` on the configs[3] 1024-group batch (pageable
 numpy in, ``bytes`` out).
 
     python tools/latency_table.py [--calls 20] [--out profiles/r2_latency.json]
@@ -26,8 +27,9 @@ sys.path.insert(0, ROOT)
 import numpy as np  # noqa: E402
 
 import bench  # noqa: E402
+from oracle import decode as odec  # noqa: E402
 from oracle import oracle  # noqa: E402
-from paper_2008_06972_b200 import compress, compress_groups, synth  # noqa: E402
+from paper_2008_06972_b200 import compress, compress_groups, decompress, synth  # noqa: E402
 
 
 def timed(fn, calls):
@@ -64,6 +66,13 @@ def main():
                "oracle_port_ms_1core": round(statistics.median(oms), 1),
                "speedup_vs_port": round(statistics.median(oms) / statistics.median(ms), 1),
                "identical": call()[0] == ref_blob, "calls": a.calls}
+        for _ in range(3):
+            decompress(ref_blob)
+        dms = timed(lambda: decompress(ref_blob), a.calls)
+        odms = timed(lambda: odec.decompress(ref_blob), 3)
+        row.update({"decompress_ms_median": round(statistics.median(dms), 3),
+                    "oracle_decoder_ms_1core": round(statistics.median(odms), 1),
+                    "decompress_speedup_vs_port": round(statistics.median(odms) / statistics.median(dms), 1)})
         rows.append(row)
         print(json.dumps(row), flush=True)
     # the batch form through the public API
