@@ -756,7 +756,7 @@ __device__ __forceinline__ unsigned group_max(unsigned v, int sub, unsigned neut
 // `has`: the lane holds a valid pixel (r, direction) of the tile.
 __device__ __forceinline__ bool test_px_pair(bool active, bool has, double r, double dx, double dy, double dz,
                                              const Chain& ch, int tile, double a, double b, double c,
-                                             double tau, double r_max)
+                                             double tau, double r_max, float4* stage = nullptr)
 {
     const int lane = threadIdx.x & 31;
     const int sub = lane >> 4, gl = lane & 15;
@@ -798,7 +798,7 @@ __device__ __forceinline__ bool test_px_pair(bool active, bool has, double r, do
     kz1 = group_max(kz1, sub, NEUT_MAX);
     const bool pass = active && !fail;
     if (pass && gl == 0) {
-        float4* ce = ch.cert + CERT_F4 * tile;
+        float4* ce = stage ? stage : ch.cert + CERT_F4 * tile;
         // a tile whose pixels are all invalid certifies as empty (no neutral
         // keys leak into the float fields)
         const float xf = ux == NEUT_MIN ? CERT_EMPTY : __uint_as_float(ux);
@@ -898,6 +898,7 @@ template <bool F44>
 __global__ void __launch_bounds__(FIT_WARPS * 32, pair_minb<F44>()) fit_pair_kernel(FitArgs A)
 {
     __shared__ double smem[FIT_WARPS][2][PG * 9];
+    __shared__ float4 cstage[FIT_WARPS][2][CERT_F4];  // the growth tile's certificate until the union verdict
     const Geometry& g = A.g;
     const int lane = threadIdx.x & 31;
     const int wib = threadIdx.x >> 5;
@@ -973,10 +974,26 @@ __global__ void __launch_bounds__(FIT_WARPS * 32, pair_minb<F44>()) fit_pair_ker
         if (gl == 0) nc = (long long)atomicAdd(A.chain_counter, 1u);
         take_chain(__shfl_sync(STPC_FULL, nc, sub * 16));
     }
+    // record run [s, e) with the current plane; class its tiles (pass 2 keeps
+    // the temporally covered ones)
+    auto emit_run = [&](int e_) {
+        if (gl == 0) {
+            A.run_s[slot * g.tx + n_runs] = (uint16_t)s;
+            A.run_len[slot * g.tx + n_runs] = (uint16_t)(e_ - s);
+            float* rabc = A.run_abc + (slot * g.tx + n_runs) * 3;
+            rabc[0] = (float)a;
+            rabc[1] = (float)b;
+            rabc[2] = (float)c;
+        }
+        for (int tt = s + gl; tt < e_; tt += PG)
+            if (!(ch.skip1 && CROW[tt] == 1)) CROW[tt] = run_cls;
+        n_runs += 1;
+    };
 
     while (__any_sync(STPC_FULL, !finished)) {
         // ---- (1) chains between runs jump to their next start tile
         const bool scan = !done && !grow;
+        bool jumped = false;
         {
             bool found = false;
             int nt = g.tx;
@@ -996,7 +1013,82 @@ __global__ void __launch_bounds__(FIT_WARPS * 32, pair_minb<F44>()) fit_pair_ker
             if (scan) {
                 if (found) t = nt;
                 else done = true;
+                jumped = found;
             }
+        }
+        // ---- (1a) start: the start verdict already fixed the start tile's
+        // plane (its certificate's a, b, c are the f32-rounded solve), so the
+        // chain only folds the tile from zero here and goes on, in this same
+        // iteration, to grow into the next tile (a start needs no solve or
+        // test of its own; a start iteration of its own was ~21% of the steps)
+        if (jumped) {
+            const float4 c0 = CERT[CERT_F4 * t];
+            a = c0.x;
+            b = c0.y;
+            c = c0.z;
+            s = t;
+            grow = true;
+            t += 1;
+            if (t >= g.tx) {  // a one-tile run at the row end
+                emit_run(g.tx);
+                grow = false;
+                done = true;
+                jumped = false;
+            }
+        }
+        FIT_STAT(1, jumped && gl == 0);  // start steps (taken with the next growth step)
+        if (__any_sync(STPC_FULL, jumped)) {
+            double x = 0.0, y = 0.0, z = 0.0, one = 0.0;
+            int dv, du;
+            if (jumped) {
+                acc = 0.0;
+                const int su0 = s * g.tw;
+                double r = __longlong_as_double(0x7ff0000000000000ll);
+                const bool hs = tile_px<F44>(ch, g, su0, gl, dv, du);
+                if (hs) {
+                    if (pf_t == s) {
+                        cp_async_wait_all();
+                        r = pf_s;
+                    } else {
+                        r = ch.img[(long long)(ch.v0 + dv) * g.w + su0 + du];
+                    }
+                }
+                // prefetch tile t's pixel for the growth fold below
+                const int nu0 = t * g.tw;
+                int pv, pu;
+                cp_async_wait_all();
+                if (tile_px<F44>(ch, g, nu0, gl, pv, pu)) {
+                    cp_async8(&pf_s, ch.img + (long long)(ch.v0 + pv) * g.w + nu0 + pu);
+                } else {
+                    pf_s = __longlong_as_double(0x7ff0000000000000ll);
+                }
+                cp_async_commit();
+                pf_t = t;
+                if (hs && isfinite(r)) {
+                    double dx, dy, dz;
+                    ray_dir(A.tg, ch.v0 + dv, su0 + du, dx, dy, dz);
+                    x = r * dx;
+                    y = r * dy;
+                    z = r * dz;
+                    one = 1.0;
+                }
+            }
+            double* row = sm + gl * 9;
+            row[0] = y * y;
+            row[1] = y * z;
+            row[2] = z * z;
+            row[3] = y;
+            row[4] = z;
+            row[5] = x * y;
+            row[6] = x * z;
+            row[7] = x;
+            row[8] = one;
+            __syncwarp();
+            if (jumped) {
+#pragma unroll
+                for (int j = 0; j < PG; ++j) acc += sm[j * 9 + kk];  // zeros beyond npx: exact
+            }
+            __syncwarp();
         }
         // ---- (1b) pass 2: a growing run extends over temporally covered
         // (class-1, fully masked) tiles without changing its sums, plane or
@@ -1021,17 +1113,7 @@ __global__ void __launch_bounds__(FIT_WARPS * 32, pair_minb<F44>()) fit_pair_ker
                     CERT[CERT_F4 * tt] = make_float4(0.f, 0.f, 0.f, CERT_EMPTY);
                 t = nt;
                 if (t >= g.tx) {  // the run reaches the row end
-                    if (gl == 0) {
-                        A.run_s[slot * g.tx + n_runs] = (uint16_t)s;
-                        A.run_len[slot * g.tx + n_runs] = (uint16_t)(g.tx - s);
-                        float* rabc = A.run_abc + (slot * g.tx + n_runs) * 3;
-                        rabc[0] = (float)a;
-                        rabc[1] = (float)b;
-                        rabc[2] = (float)c;
-                    }
-                    for (int tt = s + gl; tt < g.tx; tt += PG)
-                        if (CROW[tt] != 1) CROW[tt] = run_cls;
-                    n_runs += 1;
+                    emit_run(g.tx);
                     grow = false;
                     done = true;
                 }
@@ -1103,7 +1185,6 @@ __global__ void __launch_bounds__(FIT_WARPS * 32, pair_minb<F44>()) fit_pair_ker
         }
         // ---- (3) solve: starts (verdict known ok) and growing chains with new pixels
         FIT_STAT(0, live && gl == 0);                      // chain steps
-        FIT_STAT(1, live && !grow && gl == 0);             // start steps
         FIT_STAT(2, live && grow && cnt == 0 && gl == 0);  // empty growth steps
         const bool need = live && (!grow || cnt > 0);
         double na = 0.0, nb = 0.0, nc = 0.0;
@@ -1127,8 +1208,11 @@ __global__ void __launch_bounds__(FIT_WARPS * 32, pair_minb<F44>()) fit_pair_ker
             // tile's verdict: its loads and checks are issued before the pixel
             // test so the two latency chains overlap
             const bool weak0 = testing && s + gl < t && !cert_holds_bf(ch.cert, s + gl, na, nb, nc, A.r_max);
+            // the new tile's certificate is staged and stored only if the
+            // whole union passes: a failed growth leaves tile t's start
+            // certificate (whose plane (1a) takes as the start plane) intact
             pass = test_px_pair(testing, testing && one != 0.0, row[0], row[1], row[2], row[3], ch, t, na, nb, nc,
-                                A.tau, A.r_max);
+                                A.tau, A.r_max, cstage[wib][sub]);
             FIT_STAT(5, testing && gl == 0);        // growth tests
             FIT_STAT(6, testing && pass && gl == 0);  // growth tests passed (new tile)
             int base = s;
@@ -1149,16 +1233,13 @@ __global__ void __launch_bounds__(FIT_WARPS * 32, pair_minb<F44>()) fit_pair_ker
                 }
                 base += PG;
             }
+            __syncwarp();
+            if (pass && gl < CERT_F4) CERT[CERT_F4 * t + gl] = cstage[wib][sub][gl];
         }
         // ---- (5) state update (uniform within each chain's 16 lanes)
-        if (!done) {
+        if (!done) {  // every live chain is growing here (starts are taken in (1a))
             int emit_e = -1;
-            if (!grow) {
-                s = t;
-                a = na; b = nb; c = nc;
-                grow = true;
-                t += 1;
-            } else if (cnt == 0) {
+            if (cnt == 0) {
                 if (gl == 0) CERT[CERT_F4 * t] = make_float4(0.f, 0.f, 0.f, CERT_EMPTY);
                 t += 1;
             } else if (pass) {
@@ -1175,19 +1256,7 @@ __global__ void __launch_bounds__(FIT_WARPS * 32, pair_minb<F44>()) fit_pair_ker
                 }
                 done = true;
             }
-            if (emit_e >= 0) {
-                if (gl == 0) {
-                    A.run_s[slot * g.tx + n_runs] = (uint16_t)s;
-                    A.run_len[slot * g.tx + n_runs] = (uint16_t)(emit_e - s);
-                    float* rabc = A.run_abc + (slot * g.tx + n_runs) * 3;
-                    rabc[0] = (float)a;
-                    rabc[1] = (float)b;
-                    rabc[2] = (float)c;
-                }
-                for (int tt = s + gl; tt < emit_e; tt += PG)
-                    if (!(ch.skip1 && CROW[tt] == 1)) CROW[tt] = run_cls;
-                n_runs += 1;
-            }
+            if (emit_e >= 0) emit_run(emit_e);
         }
         // ---- (6) hand-over: a finished chain records its run count and its
         // half-warp steals the next chain
