@@ -130,7 +130,7 @@ struct stpc_encoder {
     cudaEvent_t ev_fill[2] = {};
     DevBuf vbits, ebits, cls, fstats;
     // chain level
-    DevBuf cert, start_ok, chain_counter;
+    DevBuf cert, start_ok, start_sums, chain_counter;
     DevBuf run_s, run_len, run_abc, n_runs, ref_ok, ref_c, chain_tbytes, chain_off;
     // plan
     DevBuf rowstat, rowoff, res_cnt, res_vb, res_esc, fb_rows, sec, payload_len, payload_off;
@@ -375,6 +375,8 @@ static int encode_impl(stpc_encoder* e, int G, const void* d_points, const int64
     ENS(e->n_runs, sizeof(int) * F * g.ty);
     ENS(e->cert, sizeof(float4) * 3 * F * TT);
     ENS(e->start_ok, (size_t)F * TT);
+    const bool keep_sums = g.tw * g.th <= 16;  // the pair chains take a start's sums from its verdict
+    if (keep_sums) ENS(e->start_sums, sizeof(double) * 9 * F * TT);
     ENS(e->chain_counter, 64);
     ENS(e->ref_ok, (size_t)G * TT * n);
     ENS(e->ref_c, sizeof(float) * G * TT * n);
@@ -453,6 +455,8 @@ static int encode_impl(stpc_encoder* e, int G, const void* d_points, const int64
     fa.n_runs = e->n_runs.as<int>();
     fa.cert = e->cert.as<float4>();
     fa.start_ok = e->start_ok.as<uint8_t>();
+    fa.start_sums = g.tw * g.th <= 16 ? e->start_sums.as<double>() : nullptr;
+    fa.sums_stride = F * TT;
     fa.chain_counter = e->chain_counter.as<unsigned>();
     RefitArgs ra;
     ra.best = best.as<double>();

@@ -398,6 +398,12 @@ __global__ void __launch_bounds__(START_TPB, STPC_STAGED_MINB) start_tiles_stage
             sm[6] += x * z; sm[7] += x;     sm[8] += valid ? 1.0 : 0.0;
         }
     }
+    // the chain's start step takes these sums instead of re-folding the tile
+    // (stored for every tile with enough points; read only where the verdict passes)
+    if (A.start_sums && sm[8] >= 3.0) {
+#pragma unroll
+        for (int k = 0; k < 9; ++k) A.start_sums[k * A.sums_stride + slot * g.tx + t] = sm[k];
+    }
     double a, b, c;
     bool ok = sm[8] >= 3.0 && plane_from_sums(sm, A.cond_limit, a, b, c);
     double m = 1e300, dmin = 1e300, rmin = 1e300, rmax = 0.0;
@@ -514,6 +520,12 @@ __global__ void __launch_bounds__(256, STPC_START_MINB) start_tiles_kernel(FitAr
             sm[3] += y;     sm[4] += z;     sm[5] += x * y;
             sm[6] += x * z; sm[7] += x;     sm[8] += 1.0;
         }
+    }
+    // the chain's start step takes these sums instead of re-folding the tile
+    // (stored for every tile with enough points; read only where the verdict passes)
+    if (A.start_sums && sm[8] >= 3.0) {
+#pragma unroll
+        for (int k = 0; k < 9; ++k) A.start_sums[k * A.sums_stride + slot * g.tx + t] = sm[k];
     }
     double a, b, c;
     bool ok = sm[8] >= 3.0 && plane_from_sums(sm, A.cond_limit, a, b, c);
@@ -1016,11 +1028,12 @@ __global__ void __launch_bounds__(FIT_WARPS * 32, pair_minb<F44>()) fit_pair_ker
                 jumped = found;
             }
         }
-        // ---- (1a) start: the start verdict already fixed the start tile's
-        // plane (its certificate's a, b, c are the f32-rounded solve), so the
-        // chain only folds the tile from zero here and goes on, in this same
-        // iteration, to grow into the next tile (a start needs no solve or
-        // test of its own; a start iteration of its own was ~21% of the steps)
+        // ---- (1a) start: the start verdict already folded the start tile from
+        // zero (its sums) and fixed its plane (its certificate's a, b, c are
+        // the f32-rounded solve), so the chain takes both and goes on, in
+        // this same iteration, to grow into the next tile (a start needs no
+        // fold, solve or test of its own; a start iteration of its own was
+        // ~21% of the steps)
         if (jumped) {
             const float4 c0 = CERT[CERT_F4 * t];
             a = c0.x;
@@ -1037,58 +1050,20 @@ __global__ void __launch_bounds__(FIT_WARPS * 32, pair_minb<F44>()) fit_pair_ker
             }
         }
         FIT_STAT(1, jumped && gl == 0);  // start steps (taken with the next growth step)
-        if (__any_sync(STPC_FULL, jumped)) {
-            double x = 0.0, y = 0.0, z = 0.0, one = 0.0;
-            int dv, du;
-            if (jumped) {
-                acc = 0.0;
-                const int su0 = s * g.tw;
-                double r = __longlong_as_double(0x7ff0000000000000ll);
-                const bool hs = tile_px<F44>(ch, g, su0, gl, dv, du);
-                if (hs) {
-                    if (pf_t == s) {
-                        cp_async_wait_all();
-                        r = pf_s;
-                    } else {
-                        r = ch.img[(long long)(ch.v0 + dv) * g.w + su0 + du];
-                    }
-                }
-                // prefetch tile t's pixel for the growth fold below
-                const int nu0 = t * g.tw;
-                int pv, pu;
-                cp_async_wait_all();
-                if (tile_px<F44>(ch, g, nu0, gl, pv, pu)) {
-                    cp_async8(&pf_s, ch.img + (long long)(ch.v0 + pv) * g.w + nu0 + pu);
-                } else {
-                    pf_s = __longlong_as_double(0x7ff0000000000000ll);
-                }
-                cp_async_commit();
-                pf_t = t;
-                if (hs && isfinite(r)) {
-                    double dx, dy, dz;
-                    ray_dir(A.tg, ch.v0 + dv, su0 + du, dx, dy, dz);
-                    x = r * dx;
-                    y = r * dy;
-                    z = r * dz;
-                    one = 1.0;
-                }
+        if (jumped) {
+            // the start tile's sums, folded from zero by the start verdict
+            acc = A.start_sums[kk * A.sums_stride + slot * g.tx + s];
+            // prefetch tile t's pixel for the growth fold below
+            const int nu0 = t * g.tw;
+            int pv, pu;
+            cp_async_wait_all();
+            if (tile_px<F44>(ch, g, nu0, gl, pv, pu)) {
+                cp_async8(&pf_s, ch.img + (long long)(ch.v0 + pv) * g.w + nu0 + pu);
+            } else {
+                pf_s = __longlong_as_double(0x7ff0000000000000ll);
             }
-            double* row = sm + gl * 9;
-            row[0] = y * y;
-            row[1] = y * z;
-            row[2] = z * z;
-            row[3] = y;
-            row[4] = z;
-            row[5] = x * y;
-            row[6] = x * z;
-            row[7] = x;
-            row[8] = one;
-            __syncwarp();
-            if (jumped) {
-#pragma unroll
-                for (int j = 0; j < PG; ++j) acc += sm[j * 9 + kk];  // zeros beyond npx: exact
-            }
-            __syncwarp();
+            cp_async_commit();
+            pf_t = t;
         }
         // ---- (1b) pass 2: a growing run extends over temporally covered
         // (class-1, fully masked) tiles without changing its sums, plane or

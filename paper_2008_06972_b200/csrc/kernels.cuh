@@ -90,6 +90,8 @@ struct FitArgs {
     int* n_runs;
     float4* cert;       // [F*TY][TX][3] per-tile test certificates (scratch)
     uint8_t* start_ok;  // [F*TY][TX] start verdicts (scratch)
+    double* start_sums;  // [9][F*TY*TX] a passing start tile's moment sums (scratch; null: not kept)
+    long long sums_stride;  // F*TY*TX
     unsigned* chain_counter;  // work-stealing counter (scratch)
 };
 void launch_fit_rows(const FitArgs& a, cudaStream_t s);  // = start_tiles + fit_chains
