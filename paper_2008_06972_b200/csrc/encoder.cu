@@ -335,6 +335,8 @@ static int encode_impl(stpc_encoder* e, int G, const void* d_points, const int64
     const int n = e->n, k = e->k;
     const long long F = (long long)G * n;
     const long long TT = (long long)g.tx * g.ty;
+    // the chain kernels index a batch's tiles with 32-bit offsets
+    if (F * TT >= (1LL << 32)) return STPC_ERR_ARG;
     e->mark(ST_INIT, s);
     // --- inputs (offsets + transforms through pinned staging)
     long long max_pts = 0;

@@ -854,7 +854,7 @@ __device__ bool test_tile_pair(bool active, const Chain& ch, const Geometry& g, 
         int dv, du;
         if (tile_px<F44>(ch, g, u0, gl, dv, du)) {
             const int v = ch.v0 + dv, u = u0 + du;
-            r = ch.img[(long long)v * g.w + u];
+            r = ch.img[v * g.w + u];
             if (isfinite(r)) {
                 ray_dir(tg, v, u, dx, dy, dz);
                 has = true;
@@ -929,7 +929,7 @@ __global__ void __launch_bounds__(FIT_WARPS * 32, pair_minb<F44>()) fit_pair_ker
     // per-chain arrays are addressed from `slot` on use.
     bool finished = false;  // no chains left for this half
     bool done = true;       // current chain complete
-    long long slot = 0;     // frame * ty + tile-row
+    unsigned sb = 0;        // (frame * ty + tile-row) * tx: the chain's first tile (32-bit: host-checked)
     Chain ch;
     ch.skip1 = A.mode != 0;
     int t = 0, s = 0, n_runs = 0;
@@ -946,9 +946,9 @@ __global__ void __launch_bounds__(FIT_WARPS * 32, pair_minb<F44>()) fit_pair_ker
 #define SOK sokp
 #define CERT certp
 #else
-#define CROW (A.cls + slot * g.tx)
-#define SOK (A.start_ok + slot * g.tx)
-#define CERT (A.cert + slot * g.tx * CERT_F4)
+#define CROW (A.cls + sb)
+#define SOK (A.start_ok + sb)
+#define CERT (A.cert + (size_t)sb * CERT_F4)
 #endif
     auto take_chain = [&](long long cid) {
         if (cid >= n_chains) {
@@ -966,11 +966,12 @@ __global__ void __launch_bounds__(FIT_WARPS * 32, pair_minb<F44>()) fit_pair_ker
             int grp = job / np, i = job % np;
             frame = grp * A.n_frames_group + (i < A.k ? i : i + 1);
         }
-        slot = (long long)frame * g.ty + tr;
+        const long long slot = (long long)frame * g.ty + tr;
+        sb = (unsigned)(slot * g.tx);
 #ifdef STPC_PAIR_PTRS
-        crowp = A.cls + slot * g.tx;
-        sokp = A.start_ok + slot * g.tx;
-        certp = A.cert + slot * g.tx * CERT_F4;
+        crowp = A.cls + sb;
+        sokp = A.start_ok + sb;
+        certp = A.cert + (size_t)sb * CERT_F4;
 #endif
         ch.img = A.best + (long long)frame * g.P;
         ch.v0 = tr * g.th;
@@ -992,9 +993,9 @@ __global__ void __launch_bounds__(FIT_WARPS * 32, pair_minb<F44>()) fit_pair_ker
     // the temporally covered ones)
     auto emit_run = [&](int e_) {
         if (gl == 0) {
-            A.run_s[slot * g.tx + n_runs] = (uint16_t)s;
-            A.run_len[slot * g.tx + n_runs] = (uint16_t)(e_ - s);
-            float* rabc = A.run_abc + (slot * g.tx + n_runs) * 3;
+            A.run_s[sb + n_runs] = (uint16_t)s;
+            A.run_len[sb + n_runs] = (uint16_t)(e_ - s);
+            float* rabc = A.run_abc + (size_t)(sb + n_runs) * 3;
             rabc[0] = (float)a;
             rabc[1] = (float)b;
             rabc[2] = (float)c;
@@ -1054,13 +1055,13 @@ __global__ void __launch_bounds__(FIT_WARPS * 32, pair_minb<F44>()) fit_pair_ker
         FIT_STAT(1, jumped && gl == 0);  // start steps (taken with the next growth step)
         if (jumped) {
             // the start tile's sums, folded from zero by the start verdict
-            acc = A.start_sums[kk * A.sums_stride + slot * g.tx + s];
+            acc = A.start_sums[kk * A.sums_stride + sb + s];
             // prefetch tile t's pixel for the growth fold below
             const int nu0 = t * g.tw;
             int pv, pu;
             cp_async_wait_all();
             if (tile_px<F44>(ch, g, nu0, gl, pv, pu)) {
-                cp_async8(&pf_s, ch.img + (long long)(ch.v0 + pv) * g.w + nu0 + pu);
+                cp_async8(&pf_s, ch.img + ((ch.v0 + pv) * g.w + nu0 + pu));
             } else {
                 pf_s = __longlong_as_double(0x7ff0000000000000ll);
             }
@@ -1077,7 +1078,7 @@ __global__ void __launch_bounds__(FIT_WARPS * 32, pair_minb<F44>()) fit_pair_ker
                 cp_async_wait_all();
                 r = pf_s;
             } else {
-                r = ch.img[(long long)(ch.v0 + dv) * g.w + t * g.tw + du];
+                r = ch.img[(ch.v0 + dv) * g.w + t * g.tw + du];
             }
         }
         int cnt = __popc(__ballot_sync(STPC_FULL, isfinite(r)) & gmask);
@@ -1113,7 +1114,7 @@ __global__ void __launch_bounds__(FIT_WARPS * 32, pair_minb<F44>()) fit_pair_ker
                     done = true;
                     live = false;
                 } else if (tile_px<F44>(ch, g, t * g.tw, gl, dv, du)) {
-                    r = ch.img[(long long)(ch.v0 + dv) * g.w + t * g.tw + du];
+                    r = ch.img[(ch.v0 + dv) * g.w + t * g.tw + du];
                 }
             }
             cnt = __popc(__ballot_sync(STPC_FULL, isfinite(r)) & gmask);
@@ -1158,7 +1159,7 @@ __global__ void __launch_bounds__(FIT_WARPS * 32, pair_minb<F44>()) fit_pair_ker
             const int nu0 = (t + 1) * g.tw;
             cp_async_wait_all();  // an unconsumed earlier copy into the slot has landed
             if (tile_px<F44>(ch, g, nu0, gl, dv, du)) {
-                cp_async8(&pf_s, ch.img + (long long)(ch.v0 + dv) * g.w + nu0 + du);
+                cp_async8(&pf_s, ch.img + ((ch.v0 + dv) * g.w + nu0 + du));
             } else {
                 pf_s = __longlong_as_double(0x7ff0000000000000ll);
             }
@@ -1243,7 +1244,7 @@ __global__ void __launch_bounds__(FIT_WARPS * 32, pair_minb<F44>()) fit_pair_ker
         // ---- (6) hand-over: a finished chain records its run count and its
         // half-warp steals the next chain
         const bool handover = done && !finished;
-        if (handover && gl == 0) A.n_runs[slot] = n_runs;
+        if (handover && gl == 0) A.n_runs[sb / g.tx] = n_runs;
         if (__any_sync(STPC_FULL, handover)) {
             long long nc = 0;
             if (handover && gl == 0) nc = (long long)atomicAdd(A.chain_counter, 1u);
