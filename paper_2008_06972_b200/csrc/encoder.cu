@@ -337,6 +337,8 @@ static int encode_impl(stpc_encoder* e, int G, const void* d_points, const int64
     const long long TT = (long long)g.tx * g.ty;
     // the chain kernels index a batch's tiles with 32-bit offsets
     if (F * TT >= (1LL << 32)) return STPC_ERR_ARG;
+    // the refit indexes the pixels of one group's frames with 32-bit offsets
+    if ((long long)n * g.P >= (1LL << 31)) return STPC_ERR_ARG;
     e->mark(ST_INIT, s);
     // --- inputs (offsets + transforms through pinned staging)
     long long max_pts = 0;

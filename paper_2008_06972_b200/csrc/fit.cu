@@ -23,6 +23,7 @@
 // refit kernel overwriting covered P-frame pixels with +inf (= invalid), so
 // the fit needs no per-pixel exclusion test.
 #include "kernels.cuh"
+#include <cstdlib>
 
 namespace stpc {
 
@@ -1501,6 +1502,311 @@ __global__ void __launch_bounds__(128, STPC_REFIT_MINB) refit_kernel(RefitArgs A
     }
 }
 
+// ---------------------------------------------------------------------------
+// K3a, channel-batched (the product path; refit_kernel above is the
+// -DSTPC_REFIT_V1 A/B baseline).  One warp per (key chain, slice of its runs)
+// refits a run against ALL P channels at once: a lane owns a pixel position of
+// the span, and the ray, the denominator (dx + a dy) + b dz and the pixel
+// index are the same for every channel, so they are computed once per pixel
+// and each channel costs one load and one product.  The ordered fold, which a
+// warp can only do with every lane repeating the same sequential adds, now
+// serves up to RF_CB channels per instruction: lane c folds channel c's terms
+// from shared memory (the same v-major order and +0.0 padding as refit_span).
+// Two consecutive one-tile runs (<= 16 pixels each) are taken side by side,
+// one per half-warp.  Arithmetic and order per (run, channel) are
+// refit_spans' (_kernels.py:231-279), so the bits are the per-channel
+// kernel's.
+// ---------------------------------------------------------------------------
+#ifndef STPC_REFIT2_MINB
+#define STPC_REFIT2_MINB 8
+#endif
+#ifndef STPC_REFIT_SPLIT_MIN
+#define STPC_REFIT_SPLIT_MIN 2
+#endif
+constexpr long long REFIT_TARGET_WARPS = 148LL * STPC_REFIT2_MINB * 4 * 4;  // four waves of resident warps
+constexpr int RF_CB = 8;    // P channels per pass (n - 1 <= 8: one pass)
+constexpr int RF_ROW = 33;  // 32 terms per channel + 1 of padding (conflict-free folds)
+
+__global__ void __launch_bounds__(128, STPC_REFIT2_MINB) refit_all_kernel(RefitArgs A, int split)
+{
+    __shared__ double smem[4][RF_CB * RF_ROW];
+    __shared__ double s_pf[4][2][RF_CB * 32];  // the lanes' prefetched pixels, two visits deep: [buffer][channel][lane]
+    __shared__ double s_cc[4][2 * RF_CB];
+    const Geometry& g = A.g;
+    const int lane = threadIdx.x & 31, half = lane >> 4, hl = lane & 15;
+    const int wib = threadIdx.x >> 5;
+    double* sm = smem[wib];
+    double* scc = s_cc[wib];
+    double* pf = &s_pf[wib][0][lane];  // buffer b, channel ch: pf[b * RF_CB * 32 + ch * 32]
+    const int np = A.n - 1;
+    const long long wid = (long long)blockIdx.x * 4 + wib;
+    if (np < 1 || wid >= (long long)A.n_groups * g.ty * split) return;
+    const long long kc = wid / split;  // key chain
+    const int q = (int)(wid % split);
+    const int grp = (int)(kc / g.ty);
+    const int tr = (int)(kc % g.ty);
+    const long long kslot = ((long long)grp * A.n + A.k) * g.ty + tr;
+    const int nr = A.n_runs[kslot];
+    const int j0 = (int)((long long)nr * q / split), j1 = (int)((long long)nr * (q + 1) / split);
+    if (j0 >= j1) return;
+    const int v0 = tr * g.th;
+    const int rows = min(g.th, g.h - v0);
+    const int P = (int)g.P;  // pixel indices are ints (host-checked: n * P < 2^31)
+    const double INF = __longlong_as_double(0x7ff0000000000000ll);
+    double* gbase = A.best + (long long)grp * A.n * g.P;  // the group's frames
+#define RF_CHN(pi) ((pi) < A.k ? (pi) : (pi) + 1)
+    // pointer step from P channel pi to pi + 1 (the key frame lies between k - 1 and k)
+#define RF_STEP(pi) ((pi) + 1 == A.k ? 2 * P : P)
+    auto load_run = [&](int jr, int& s_, int& len_, float& af_, float& bf_) {
+        const long long ri = kslot * g.tx + min(jr, j1 - 1);
+        s_ = A.run_s[ri];
+        len_ = A.run_len[ri];
+        af_ = A.run_abc[3 * ri];
+        bf_ = A.run_abc[3 * ri + 1];
+    };
+    auto span_px = [&](int s_, int len_) { return rows * (min((s_ + len_) * g.tw, g.w) - s_ * g.tw); };
+    // pixel index of position p of run (s_, len_)'s span in v-major order; -1 past the span
+    auto px_index = [&](int s_, int len_, int p) -> int {
+        const int U0 = s_ * g.tw;
+        const int U = min((s_ + len_) * g.tw, g.w) - U0;
+        if (p >= rows * U) return -1;
+        int dv, du;
+        divmod_small(p, U, __frcp_rn((float)U), dv, du);
+        return (v0 + dv) * g.w + U0 + du;
+    };
+    for (int cb = 0; cb < np; cb += RF_CB) {
+        const int nch = min(RF_CB, np - cb);
+        double* const img0 = gbase + (long long)RF_CHN(cb) * P;  // the pass's first channel
+        // Visits of chunks alternate between the two prefetch buffers: a visit
+        // first issues the copies of the next visit in the stream (the next
+        // chunk, the re-test's first chunk of a long span, or the next run's
+        // first chunk) into the other buffer, then works on its own, so a
+        // visit's DRAM latency hides behind the previous visit's arithmetic.
+        int vb = 0;
+        auto pf_issue = [&](int idx, int buf) {
+            if (idx >= 0) {
+                double* d = pf + buf * (RF_CB * 32);
+                const double* src = img0 + idx;
+#pragma unroll 1
+                for (int ch = 0; ch < nch; ++ch) {
+                    cp_async8(d, src);
+                    d += 32;
+                    src += RF_STEP(cb + ch);
+                }
+            }
+            cp_async_commit();
+        };
+        int j = j0;
+        // candidates: half 0 holds run j, half 1 run j + 1 (cs..), and runs
+        // j + 2, j + 3 behind them (ns..), loaded an iteration ahead
+        int cs, clen, ns, nlen;
+        float caf, cbf, naf, nbf;
+        load_run(j + half, cs, clen, caf, cbf);
+        load_run(j + 2 + half, ns, nlen, naf, nbf);
+        {
+            const bool pr = __all_sync(STPC_FULL, span_px(cs, clen) <= 16) && j + 1 < j1;
+            const int s0 = pr ? cs : __shfl_sync(STPC_FULL, cs, 0);
+            const int l0 = pr ? clen : __shfl_sync(STPC_FULL, clen, 0);
+            pf_issue(px_index(s0, l0, pr ? hl : lane), vb);
+        }
+        while (j < j1) {
+            // two one-tile runs side by side (one per half-warp), else run j alone
+            const bool paired = __all_sync(STPC_FULL, span_px(cs, clen) <= 16) && j + 1 < j1;
+            int s = cs, len = clen;
+            float af = caf, bf = cbf;
+            if (!paired) {
+                s = __shfl_sync(STPC_FULL, s, 0);
+                len = __shfl_sync(STPC_FULL, len, 0);
+                af = __shfl_sync(STPC_FULL, af, 0);
+                bf = __shfl_sync(STPC_FULL, bf, 0);
+            }
+            const int U0 = s * g.tw;
+            const int U = min((s + len) * g.tw, g.w) - U0;
+            const int npx = rows * U;
+            const int gw = paired ? 16 : 32;    // lanes per run
+            const int gl = paired ? hl : lane;  // lane within the run's group
+            const int gsh = paired ? half : 0;  // group index
+            const unsigned gmask = paired ? 0xffffu << (half * 16) : STPC_FULL;
+            const double a = (double)af, b = (double)bf;
+            const float ru = __frcp_rn((float)U);
+            const long long rj = (kc * g.tx + (paired ? j + half : j)) * A.n;
+            if (cb == 0 && gl == 0) A.ref_ok[rj + A.k] = 1;
+            const int nchunks = paired ? 1 : (npx + 31) >> 5;
+
+            // the next iteration's candidates and the lane's first pixel there
+            const int jn = j + (paired ? 2 : 1);
+            if (paired) {
+                cs = ns; clen = nlen; caf = naf; cbf = nbf;
+            } else {
+                const int t_s = __shfl_sync(STPC_FULL, cs, 16), t_l = __shfl_sync(STPC_FULL, clen, 16);
+                const float t_a = __shfl_sync(STPC_FULL, caf, 16), t_b = __shfl_sync(STPC_FULL, cbf, 16);
+                const int u_s = __shfl_sync(STPC_FULL, ns, 0), u_l = __shfl_sync(STPC_FULL, nlen, 0);
+                const float u_a = __shfl_sync(STPC_FULL, naf, 0), u_b = __shfl_sync(STPC_FULL, nbf, 0);
+                cs = half ? u_s : t_s;
+                clen = half ? u_l : t_l;
+                caf = half ? u_a : t_a;
+                cbf = half ? u_b : t_b;
+            }
+            load_run(jn + 2 + half, ns, nlen, naf, nbf);
+            int nidx0 = -1;
+            if (jn < j1) {
+                const bool pr = __all_sync(STPC_FULL, span_px(cs, clen) <= 16) && jn + 1 < j1;
+                const int s0 = pr ? cs : __shfl_sync(STPC_FULL, cs, 0);
+                const int l0 = pr ? clen : __shfl_sync(STPC_FULL, clen, 0);
+                nidx0 = px_index(s0, l0, pr ? hl : lane);
+            }
+
+            // the lane's pixel of chunk ck: index and denominator (dx + a dy) + b dz
+            auto pixel = [&](int ck, int& idx, double& den) {
+                const int p = ck * 32 + gl;
+                idx = -1;
+                den = 0.0;
+                if (p < npx) {
+                    int dv, du;
+                    divmod_small(p, U, ru, dv, du);
+                    const int v = v0 + dv, u = U0 + du;
+                    double dx, dy, dz;
+                    ray_dir(A.tg, v, u, dx, dy, dz);
+                    den = (dx + a * dy) + b * dz;
+                    idx = v * g.w + u;
+                }
+            };
+
+            // ---- pass 1: the channels' ordered sums of r * (d . n)
+            double acc = 0.0;
+            int mycnt = 0;
+            int idx0 = -1;
+            double den0 = 0.0;
+#pragma unroll 1
+            for (int ck = 0; ck < nchunks; ++ck) {
+                int idx;
+                double den;
+                pixel(ck, idx, den);
+                if (ck == 0) {
+                    idx0 = idx;
+                    den0 = den;
+                }
+                // the next visit: next chunk | the re-test's first chunk | the next run
+                pf_issue(ck + 1 < nchunks ? px_index(s, len, ck * 32 + 32 + gl) : nchunks > 1 ? idx0 : nidx0, vb ^ 1);
+                asm volatile("cp.async.wait_group 1;\n" ::: "memory");  // this visit's copies have landed
+                const double* rp = pf + vb * (RF_CB * 32);
+#pragma unroll 1
+                for (int ch = 0; ch < nch; ++ch) {
+                    double prod = 0.0;  // +0.0 for invalid pixels and lanes past the span: exact
+                    bool valid = false;
+                    if (idx >= 0) {
+                        const double r = rp[ch * 32];
+                        if (isfinite(r)) {
+                            prod = r * den;
+                            valid = true;
+                        }
+                    }
+                    const unsigned bm = __ballot_sync(STPC_FULL, valid) & gmask;
+                    if (gl == ch) mycnt += __popc(bm);
+                    sm[ch * RF_ROW + lane] = prod;
+                }
+                __syncwarp();
+                if (gl < nch) {  // lane c of the group folds channel c
+                    const double* row = sm + gl * RF_ROW + (paired ? half * 16 : 0);
+                    const int nf = (paired || npx - ck * 32 <= 16) ? 16 : 32;
+#pragma unroll 8
+                    for (int jj = 0; jj < nf; ++jj) acc += row[jj];
+                }
+                __syncwarp();
+                vb ^= 1;
+            }
+            double cme = 0.0;
+            if (gl < nch) {
+                if (mycnt > 0) cme = f32_round(acc / (double)mycnt);
+                scc[gsh * RF_CB + gl] = cme;
+            }
+            __syncwarp();
+
+            // ---- pass 2: the span re-test with (a, b, c') per channel.  A
+            // one-chunk span re-reads its pass-1 buffer; a longer span streams
+            // its chunks through the buffers again.
+            unsigned failed = 0;  // bit ch: channel ch failed (uniform within the group)
+            const int rb = nchunks == 1 ? vb ^ 1 : vb;  // pass 1 left vb at the next visit's buffer
+#pragma unroll 1
+            for (int ck = 0; ck < nchunks; ++ck) {
+                int idx = idx0;
+                double den = den0;
+                if (ck > 0) pixel(ck, idx, den);
+                int cur = rb;
+                if (nchunks > 1) {
+                    pf_issue(ck + 1 < nchunks ? px_index(s, len, ck * 32 + 32 + gl) : nidx0, vb ^ 1);
+                    asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+                    cur = vb;
+                    vb ^= 1;
+                }
+                const double* rp = pf + cur * (RF_CB * 32);
+                const bool par = fabs(den) < STPC_PARALLEL_EPS;
+                unsigned bad = 0;
+                if (idx >= 0) {
+#pragma unroll 1
+                    for (int ch = 0; ch < nch; ++ch) {
+                        if ((failed >> ch) & 1) continue;
+                        const double r = rp[ch * 32];
+                        if (isfinite(r)) {
+                            bool fits = !par;
+                            if (fits) {
+                                const double r_hat = scc[gsh * RF_CB + ch] / den;
+                                fits = !(r_hat <= 0.0 || r_hat > A.r_max) && !(fabs(r - r_hat) > A.tau);
+                            }
+                            if (!fits) bad |= 1u << ch;
+                        }
+                    }
+                }
+                const unsigned red = __reduce_or_sync(STPC_FULL, bad << (gsh * RF_CB));
+                failed |= (red >> (gsh * RF_CB)) & 0xffu;
+                if (!paired && failed == (1u << nch) - 1u && ck + 1 < nchunks) {
+                    // uniform: every channel failed; the copies in flight are
+                    // this run's next chunk: replace them with the next run's
+                    cp_async_wait_all();
+                    pf_issue(nidx0, vb);
+                    break;
+                }
+            }
+
+            // ---- results, classes and poisoning
+            bool okc = false;
+            if (gl < nch) {
+                okc = mycnt > 0 && !((failed >> gl) & 1);
+                const int chn = RF_CHN(cb + gl);
+                A.ref_ok[rj + chn] = okc;
+                A.ref_c[rj + chn] = (float)cme;
+            }
+            const unsigned okb = __ballot_sync(STPC_FULL, okc);
+            const unsigned okmask = (okb >> (gsh * 16)) & 0xffu;
+            if (okmask) {
+                uint8_t* crow = A.cls + (((long long)grp * A.n + RF_CHN(cb)) * g.ty + tr) * g.tx;
+#pragma unroll 1
+                for (int ch = 0; ch < nch; ++ch) {
+                    if ((okmask >> ch) & 1)
+                        for (int tt = s + gl; tt < s + len; tt += gw) crow[tt] = 1;
+                    crow += (long long)(RF_STEP(cb + ch) / P) * g.ty * g.tx;
+                }
+#pragma unroll 1
+                for (int ck = 0; ck < nchunks; ++ck) {
+                    const int idx = ck == 0 ? idx0 : px_index(s, len, ck * 32 + gl);
+                    if (idx >= 0) {
+                        double* dst = img0 + idx;
+#pragma unroll 1
+                        for (int ch = 0; ch < nch; ++ch) {
+                            if ((okmask >> ch) & 1) *dst = INF;
+                            dst += RF_STEP(cb + ch);
+                        }
+                    }
+                }
+            }
+            j = jn;
+        }
+        cp_async_wait_all();
+    }
+#undef RF_CHN
+#undef RF_STEP
+}
+
 // temporal record bytes per key chain: lanes over runs, popcount of present P channels
 __global__ void __launch_bounds__(128) record_bytes_kernel(RefitArgs A)
 {
@@ -1528,12 +1834,24 @@ void launch_refit(const RefitArgs& a, cudaStream_t s)
 {
     long long kchains = (long long)a.n_groups * a.g.ty;
     if (kchains <= 0) return;
+#ifdef STPC_REFIT_V1
     const int per = a.g.tw * a.g.th <= 16 ? 2 : 1;  // P channels per warp (refit_kernel)
     long long warps = kchains * ((a.n - 1 + per - 1) / per);
     if (warps > 0) {
         STPC_LAUNCH();
         refit_kernel<<<(unsigned)((warps + 3) / 4), 128, 0, s>>>(a);
     }
+#else
+    if (a.n > 1) {
+        // warps per key chain (contiguous slices of its runs): enough warps to
+        // fill the machine a few times over when the batch has few chains
+        static const int forced = getenv("STPC_REFIT_SPLIT") ? atoi(getenv("STPC_REFIT_SPLIT")) : 0;
+        int split = forced > 0 ? forced : (int)std::min<long long>(32, std::max<long long>(STPC_REFIT_SPLIT_MIN, (REFIT_TARGET_WARPS + kchains - 1) / kchains));
+        const long long warps = kchains * split;
+        STPC_LAUNCH();
+        refit_all_kernel<<<(unsigned)((warps + 3) / 4), 128, 0, s>>>(a, split);
+    }
+#endif
     STPC_LAUNCH();
     record_bytes_kernel<<<(unsigned)((kchains + 3) / 4), 128, 0, s>>>(a);
 }
