@@ -1518,20 +1518,24 @@ __global__ void __launch_bounds__(128, STPC_REFIT_MINB) refit_kernel(RefitArgs A
 // kernel's.
 // ---------------------------------------------------------------------------
 #ifndef STPC_REFIT2_MINB
-#define STPC_REFIT2_MINB 8
+#define STPC_REFIT2_MINB 6  // measured (refit, split 1): 5 -> 3.46 ms, 6 -> 3.12-3.18, 7 -> 3.36, 8 -> 3.22-3.61
 #endif
 #ifndef STPC_REFIT_SPLIT_MIN
-#define STPC_REFIT_SPLIT_MIN 2
+#define STPC_REFIT_SPLIT_MIN 1  // measured at 16 k key chains: split 1 -> 3.12 ms, 2 -> 3.44, 4 -> 4.3
 #endif
+#ifndef STPC_REFIT2_WPB
+#define STPC_REFIT2_WPB 2  // warps per block (a block's slot is held until its slowest warp ends); measured 1 -> 3.18 ms, 2 -> 3.12, 4 -> 3.17
+#endif
+constexpr int RF_WPB = STPC_REFIT2_WPB;
 constexpr long long REFIT_TARGET_WARPS = 148LL * STPC_REFIT2_MINB * 4 * 4;  // four waves of resident warps
 constexpr int RF_CB = 8;    // P channels per pass (n - 1 <= 8: one pass)
 constexpr int RF_ROW = 33;  // 32 terms per channel + 1 of padding (conflict-free folds)
 
-__global__ void __launch_bounds__(128, STPC_REFIT2_MINB) refit_all_kernel(RefitArgs A, int split)
+__global__ void __launch_bounds__(32 * RF_WPB, STPC_REFIT2_MINB * 4 / RF_WPB) refit_all_kernel(RefitArgs A, int split)
 {
-    __shared__ double smem[4][RF_CB * RF_ROW];
-    __shared__ double s_pf[4][2][RF_CB * 32];  // the lanes' prefetched pixels, two visits deep: [buffer][channel][lane]
-    __shared__ double s_cc[4][2 * RF_CB];
+    __shared__ double smem[RF_WPB][RF_CB * RF_ROW];
+    __shared__ double s_pf[RF_WPB][2][RF_CB * 32];  // the lanes' prefetched pixels, two visits deep: [buffer][channel][lane]
+    __shared__ double s_cc[RF_WPB][2 * RF_CB];
     const Geometry& g = A.g;
     const int lane = threadIdx.x & 31, half = lane >> 4, hl = lane & 15;
     const int wib = threadIdx.x >> 5;
@@ -1539,7 +1543,7 @@ __global__ void __launch_bounds__(128, STPC_REFIT2_MINB) refit_all_kernel(RefitA
     double* scc = s_cc[wib];
     double* pf = &s_pf[wib][0][lane];  // buffer b, channel ch: pf[b * RF_CB * 32 + ch * 32]
     const int np = A.n - 1;
-    const long long wid = (long long)blockIdx.x * 4 + wib;
+    const long long wid = (long long)blockIdx.x * RF_WPB + wib;
     if (np < 1 || wid >= (long long)A.n_groups * g.ty * split) return;
     const long long kc = wid / split;  // key chain
     const int q = (int)(wid % split);
@@ -1849,7 +1853,7 @@ void launch_refit(const RefitArgs& a, cudaStream_t s)
         int split = forced > 0 ? forced : (int)std::min<long long>(32, std::max<long long>(STPC_REFIT_SPLIT_MIN, (REFIT_TARGET_WARPS + kchains - 1) / kchains));
         const long long warps = kchains * split;
         STPC_LAUNCH();
-        refit_all_kernel<<<(unsigned)((warps + 3) / 4), 128, 0, s>>>(a, split);
+        refit_all_kernel<<<(unsigned)((warps + RF_WPB - 1) / RF_WPB), 32 * RF_WPB, 0, s>>>(a, split);
     }
 #endif
     STPC_LAUNCH();
