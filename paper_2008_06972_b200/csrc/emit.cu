@@ -546,7 +546,7 @@ __global__ void __launch_bounds__(256, STPC_EMIT_MINB) emit_residual_kernel(Emit
 // workload).
 constexpr int EC_WARPS = 8;
 #ifndef STPC_EMITC_MINB
-#define STPC_EMITC_MINB 8
+#define STPC_EMITC_MINB 6  // measured with the range loads issued a round ahead: 4 -> 3.38 ms, 5 -> 3.11, 6 -> 2.98, 7 -> 3.50, 8 -> 3.61 (without: 8 -> 3.26, 6 -> 3.20)
 #endif
 __global__ void __launch_bounds__(EC_WARPS * 32, STPC_EMITC_MINB) emit_residual_compact_kernel(EmitArgs E)
 {
@@ -576,7 +576,7 @@ __global__ void __launch_bounds__(EC_WARPS * 32, STPC_EMITC_MINB) emit_residual_
     const uint8_t* crow = A.cls + (f * g.ty + v / g.th) * g.tx;
     const double* img = E.best + f * g.P;
     RowWalk rw = row_walk(g, v);
-    long long last = ro.prev;  // previous residual of the frame (0 if none)
+    int last = ro.prev;  // previous residual of the frame (0 if none); pixel indices fit 32 bits (P < 2^31)
     for (long long wbase = rw.w0; wbase < rw.w1; wbase += 32) {
         const long long wd = wbase + lane;
         uint32_t res = 0, tmp, fb, esc = 0;
@@ -601,16 +601,26 @@ __global__ void __launch_bounds__(EC_WARPS * 32, STPC_EMITC_MINB) emit_residual_
         }
         __syncwarp();
         // emit them, lane per residual pixel
-        const long long p0 = wbase * 32;
+        const int p0 = (int)(wbase * 32);
+        // the ranges are scattered DRAM reads: each round's load is issued a
+        // round ahead, so its latency hides behind the previous round's stores
+        unsigned e_n = lane < n ? list[lane] : 0u;
+        double r_n = lane < n ? img[p0 + (e_n & 1023u)] : 0.0;
         for (int k0 = 0; k0 < n; k0 += 32) {
             const int k = k0 + lane;
             const bool act = k < n;
             const int na = min(32, n - k0);
-            const unsigned e = act ? list[k] : 0u;
-            const long long idx = p0 + (e & 1023u);
+            const unsigned e = e_n;
+            const double r = r_n;
+            if (k0 + 32 < n) {
+                const bool an = k + 32 < n;
+                e_n = an ? list[k + 32] : 0u;
+                r_n = an ? img[p0 + (e_n & 1023u)] : 0.0;
+            }
+            const int idx = p0 + (int)(e & 1023u);
             const bool isesc = act && (e >> 15);
-            const long long pl = __shfl_up_sync(STPC_FULL, idx, 1);
-            const long long prev = lane == 0 ? last : pl;
+            const int pl = __shfl_up_sync(STPC_FULL, idx, 1);
+            const int prev = lane == 0 ? last : pl;
             uint32_t d = (uint32_t)(idx - prev);
             const int len = act ? varint_len(d) : 0;
             // one-byte deltas everywhere: the offsets are the lane numbers
@@ -623,7 +633,6 @@ __global__ void __launch_bounds__(EC_WARPS * 32, STPC_EMITC_MINB) emit_residual_
                     d >>= 7;
                 }
                 *vo = (uint8_t)d;
-                const double r = img[idx];
                 uint32_t code = 0xFFFFu;
                 if (isesc) {
                     put_f32(eptr + 4 * __popc(eball & lt), (float)r);
