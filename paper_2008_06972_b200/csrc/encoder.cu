@@ -377,7 +377,7 @@ static int encode_impl(stpc_encoder* e, int G, const void* d_points, const int64
     ENS(e->run_len, sizeof(uint16_t) * F * TT);
     ENS(e->run_abc, sizeof(float) * 3 * F * TT);
     ENS(e->n_runs, sizeof(int) * F * g.ty);
-    ENS(e->cert, sizeof(float4) * 3 * F * TT);
+    ENS(e->cert, sizeof(float4) * CERT_F4 * F * TT);
     ENS(e->start_ok, (size_t)F * TT);
     const bool keep_sums = g.tw * g.th <= 16;  // the pair chains take a start's sums from its verdict
     if (keep_sums) ENS(e->start_sums, sizeof(double) * 9 * F * TT);

@@ -28,7 +28,6 @@
 namespace stpc {
 
 constexpr int FIT_WARPS = 4;  // warps per block
-constexpr int CERT_F4 = 3;    // float4 per tile certificate
 
 // q, r = p / d, p % d for 0 <= p < 2^24 without an integer divide: float
 // reciprocal estimate, then an exact +-1 correction.
@@ -156,13 +155,14 @@ __device__ __forceinline__ int fold_tile(const Chain& ch, const Geometry& g, con
 // otherwise it is tested pixel by pixel (and re-certified).  Verdicts are
 // identical; only the work changes.
 //
-// Layout (CERT_F4 float4): c0 = (a, b, c, m), c1 = (dmin, rmin, rmax, 0),
-// c2 = (ymin, ymax, zmin, zmax).  The chain kernels' own tests store the
-// per-pixel slack X = min(tau - |r - r_hat|, r_hat, r_max - r_hat) instead:
-// c0.w = c1.y = min X, c1.z = 0, which the same three comparisons read as
-// B < min X (the start kernels keep the three fields).  The check itself is
-// division-free: B (1 + 1e-6) + 1e-9 < F becomes
-// max|n| (1 + 2e-6) < (F - 1e-9) (dmin - |da| - |db|), at least as strict.
+// Layout (CERT_F4 = 2 float4): c0 = (a, b, c, X), c1 = (dmin, yc, zc, radii).
+// X is the slack min over the pixels of min(tau - |r - r_hat|, r_hat,
+// r_max - r_hat), so the three conditions B < m, B < rmin, B < r_max - rmax
+// are the single B < X.  The box is stored as centre (yc, zc) and radii
+// (two bf16 values rounded up, packed in one word): the largest |n| over a
+// box is |n(centre)| + |da| ry + |db| rz, one evaluation instead of four
+// corners.  The check (cert_holds_f) is division-free and runs in fp32 with
+// every rounding covered: max|n| (1 + 3e-6) < (X - 1e-9) (dmin - |da| - |db|).
 // ---------------------------------------------------------------------------
 
 // Order-preserving map of a float to unsigned (for REDUX min/max of signed values).
@@ -177,6 +177,25 @@ __device__ __forceinline__ float key2f(unsigned k)
 }
 
 constexpr float CERT_EMPTY = 3.4e38f;  // m of a tile with no valid pixels
+
+// The certificate of a tile that passed under plane (a, b, c), from its
+// outward-rounded statistics: slack X, min |den| and the box of the
+// reconstructed points.  The box is kept as centre and radii (the largest
+// magnitude of an affine function over a box is its centre value plus the
+// radius terms), the radii rounded up to 16 significant bits and packed.
+__device__ __forceinline__ unsigned radius_bits(float r)  // r >= 0, rounded up to bf16 precision
+{
+    return (__float_as_uint(r) + 0xffffu) & 0xffff0000u;
+}
+__device__ __forceinline__ void cert_store(float4* ce, float a, float b, float c, float X, float dmin, float ylo,
+                                           float yhi, float zlo, float zhi)
+{
+    const float yc = 0.5f * (ylo + yhi), zc = 0.5f * (zlo + zhi);
+    const float ry = fmaxf(__fsub_ru(yhi, yc), __fsub_ru(yc, ylo));
+    const float rz = fmaxf(__fsub_ru(zhi, zc), __fsub_ru(zc, zlo));
+    ce[0] = make_float4(a, b, c, X);
+    ce[1] = make_float4(dmin, yc, zc, __uint_as_float(radius_bits(ry) | (radius_bits(rz) >> 16)));
+}
 
 // Full pixel test of tile t under (a, b, c); on pass, lane 0 stores the
 // tile's certificate.  Returns the verdict (warp-uniform).
@@ -232,52 +251,36 @@ __device__ bool test_tile(const Chain& ch, const Geometry& g, const Trig& tg, in
     const unsigned ky1 = __reduce_max_sync(STPC_FULL, f2key(__double2float_ru(fmin(fmax(yhi, -3.0e38), 3.0e38))));
     const unsigned kz0 = __reduce_min_sync(STPC_FULL, f2key(__double2float_rd(fmax(fmin(zlo, 3.0e38), -3.0e38))));
     const unsigned kz1 = __reduce_max_sync(STPC_FULL, f2key(__double2float_ru(fmin(fmax(zhi, -3.0e38), 3.0e38))));
-    if (lane == 0) {
-        float4* ce = ch.cert + CERT_F4 * t;
-        ce[0] = make_float4((float)a, (float)b, (float)c, __uint_as_float(ux));  // a/b/c are f32-exact
-        ce[1] = make_float4(__uint_as_float(ud), __uint_as_float(ux), 0.0f, 0.0f);
-        ce[2] = make_float4(key2f(ky0), key2f(ky1), key2f(kz0), key2f(kz1));
-    }
+    if (lane == 0)
+        cert_store(ch.cert + CERT_F4 * t, (float)a, (float)b, (float)c, __uint_as_float(ux), __uint_as_float(ud),
+                   key2f(ky0), key2f(ky1), key2f(kz0), key2f(kz1));  // a/b/c are f32-exact
     return true;
 }
 
-// Does tile j's certificate prove it passes under (a, b, c)?
-__device__ __forceinline__ bool cert_holds(const float4* cert, int j, double a, double b, double c,
-                                           double r_max)
+// Does tile j's certificate prove it passes under (a, b, c)?  Evaluated in
+// fp32 (a, b, c and the certificate's plane are f32-exact) with every
+// rounding covered: u = 2^-24 per operation, so the centre value n carries
+// at most ~4u (|dc| + |da yc| + |db zc|) of error (E below takes 8u), the
+// sums and products of lhs at most 4u relative (it takes 4e-6), dlo errs low
+// by its 1e-6 factors and X high by 2e-6; the result implies the exact
+//     (max_box |dc - da y - db z| / (dmin - |da| - |db|)) (1 + 1e-6) + 1e-9 < X.
+// Branch-free: both loads issue at once; a NaN field fails the comparison;
+// stale fields of an empty tile are ignored.
+__device__ __forceinline__ bool cert_holds_f(const float4* cert, int j, float a, float b, float c)
 {
-    const float4 c0 = cert[CERT_F4 * j];
-    if (c0.w >= CERT_EMPTY) return true;  // no valid pixels: passes under any plane
-    const float4 c1 = cert[CERT_F4 * j + 1], c2 = cert[CERT_F4 * j + 2];
-    const double da = a - (double)c0.x, db = b - (double)c0.y, dc = c - (double)c0.z;
-    const double dlo = (double)c1.x - (fabs(da) + fabs(db));
-    if (!(dlo > 2e-12)) return false;
-    const double n00 = fabs((dc - da * (double)c2.x) - db * (double)c2.z);
-    const double n01 = fabs((dc - da * (double)c2.x) - db * (double)c2.w);
-    const double n10 = fabs((dc - da * (double)c2.y) - db * (double)c2.z);
-    const double n11 = fabs((dc - da * (double)c2.y) - db * (double)c2.w);
-    // Division-free form of  B (1 + 1e-6) + 1e-9 < min(m, rmin, r_max - rmax)
-    // with B = max|n| / dlo (dlo > 0): the doubled relative slack absorbs the
-    // rounding of the rearranged products, so this is at least as strict.
-    const double lhs = fmax(fmax(n00, n01), fmax(n10, n11)) * (1.0 + 2e-6);
-    return lhs < ((double)c0.w - 1e-9) * dlo && lhs < ((double)c1.y - 1e-9) * dlo &&
-           lhs < ((r_max - (double)c1.z) - 1e-9) * dlo;  // a NaN field fails every comparison
-}
-
-// cert_holds without branches: all three loads issue at once (their latency
-// can overlap other work), stale fields of an empty tile are ignored.
-__device__ __forceinline__ bool cert_holds_bf(const float4* cert, int j, double a, double b, double c,
-                                              double r_max)
-{
-    const float4 c0 = cert[CERT_F4 * j], c1 = cert[CERT_F4 * j + 1], c2 = cert[CERT_F4 * j + 2];
-    const double da = a - (double)c0.x, db = b - (double)c0.y, dc = c - (double)c0.z;
-    const double dlo = (double)c1.x - (fabs(da) + fabs(db));
-    const double n00 = fabs((dc - da * (double)c2.x) - db * (double)c2.z);
-    const double n01 = fabs((dc - da * (double)c2.x) - db * (double)c2.w);
-    const double n10 = fabs((dc - da * (double)c2.y) - db * (double)c2.z);
-    const double n11 = fabs((dc - da * (double)c2.y) - db * (double)c2.w);
-    const double lhs = fmax(fmax(n00, n01), fmax(n10, n11)) * (1.0 + 2e-6);
-    const bool proven = dlo > 2e-12 && lhs < ((double)c0.w - 1e-9) * dlo && lhs < ((double)c1.y - 1e-9) * dlo &&
-                        lhs < ((r_max - (double)c1.z) - 1e-9) * dlo;
+    const float4 c0 = cert[CERT_F4 * j], c1 = cert[CERT_F4 * j + 1];
+    const float da = a - c0.x, db = b - c0.y, dc = c - c0.z;
+    const float ada = fabsf(da), adb = fabsf(db);
+    const float dlo = __fmaf_rn(-(1.0f + 1e-6f), ada + adb, c1.x * (1.0f - 1e-6f));
+    const float ry = __uint_as_float(__float_as_uint(c1.w) & 0xffff0000u);
+    const float rz = __uint_as_float(__float_as_uint(c1.w) << 16);
+    const float t1 = da * c1.y, t2 = db * c1.z;
+    const float n = (dc - t1) - t2;
+    const float E = 5e-7f * ((fabsf(dc) + fabsf(t1)) + fabsf(t2));
+    const float T = __fmaf_rn(adb, rz, ada * ry);
+    const float lhs = ((fabsf(n) + E) + T) * (1.0f + 4e-6f);
+    const float rhs = __fmaf_rn(c0.w, 1.0f - 2e-6f, -1e-9f) * dlo;
+    const bool proven = dlo > 1e-6f && lhs < rhs;
     return c0.w >= CERT_EMPTY || proven;
 }
 
@@ -288,9 +291,10 @@ __device__ bool union_fits(const Chain& ch, const Geometry& g, const Trig& tg, i
 {
     const int lane = threadIdx.x & 31;
     if (!test_tile(ch, g, tg, e, a, b, c, tau, r_max)) return false;
+    const float af = (float)a, bf = (float)b, cf = (float)c;  // f32-exact
     for (int base = s; base < e; base += 32) {
         const int j = base + lane;
-        bool weak = j < e && !cert_holds(ch.cert, j, a, b, c, r_max);
+        bool weak = j < e && !cert_holds_f(ch.cert, j, af, bf, cf);
         uint32_t wm = __ballot_sync(STPC_FULL, weak);
         while (wm) {
             const int jj = base + __ffs(wm) - 1;
@@ -447,11 +451,11 @@ __global__ void __launch_bounds__(START_TPB, STPC_STAGED_MINB) start_tiles_stage
     *sok = ok ? 1 : (empty ? 2 : 0);
     if (!ok) return;
     float4* ce = A.cert + (slot * g.tx + t) * CERT_F4;
-    ce[0] = make_float4((float)a, (float)b, (float)c, __double2float_rd(fmin(m, 3.0e38)));
-    ce[1] = make_float4(__double2float_rd(fmin(dmin, 3.0e38)), __double2float_rd(fmin(rmin, 3.0e38)),
-                        __double2float_ru(rmax), 0.0f);
-    ce[2] = make_float4(__double2float_rd(ylo), __double2float_ru(yhi), __double2float_rd(zlo),
-                        __double2float_ru(zhi));
+    // one slack field: B < m, B < rmin and B < r_max - rmax are B < min of the three
+    cert_store(ce, (float)a, (float)b, (float)c,
+               __double2float_rd(fmin(fmin(fmin(m, rmin), A.r_max - rmax), 3.0e38)),
+               __double2float_rd(fmin(dmin, 3.0e38)), __double2float_rd(ylo), __double2float_ru(yhi),
+               __double2float_rd(zlo), __double2float_ru(zhi));
 }
 
 #ifndef STPC_START_MINB
@@ -577,11 +581,11 @@ __global__ void __launch_bounds__(256, STPC_START_MINB) start_tiles_kernel(FitAr
         }
     }
     float4* ce = A.cert + (slot * g.tx + t) * CERT_F4;
-    ce[0] = make_float4((float)a, (float)b, (float)c, __double2float_rd(fmin(m, 3.0e38)));
-    ce[1] = make_float4(__double2float_rd(fmin(dmin, 3.0e38)), __double2float_rd(fmin(rmin, 3.0e38)),
-                        __double2float_ru(rmax), 0.0f);
-    ce[2] = make_float4(__double2float_rd(ylo), __double2float_ru(yhi), __double2float_rd(zlo),
-                        __double2float_ru(zhi));
+    // one slack field: B < m, B < rmin and B < r_max - rmax are B < min of the three
+    cert_store(ce, (float)a, (float)b, (float)c,
+               __double2float_rd(fmin(fmin(fmin(m, rmin), A.r_max - rmax), 3.0e38)),
+               __double2float_rd(fmin(dmin, 3.0e38)), __double2float_rd(ylo), __double2float_ru(yhi),
+               __double2float_rd(zlo), __double2float_ru(zhi));
 }
 
 // plane_from_sums (common.cuh; _kernels.py:23-76) for the lanes b0.. that hold
@@ -766,8 +770,8 @@ __device__ __forceinline__ unsigned group_max(unsigned v, int sub, unsigned neut
 // pixel's value (or the reduction's neutral element): no per-lane min/max and
 // no clamping (a passing pixel has 0 < r_hat <= r_max).  The margin, r_hat
 // lower bound and r_max headroom share one field, the pixel's slack
-// X = min(tau - |r - r_hat|, r_hat, r_max - r_hat): cert_holds' three tests
-// B < m, B < rmin, B < r_max - rmax become B < X with c1.y = X, c1.z = 0.
+// X = min(tau - |r - r_hat|, r_hat, r_max - r_hat): the three tests
+// B < m, B < rmin, B < r_max - rmax become B < X.
 // `has`: the lane holds a valid pixel (r, direction) of the tile.
 __device__ __forceinline__ bool test_px_pair(bool active, bool has, double r, double dx, double dy, double dz,
                                              const Chain& ch, int tile, double a, double b, double c,
@@ -817,9 +821,8 @@ __device__ __forceinline__ bool test_px_pair(bool active, bool has, double r, do
         // a tile whose pixels are all invalid certifies as empty (no neutral
         // keys leak into the float fields)
         const float xf = ux == NEUT_MIN ? CERT_EMPTY : __uint_as_float(ux);
-        ce[0] = make_float4((float)a, (float)b, (float)c, xf);
-        ce[1] = make_float4(__uint_as_float(ud), xf, 0.0f, 0.0f);
-        ce[2] = make_float4(key2f(ky0), key2f(ky1), key2f(kz0), key2f(kz1));
+        cert_store(ce, (float)a, (float)b, (float)c, xf, __uint_as_float(ud), key2f(ky0), key2f(ky1), key2f(kz0),
+                   key2f(kz1));
     }
     return pass;
 }
@@ -1191,7 +1194,8 @@ __global__ void __launch_bounds__(FIT_WARPS * 32, pair_minb<F44>()) fit_pair_ker
             // the first certificate batch of [s, t) does not depend on the new
             // tile's verdict: its loads and checks are issued before the pixel
             // test so the two latency chains overlap
-            const bool weak0 = testing && s + gl < t && !cert_holds_bf(ch.cert, s + gl, na, nb, nc, A.r_max);
+            const float naf = (float)na, nbf = (float)nb, ncf = (float)nc;  // f32-exact
+            const bool weak0 = testing && s + gl < t && !cert_holds_f(ch.cert, s + gl, naf, nbf, ncf);
             // the new tile's certificate is staged and stored only if the
             // whole union passes: a failed growth leaves tile t's start
             // certificate (whose plane (1a) takes as the start plane) intact
@@ -1203,7 +1207,7 @@ __global__ void __launch_bounds__(FIT_WARPS * 32, pair_minb<F44>()) fit_pair_ker
             while (__any_sync(STPC_FULL, pass && base < t)) {
                 const int j = base + gl;
                 const bool weak =
-                    pass && j < t && (base == s ? weak0 : !cert_holds_bf(ch.cert, j, na, nb, nc, A.r_max));
+                    pass && j < t && (base == s ? weak0 : !cert_holds_f(ch.cert, j, naf, nbf, ncf));
                 FIT_STAT(3, pass && j < t);  // certificate checks
                 FIT_STAT(4, weak);           // weak certificates -> full re-test
                 unsigned wm = (__ballot_sync(STPC_FULL, weak) & gmask) >> (sub * 16);

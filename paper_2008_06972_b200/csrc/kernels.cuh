@@ -75,6 +75,9 @@ void launch_convert_win(const ConvertArgs& a, int max_pts, cudaStream_t s);
 void launch_bitmaps(const double* best, int n_frames, const Geometry& g, double range_quant,
                     uint8_t* vbits, uint8_t* ebits, long long* fstats, cudaStream_t s);
 
+// float4 per tile certificate: (a, b, c, slack), (min |den|, box centre y, z, packed radii)
+constexpr int CERT_F4 = 2;
+
 struct FitArgs {
     const double* best;
     Trig tg;
@@ -88,7 +91,7 @@ struct FitArgs {
     uint16_t* run_len;
     float* run_abc;
     int* n_runs;
-    float4* cert;       // [F*TY][TX][3] per-tile test certificates (scratch)
+    float4* cert;       // [F*TY][TX][CERT_F4] per-tile test certificates (scratch)
     uint8_t* start_ok;  // [F*TY][TX] start verdicts (scratch)
     double* start_sums;  // [9][F*TY*TX] a passing start tile's moment sums (scratch; null: not kept)
     long long sums_stride;  // F*TY*TX
