@@ -394,10 +394,13 @@ __global__ void __launch_bounds__(START_TPB, STPC_STAGED_MINB) start_tiles_stage
         const double sp = __ldg(A.tg.sin_p + v0 + dv), cp = __ldg(A.tg.cos_p + v0 + dv);
 #pragma unroll
         for (int du = 0; du < TW; ++du) {
-            const double r = rr[dv * TW + du];
-            const bool valid = du < cols && isfinite(r);
+            const double rv = rr[dv * TW + du];
+            const bool valid = du < cols && isfinite(rv);
+            // an invalid pixel folds as r = 0: its products are +-0.0, and
+            // adding either zero to a sum that started at +0.0 is exact
+            const double r = valid ? rv : 0.0;
             const double dx = sp * st[du], dy = sp * ct[du], dz = cp;
-            const double x = valid ? r * dx : 0.0, y = valid ? r * dy : 0.0, z = valid ? r * dz : 0.0;
+            const double x = r * dx, y = r * dy, z = r * dz;
             sm[0] += y * y; sm[1] += y * z; sm[2] += z * z;
             sm[3] += y;     sm[4] += z;     sm[5] += x * y;
             sm[6] += x * z; sm[7] += x;     sm[8] += valid ? 1.0 : 0.0;
@@ -412,8 +415,10 @@ __global__ void __launch_bounds__(START_TPB, STPC_STAGED_MINB) start_tiles_stage
     const bool empty = sm[8] == 0.0;  // no valid pixel: 2, which the chains skip over in bulk
     double a, b, c;
     bool ok = sm[8] >= 3.0 && plane_from_sums(sm, A.cond_limit, a, b, c);
-    double m = 1e300, dmin = 1e300, rmin = 1e300, rmax = 0.0;
-    double ylo = 1e300, yhi = -1e300, zlo = 1e300, zhi = -1e300;
+    // certificate statistics in fp32, each rounded outward on conversion
+    // (half the registers and selects of fp64 min/max)
+    float X = 3.4e38f, dmin = 3.4e38f;
+    float ylo = 3.4e38f, yhi = -3.4e38f, zlo = 3.4e38f, zhi = -3.4e38f;
     if (ok) {
         a = f32_round(a);
         b = f32_round(b);
@@ -437,25 +442,20 @@ __global__ void __launch_bounds__(START_TPB, STPC_STAGED_MINB) start_tiles_stage
                 ok = ok && !(valid && bad);
                 const bool use = valid && !bad;
                 const double yh = r_hat * dy, zh = r_hat * cp;
-                m = use ? fmin(m, A.tau - err) : m;
-                dmin = use ? fmin(dmin, ad) : dmin;
-                rmin = use ? fmin(rmin, r_hat) : rmin;
-                rmax = use ? fmax(rmax, r_hat) : rmax;
-                ylo = use ? fmin(ylo, yh) : ylo;
-                yhi = use ? fmax(yhi, yh) : yhi;
-                zlo = use ? fmin(zlo, zh) : zlo;
-                zhi = use ? fmax(zhi, zh) : zhi;
+                // the pixel's slack: B < tau - err, B < r_hat, B < r_max - r_hat in one field
+                const float xs = __double2float_rd(fmin(fmin(A.tau - err, r_hat), A.r_max - r_hat));
+                X = use ? fminf(X, xs) : X;
+                dmin = use ? fminf(dmin, __double2float_rd(ad)) : dmin;
+                ylo = use ? fminf(ylo, __double2float_rd(yh)) : ylo;
+                yhi = use ? fmaxf(yhi, __double2float_ru(yh)) : yhi;
+                zlo = use ? fminf(zlo, __double2float_rd(zh)) : zlo;
+                zhi = use ? fmaxf(zhi, __double2float_ru(zh)) : zhi;
             }
         }
     }
     *sok = ok ? 1 : (empty ? 2 : 0);
     if (!ok) return;
-    float4* ce = A.cert + (slot * g.tx + t) * CERT_F4;
-    // one slack field: B < m, B < rmin and B < r_max - rmax are B < min of the three
-    cert_store(ce, (float)a, (float)b, (float)c,
-               __double2float_rd(fmin(fmin(fmin(m, rmin), A.r_max - rmax), 3.0e38)),
-               __double2float_rd(fmin(dmin, 3.0e38)), __double2float_rd(ylo), __double2float_ru(yhi),
-               __double2float_rd(zlo), __double2float_ru(zhi));
+    cert_store(A.cert + (slot * g.tx + t) * CERT_F4, (float)a, (float)b, (float)c, X, dmin, ylo, yhi, zlo, zhi);
 }
 
 #ifndef STPC_START_MINB
