@@ -237,23 +237,30 @@ __global__ void __launch_bounds__(PACK_THREADS, STPC_PACK_MINB) pack_write_kerne
 {
     const int grp = blockIdx.y, c = blockIdx.x;
     if (E.prefill) {  // this block's slice of the next grid's +inf fill (16-byte stores)
-        const long long nblk = (long long)gridDim.x * gridDim.y;
         const long long bid = (long long)blockIdx.y * gridDim.x + blockIdx.x;
-        const long long n2 = E.prefill_n / 2;
-        const long long per = (n2 + nblk - 1) / nblk;
-        ulonglong2* dst = reinterpret_cast<ulonglong2*>(E.prefill);
+        const long long lo = bid * E.prefill_per;  // 16-byte elements per block: host-computed (no 64-bit divide here)
+        const long long cntl = max(0LL, min(E.prefill_per, (E.prefill_n >> 1) - lo));
+        ulonglong2* dst = reinterpret_cast<ulonglong2*>(E.prefill) + lo;
         const ulonglong2 inf2 = make_ulonglong2(0x7ff0000000000000ull, 0x7ff0000000000000ull);
-        for (long long i = bid * per + threadIdx.x; i < min(n2, (bid + 1) * per); i += PACK_THREADS) dst[i] = inf2;
+        if (cntl <= 0x7fffffffLL) {  // 32-bit loop (always, in practice)
+            const int cnt = (int)cntl;
+            for (int i = threadIdx.x; i < cnt; i += PACK_THREADS) dst[i] = inf2;
+        } else {
+            for (long long i = threadIdx.x; i < cntl; i += PACK_THREADS) dst[i] = inf2;
+        }
     }
     long long b, e;
     chunk_range(E, grp, c, b, e);
     if (b >= e) return;
     __shared__ uint8_t lens[256];
-    __shared__ unsigned int codes[256];
+    __shared__ uint2 cl[256];  // (code, length): one 8-byte load per symbol in the assembly pass
     __shared__ unsigned int buf[PACK_CHUNK + 2];  // 32 bits per byte worst case
     __shared__ int wsum[PACK_THREADS / 32];
-    lens[threadIdx.x] = E.lens[grp * 256 + threadIdx.x];
-    codes[threadIdx.x] = E.codes[grp * 256 + threadIdx.x];
+    {
+        const uint8_t l = E.lens[grp * 256 + threadIdx.x];
+        lens[threadIdx.x] = l;
+        cl[threadIdx.x] = make_uint2(E.codes[grp * 256 + threadIdx.x], l);
+    }
     __syncthreads();
     const uint8_t* p = E.payload + E.payload_off[grp];
     const long long O = E.chunk_bits[(long long)grp * E.max_chunks + c];  // chunk's first bit
@@ -273,9 +280,14 @@ __global__ void __launch_bounds__(PACK_THREADS, STPC_PACK_MINB) pack_write_kerne
         for (int q = 0; q < nq; ++q) wv[q >> 2] |= (uint32_t)p[tb + q] << (8 * (q & 3));
     }
     int mybits = 0;
+    if (nq == PACK_PER_THREAD) {  // every chunk but a payload's last: no per-byte bound
 #pragma unroll
-    for (int q = 0; q < PACK_PER_THREAD; ++q)
-        mybits += q < nq ? lens[(wv[q >> 2] >> (8 * (q & 3))) & 0xff] : 0;
+        for (int q = 0; q < PACK_PER_THREAD; ++q) mybits += lens[(wv[q >> 2] >> (8 * (q & 3))) & 0xff];
+    } else {
+#pragma unroll
+        for (int q = 0; q < PACK_PER_THREAD; ++q)
+            mybits += q < nq ? lens[(wv[q >> 2] >> (8 * (q & 3))) & 0xff] : 0;
+    }
     const int inc = warp_incl_scan(mybits);
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     if (lane == 31) wsum[wid] = inc;
@@ -307,8 +319,9 @@ __global__ void __launch_bounds__(PACK_THREADS, STPC_PACK_MINB) pack_write_kerne
         for (int q = 0; q < PACK_PER_THREAD; ++q) {
             if (q < nq) {
                 const unsigned s = (wv[q >> 2] >> (8 * (q & 3))) & 0xff;
-                const int l = lens[s];
-                acc = (acc << l) | codes[s];
+                const uint2 e = cl[s];
+                const int l = (int)e.y;
+                acc = (acc << l) | e.x;
                 nacc += l;
                 if (nacc >= 32) {
                     nacc -= 32;
@@ -342,7 +355,12 @@ void launch_pack(const EntropyArgs& E, cudaStream_t s)
     STPC_LAUNCH();
     pack_scan_kernel<<<E.G, 32, 0, s>>>(E);
     STPC_LAUNCH();
-    pack_write_kernel<<<grid, PACK_THREADS, 0, s>>>(E);
+    EntropyArgs W = E;
+    if (W.prefill) {
+        const long long nblk = (long long)grid.x * grid.y, n2 = W.prefill_n / 2;
+        W.prefill_per = (n2 + nblk - 1) / nblk;
+    }
+    pack_write_kernel<<<grid, PACK_THREADS, 0, s>>>(W);
 }
 
 // --------------------------------------------------------------------- CRC

@@ -187,6 +187,7 @@ struct EntropyArgs {
     // blocks (background stores behind the instruction-bound packing)
     unsigned long long* prefill = nullptr;
     long long prefill_n = 0;  // u64 elements (even)
+    long long prefill_per = 0;  // 16-byte elements per pack block (set by launch_pack)
 };
 constexpr int PACK_CHUNK = 4096;  // payload bytes per pack block
 constexpr int CRC_PIECE = 256;    // bytes per CRC thread
