@@ -76,35 +76,44 @@ __global__ void __launch_bounds__(32) code_lengths_kernel(EntropyArgs E)
     for (int o = 16; o > 0; o >>= 1) nsym += __shfl_xor_sync(STPC_FULL, nsym, o);
     __syncwarp();
 
-    for (int m = 0; m + 1 < nsym; ++m) {
-        int pick[2];
-        unsigned long long wsum = 0;
-        for (int q = 0; q < 2; ++q) {
-            unsigned long long best = INACTIVE;
-            int bi = -1;
-            for (int i = lane; i < 256 + m; i += 32) {
-                unsigned long long k = key[i];
-                if (k < best) { best = k; bi = i; }
+    // The heap's pops in (weight, serial) order without a heap: the leaves
+    // are sorted once (bitonic, in shared memory), and merged nodes are
+    // created in non-decreasing (weight, serial) order, so the smallest node
+    // is always at the head of one of two queues -- the classic two-queue
+    // construction, with the reference's tie-break (a leaf's serial is its
+    // symbol < 256 <= any merged node's) decided by the same key compare.
+    for (int k = 2; k <= 256; k <<= 1) {
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            for (int t = lane; t < 128; t += 32) {
+                const int i = 2 * j * (t / j) + (t % j), p = i + j;
+                const unsigned long long x = key[i], y = key[p];
+                const bool up = (i & k) == 0;
+                if ((x > y) == up) {
+                    key[i] = y;
+                    key[p] = x;
+                }
             }
-            for (int o = 16; o > 0; o >>= 1) {
-                unsigned long long ob = __shfl_xor_sync(STPC_FULL, best, o);
-                int oi = __shfl_xor_sync(STPC_FULL, bi, o);
-                if (ob < best) { best = ob; bi = oi; }
-            }
-            pick[q] = bi;
-            wsum += best >> 10;
-            __syncwarp();
-            if (lane == 0) key[bi] = INACTIVE;
             __syncwarp();
         }
-        if (lane == 0) {
-            int node = 256 + m;
-            key[node] = (wsum << 10) | (unsigned)node;
-            parent[pick[0]] = (short)node;
-            parent[pick[1]] = (short)node;
-        }
-        __syncwarp();
     }
+    if (lane == 0) {
+        int q1 = 0, q2 = 256;  // heads of the leaf queue [0, nsym) and the merged-node queue [256, 256 + m)
+        for (int m = 0; m + 1 < nsym; ++m) {
+            const int node = 256 + m;
+            unsigned long long wsum = 0;
+            for (int q = 0; q < 2; ++q) {
+                const unsigned long long k1 = q1 < nsym ? key[q1] : INACTIVE;
+                const unsigned long long k2 = q2 < node ? key[q2] : INACTIVE;
+                const unsigned long long best = k1 < k2 ? k1 : k2;
+                if (k1 < k2) ++q1;
+                else ++q2;
+                parent[(int)(best & 1023u)] = (short)node;
+                wsum += best >> 10;
+            }
+            key[node] = (wsum << 10) | (unsigned)node;
+        }
+    }
+    __syncwarp();
     // depth = merges a leaf's subtree took part in = hops to the root
     int maxlen = 0;
     for (int s = lane; s < 256; s += 32) {
@@ -215,15 +224,16 @@ __global__ void __launch_bounds__(PACK_THREADS) pack_count_kernel(EntropyArgs E)
 __global__ void pack_scan_kernel(EntropyArgs E)
 {
     const int grp = blockIdx.x;
-    long long nch = (E.payload_len[grp] + PACK_CHUNK - 1) / PACK_CHUNK;
-    if (threadIdx.x == 0) {
-        long long* cb = E.chunk_bits + (long long)grp * E.max_chunks;
-        long long run = 0;
-        for (long long c = 0; c < nch; ++c) {
-            long long v = cb[c];
-            cb[c] = run;
-            run += v;
-        }
+    const long long nch = (E.payload_len[grp] + PACK_CHUNK - 1) / PACK_CHUNK;
+    long long* cb = E.chunk_bits + (long long)grp * E.max_chunks;
+    const int lane = threadIdx.x;  // one warp per group
+    long long run = 0;
+    for (long long base = 0; base < nch; base += 32) {
+        const long long c = base + lane;
+        const long long v = c < nch ? cb[c] : 0;
+        const long long inc = warp_incl_scan_ll(v);
+        if (c < nch) cb[c] = run + inc - v;
+        run += __shfl_sync(STPC_FULL, inc, 31);
     }
 }
 
@@ -496,16 +506,30 @@ __global__ void crc_finish_kernel(EntropyArgs E, CrcConsts K)
     const int grp = blockIdx.x;
     uint8_t* blob = E.blobs + E.blob_off[grp];
     for (int i = threadIdx.x; i < 256; i += blockDim.x) blob[28 + i] = E.lens[grp * 256 + i];
-    if (threadIdx.x != 0) return;
+    if (threadIdx.x >= 32) return;
     const long long L = E.enc_len[grp];
     const long long npieces = L / CRC_PIECE;
     const long long nseg = (npieces + 31) / 32;
+    // the segments' CRCs combine by Horner's rule; lane l folds a contiguous
+    // range of them, weights its partial by x^(8 * bytes of the pieces after
+    // the range), and the partials XOR together (CRC is linear)
     unsigned int raw = 0;
-    for (long long sgi = 0; sgi < nseg; ++sgi) {
-        const long long np = min(32LL, npieces - sgi * 32);
-        const unsigned int X = np == 32 ? K.seg : x8nmodp((unsigned long long)np * CRC_PIECE);
-        raw = multmodp(X, raw) ^ E.seg_crc[(long long)grp * E.max_segs + sgi];
+    {
+        const long long per = (nseg + 31) / 32;
+        const long long s0 = threadIdx.x * per, s1 = min(nseg, s0 + per);
+        unsigned int r = 0;
+        for (long long sgi = s0; sgi < s1; ++sgi) {
+            const long long np = min(32LL, npieces - sgi * 32);
+            const unsigned int X = np == 32 ? K.seg : x8nmodp((unsigned long long)np * CRC_PIECE);
+            r = multmodp(X, r) ^ E.seg_crc[(long long)grp * E.max_segs + sgi];
+        }
+        if (s0 < s1) {
+            const long long after = npieces - min(npieces, s1 * 32);
+            r = multmodp(x8nmodp((unsigned long long)after * CRC_PIECE), r);
+        }
+        raw = __reduce_xor_sync(STPC_FULL, r);
     }
+    if (threadIdx.x != 0) return;
     // tail (< 256 bytes) byte-wise
     const uint8_t* enc = blob + HDR;
     const long long tb = npieces * CRC_PIECE;
