@@ -633,7 +633,6 @@ static int encode_impl(stpc_encoder* e, int G, const void* d_points, const int64
     en.chunk_bits = e->chunk_bits.as<long long>();
     en.seg_crc = e->seg_crc.as<unsigned>();
     en.blobs = e->blobs.as<uint8_t>();
-    launch_zero(en.blobs, blob_total, s);
     e->mark(ST_PACK, s);
     launch_pack(en, s);
     if (!e->ev_fill[0]) for (auto& x : e->ev_fill) CK(cudaEventCreateWithFlags(&x, cudaEventDisableTiming));
@@ -1176,7 +1175,6 @@ int stpc_entropy_encode(const uint8_t* h_payloads, const int64_t* offsets, int32
     en.chunk_bits = chunk_bits.as<long long>();
     en.seg_crc = seg_crc.as<unsigned>();
     en.blobs = blobs.as<uint8_t>();
-    launch_zero(en.blobs, bo[n], s);
     launch_pack(en, s);
     launch_crc(en, s);
     CK(cudaGetLastError());

@@ -227,19 +227,29 @@ __global__ void pack_scan_kernel(EntropyArgs E)
     const long long nch = (E.payload_len[grp] + PACK_CHUNK - 1) / PACK_CHUNK;
     long long* cb = E.chunk_bits + (long long)grp * E.max_chunks;
     const int lane = threadIdx.x;  // one warp per group
+    // pack_write ORs a chunk's first and last word into the blob (a word can
+    // be shared with the neighbouring chunk) and stores the words in between:
+    // only those boundary words need to start at zero, so they are cleared
+    // here instead of the whole blob arena
+    unsigned int* gw = reinterpret_cast<unsigned int*>(E.blobs + E.blob_off[grp] + HDR);
     long long run = 0;
     for (long long base = 0; base < nch; base += 32) {
         const long long c = base + lane;
         const long long v = c < nch ? cb[c] : 0;
         const long long inc = warp_incl_scan_ll(v);
-        if (c < nch) cb[c] = run + inc - v;
+        if (c < nch) {
+            const long long O = run + inc - v;
+            cb[c] = O;
+            gw[O >> 5] = 0u;
+            if (v > 0) gw[(O + v - 1) >> 5] = 0u;
+        }
         run += __shfl_sync(STPC_FULL, inc, 31);
     }
 }
 
 // phase C: compose each chunk's bits in shared memory (big-endian u32 words),
 // store interior words, atomicOr the two boundary words shared with
-// neighbouring chunks (the encoded region is zeroed beforehand).
+// neighbouring chunks (pack_scan zeroes exactly those words beforehand).
 #ifndef STPC_PACK_MINB
 #define STPC_PACK_MINB 8  // measured: 1 -> 2.98 ms (pack stage), 8 -> 2.87
 #endif
