@@ -74,6 +74,21 @@ __device__ __forceinline__ void word_classes(const Geometry& g, const uint8_t* c
     const long long p0 = wd * 32;
     const int lo = (int)max(0LL, rb - p0), hi = (int)min(32LL, re - p0);
     if (lo >= hi) return;
+    if (g.tw == 4 && (g.w & 15) == 0 && lo == 0 && hi == 32) {
+        // a whole word of 4-pixel tiles (w % 16 == 0 makes its first tile
+        // index a multiple of 4): eight class bytes by two aligned loads,
+        // compared four at a time, each byte spread to its tile's nibble
+        const int t0 = (int)(p0 - rb) >> 2;
+        const uint32_t c0 = *reinterpret_cast<const uint32_t*>(crow + t0);
+        const uint32_t c1 = *reinterpret_cast<const uint32_t*>(crow + t0 + 4);
+        auto nib = [](uint32_t m) {  // 0xFF / 0x00 per byte -> 0xF / 0x0 per nibble
+            return (m & 0xFu) | ((m >> 4) & 0xF0u) | ((m >> 8) & 0xF00u) | ((m >> 12) & 0xF000u);
+        };
+        res = (nib(__vcmpeq4(c0, 0u)) | (nib(__vcmpeq4(c1, 0u)) << 16)) & valid;
+        tmp = (nib(__vcmpeq4(c0, 0x01010101u)) | (nib(__vcmpeq4(c1, 0x01010101u)) << 16)) & valid;
+        fb = (nib(__vcmpeq4(c0, 0x02020202u)) | (nib(__vcmpeq4(c1, 0x02020202u)) << 16)) & valid;
+        return;
+    }
     int u = (int)(p0 + lo - rb);  // column of bit lo
     int tile = __float2int_rz(((float)u + 0.5f) * __frcp_rn((float)g.tw));
     {
