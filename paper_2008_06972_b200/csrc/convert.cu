@@ -490,7 +490,10 @@ constexpr int CONVERT_UNROLL = STPC_CONVERT_UNROLL;
 #ifndef STPC_CONVERT_STAGED_MINB
 #define STPC_CONVERT_STAGED_MINB 4
 #endif
-template <class T>
+// IDX32: the batch's grids hold fewer than 2^32 pixels, so a pixel's element
+// index is one 32-bit add from the frame's base (a single register held per
+// unit) instead of a 64-bit frame * P product rematerialised per point.
+template <class T, bool IDX32>
 __global__ void __launch_bounds__(256, STPC_CONVERT_STAGED_MINB)
     convert_staged_kernel(ConvertArgs a, const T* pts, int n_units, int mc, int seg)
 {
@@ -535,7 +538,8 @@ __global__ void __launch_bounds__(256, STPC_CONVERT_STAGED_MINB)
 #pragma unroll
             for (int t = 0; t < 12; ++t) c[t] = xfs[t];
             const uint8_t* sp = stage + SC::HDR_BYTES + SC::XF_BYTES + h.lead;
-            unsigned long long* best = a.best + (long long)h.f * a.g.P;
+            unsigned long long* best = a.best + (IDX32 ? 0ll : (long long)h.f * a.g.P);
+            const unsigned fb = IDX32 ? (unsigned)h.f * (unsigned)a.g.P : 0u;
             auto bin = [&](int j, T px, T py, T pz) {
                 const double qx = (double)px, qy = (double)py, qz = (double)pz;
                 const double x = xform_coord(qx, qy, qz, c[0], c[1], c[2], c[9]);
@@ -550,7 +554,10 @@ __global__ void __launch_bounds__(256, STPC_CONVERT_STAGED_MINB)
 #elif defined(STPC_CONVERT_EXP) && STPC_CONVERT_EXP == 2
                     atomicMin(best + (pix & 0x3fff), (unsigned long long)__double_as_longlong(rr));
 #else
-                    atomicMin(best + pix, (unsigned long long)__double_as_longlong(rr));
+                    if (IDX32)
+                        atomicMin(best + (fb + (unsigned)pix), (unsigned long long)__double_as_longlong(rr));
+                    else
+                        atomicMin(best + pix, (unsigned long long)__double_as_longlong(rr));
 #endif
                 } else if (cls == PT_QUEUE) {
                     nq += 1;
@@ -785,9 +792,10 @@ static void launch_staged(const ConvertArgs& a, int max_pts, cudaStream_t s)
     cudaGetDevice(&dev);
     int& grid_max = grid_max_dev[dev < MAX_DEV ? dev : MAX_DEV - 1];
     if (!grid_max) {
-        cudaFuncSetAttribute(convert_staged_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, SC::SMEM);
+        cudaFuncSetAttribute(convert_staged_kernel<T, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, SC::SMEM);
+        cudaFuncSetAttribute(convert_staged_kernel<T, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, SC::SMEM);
         int per_sm = 0, sms = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, convert_staged_kernel<T>, 32 * SC::WARPS, SC::SMEM);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, convert_staged_kernel<T, true>, 32 * SC::WARPS, SC::SMEM);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
         grid_max = std::max(1, std::min(per_sm * sms, CONVERT_MAX_GRID));
     }
@@ -797,7 +805,10 @@ static void launch_staged(const ConvertArgs& a, int max_pts, cudaStream_t s)
     const int grid = (int)std::min<long long>(grid_max, (n_units + SC::WARPS - 1) / SC::WARPS);
     const int seg = (int)std::max<long long>(1, a.q_cap / grid);
     STPC_LAUNCH();
-    convert_staged_kernel<T><<<grid, 32 * SC::WARPS, SC::SMEM, s>>>(a, (const T*)a.pts, (int)n_units, mc, seg);
+    if ((long long)a.n_frames * a.g.P < (1ll << 32))
+        convert_staged_kernel<T, true><<<grid, 32 * SC::WARPS, SC::SMEM, s>>>(a, (const T*)a.pts, (int)n_units, mc, seg);
+    else
+        convert_staged_kernel<T, false><<<grid, 32 * SC::WARPS, SC::SMEM, s>>>(a, (const T*)a.pts, (int)n_units, mc, seg);
     STPC_LAUNCH();
     convert_exact_seg_kernel<T><<<dim3(grid, EXACT_SPLIT), 256, 0, s>>>(a, (const T*)a.pts, seg);
     STPC_LAUNCH();
