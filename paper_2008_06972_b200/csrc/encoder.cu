@@ -15,6 +15,7 @@
 #include <vector>
 #include <algorithm>
 
+#include <cmath>
 #include "kernels.cuh"
 #include "runtime.cuh"
 #include "../../include/stpc_b200.h"
@@ -448,6 +449,7 @@ static int encode_impl(stpc_encoder* e, int G, const void* d_points, const int64
     fa.tau = e->cfg.tau;
     fa.r_max = e->cfg.r_max;
     fa.cond_limit = e->cfg.cond_limit;
+    fa.ybias = std::exp2(std::ceil(std::log2(std::max(fa.r_max, 1.0))) + 1.0);  // power of two >= 2 r_max
     fa.n_frames_group = n;
     fa.k = k;
     fa.mode = 0;

@@ -775,7 +775,7 @@ __device__ __forceinline__ unsigned group_max(unsigned v, int sub, unsigned neut
 // `has`: the lane holds a valid pixel (r, direction) of the tile.
 __device__ __forceinline__ bool test_px_pair(bool active, bool has, double r, double dx, double dy, double dz,
                                              const Chain& ch, int tile, double a, double b, double c,
-                                             double tau, double r_max, float4* stage = nullptr)
+                                             double tau, double r_max, double ybias, float4* stage = nullptr)
 {
     const int lane = threadIdx.x & 31;
     const int sub = lane >> 4, gl = lane & 15;
@@ -798,10 +798,13 @@ __device__ __forceinline__ bool test_px_pair(bool active, bool has, double r, do
                     kx = __float_as_uint(__double2float_rd(fmin(fmin(tau - err, r_hat), r_max - r_hat)));
                     kd = __float_as_uint(__double2float_rd(ad));
                     const double yh = r_hat * dy, zh = r_hat * dz;
-                    ky0 = f2key(__double2float_rd(yh));
-                    ky1 = f2key(__double2float_ru(yh));
-                    kz0 = f2key(__double2float_rd(zh));
-                    kz1 = f2key(__double2float_ru(zh));
+                    // |yh|, |zh| <= r_max <= ybias / 2: biased, they are positive
+                    // floats, whose bit patterns order like their values (no
+                    // order-preserving key transform on either side of the REDUX)
+                    ky0 = __float_as_uint(__double2float_rd(__dadd_rd(yh, ybias)));
+                    ky1 = __float_as_uint(__double2float_ru(__dadd_ru(yh, ybias)));
+                    kz0 = __float_as_uint(__double2float_rd(__dadd_rd(zh, ybias)));
+                    kz1 = __float_as_uint(__double2float_ru(__dadd_ru(zh, ybias)));
                 }
             }
         }
@@ -821,8 +824,10 @@ __device__ __forceinline__ bool test_px_pair(bool active, bool has, double r, do
         // a tile whose pixels are all invalid certifies as empty (no neutral
         // keys leak into the float fields)
         const float xf = ux == NEUT_MIN ? CERT_EMPTY : __uint_as_float(ux);
-        cert_store(ce, (float)a, (float)b, (float)c, xf, __uint_as_float(ud), key2f(ky0), key2f(ky1), key2f(kz0),
-                   key2f(kz1));
+        const float bf = (float)ybias;  // a power of two: the subtractions are exact
+        cert_store(ce, (float)a, (float)b, (float)c, xf, __uint_as_float(ud), __fsub_rd(__uint_as_float(ky0), bf),
+                   __fsub_ru(__uint_as_float(ky1), bf), __fsub_rd(__uint_as_float(kz0), bf),
+                   __fsub_ru(__uint_as_float(kz1), bf));
     }
     return pass;
 }
@@ -848,7 +853,7 @@ __device__ __forceinline__ bool tile_px(const Chain& ch, const Geometry& g, int 
 // test_px_pair with the lane's pixel of `tile` loaded from global memory.
 template <bool F44>
 __device__ bool test_tile_pair(bool active, const Chain& ch, const Geometry& g, const Trig& tg, int tile,
-                               double a, double b, double c, double tau, double r_max)
+                               double a, double b, double c, double tau, double r_max, double ybias)
 {
     const int gl = threadIdx.x & 15;
     bool has = false;
@@ -865,7 +870,7 @@ __device__ bool test_tile_pair(bool active, const Chain& ch, const Geometry& g, 
             }
         }
     }
-    return test_px_pair(active, has, r, dx, dy, dz, ch, tile, a, b, c, tau, r_max);
+    return test_px_pair(active, has, r, dx, dy, dz, ch, tile, a, b, c, tau, r_max, ybias);
 }
 
 // plane_from_sums for a half-warp (see plane_from_sums_lanes).
@@ -1200,7 +1205,7 @@ __global__ void __launch_bounds__(FIT_WARPS * 32, pair_minb<F44>()) fit_pair_ker
             // whole union passes: a failed growth leaves tile t's start
             // certificate (whose plane (1a) takes as the start plane) intact
             pass = test_px_pair(testing, testing && one != 0.0, row[0], row[1], row[2], row[3], ch, t, na, nb, nc,
-                                A.tau, A.r_max, cstage[wib][sub]);
+                                A.tau, A.r_max, A.ybias, cstage[wib][sub]);
             FIT_STAT(5, testing && gl == 0);        // growth tests
             FIT_STAT(6, testing && pass && gl == 0);  // growth tests passed (new tile)
             int base = s;
@@ -1215,7 +1220,7 @@ __global__ void __launch_bounds__(FIT_WARPS * 32, pair_minb<F44>()) fit_pair_ker
                     const bool act = pass && wm != 0;
                     const int jj = act ? base + __ffs(wm) - 1 : 0;
                     if (act) wm &= wm - 1;
-                    const bool r = test_tile_pair<F44>(act, ch, g, A.tg, jj, na, nb, nc, A.tau, A.r_max);
+                    const bool r = test_tile_pair<F44>(act, ch, g, A.tg, jj, na, nb, nc, A.tau, A.r_max, A.ybias);
                     FIT_STAT(7, act && !r && gl == 0);  // re-tests that fail the union
                     if (act && !r) pass = false;
                 }

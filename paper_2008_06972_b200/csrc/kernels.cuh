@@ -83,6 +83,7 @@ struct FitArgs {
     Trig tg;
     Geometry g;
     double tau, r_max, cond_limit;
+    double ybias = 0.0;     // power of two >= 2 r_max: biases the certificates' box coordinates positive (pair kernel)
     int n_frames_group, k;  // group layout
     int mode;               // 0: key frames (pass 1), 1: P frames (pass 2)
     int n_jobs;             // frames in this pass
