@@ -943,7 +943,8 @@ __global__ void __launch_bounds__(FIT_WARPS * 32, pair_minb<F44>()) fit_pair_ker
     ch.skip1 = A.mode != 0;
     int t = 0, s = 0, n_runs = 0;
     bool grow = false;
-    double acc = 0.0, a = 0.0, b = 0.0, c = 0.0;
+    double acc = 0.0;
+    float a = 0.f, b = 0.f, c = 0.f;  // the run's plane: f32-exact by construction, kept as floats (3 registers, not 6)
     int pf_t = -1;
     __shared__ double pf_slot[FIT_WARPS * 32];  // the lane's prefetched pixel (cp.async: no register)
     double& pf_s = pf_slot[threadIdx.x];
@@ -1005,9 +1006,9 @@ __global__ void __launch_bounds__(FIT_WARPS * 32, pair_minb<F44>()) fit_pair_ker
             A.run_s[sb + n_runs] = (uint16_t)s;
             A.run_len[sb + n_runs] = (uint16_t)(e_ - s);
             float* rabc = A.run_abc + (size_t)(sb + n_runs) * 3;
-            rabc[0] = (float)a;
-            rabc[1] = (float)b;
-            rabc[2] = (float)c;
+            rabc[0] = a;
+            rabc[1] = b;
+            rabc[2] = c;
         }
         for (int tt = s + gl; tt < e_; tt += PG)
             if (!(ch.skip1 && CROW[tt] == 1)) CROW[tt] = run_cls;
@@ -1179,15 +1180,17 @@ __global__ void __launch_bounds__(FIT_WARPS * 32, pair_minb<F44>()) fit_pair_ker
         FIT_STAT(0, live && gl == 0);                      // chain steps
         FIT_STAT(2, live && grow && cnt == 0 && gl == 0);  // empty growth steps
         const bool need = live && (!grow || cnt > 0);
-        double na = 0.0, nb = 0.0, nc = 0.0;
+        // the new plane, f32-rounded (_kernels.py:196-198): held as floats and
+        // widened (exactly) where the fp64 tests use it
+        float naf = 0.f, nbf = 0.f, ncf = 0.f;
         bool ok = false;
         {
             double pa, pb, pc;
             const bool solved = plane_from_sums_pair(acc, sub, gl, A.cond_limit, pa, pb, pc);
             if (need && solved) {
-                na = f32_round(pa);
-                nb = f32_round(pb);
-                nc = f32_round(pc);
+                naf = __double2float_rn(pa);
+                nbf = __double2float_rn(pb);
+                ncf = __double2float_rn(pc);
                 ok = true;
             }
         }
@@ -1199,12 +1202,12 @@ __global__ void __launch_bounds__(FIT_WARPS * 32, pair_minb<F44>()) fit_pair_ker
             // the first certificate batch of [s, t) does not depend on the new
             // tile's verdict: its loads and checks are issued before the pixel
             // test so the two latency chains overlap
-            const float naf = (float)na, nbf = (float)nb, ncf = (float)nc;  // f32-exact
             const bool weak0 = testing && s + gl < t && !cert_holds_f(ch.cert, s + gl, naf, nbf, ncf);
             // the new tile's certificate is staged and stored only if the
             // whole union passes: a failed growth leaves tile t's start
             // certificate (whose plane (1a) takes as the start plane) intact
-            pass = test_px_pair(testing, testing && one != 0.0, row[0], row[1], row[2], row[3], ch, t, na, nb, nc,
+            pass = test_px_pair(testing, testing && one != 0.0, row[0], row[1], row[2], row[3], ch, t, (double)naf,
+                                (double)nbf, (double)ncf,
                                 A.tau, A.r_max, A.ybias, cstage[wib][sub]);
             FIT_STAT(5, testing && gl == 0);        // growth tests
             FIT_STAT(6, testing && pass && gl == 0);  // growth tests passed (new tile)
@@ -1220,7 +1223,8 @@ __global__ void __launch_bounds__(FIT_WARPS * 32, pair_minb<F44>()) fit_pair_ker
                     const bool act = pass && wm != 0;
                     const int jj = act ? base + __ffs(wm) - 1 : 0;
                     if (act) wm &= wm - 1;
-                    const bool r = test_tile_pair<F44>(act, ch, g, A.tg, jj, na, nb, nc, A.tau, A.r_max, A.ybias);
+                    const bool r = test_tile_pair<F44>(act, ch, g, A.tg, jj, (double)naf, (double)nbf, (double)ncf, A.tau,
+                                                       A.r_max, A.ybias);
                     FIT_STAT(7, act && !r && gl == 0);  // re-tests that fail the union
                     if (act && !r) pass = false;
                 }
@@ -1236,7 +1240,7 @@ __global__ void __launch_bounds__(FIT_WARPS * 32, pair_minb<F44>()) fit_pair_ker
                 if (gl == 0) CERT[CERT_F4 * t] = make_float4(0.f, 0.f, 0.f, CERT_EMPTY);
                 t += 1;
             } else if (pass) {
-                a = na; b = nb; c = nc;
+                a = naf; b = nbf; c = ncf;
                 t += 1;
             } else {
                 emit_e = t;  // close [s, t); t becomes a start candidate again
